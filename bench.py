@@ -1,0 +1,463 @@
+#!/usr/bin/env python
+"""ALISE hot-path benchmark (BASELINE.json metric: KV quant+swap GB/s & predictor
+queries/s vs roofline at 1/2/4/8 B200).
+
+One step = BASELINE config 2 (``configs[1]``): every preempted job's KV
+(Llama-2-7B shape: 32 layers x 2 x 2048 tokens x 4096 fp16 = 1 GiB per job) is
+INT8-quantized and offloaded to pinned host memory, and uploaded back and
+dequantized into HBM.  Offload of job j overlaps upload of job j-1, so both
+directions of the host link stream concurrently.  Jobs are assigned to GPUs by
+LPT with no collective (weak per-GPU share of a fixed 64-job pool -> "strong").
+
+  value  : fp16 KV bytes swapped (out + in) per second, whole job, C-ABI swapper
+  e2e    : same metric through the drop-in DeviceMemoryState API
+           (start_offload / complete / start_upload / complete per job)
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl alise|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KV quant+swap GB/s & predictor queries/s vs roofline at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="alise", choices=["alise", "reference"])
+    ap.add_argument("--jobs", type=int, default=64)
+    ap.add_argument("--tokens", type=int, default=2048)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--hidden", type=int, default=4096)
+    ap.add_argument("--head-dim", type=int, default=128)
+    ap.add_argument("--kind", default="rows", choices=["rows", "channel", "head"])
+    ap.add_argument("--group", type=int, default=128)
+    ap.add_argument("--bits", type=int, default=8)
+    ap.add_argument("--packed", action="store_true")
+    ap.add_argument("--mode", default="staged", choices=["staged", "zerocopy"])
+    ap.add_argument("--host-slabs", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-planes", type=int, default=16)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks sampler
+class Clocks:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[5:9]):
+                if "Active" in v and "Not" not in v:
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- distributed plumbing
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), float(p.get("bf16_tflops", 1590.0)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ----------------------------------------------------------------- CPU baseline (oracle port)
+def _cpu_worker(payload):
+    import numpy as np
+
+    from oracle import kv_oracle
+    from paper_2410_23537_b200 import synthetic
+    (plane_idx, tokens, hidden, group, bits) = payload
+    x = synthetic.kv_job(1, tokens, hidden, seed=0, job=1000 + plane_idx, group=group)[0, 0]
+    rows = x.reshape(-1, group)
+    t0 = time.perf_counter()
+    codes, scale, zero = kv_oracle.quantize_rows(rows, bits)
+    t1 = time.perf_counter()
+    y = kv_oracle.dequantize_rows(codes, scale, zero).astype(np.float16)
+    t2 = time.perf_counter()
+    return rows.size, t1 - t0, t2 - t1, int(y.size)
+
+
+def cpu_kv_sample(args, planes: int):
+    """The reference algorithm (oracle numpy port of kvmanager.quantize/dequantize) on
+    `planes` (layer, K|V) planes of one job, one process per host core."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    payload = [(i, args.tokens, args.hidden, args.group, args.bits) for i in range(planes)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(min(cores, planes)) as pool:
+        pool.map(_cpu_worker, payload[: min(cores, planes)])  # warm imports
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_worker, payload)
+        wall = time.perf_counter() - t0
+    elems = sum(r[0] for r in res)
+    procs = min(cores, planes)
+    # compute time only (input generation inside the workers is excluded), assuming
+    # perfect scaling over the worker processes: an upper bound for the CPU path
+    busy = sum(r[1] + r[2] for r in res) / procs
+    return {"elements": elems, "wall_s": busy, "cores": procs,
+            "GBps": 2 * 2 * elems / busy / 1e9}
+
+
+# ----------------------------------------------------------------- link peaks
+def link_peaks(dev_index: int):
+    import torch
+    n = 1 << 30
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t) / reps
+
+    d2h = n / timed(lambda: h.copy_(d, non_blocking=True)) / 1e9
+    h2d = n / timed(lambda: d.copy_(h, non_blocking=True)) / 1e9
+
+    def both():
+        with torch.cuda.stream(s1):
+            h.copy_(d, non_blocking=True)
+        with torch.cuda.stream(s2):
+            d2.copy_(h2, non_blocking=True)
+    duplex = 2 * n / timed(both) / 1e9
+    del d, d2, h, h2
+    return {"d2h_GBs": d2h, "h2d_GBs": h2d, "duplex_total_GBs": duplex}
+
+
+# ----------------------------------------------------------------- KV bench
+def kv_bench(args, world, rank, local):
+    import torch
+
+    from paper_2410_23537_b200 import kvmanager as km
+    from paper_2410_23537_b200 import synthetic
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    layout = km.KVLayout(args.layers, args.tokens, args.hidden, args.head_dim, kind=args.kind,
+                         group=args.group, bits=args.bits, packed=args.packed)
+    geo = layout.geometry()
+    job_bytes = layout.elements * 2
+    sizes = [job_bytes] * args.jobs
+    mine = synthetic.lpt_assign(sizes, world)[rank]
+    kvs = [synthetic.kv_job_torch(args.layers, args.tokens, args.hidden, seed=0, job=j,
+                                  group=args.group if args.kind == "rows" else 64, device=dev)
+           for j in mine]
+    H = max(2, args.host_slabs)
+    pool = km.HostSlabPool(H * ((geo["slab_bytes"] + 255) // 256 * 256))
+    slabs = [pool.alloc(geo["slab_bytes"]) for _ in range(H)]
+    eng = km.KVSwapEngine(device=local, mode=args.mode)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    ev_off = [km._Event() for _ in range(H)]
+    ev_up = [km._Event() for _ in range(H)]
+    used_up = [False] * H
+    stream = torch.cuda.current_stream()
+
+    def step():
+        n = len(kvs)
+        for j in range(n + 1):
+            if j < n:
+                s = j % H
+                if used_up[s]:
+                    eng.depend(ev_up[s].h)      # slab s was being read by an upload
+                eng.offload(layout, kvs[j], slabs[s], flag=flag, event=ev_off[s].h)
+            if j > 0:
+                s = (j - 1) % H
+                eng.depend(ev_off[s].h)         # upload reads what the offload wrote
+                eng.upload(layout, slabs[s], kvs[j - 1], event=ev_up[s].h)
+                used_up[s] = True
+        # the step ends when both directions are done
+        for e in (ev_off[(n - 1) % H], ev_up[(n - 1) % H]):
+            km._lib.call("alise_stream_wait", km._lib.stream_ptr(), e.h)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    eng.kernel_stats()
+    eng.set_timing(True)
+    clocks = Clocks(local)
+    clocks.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ck = clocks.stop()
+    eng.set_timing(False)
+    qms, qn, dms, dn = eng.kernel_stats()
+    ms = t0.elapsed_time(t1)
+    ms_max = max_over_ranks(ms, world)
+    bad = int(flag.item())
+    fp16_bytes_all = 2 * job_bytes * args.jobs  # out + in, every job, one step
+    value = fp16_bytes_all * args.steps / (ms_max / 1e3) / 1e9
+    link_bytes_rank = 2 * geo["slab_bytes"] * len(kvs) * args.steps
+    link_total = sum_over_ranks(link_bytes_rank, world)
+    res = {"ms_per_step": ms_max / args.steps, "value": value, "nonfinite": bad,
+           "link_GBs_total": link_total / (ms_max / 1e3) / 1e9,
+           "quant_ms_total": qms, "quant_launches": qn, "deq_ms_total": dms, "deq_launches": dn,
+           "clocks": ck, "geo": geo, "kernels_per_step": (qn + dn) / max(1, args.steps)}
+
+    # e2e through the drop-in API (DeviceMemoryState), host slabs from its own pool
+    if not args.no_e2e:
+        m = km.ModelConfig("llama-2-7b", args.hidden // args.head_dim, args.layers, args.hidden)
+        link_acc = km.quantized_kv_bytes(m, args.tokens, args.bits)
+        gpu_b = km.kv_bytes(m, args.tokens)
+        mstate = km.DeviceMemoryState(gpu_capacity=gpu_b * (len(kvs) + 1), cpu_capacity=link_acc * (len(kvs) + 1),
+                                      pcie_bytes_per_ms=25e6, host_pool_bytes=3 * geo["slab_bytes"] + (1 << 20),
+                                      engine=eng, host_pool=None)
+        for j, kv in enumerate(kvs):
+            mstate.bind(j, kv, layout)
+            mstate.reserve_gpu(gpu_b)
+
+        def e2e_step():
+            n = len(kvs)
+            pend_up = None
+            now = 0
+            for j in range(n + 1):
+                off = mstate.start_offload(j, link_acc, gpu_b, now) if j < n else None
+                if j > 0:
+                    mstate.complete(prev_off)
+                    if pend_up is not None:
+                        mstate.complete(pend_up)
+                    pend_up = mstate.start_upload(j - 1, link_acc, gpu_b, now)
+                prev_off = off
+            mstate.complete(pend_up)
+            torch.cuda.synchronize()
+
+        e2e_step()  # warm (allocates the pool)
+        barrier(world)
+        torch.cuda.synchronize()
+        ta = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - ta, world)
+        res["e2e"] = {"value": fp16_bytes_all * args.e2e_steps / e2e_s / 1e9, "unit": "GB/s",
+                      "h2d_bytes_per_step": geo["slab_bytes"] * args.jobs,
+                      "d2h_bytes_per_step": geo["slab_bytes"] * args.jobs,
+                      "api": "DeviceMemoryState.start_offload/complete/start_upload/complete",
+                      "steps": args.e2e_steps}
+        mstate.host_pool.close()
+    eng.close()
+    pool.close()
+    del kvs
+    torch.cuda.empty_cache()
+    return res
+
+
+# ----------------------------------------------------------------- main
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    hbm_peak, bf16_peak, peak_src = load_peaks()
+    links = link_peaks(local)
+    kv = kv_bench(args, world, rank, local)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_kv_sample(args, args.cpu_planes)
+    if rank == 0:
+        layout_elems = args.layers * 2 * args.tokens * args.hidden
+        geo = kv["geo"]
+        chunk_elems = layout_elems / geo["n_chunks"]
+        rows_per_chunk = geo["rows"] / geo["n_chunks"]
+        q_bytes = chunk_elems * (2 + args.bits / 8 / (2 if args.packed else 1) * (2 if args.packed else 1)) \
+            + rows_per_chunk * 12
+        if args.packed:
+            q_bytes = chunk_elems * (2 + 0.5) + rows_per_chunk * 12
+        q_avg_ms = kv["quant_ms_total"] / max(1, kv["quant_launches"])
+        d_avg_ms = kv["deq_ms_total"] / max(1, kv["deq_launches"])
+        q_ach = q_bytes / (q_avg_ms / 1e3) / 1e9 if q_avg_ms > 0 else None
+        d_ach = q_bytes / (d_avg_ms / 1e3) / 1e9 if d_avg_ms > 0 else None
+        link_peak = links["duplex_total_GBs"]
+        out = {
+            "metric": METRIC,
+            "value": round(kv["value"], 3),
+            "unit": "GB/s (fp16 KV swapped out+in per s)",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(kv["ms_per_step"], 3),
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "u8" if args.bits == 8 else "u4",
+            "data": "synthetic (seeded C1 value mix: normal, x40 outlier channels, 1% constant, "
+                    "10% single-sign groups)",
+            "config": {"workload": f"C2: {args.jobs} jobs Llama-2-7B KV ({args.layers}L x 2 x "
+                                   f"{args.tokens} tok x {args.hidden}) INT{args.bits} "
+                                   f"{args.kind}{'' if args.kind != 'rows' else ' g=' + str(args.group)}"
+                                   f" quantize+offload then upload+dequant",
+                       "jobs": args.jobs, "tokens": args.tokens, "layers": args.layers,
+                       "hidden": args.hidden, "kind": args.kind, "group": args.group,
+                       "bits": args.bits, "packed": args.packed, "mode": args.mode,
+                       "host_slabs": args.host_slabs, "job_assignment": "LPT, no collective",
+                       "l2": "inputs (1 GiB per job) >> 126 MB L2; no flush needed",
+                       "parallelism": f"jobs sharded over {world} GPU(s)"},
+            "roofline": {"bound": "hbm", "kernel": "k_quant_tile (quantize one transfer chunk)",
+                         "achieved": round(q_ach, 1) if q_ach else None, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": round(q_ach / hbm_peak, 4) if q_ach else None,
+                         "peak_source": peak_src,
+                         "bytes_per_launch": q_bytes, "avg_launch_ms": q_avg_ms,
+                         "traffic": None},
+            "roofline_dequant": {"bound": "hbm", "kernel": "k_dequant", "achieved":
+                                 round(d_ach, 1) if d_ach else None, "peak": hbm_peak,
+                                 "frac": round(d_ach / hbm_peak, 4) if d_ach else None,
+                                 "avg_launch_ms": d_avg_ms},
+            "roofline_link": {"bound": "host link (PCIe Gen5 x16, both directions)",
+                              "achieved": round(kv["link_GBs_total"] / world, 2),
+                              "peak": round(link_peak, 2), "unit": "GB/s per GPU",
+                              "frac": round(kv["link_GBs_total"] / world / link_peak, 4),
+                              "peaks_measured": links},
+            "gpu_launches": int(kv["quant_launches"] + kv["deq_launches"]),
+            "clocks": kv["clocks"],
+            "nonfinite_flag": kv["nonfinite"],
+        }
+        if "e2e" in kv:
+            out["e2e"] = kv["e2e"]
+        if cpu is not None:
+            out["cpu_baseline"] = {"value": round(cpu["GBps"], 4), "unit": "GB/s", "cores": cpu["cores"],
+                                   "kind": "port",
+                                   "sample": f"{args.cpu_planes} (layer,K|V) planes of one job "
+                                             f"({cpu['elements']} fp16 values): oracle numpy "
+                                             f"quantize+dequantize (kvmanager.py:108-154), "
+                                             f"one process per core, {cpu['wall_s']:.2f}s"}
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def reference_arm(args, world, rank):
+    """The reference's CPU path (oracle numpy port of kvmanager.quantize/dequantize;
+    the reference is pure Python/numpy and has no GPU or link) on the host cores."""
+    if rank != 0:
+        return
+    samples = []
+    for _ in range(args.warmup):
+        cpu_kv_sample(args, args.cpu_planes)
+    for _ in range(args.steps):
+        samples.append(cpu_kv_sample(args, args.cpu_planes))
+    wall = sum(s["wall_s"] for s in samples)
+    elems = sum(s["elements"] for s in samples)
+    v = 2 * 2 * elems / wall / 1e9
+    cores = samples[0]["cores"]
+    out = {"metric": METRIC, "impl": "reference", "value": round(v, 4),
+           "unit": "GB/s (fp16 KV swapped out+in per s)", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(1e3 * wall / args.steps, 3),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "u8" if args.bits == 8 else "u4", "data": "synthetic",
+           "config": {"workload": f"C2 sample: {args.cpu_planes} (layer,K|V) planes of a Llama-2-7B "
+                                  f"job, INT{args.bits} g={args.group} quantize+dequantize",
+                      "jobs": args.jobs, "tokens": args.tokens, "bits": args.bits},
+           "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                            "sample": f"{args.cpu_planes} planes per step, {elems // args.steps} values"},
+           "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

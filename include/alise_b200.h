@@ -1,0 +1,168 @@
+/* alise_b200.h — C ABI of libalise_b200.so, the B200 data plane behind the
+ * reference servesim package's quantizer / swap / predictor API.
+ *
+ * Conventions (all entry points):
+ *   - return int status: ALISE_OK, or an ALISE_E* code; alise_last_error()
+ *     returns a thread-local message for the last failure.
+ *   - every device pointer is caller-owned (torch tensors or alise_* allocations);
+ *     calls are stream-ordered on the `stream` argument (a cudaStream_t, NULL =
+ *     legacy default stream) and never synchronise the host unless stated.
+ *   - non-finite inputs are reported through a caller-provided device int flag
+ *     (set to non-zero), read by the host after the work completes; the Python
+ *     layer turns it into ValueError("tensor contains non-finite values"),
+ *     exactly as kvmanager.py:127-128 does.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference):
+ *   alise_quantize_rows      <- servesim.kvmanager.quantize     pkg/src/servesim/kvmanager.py:108
+ *   alise_dequantize_rows    <- servesim.kvmanager.dequantize   pkg/src/servesim/kvmanager.py:152
+ *   alise_kv_*  / swapper    <- servesim.kvmanager.MemoryState.start_offload / start_upload /
+ *                               complete (kvmanager.py:241-268) — the reference only does the
+ *                               byte accounting; these move and (de)quantize the bytes
+ *   alise_db_* / alise_pred* <- servesim.predictor.VectorStore.add/search (predictor.py:135-163),
+ *                               LengthPredictor.predict_vector (predictor.py:311-325),
+ *                               FallbackRegressor.predict_len (predictor.py:209-219)
+ */
+#ifndef ALISE_B200_H
+#define ALISE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ALISE_OK 0
+#define ALISE_EINVAL 1      /* bad argument -> ValueError                      */
+#define ALISE_ENONFINITE 2  /* non-finite input -> ValueError                  */
+#define ALISE_ECAPACITY 3   /* capacity / accounting violation                 */
+#define ALISE_ECUDA 4       /* CUDA runtime error -> RuntimeError              */
+
+#define ALISE_DT_F16 0
+#define ALISE_DT_F32 1
+#define ALISE_DT_F64 2
+
+#define ALISE_KIND_ROWS 0     /* rows of row_len contiguous values (group-wise g)       */
+#define ALISE_KIND_CHANNEL 1  /* (layer, k|v, hidden column) along tokens (reference)   */
+#define ALISE_KIND_HEAD 2     /* (layer, k|v, head) over tokens x head_dim              */
+
+#define ALISE_SWAP_STAGED 0   /* quantize to an HBM ring, copy engine D2H/H2D (default) */
+#define ALISE_SWAP_ZEROCOPY 1 /* kernels read/write mapped pinned host memory directly  */
+
+const char *alise_last_error(void);
+int alise_version(void);
+int alise_sm_count(int device, int *out);
+
+/* ---------------------------------------------------------------- quantizer ---- */
+/* Drop-in for kvmanager.quantize: rows x row_len values (row i at src + i*row_stride
+ * elements, dtype ALISE_DT_*), bits in {4,8}.  codes: rows*row_len bytes (one code
+ * per byte, the reference's uint8 layout, kvmanager.py:94).  scale, zero: float64[rows].
+ * nonfinite_flag: device int (OR-ed with 1 on a non-finite value).  workspace:
+ * device scratch of alise_quantize_rows_workspace() bytes (may be NULL if 0). */
+int alise_quantize_rows_workspace(int64_t rows, int64_t row_len, int src_dtype, int64_t *bytes);
+int alise_quantize_rows(const void *src, int src_dtype, int64_t rows, int64_t row_len,
+                        int64_t row_stride, int bits, uint8_t *codes, double *scale,
+                        double *zero, int *nonfinite_flag, void *workspace, void *stream);
+/* Drop-in for kvmanager.dequantize: out = scale*(code - zero), out_dtype F64 (reference
+ * bit-exact) or F16 (one rounding of the float64 value). */
+int alise_dequantize_rows(const uint8_t *codes, const double *scale, const double *zero,
+                          int64_t rows, int64_t row_len, int out_dtype, void *out, void *stream);
+
+/* ------------------------------------------------------------ KV data plane ---- */
+/* One job's KV cache in HBM: kv[layers][2][tokens][hidden] fp16 (hidden = heads*head_dim). */
+typedef struct {
+  int64_t layers;
+  int64_t tokens;
+  int64_t hidden;
+  int64_t head_dim;
+  int32_t kind;       /* ALISE_KIND_* */
+  int32_t group;      /* KIND_ROWS: values per group (multiple of 8, divides hidden) */
+  int32_t bits;       /* 4 or 8 */
+  int32_t packed;     /* 1: two INT4 codes per byte (low nibble = even element) */
+  int32_t planes_per_chunk; /* transfer granularity in (layer, k|v) planes; 0 = auto */
+  int32_t reserved;
+} alise_kv_desc;
+
+/* Host slab layout: ceil(planes/planes_per_chunk) chunk records, each
+ *   [codes of its planes, native element order][scale f64 per row][zero f32 per row]
+ * with every section 256-byte aligned.  rows = groups; link bytes = slab bytes. */
+int alise_kv_layout(const alise_kv_desc *d, int64_t *slab_bytes, int64_t *rows,
+                    int64_t *chunk_bytes, int64_t *n_chunks);
+/* Device-to-device quantize of a whole job into a device slab (same layout). */
+int alise_kv_quantize(const alise_kv_desc *d, const uint16_t *kv, uint8_t *slab,
+                      int *nonfinite_flag, void *stream);
+/* Device slab -> fp16 KV. */
+int alise_kv_dequantize(const alise_kv_desc *d, const uint8_t *slab, uint16_t *kv, void *stream);
+
+typedef struct alise_swapper alise_swapper;
+/* ring_bytes: HBM staging per direction (0 = 3 chunks of the largest desc seen). */
+int alise_swapper_create(int device, int mode, int64_t ring_bytes, alise_swapper **out);
+int alise_swapper_destroy(alise_swapper *sw);
+/* Quantize kv (HBM) chunk by chunk and stream the slab to host_slab (pinned host),
+ * overlapping kernel and D2H copy engine.  Kernels run on `stream`, copies on the
+ * swapper's side stream.  done_event (cudaEvent_t, may be NULL) fires when the
+ * last byte has landed in host memory.  The kv buffer may be reused once
+ * `stream` passes this point (all reads are ordered on it). */
+int alise_kv_offload(alise_swapper *sw, const alise_kv_desc *d, const uint16_t *kv,
+                     void *host_slab, int *nonfinite_flag, void *stream, void *done_event);
+/* Stream host_slab to HBM chunk by chunk (H2D copy engine) and dequantize into kv.
+ * done_event fires (on `stream`) when kv is complete. */
+int alise_kv_upload(alise_swapper *sw, const alise_kv_desc *d, const void *host_slab,
+                    uint16_t *kv, void *stream, void *done_event);
+
+/* Order every later transfer of this swapper after `event` (cudaEvent_t), e.g. an
+ * upload that reads a host slab an earlier offload wrote. */
+int alise_swapper_depend(alise_swapper *sw, void *event);
+
+/* Bench instrumentation: record CUDA events around every quantize / dequantize chunk
+ * on the compute stream; kernel_stats sums their durations (and synchronises). */
+int alise_swapper_timing(alise_swapper *sw, int enable);
+int alise_swapper_kernel_stats(alise_swapper *sw, double *quant_ms, int64_t *n_quant,
+                               double *deq_ms, int64_t *n_deq);
+
+/* Pinned host memory and events (thin wrappers so non-torch hosts can drive the ABI). */
+int alise_host_alloc(int64_t bytes, void **out);
+int alise_host_free(void *p);
+int alise_event_create(void **ev);
+int alise_event_destroy(void *ev);
+int alise_event_record(void *ev, void *stream);
+int alise_event_query(void *ev, int *done);
+int alise_event_sync(void *ev);
+int alise_stream_wait(void *stream, void *ev);
+int alise_event_elapsed_ms(void *start, void *stop, float *ms);
+
+/* ---------------------------------------------------------------- predictor ---- */
+typedef struct alise_db alise_db;
+/* FIFO ring of `capacity` fp32 vectors of `dim` (plus an fp16 copy for the coarse
+ * tensor-core scan), observed lengths (int32) and insert sequence numbers (int64).
+ * Mirrors VectorStore (predictor.py:120-152): slot = seq % capacity. */
+int alise_db_create(int device, int64_t capacity, int64_t dim, alise_db **out);
+int alise_db_destroy(alise_db *db);
+/* Append n rows (device pointers): vecs fp32 [n][dim], lens int32 [n], seqs int64 [n]
+ * (seqs must be consecutive from the db's next sequence number). */
+int alise_db_append(alise_db *db, const float *vecs, const int32_t *lens, const int64_t *seqs,
+                    int64_t n, void *stream);
+int alise_db_size(alise_db *db, int64_t *size, int64_t *next_seq);
+/* Exact top-k of B queries (fp32 [B][dim], device) against the db: sims are the
+ * correctly rounded float64 dot products, ordered by (-sim, seq) (ties -> older
+ * first).  Outputs [B][k]; count[b] = min(k, size). */
+int alise_db_topk(alise_db *db, const float *queries, int64_t B, int k, double *out_sim,
+                  int64_t *out_seq, int32_t *out_len, int32_t *out_count, void *stream);
+/* Merge G per-shard top-k lists ([G][B][k] each) into a global top-k by (-sim, seq). */
+int alise_topk_merge(int G, int64_t B, int k, const double *sims, const int64_t *seqs,
+                     const int32_t *lens, const int32_t *counts, double *out_sim,
+                     int64_t *out_seq, int32_t *out_len, int32_t *out_count, void *stream);
+/* Aggregate + all-MLP fallback (predictor.py:311-325, 209-219): per query, if any of
+ * its count neighbours has sim >= s0, the similarity-weighted mean length (numpy
+ * summation order), else the float64 MLP tanh(x.W1+b1).w2+b2 -> exp -> round.
+ * W1 [dim][hidden] f64, b1 [hidden], w2 [hidden], b2 scalar; queries fp32 [B][dim].
+ * out_len int32 [B]; out_retrieved uint8 [B] (1 = "retrieved", 0 = "fallback"). */
+int alise_predict_finish(int64_t B, int k, const double *sims, const int32_t *lens,
+                         const int32_t *counts, double s0, const float *queries, int64_t dim,
+                         const double *W1, const double *b1, const double *w2, double b2,
+                         int64_t hidden, int64_t max_len, double log_cap, int32_t *out_len,
+                         uint8_t *out_retrieved, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ALISE_B200_H */

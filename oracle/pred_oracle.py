@@ -1,0 +1,111 @@
+"""Restated CPU oracle for the retrieval length predictor — TEST INFRASTRUCTURE ONLY.
+
+Reference: /root/reference/pkg/src/servesim/predictor.py
+  * VectorStore.search        :154-163  (sims = vecs @ q, argpartition, lexsort)
+  * LengthPredictor.predict_vector :311-325 (threshold, clip, weighted mean, round, clamp)
+  * FallbackRegressor._forward / predict_len :209-219
+
+Why restated rather than called: the reference's arithmetic lives in numpy /
+OpenBLAS (absent from /root/reference; numpy 2.3.5 + scipy-openblas 0.3.30 here),
+whose dot-product summation order is unspecified, and ``argpartition`` picks an
+arbitrary subset of rows tied at the k-boundary.  The restatement
+pins what the north star asks for:
+  * sims = the correctly rounded float64 value of the exact dot product
+    (fp32 x fp32 products are exact in float64; summed with math.fsum);
+  * order = full (-sim, seq) sort, so ties are broken by insert order everywhere;
+  * aggregate = numpy's own ops on the same arrays (summation order: sequential for
+    n < 8, 8-accumulator tree for n >= 8 — see tests/test_oracle_pred.py);
+  * MLP = float64, separate multiply/add, hidden pre-activations summed over the
+    input dimension in index order, output summed over hidden units in index order.
+It agrees with the raw reference wherever the reference is well defined
+(untied top-k, lengths) — checked against tests/golden/pred_golden.npz.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def exact_dot(a32, b32) -> float:
+    """Correctly rounded float64 dot product of two fp32 vectors."""
+    a = np.asarray(a32, dtype=np.float32).astype(np.float64)
+    b = np.asarray(b32, dtype=np.float32).astype(np.float64)
+    return math.fsum((a * b).tolist())
+
+
+def search_exact(db32, lens, seqs, q32, k: int):
+    """Exact top-k by (-sim, seq) over fp32 rows. Returns (sims f64, lens, seqs)."""
+    db32 = np.asarray(db32, dtype=np.float32)
+    n = db32.shape[0]
+    if n == 0:
+        return np.array([]), np.array([], dtype=np.int64), np.array([], dtype=np.int64)
+    k = min(k, n)
+    q = np.asarray(q32, dtype=np.float32).astype(np.float64)
+    coarse = db32.astype(np.float64) @ q           # |error| <= ~dim * 2^-53 * |q| * max|v|
+    margin = 1e-9 * max(1.0, float(np.abs(q).sum())) * max(1.0, float(np.abs(db32).max()))
+    kth = np.partition(coarse, n - k)[n - k]
+    cand = np.flatnonzero(coarse >= kth - 2 * margin)
+    exact = np.array([exact_dot(db32[r], q32) for r in cand])
+    order = np.lexsort((np.asarray(seqs)[cand], -exact))[:k]
+    pick = cand[order]
+    return exact[order], np.asarray(lens)[pick].astype(np.int64), np.asarray(seqs)[pick].astype(np.int64)
+
+
+def aggregate(sims, lens, s0: float, max_len: int):
+    """predict_vector's retrieval branch (predictor.py:314-324).
+
+    Returns the length, or None when no neighbour qualifies (-> fallback MLP).
+    """
+    sims = np.asarray(sims, dtype=np.float64)
+    if sims.size == 0:
+        return None
+    qualify = sims >= s0
+    if not qualify.any():
+        return None
+    w = np.clip(sims[qualify], 0.0, None)
+    vals = np.asarray(lens)[qualify].astype(np.float64)
+    if w.sum() > 0.0:
+        pred = float((w * vals).sum() / w.sum())
+    else:
+        pred = float(vals.mean())
+    return int(min(max(round(pred), 1), max_len))
+
+
+def mlp_forward(X, W1, b1, w2, b2):
+    """Batched float64 MLP in the canonical order the CUDA kernel uses."""
+    X = np.asarray(X, dtype=np.float64)
+    W1 = np.asarray(W1, dtype=np.float64)
+    acc = np.zeros((X.shape[0], W1.shape[1]))
+    for d in range(X.shape[1]):
+        acc = acc + X[:, d:d + 1] * W1[d]
+    h = np.tanh(acc + np.asarray(b1, dtype=np.float64))
+    out = np.zeros(X.shape[0])
+    for j in range(h.shape[1]):
+        out = out + h[:, j] * float(w2[j])
+    return out + float(b2)
+
+
+def mlp_predict_len(X, W1, b1, w2, b2, max_len: int):
+    """FallbackRegressor.predict_len (predictor.py:217-219) for a batch."""
+    out = mlp_forward(X, W1, b1, w2, b2)
+    cap = math.log(max_len) + 1.0
+    raw = np.exp(np.minimum(out, cap))
+    return np.clip(np.rint(raw), 1, max_len).astype(np.int64)
+
+
+def predict_batch(db32, lens, seqs, Q32, W1, b1, w2, b2, k=8, s0=0.80, max_len=2048):
+    """Full predict_vector for a batch (search + aggregate, else MLP)."""
+    fallback = mlp_predict_len(np.asarray(Q32, dtype=np.float32).astype(np.float64), W1, b1, w2, b2,
+                               max_len)
+    out_len = np.empty(len(Q32), dtype=np.int64)
+    retrieved = np.zeros(len(Q32), dtype=bool)
+    for i, q in enumerate(Q32):
+        s, ln, _ = search_exact(db32, lens, seqs, q, k)
+        a = aggregate(s, ln, s0, max_len)
+        if a is None:
+            out_len[i] = fallback[i]
+        else:
+            out_len[i] = a
+            retrieved[i] = True
+    return out_len, retrieved

@@ -1,0 +1,652 @@
+// C ABI for the KV data plane: drop-in quantize/dequantize, whole-job KV
+// quantize/dequantize, and the swapper that fuses them with host-link transfers.
+// Declarations and reference citations: include/alise_b200.h.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/alise_b200.h"
+#include "kv_quant.cuh"
+
+namespace alise {
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+}  // namespace alise
+
+using namespace alise;
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) return fail(ALISE_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+#define CKL()                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess) return fail(ALISE_ECUDA, "launch: %s", cudaGetErrorString(e_)); \
+  } while (0)
+
+static inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static int g_sm_count = 0;
+static int sm_count() {
+  if (!g_sm_count) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sm_count <= 0) g_sm_count = 148;
+  }
+  return g_sm_count;
+}
+static inline int grid_for(int64_t work, int block, int waves = 8) {
+  int64_t g = (work + block - 1) / block;
+  int64_t cap = (int64_t)sm_count() * waves;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+extern "C" const char* alise_last_error(void) { return g_last_error.c_str(); }
+extern "C" int alise_version(void) { return 1; }
+extern "C" int alise_sm_count(int device, int* out) {
+  CK(cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, device));
+  return ALISE_OK;
+}
+
+// ------------------------------------------------------------------ fast tile launch
+template <int BITS, bool PACK, bool ZF32>
+static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
+                            double* scale, void* zero, int* flag, cudaStream_t st) {
+  const int lpr_needed = (row_len + 7) / 8;
+  const int64_t tiles_rows = (lpr_needed >= 32) ? 16 : 32;
+  const int64_t warps = (rows + tiles_rows - 1) / tiles_rows;
+  const int block = 256;
+  const int grid = grid_for(warps * 32, block, 16);
+#define TILE_CASE(L)                                                                    \
+  if (lpr_needed <= L) {                                                                \
+    k_quant_tile<BITS, PACK, L, ZF32><<<grid, block, 0, st>>>(x, rows, row_len, codes,  \
+                                                              scale, zero, flag);       \
+    CKL();                                                                              \
+    return ALISE_OK;                                                                    \
+  }
+  TILE_CASE(1) TILE_CASE(2) TILE_CASE(4) TILE_CASE(8) TILE_CASE(16) TILE_CASE(32)
+#undef TILE_CASE
+  return fail(ALISE_EINVAL, "row_len %d too long for the tile kernel", row_len);
+}
+
+static int launch_tile(int bits, bool pack, bool zf32, const uint16_t* x, int64_t rows,
+                       int row_len, uint8_t* codes, double* scale, void* zero, int* flag,
+                       cudaStream_t st) {
+  if (bits == 8) {
+    return zf32 ? launch_tile_bits<8, false, true>(x, rows, row_len, codes, scale, zero, flag, st)
+                : launch_tile_bits<8, false, false>(x, rows, row_len, codes, scale, zero, flag, st);
+  }
+  if (pack)
+    return zf32 ? launch_tile_bits<4, true, true>(x, rows, row_len, codes, scale, zero, flag, st)
+                : launch_tile_bits<4, true, false>(x, rows, row_len, codes, scale, zero, flag, st);
+  return zf32 ? launch_tile_bits<4, false, true>(x, rows, row_len, codes, scale, zero, flag, st)
+              : launch_tile_bits<4, false, false>(x, rows, row_len, codes, scale, zero, flag, st);
+}
+
+static bool tile_ok(int dtype, int64_t row_len, int64_t row_stride, const void* src,
+                    const void* codes, bool pack) {
+  if (dtype != ALISE_DT_F16 || row_len % 8 || row_len > 256 || row_stride != row_len) return false;
+  if (((uintptr_t)src & 15) || ((uintptr_t)codes & (pack ? 3 : 7))) return false;
+  return true;
+}
+
+// ------------------------------------------------------------------ generic rows path
+static int64_t rows_chunk(int64_t row_len) { return row_len <= 16384 ? row_len : 16384; }
+
+extern "C" int alise_quantize_rows_workspace(int64_t rows, int64_t row_len, int src_dtype,
+                                             int64_t* bytes) {
+  if (rows <= 0 || row_len <= 0) return fail(ALISE_EINVAL, "expected a non-empty channel-major 2D tensor");
+  const int64_t ch = rows_chunk(row_len);
+  const int64_t nch = (row_len + ch - 1) / ch;
+  *bytes = align256(rows * nch * 8) * 2 + align256(rows * 16);
+  (void)src_dtype;
+  return ALISE_OK;
+}
+
+template <typename T>
+static int rows_generic(const T* x, int64_t rows, int64_t row_len, int64_t row_stride, int bits,
+                        bool pack, uint8_t* codes, double* scale, void* zero, bool zf32,
+                        int* flag, void* ws, cudaStream_t st) {
+  const int64_t ch = rows_chunk(row_len);
+  const int nch = (int)((row_len + ch - 1) / ch);
+  char* w = reinterpret_cast<char*>(ws);
+  double* pmn = reinterpret_cast<double*>(w);
+  double* pmx = reinterpret_cast<double*>(w + align256(rows * nch * 8));
+  float4* fastp = reinterpret_cast<float4*>(w + 2 * align256(rows * nch * 8));
+  const int64_t blocks = rows * nch;
+  if (blocks > 0x7fffffff) return fail(ALISE_EINVAL, "too many rows");
+  const int bt = row_len >= 4096 ? 256 : (row_len >= 1024 ? 128 : 32);
+  k_minmax_rows<T><<<(unsigned)blocks, bt, 0, st>>>(x, rows, row_len, row_stride, ch, nch, pmn, pmx, flag);
+  CKL();
+  k_params<false><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
+      KIND_ROWS, rows, nch, pmn, pmx, nullptr, nullptr, 0, 1, bits, InTraits<T>::wide, scale,
+      zero, fastp);
+  CKL();
+  (void)zf32;
+  const int64_t n = rows * row_len;
+  const int grid = grid_for(pack ? (n + 1) / 2 : n, 256, 16);
+  if (bits == 8)
+    k_codes_rows<T, 8, false><<<grid, 256, 0, st>>>(x, rows, row_len, row_stride, fastp, scale, zero, false, codes);
+  else if (pack)
+    k_codes_rows<T, 4, true><<<grid, 256, 0, st>>>(x, rows, row_len, row_stride, fastp, scale, zero, false, codes);
+  else
+    k_codes_rows<T, 4, false><<<grid, 256, 0, st>>>(x, rows, row_len, row_stride, fastp, scale, zero, false, codes);
+  CKL();
+  return ALISE_OK;
+}
+
+extern "C" int alise_quantize_rows(const void* src, int src_dtype, int64_t rows, int64_t row_len,
+                                   int64_t row_stride, int bits, uint8_t* codes, double* scale,
+                                   double* zero, int* flag, void* workspace, void* stream) {
+  if (bits != 4 && bits != 8) return fail(ALISE_EINVAL, "bits must be 4 or 8");
+  if (rows <= 0 || row_len <= 0) return fail(ALISE_EINVAL, "expected a non-empty channel-major 2D tensor");
+  if (row_stride < row_len) return fail(ALISE_EINVAL, "row_stride < row_len");
+  cudaStream_t st = S(stream);
+  if (tile_ok(src_dtype, row_len, row_stride, src, codes, false))
+    return launch_tile(bits, false, false, reinterpret_cast<const uint16_t*>(src), rows,
+                       (int)row_len, codes, scale, zero, flag, st);
+  if (!workspace) return fail(ALISE_EINVAL, "workspace required for this shape");
+  switch (src_dtype) {
+    case ALISE_DT_F16:
+      return rows_generic(reinterpret_cast<const uint16_t*>(src), rows, row_len, row_stride, bits,
+                          false, codes, scale, zero, false, flag, workspace, st);
+    case ALISE_DT_F32:
+      return rows_generic(reinterpret_cast<const float*>(src), rows, row_len, row_stride, bits,
+                          false, codes, scale, zero, false, flag, workspace, st);
+    case ALISE_DT_F64:
+      return rows_generic(reinterpret_cast<const double*>(src), rows, row_len, row_stride, bits,
+                          false, codes, scale, zero, false, flag, workspace, st);
+  }
+  return fail(ALISE_EINVAL, "unknown dtype %d", src_dtype);
+}
+
+template <typename OUT>
+static int dequant_launch(int kind, const uint8_t* codes, const double* scale, const void* zero,
+                          bool zf32, int64_t n, int64_t row_len, int64_t T, int64_t Hd, int64_t D,
+                          int bits, bool pack, OUT* out, cudaStream_t st) {
+  const int64_t nv = n / 8;
+  if (nv > 0) {
+    const int grid = grid_for(nv, 256, 16);
+#define DQ(B, P) k_dequant<OUT, B, P><<<grid, 256, 0, st>>>(kind, codes, scale, zero, zf32, nv * 8, row_len, T, Hd, D, out)
+    if (bits == 8) DQ(8, false);
+    else if (pack) DQ(4, true);
+    else DQ(4, false);
+#undef DQ
+    CKL();
+  }
+  if (n % 8) {
+    if (kind != KIND_ROWS) return fail(ALISE_EINVAL, "element count must be a multiple of 8");
+    const int64_t e0 = nv * 8;
+    if (bits == 8) k_dequant_tail<OUT, 8, false><<<1, 8, 0, st>>>(codes, scale, zero, zf32, e0, n, row_len, out);
+    else if (pack) k_dequant_tail<OUT, 4, true><<<1, 8, 0, st>>>(codes, scale, zero, zf32, e0, n, row_len, out);
+    else k_dequant_tail<OUT, 4, false><<<1, 8, 0, st>>>(codes, scale, zero, zf32, e0, n, row_len, out);
+    CKL();
+  }
+  return ALISE_OK;
+}
+
+extern "C" int alise_dequantize_rows(const uint8_t* codes, const double* scale, const double* zero,
+                                     int64_t rows, int64_t row_len, int out_dtype, void* out,
+                                     void* stream) {
+  if (rows <= 0 || row_len <= 0) return fail(ALISE_EINVAL, "empty tensor");
+  // the vector kernel reads codes 8 at a time; unaligned tails go through the scalar kernel
+  const int64_t n = rows * row_len;
+  if ((uintptr_t)codes & 7) return fail(ALISE_EINVAL, "codes must be 8-byte aligned");
+  if (out_dtype == ALISE_DT_F64)
+    return dequant_launch<double>(KIND_ROWS, codes, scale, zero, false, n, row_len, 0, 1, 1, 8,
+                                  false, reinterpret_cast<double*>(out), S(stream));
+  if (out_dtype == ALISE_DT_F16)
+    return dequant_launch<uint16_t>(KIND_ROWS, codes, scale, zero, false, n, row_len, 0, 1, 1, 8,
+                                    false, reinterpret_cast<uint16_t*>(out), S(stream));
+  return fail(ALISE_EINVAL, "out dtype must be f16 or f64");
+}
+// note: bits only matters for packed codes; the drop-in API never packs.
+
+// ------------------------------------------------------------------ KV job layout
+struct KvGeom {
+  int64_t planes, plane_elems, rows_pp, code_bytes_pp, ppc, n_chunks, rec_bytes, slab_bytes;
+  int64_t codes_sec(int64_t np) const { return align256(np * code_bytes_pp); }
+  int64_t scale_sec(int64_t np) const { return align256(np * rows_pp * 8); }
+  int64_t zero_sec(int64_t np) const { return align256(np * rows_pp * 4); }
+  int64_t rec(int64_t np) const { return codes_sec(np) + scale_sec(np) + zero_sec(np); }
+  int64_t np_of(int64_t c) const { return std::min(ppc, planes - c * ppc); }
+};
+
+static int geom(const alise_kv_desc* d, KvGeom* g) {
+  if (!d || d->layers <= 0 || d->tokens <= 0 || d->hidden <= 0)
+    return fail(ALISE_EINVAL, "kv desc: layers/tokens/hidden must be positive");
+  if (d->bits != 4 && d->bits != 8) return fail(ALISE_EINVAL, "bits must be 4 or 8");
+  if (d->packed && d->bits != 4) return fail(ALISE_EINVAL, "packing is INT4 only");
+  if (d->hidden % 8) return fail(ALISE_EINVAL, "hidden must be a multiple of 8");
+  g->planes = d->layers * 2;
+  g->plane_elems = d->tokens * d->hidden;
+  switch (d->kind) {
+    case ALISE_KIND_ROWS:
+      if (d->group <= 0 || d->group % 8 || d->hidden % d->group || d->group > 256)
+        return fail(ALISE_EINVAL, "group must be a multiple of 8, <= 256, dividing hidden");
+      g->rows_pp = d->tokens * (d->hidden / d->group);
+      break;
+    case ALISE_KIND_CHANNEL:
+      g->rows_pp = d->hidden;
+      break;
+    case ALISE_KIND_HEAD:
+      if (d->head_dim <= 0 || d->hidden % d->head_dim || d->head_dim % 8)
+        return fail(ALISE_EINVAL, "head_dim must be a multiple of 8 dividing hidden");
+      g->rows_pp = d->hidden / d->head_dim;
+      break;
+    default:
+      return fail(ALISE_EINVAL, "unknown group kind %d", d->kind);
+  }
+  g->code_bytes_pp = d->packed ? g->plane_elems / 2 : g->plane_elems;
+  int64_t ppc = d->planes_per_chunk;
+  if (ppc <= 0) ppc = std::max<int64_t>(1, (int64_t(16) << 20) / g->code_bytes_pp);
+  g->ppc = std::min(ppc, g->planes);
+  g->n_chunks = (g->planes + g->ppc - 1) / g->ppc;
+  g->rec_bytes = g->rec(g->ppc);
+  g->slab_bytes = (g->n_chunks - 1) * g->rec_bytes + g->rec(g->np_of(g->n_chunks - 1));
+  return ALISE_OK;
+}
+
+extern "C" int alise_kv_layout(const alise_kv_desc* d, int64_t* slab_bytes, int64_t* rows,
+                               int64_t* chunk_bytes, int64_t* n_chunks) {
+  KvGeom g;
+  int st = geom(d, &g);
+  if (st) return st;
+  if (slab_bytes) *slab_bytes = g.slab_bytes;
+  if (rows) *rows = g.rows_pp * g.planes;
+  if (chunk_bytes) *chunk_bytes = g.rec_bytes;
+  if (n_chunks) *n_chunks = g.n_chunks;
+  return ALISE_OK;
+}
+
+static int64_t cols_workspace(const alise_kv_desc* d, const KvGeom& g, int* nch_out, int64_t* tchunk_out) {
+  if (d->kind == ALISE_KIND_ROWS) return 0;
+  // enough (plane, token-chunk, column-block) blocks for ~4 waves
+  const int64_t colblocks = (d->hidden / 8 + 127) / 128;
+  int64_t nch = std::max<int64_t>(1, (4 * sm_count() + colblocks * g.ppc - 1) / (colblocks * g.ppc));
+  nch = std::min<int64_t>(nch, d->tokens);
+  const int64_t tchunk = (d->tokens + nch - 1) / nch;
+  nch = (d->tokens + tchunk - 1) / tchunk;
+  *nch_out = (int)nch;
+  *tchunk_out = tchunk;
+  return 2 * align256(g.ppc * nch * d->hidden * 4) + align256(g.ppc * g.rows_pp * 16);
+}
+
+// Quantize np planes starting at kv into one chunk record at rec.
+static int quant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, const uint16_t* kv,
+                       uint8_t* rec, int* flag, void* ws, cudaStream_t st) {
+  uint8_t* codes = rec;
+  double* scale = reinterpret_cast<double*>(rec + g.codes_sec(np));
+  float* zero = reinterpret_cast<float*>(rec + g.codes_sec(np) + g.scale_sec(np));
+  const int64_t rows = np * g.rows_pp;
+  if (d->kind == ALISE_KIND_ROWS)
+    return launch_tile(d->bits, d->packed != 0, true, kv, rows, d->group, codes, scale, zero, flag, st);
+  int nch;
+  int64_t tchunk;
+  cols_workspace(d, g, &nch, &tchunk);
+  char* w = reinterpret_cast<char*>(ws);
+  float* pmn = reinterpret_cast<float*>(w);
+  float* pmx = reinterpret_cast<float*>(w + align256(g.ppc * nch * d->hidden * 4));
+  float4* fastp = reinterpret_cast<float4*>(w + 2 * align256(g.ppc * nch * d->hidden * 4));
+  dim3 grid((unsigned)((d->hidden / 8 + 127) / 128), (unsigned)nch, (unsigned)np);
+  k_minmax_cols<<<grid, 128, 0, st>>>(kv, d->tokens, d->hidden, tchunk, pmn, pmx, flag);
+  CKL();
+  k_params<true><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
+      d->kind, rows, nch, nullptr, nullptr, pmn, pmx, d->hidden, d->head_dim > 0 ? d->head_dim : 1,
+      d->bits, false, scale, zero, fastp);
+  CKL();
+  const int64_t nvec = np * g.plane_elems / 8;
+  const int gr = grid_for(nvec, 256, 16);
+  const int64_t D = d->head_dim > 0 ? d->head_dim : 1;
+  if (d->bits == 8)
+    k_codes_cols<8, false><<<gr, 256, 0, st>>>(kv, d->kind, np, d->tokens, d->hidden, D, fastp, scale, zero, true, codes);
+  else if (d->packed)
+    k_codes_cols<4, true><<<gr, 256, 0, st>>>(kv, d->kind, np, d->tokens, d->hidden, D, fastp, scale, zero, true, codes);
+  else
+    k_codes_cols<4, false><<<gr, 256, 0, st>>>(kv, d->kind, np, d->tokens, d->hidden, D, fastp, scale, zero, true, codes);
+  CKL();
+  return ALISE_OK;
+}
+
+static int dequant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, const uint8_t* rec,
+                         uint16_t* kv, cudaStream_t st) {
+  const uint8_t* codes = rec;
+  const double* scale = reinterpret_cast<const double*>(rec + g.codes_sec(np));
+  const float* zero = reinterpret_cast<const float*>(rec + g.codes_sec(np) + g.scale_sec(np));
+  const int64_t D = d->head_dim > 0 ? d->head_dim : 1;
+  return dequant_launch<uint16_t>(d->kind, codes, scale, zero, true, np * g.plane_elems,
+                                  d->kind == ALISE_KIND_ROWS ? d->group : 1, d->tokens, d->hidden,
+                                  D, d->bits, d->packed != 0, kv, st);
+}
+
+extern "C" int alise_kv_quantize(const alise_kv_desc* d, const uint16_t* kv, uint8_t* slab,
+                                 int* flag, void* stream) {
+  KvGeom g;
+  int s = geom(d, &g);
+  if (s) return s;
+  cudaStream_t st = S(stream);
+  int nch;
+  int64_t tchunk;
+  const int64_t wsb = cols_workspace(d, g, &nch, &tchunk);
+  void* ws = nullptr;
+  if (wsb) CK(cudaMallocAsync(&ws, wsb, st));
+  for (int64_t c = 0; c < g.n_chunks; ++c) {
+    s = quant_chunk(d, g, g.np_of(c), kv + c * g.ppc * g.plane_elems, slab + c * g.rec_bytes, flag, ws, st);
+    if (s) break;
+  }
+  if (ws) CK(cudaFreeAsync(ws, st));
+  return s;
+}
+
+extern "C" int alise_kv_dequantize(const alise_kv_desc* d, const uint8_t* slab, uint16_t* kv,
+                                   void* stream) {
+  KvGeom g;
+  int s = geom(d, &g);
+  if (s) return s;
+  for (int64_t c = 0; c < g.n_chunks; ++c) {
+    s = dequant_chunk(d, g, g.np_of(c), slab + c * g.rec_bytes, kv + c * g.ppc * g.plane_elems, S(stream));
+    if (s) return s;
+  }
+  return ALISE_OK;
+}
+
+// ------------------------------------------------------------------ swapper
+static constexpr int kSlots = 3;
+struct alise_swapper {
+  int device = 0;
+  int mode = ALISE_SWAP_STAGED;
+  cudaStream_t s_out = nullptr, s_in = nullptr;
+  int64_t slot_bytes = 0;
+  uint8_t* ring_out[kSlots] = {};
+  uint8_t* ring_in[kSlots] = {};
+  cudaEvent_t out_ready[kSlots] = {}, out_free[kSlots] = {}, in_ready[kSlots] = {}, in_free[kSlots] = {};
+  int next_out = 0, next_in = 0;
+  void* ws = nullptr;
+  int64_t ws_bytes = 0;
+  // optional per-chunk kernel timing (bench roofline): event pairs around each
+  // quantize / dequantize chunk on the compute stream
+  bool timing = false;
+  std::vector<cudaEvent_t> t_q, t_d, pool;
+  cudaEvent_t take() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+};
+
+static int sw_release_rings(alise_swapper* sw) {
+  for (int i = 0; i < kSlots; ++i) {
+    if (sw->ring_out[i]) CK(cudaFree(sw->ring_out[i]));
+    if (sw->ring_in[i]) CK(cudaFree(sw->ring_in[i]));
+    sw->ring_out[i] = sw->ring_in[i] = nullptr;
+  }
+  sw->slot_bytes = 0;
+  return ALISE_OK;
+}
+
+static int sw_ensure(alise_swapper* sw, int64_t slot_bytes, int64_t ws_bytes) {
+  if (sw->mode == ALISE_SWAP_STAGED && slot_bytes > sw->slot_bytes) {
+    CK(cudaStreamSynchronize(sw->s_out));
+    CK(cudaStreamSynchronize(sw->s_in));
+    CK(cudaDeviceSynchronize());
+    int s = sw_release_rings(sw);
+    if (s) return s;
+    for (int i = 0; i < kSlots; ++i) {
+      CK(cudaMalloc(&sw->ring_out[i], slot_bytes));
+      CK(cudaMalloc(&sw->ring_in[i], slot_bytes));
+    }
+    sw->slot_bytes = slot_bytes;
+  }
+  if (ws_bytes > sw->ws_bytes) {
+    CK(cudaDeviceSynchronize());
+    if (sw->ws) CK(cudaFree(sw->ws));
+    CK(cudaMalloc(&sw->ws, ws_bytes));
+    sw->ws_bytes = ws_bytes;
+  }
+  return ALISE_OK;
+}
+
+extern "C" int alise_swapper_create(int device, int mode, int64_t ring_bytes, alise_swapper** out) {
+  if (mode != ALISE_SWAP_STAGED && mode != ALISE_SWAP_ZEROCOPY) return fail(ALISE_EINVAL, "bad swap mode");
+  CK(cudaSetDevice(device));
+  alise_swapper* sw = new alise_swapper();
+  sw->device = device;
+  sw->mode = mode;
+  CK(cudaStreamCreateWithFlags(&sw->s_out, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&sw->s_in, cudaStreamNonBlocking));
+  for (int i = 0; i < kSlots; ++i) {
+    CK(cudaEventCreateWithFlags(&sw->out_ready[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sw->out_free[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sw->in_ready[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sw->in_free[i], cudaEventDisableTiming));
+  }
+  if (ring_bytes > 0) {
+    int s = sw_ensure(sw, ring_bytes / kSlots, 0);
+    if (s) return s;
+  }
+  *out = sw;
+  return ALISE_OK;
+}
+
+extern "C" int alise_swapper_destroy(alise_swapper* sw) {
+  if (!sw) return ALISE_OK;
+  CK(cudaDeviceSynchronize());
+  sw_release_rings(sw);
+  if (sw->ws) cudaFree(sw->ws);
+  for (int i = 0; i < kSlots; ++i) {
+    cudaEventDestroy(sw->out_ready[i]);
+    cudaEventDestroy(sw->out_free[i]);
+    cudaEventDestroy(sw->in_ready[i]);
+    cudaEventDestroy(sw->in_free[i]);
+  }
+  cudaStreamDestroy(sw->s_out);
+  cudaStreamDestroy(sw->s_in);
+  delete sw;
+  return ALISE_OK;
+}
+
+#define TSTART(v)                                   \
+  if (sw->timing) {                                 \
+    cudaEvent_t ev_ = sw->take();                   \
+    CK(cudaEventRecord(ev_, st));                   \
+    sw->v.push_back(ev_);                           \
+  }
+#define TSTOP(v) TSTART(v)
+
+// Make both side (copy) streams wait for `event` before any later transfer, e.g. an
+// upload that reads a host slab written by an earlier offload.
+extern "C" int alise_swapper_depend(alise_swapper* sw, void* event) {
+  CK(cudaStreamWaitEvent(sw->s_out, reinterpret_cast<cudaEvent_t>(event), 0));
+  CK(cudaStreamWaitEvent(sw->s_in, reinterpret_cast<cudaEvent_t>(event), 0));
+  return ALISE_OK;
+}
+
+extern "C" int alise_swapper_timing(alise_swapper* sw, int enable) {
+  sw->timing = enable != 0;
+  return ALISE_OK;
+}
+
+// Sums kernel time of the instrumented chunks since the last call (synchronises).
+extern "C" int alise_swapper_kernel_stats(alise_swapper* sw, double* quant_ms, int64_t* n_quant,
+                                          double* deq_ms, int64_t* n_deq) {
+  CK(cudaDeviceSynchronize());
+  std::vector<cudaEvent_t>* lists[2] = {&sw->t_q, &sw->t_d};
+  double* outs[2] = {quant_ms, deq_ms};
+  int64_t* cnts[2] = {n_quant, n_deq};
+  for (int k = 0; k < 2; ++k) {
+    double tot = 0;
+    auto& v = *lists[k];
+    for (size_t i = 0; i + 1 < v.size(); i += 2) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, v[i], v[i + 1]));
+      tot += ms;
+    }
+    *outs[k] = tot;
+    *cnts[k] = (int64_t)(v.size() / 2);
+    for (auto e : v) sw->pool.push_back(e);
+    v.clear();
+  }
+  return ALISE_OK;
+}
+
+static int host_dev_ptr(const void* host, void** dev) {
+  cudaError_t e = cudaHostGetDevicePointer(dev, const_cast<void*>(host), 0);
+  if (e != cudaSuccess) return fail(ALISE_EINVAL, "host slab is not pinned/mapped: %s", cudaGetErrorString(e));
+  return ALISE_OK;
+}
+
+extern "C" int alise_kv_offload(alise_swapper* sw, const alise_kv_desc* d, const uint16_t* kv,
+                                void* host_slab, int* flag, void* stream, void* done_event) {
+  if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
+  KvGeom g;
+  int s = geom(d, &g);
+  if (s) return s;
+  int nch;
+  int64_t tchunk;
+  const int64_t wsb = cols_workspace(d, g, &nch, &tchunk);
+  s = sw_ensure(sw, g.rec_bytes, wsb);
+  if (s) return s;
+  cudaStream_t st = S(stream);
+  uint8_t* host = reinterpret_cast<uint8_t*>(host_slab);
+  if (sw->mode == ALISE_SWAP_ZEROCOPY) {
+    void* dptr;
+    s = host_dev_ptr(host_slab, &dptr);
+    if (s) return s;
+    for (int64_t c = 0; c < g.n_chunks; ++c) {
+      TSTART(t_q);
+      s = quant_chunk(d, g, g.np_of(c), kv + c * g.ppc * g.plane_elems,
+                      reinterpret_cast<uint8_t*>(dptr) + c * g.rec_bytes, flag, sw->ws, st);
+      TSTOP(t_q);
+      if (s) return s;
+    }
+    if (done_event) CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(done_event), st));
+    return ALISE_OK;
+  }
+  for (int64_t c = 0; c < g.n_chunks; ++c) {
+    const int slot = sw->next_out;
+    sw->next_out = (slot + 1) % kSlots;
+    const int64_t np = g.np_of(c);
+    CK(cudaStreamWaitEvent(st, sw->out_free[slot], 0));
+    TSTART(t_q);
+    s = quant_chunk(d, g, np, kv + c * g.ppc * g.plane_elems, sw->ring_out[slot], flag, sw->ws, st);
+    TSTOP(t_q);
+    if (s) return s;
+    CK(cudaEventRecord(sw->out_ready[slot], st));
+    CK(cudaStreamWaitEvent(sw->s_out, sw->out_ready[slot], 0));
+    CK(cudaMemcpyAsync(host + c * g.rec_bytes, sw->ring_out[slot], g.rec(np),
+                       cudaMemcpyDeviceToHost, sw->s_out));
+    CK(cudaEventRecord(sw->out_free[slot], sw->s_out));
+  }
+  if (done_event) CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(done_event), sw->s_out));
+  return ALISE_OK;
+}
+
+extern "C" int alise_kv_upload(alise_swapper* sw, const alise_kv_desc* d, const void* host_slab,
+                               uint16_t* kv, void* stream, void* done_event) {
+  if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
+  KvGeom g;
+  int s = geom(d, &g);
+  if (s) return s;
+  s = sw_ensure(sw, g.rec_bytes, 0);
+  if (s) return s;
+  cudaStream_t st = S(stream);
+  const uint8_t* host = reinterpret_cast<const uint8_t*>(host_slab);
+  if (sw->mode == ALISE_SWAP_ZEROCOPY) {
+    void* dptr;
+    s = host_dev_ptr(host_slab, &dptr);
+    if (s) return s;
+    for (int64_t c = 0; c < g.n_chunks; ++c) {
+      TSTART(t_d);
+      s = dequant_chunk(d, g, g.np_of(c), reinterpret_cast<const uint8_t*>(dptr) + c * g.rec_bytes,
+                        kv + c * g.ppc * g.plane_elems, st);
+      TSTOP(t_d);
+      if (s) return s;
+    }
+    if (done_event) CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(done_event), st));
+    return ALISE_OK;
+  }
+  for (int64_t c = 0; c < g.n_chunks; ++c) {
+    const int slot = sw->next_in;
+    sw->next_in = (slot + 1) % kSlots;
+    const int64_t np = g.np_of(c);
+    CK(cudaStreamWaitEvent(sw->s_in, sw->in_free[slot], 0));
+    CK(cudaMemcpyAsync(sw->ring_in[slot], host + c * g.rec_bytes, g.rec(np),
+                       cudaMemcpyHostToDevice, sw->s_in));
+    CK(cudaEventRecord(sw->in_ready[slot], sw->s_in));
+    CK(cudaStreamWaitEvent(st, sw->in_ready[slot], 0));
+    TSTART(t_d);
+    s = dequant_chunk(d, g, np, sw->ring_in[slot], kv + c * g.ppc * g.plane_elems, st);
+    TSTOP(t_d);
+    if (s) return s;
+    CK(cudaEventRecord(sw->in_free[slot], st));
+  }
+  if (done_event) CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(done_event), st));
+  return ALISE_OK;
+}
+
+// ------------------------------------------------------------------ host memory, events
+extern "C" int alise_host_alloc(int64_t bytes, void** out) {
+  CK(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+  return ALISE_OK;
+}
+extern "C" int alise_host_free(void* p) {
+  CK(cudaFreeHost(p));
+  return ALISE_OK;
+}
+extern "C" int alise_event_create(void** ev) {
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  *ev = e;
+  return ALISE_OK;
+}
+extern "C" int alise_event_destroy(void* ev) {
+  CK(cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev)));
+  return ALISE_OK;
+}
+extern "C" int alise_event_record(void* ev, void* stream) {
+  CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev), S(stream)));
+  return ALISE_OK;
+}
+extern "C" int alise_event_query(void* ev, int* done) {
+  cudaError_t e = cudaEventQuery(reinterpret_cast<cudaEvent_t>(ev));
+  if (e == cudaErrorNotReady) { *done = 0; return ALISE_OK; }
+  CK(e);
+  *done = 1;
+  return ALISE_OK;
+}
+extern "C" int alise_event_sync(void* ev) {
+  CK(cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(ev)));
+  return ALISE_OK;
+}
+extern "C" int alise_stream_wait(void* stream, void* ev) {
+  CK(cudaStreamWaitEvent(S(stream), reinterpret_cast<cudaEvent_t>(ev), 0));
+  return ALISE_OK;
+}
+extern "C" int alise_event_elapsed_ms(void* a, void* b, float* ms) {
+  CK(cudaEventElapsedTime(ms, reinterpret_cast<cudaEvent_t>(a), reinterpret_cast<cudaEvent_t>(b)));
+  return ALISE_OK;
+}

@@ -1,0 +1,447 @@
+// KV quantize / dequantize kernels (sm_100a).
+//
+// Reference: /root/reference/pkg/src/servesim/kvmanager.py:108-154 (quantize, dequantize).
+// The reference quantizes the rows of a 2D "channel-major" float64 view; here
+// the same rows are addressed in place inside a job's KV tensor
+// kv[layer][k|v][token][hidden] (fp16, HBM), so nothing is transposed.
+//
+//   kind ROWS    : rows are runs of `row_len` contiguous values (group-wise g along
+//                  head_dim / per (token, head); also the drop-in 2D API)
+//   kind CHANNEL : rows are (layer, k|v, hidden column) along tokens — the
+//                  reference's accounting channel (kvmanager.py:72-75)
+//   kind HEAD    : rows are (layer, k|v, head) over tokens x head_dim
+//
+// Hot path (ROWS, fp16, row_len <= 256): one fused single-pass kernel
+// (k_quant_tile) — 128-bit coalesced loads of a 32-row tile per warp,
+// warp-shuffle min/max, lane-per-row float64 parameter solve, codes from
+// registers, 64/32-bit coalesced stores.  HBM traffic = 2 B read + b/8 B written
+// per element + 12-16 B per row.
+// Other shapes use a three-phase path: partial min/max -> per-row params -> codes.
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "qmath.cuh"
+
+namespace alise {
+
+enum { KIND_ROWS = 0, KIND_CHANNEL = 1, KIND_HEAD = 2 };
+enum { DT_F16 = 0, DT_F32 = 1, DT_F64 = 2 };
+
+template <typename T> struct InTraits;
+template <> struct InTraits<uint16_t> {
+  static __device__ __forceinline__ double d(uint16_t v) { return (double)h2f(v); }
+  static __device__ __forceinline__ bool bad(uint16_t v) { return h_nonfinite(v); }
+  static constexpr bool wide = false;
+};
+template <> struct InTraits<float> {
+  static __device__ __forceinline__ double d(float v) { return (double)v; }
+  static __device__ __forceinline__ bool bad(float v) { return !isfinite(v); }
+  static constexpr bool wide = false;
+};
+template <> struct InTraits<double> {
+  static __device__ __forceinline__ double d(double v) { return v; }
+  static __device__ __forceinline__ bool bad(double v) { return !isfinite(v); }
+  static constexpr bool wide = true;
+};
+
+__device__ __forceinline__ void raise_flag(int* flag, bool bad) {
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// ---------------------------------------------------------------------------------
+// Fused single-pass tile kernel: fp16 rows, row_len % 8 == 0, row_len <= 8*LPR.
+// A warp owns TILE consecutive rows; lane l, pass p holds 8 values of row
+// p*RPP + l/LPR at column 8*(l%LPR).
+// ---------------------------------------------------------------------------------
+template <int BITS, bool PACK, int LPR, bool ZF32>
+__global__ void __launch_bounds__(256)
+k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
+             uint8_t* __restrict__ codes, double* __restrict__ scale, void* __restrict__ zero,
+             int* __restrict__ flag) {
+  constexpr int RPP = 32 / LPR;                 // rows per pass
+  constexpr int TILE = (LPR >= 32) ? 16 : 32;   // rows per warp tile
+  constexpr int PASSES = TILE / RPP;
+  constexpr float QMAXF = (float)((1 << BITS) - 1);
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR;        // row slot within a pass
+  const int vec = lane % LPR;        // 16-byte column vector index
+  const bool col_ok = vec * 8 < row_len;
+  const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ntiles = (rows + TILE - 1) / TILE;
+
+  for (int64_t tile = warp_global; tile < ntiles; tile += nwarps) {
+    const int64_t row0 = tile * TILE;
+    uint4 v[PASSES];
+    bool bad = false;
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p) {
+      const int64_t r = row0 + p * RPP + sub;
+      if (col_ok && r < rows) {
+        v[p] = __ldcs(reinterpret_cast<const uint4*>(x + r * row_len + vec * 8));
+      } else {
+        v[p] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    // per-pass row min/max (values exact in fp32), gathered so lane j owns tile row j
+    // (pass j/RPP, slot j%RPP)
+    float my_mn = 0.f, my_mx = 0.f;
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p) {
+      const int64_t r = row0 + p * RPP + sub;
+      const bool live = col_ok && r < rows;
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v[p]);
+      float a = __int_as_float(0x7f800000), b = -a;
+      if (live) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          bad |= h_nonfinite(h[j]);
+          const float f = h2f(h[j]);
+          a = fminf(a, f);
+          b = fmaxf(b, f);
+        }
+      }
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) {
+        a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+      }
+      const int src = (lane % RPP) * LPR;
+      a = __shfl_sync(0xffffffffu, a, src);
+      b = __shfl_sync(0xffffffffu, b, src);
+      if (lane / RPP == p) { my_mn = a; my_mx = b; }
+    }
+    raise_flag(flag, bad);
+    const int64_t my_row = row0 + lane;
+    const bool own = lane < TILE && my_row < rows;
+    if (!own) { my_mn = 0.f; my_mx = 0.f; }
+    const QParams q = make_params((double)my_mn, (double)my_mx, BITS, false);
+    if (own) {
+      scale[my_row] = q.s;
+      if (ZF32) reinterpret_cast<float*>(zero)[my_row] = (float)q.z;
+      else reinterpret_cast<double*>(zero)[my_row] = q.z;
+    }
+    // broadcast params back and emit codes
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p) {
+      const int src = p * RPP + sub;
+      QParams t;
+      t.inv_s = __shfl_sync(0xffffffffu, q.inv_s, src);
+      t.zf = __shfl_sync(0xffffffffu, q.zf, src);
+      t.err = __shfl_sync(0xffffffffu, q.err, src);
+      t.s = __shfl_sync(0xffffffffu, q.s, src);
+      t.z = __shfl_sync(0xffffffffu, q.z, src);
+      const int64_t r = row0 + src;
+      if (!(col_ok && r < rows)) continue;
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v[p]);
+      uint32_t c[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float f = h2f(h[j]);
+        c[j] = quant_code(f, (double)f, t, QMAXF);
+      }
+      const int64_t e0 = r * row_len + vec * 8;
+      if (PACK) {
+        const uint32_t w = c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12) | (c[4] << 16) |
+                           (c[5] << 20) | (c[6] << 24) | (c[7] << 28);
+        __stcs(reinterpret_cast<uint32_t*>(codes + e0 / 2), w);
+      } else {
+        const uint2 w = make_uint2(c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24),
+                                   c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24));
+        __stcs(reinterpret_cast<uint2*>(codes + e0), w);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Generic path, phase 1a: partial min/max of strided rows (any dtype), block per
+// (row, chunk).  partials are float64 [rows][nch].
+// ---------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_minmax_rows(const T* __restrict__ x, int64_t rows, int64_t row_len, int64_t row_stride,
+              int64_t chunk, int nch, double* __restrict__ pmn, double* __restrict__ pmx,
+              int* __restrict__ flag) {
+  const int64_t r = blockIdx.x / nch;
+  const int ch = blockIdx.x % nch;
+  const int64_t i0 = (int64_t)ch * chunk;
+  const int64_t i1 = min(row_len, i0 + chunk);
+  double a = __longlong_as_double(0x7ff0000000000000ll), b = -a;
+  bool bad = false;
+  const T* row = x + r * row_stride;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const T v = row[i];
+    bad |= InTraits<T>::bad(v);
+    const double d = InTraits<T>::d(v);
+    a = fmin(a, d);
+    b = fmax(b, d);
+  }
+  raise_flag(flag, bad);
+  __shared__ double sa[32], sb[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { sa[w] = a; sb[w] = b; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    a = l < nw ? sa[l] : __longlong_as_double(0x7ff0000000000000ll);
+    b = l < nw ? sb[l] : -__longlong_as_double(0x7ff0000000000000ll);
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (l == 0) { pmn[r * nch + ch] = a; pmx[r * nch + ch] = b; }
+  }
+}
+
+// Phase 1b: column partials for CHANNEL / HEAD kinds.  Planes of [T][Hd] fp16.
+// grid: (Hd/8 / blockDim.x column-vector blocks, nch token chunks, planes).
+// partials float [plane][nch][Hd].
+__global__ void __launch_bounds__(128)
+k_minmax_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int64_t tchunk,
+              float* __restrict__ pmn, float* __restrict__ pmx, int* __restrict__ flag) {
+  const int64_t c8 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // column vector
+  const int ch = blockIdx.y;
+  const int64_t plane = blockIdx.z;
+  const int nch = gridDim.y;
+  const bool live = c8 * 8 < Hd;
+  float a[8], b[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) { a[j] = __int_as_float(0x7f800000); b[j] = -a[j]; }
+  bool bad = false;
+  if (live) {
+    const int64_t t0 = ch * tchunk, t1 = min(T, t0 + tchunk);
+    const uint16_t* base = x + plane * T * Hd + c8 * 8;
+#pragma unroll 4
+    for (int64_t t = t0; t < t1; ++t) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(base + t * Hd));
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        bad |= h_nonfinite(h[j]);
+        const float f = h2f(h[j]);
+        a[j] = fminf(a[j], f);
+        b[j] = fmaxf(b[j], f);
+      }
+    }
+    float* om = pmn + (plane * nch + ch) * Hd + c8 * 8;
+    float* oM = pmx + (plane * nch + ch) * Hd + c8 * 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { om[j] = a[j]; oM[j] = b[j]; }
+  }
+  raise_flag(flag, bad);
+}
+
+// Phase 2: per-row params.  Writes scale (f64), zero (f64 or f32) and fast params.
+template <bool ZF32>
+__global__ void k_params(int kind, int64_t rows, int nch, const double* __restrict__ pmn_rows,
+                         const double* __restrict__ pmx_rows, const float* __restrict__ pmn_cols,
+                         const float* __restrict__ pmx_cols, int64_t Hd, int64_t D, int bits,
+                         bool wide, double* __restrict__ scale, void* __restrict__ zero,
+                         float4* __restrict__ fastp) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
+  if (kind == KIND_ROWS) {
+    for (int c = 0; c < nch; ++c) {
+      mn = fmin(mn, pmn_rows[r * nch + c]);
+      mx = fmax(mx, pmx_rows[r * nch + c]);
+    }
+  } else {
+    const int64_t per_plane = (kind == KIND_CHANNEL) ? Hd : Hd / D;
+    const int64_t plane = r / per_plane, idx = r % per_plane;
+    const int64_t c0 = (kind == KIND_CHANNEL) ? idx : idx * D;
+    const int64_t cn = (kind == KIND_CHANNEL) ? 1 : D;
+    for (int c = 0; c < nch; ++c) {
+      const float* m0 = pmn_cols + (plane * nch + c) * Hd + c0;
+      const float* m1 = pmx_cols + (plane * nch + c) * Hd + c0;
+      for (int64_t j = 0; j < cn; ++j) {
+        mn = fmin(mn, (double)m0[j]);
+        mx = fmax(mx, (double)m1[j]);
+      }
+    }
+  }
+  const QParams q = make_params(mn, mx, bits, wide);
+  scale[r] = q.s;
+  if (ZF32) reinterpret_cast<float*>(zero)[r] = (float)q.z;
+  else reinterpret_cast<double*>(zero)[r] = q.z;
+  fastp[r] = make_float4(q.inv_s, q.zf, q.err, 0.f);
+}
+
+__device__ __forceinline__ QParams load_params(const float4* fastp, const double* scale,
+                                               const void* zero, bool zf32, int64_t r) {
+  const float4 f = fastp[r];
+  QParams q;
+  q.inv_s = f.x; q.zf = f.y; q.err = f.z;
+  q.s = scale[r];
+  q.z = zf32 ? (double)reinterpret_cast<const float*>(zero)[r]
+             : reinterpret_cast<const double*>(zero)[r];
+  return q;
+}
+
+// Phase 3a: codes for strided ROWS (any dtype); output row-major codes.
+template <typename T, int BITS, bool PACK>
+__global__ void __launch_bounds__(256)
+k_codes_rows(const T* __restrict__ x, int64_t rows, int64_t row_len, int64_t row_stride,
+             const float4* __restrict__ fastp, const double* __restrict__ scale,
+             const void* __restrict__ zero, bool zf32, uint8_t* __restrict__ codes) {
+  constexpr float QMAXF = (float)((1 << BITS) - 1);
+  const int64_t npairs = (rows * row_len + (PACK ? 1 : 0)) / (PACK ? 2 : 1);
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < npairs;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t out = 0;
+#pragma unroll
+    for (int j = 0; j < (PACK ? 2 : 1); ++j) {
+      const int64_t e = PACK ? 2 * k + j : k;
+      if (e >= rows * row_len) break;
+      const int64_t r = e / row_len, i = e - r * row_len;
+      const QParams q = load_params(fastp, scale, zero, zf32, r);
+      const T v = x[r * row_stride + i];
+      const double d = InTraits<T>::d(v);
+      out |= quant_code((float)d, d, q, QMAXF) << (4 * j);
+    }
+    codes[k] = (uint8_t)out;
+  }
+}
+
+// Phase 3b: codes for CHANNEL / HEAD planes, walking native memory 8 values at a time.
+template <int BITS, bool PACK>
+__global__ void __launch_bounds__(256)
+k_codes_cols(const uint16_t* __restrict__ x, int kind, int64_t planes, int64_t T, int64_t Hd,
+             int64_t D, const float4* __restrict__ fastp, const double* __restrict__ scale,
+             const void* __restrict__ zero, bool zf32, uint8_t* __restrict__ codes) {
+  constexpr float QMAXF = (float)((1 << BITS) - 1);
+  const int64_t vecs_per_line = Hd / 8;
+  const int64_t total = planes * T * vecs_per_line;
+  const int64_t per_plane_rows = (kind == KIND_CHANNEL) ? Hd : Hd / D;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t line = k / vecs_per_line;
+    const int64_t c = (k - line * vecs_per_line) * 8;
+    const int64_t plane = line / T;
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(x + k * 8));
+    const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+    uint32_t cc[8];
+    if (kind == KIND_HEAD) {
+      const QParams q = load_params(fastp, scale, zero, zf32, plane * per_plane_rows + c / D);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float f = h2f(h[j]);
+        cc[j] = quant_code(f, (double)f, q, QMAXF);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const QParams q = load_params(fastp, scale, zero, zf32, plane * per_plane_rows + c + j);
+        const float f = h2f(h[j]);
+        cc[j] = quant_code(f, (double)f, q, QMAXF);
+      }
+    }
+    if (PACK) {
+      const uint32_t w = cc[0] | (cc[1] << 4) | (cc[2] << 8) | (cc[3] << 12) | (cc[4] << 16) |
+                         (cc[5] << 20) | (cc[6] << 24) | (cc[7] << 28);
+      reinterpret_cast<uint32_t*>(codes)[k] = w;
+    } else {
+      reinterpret_cast<uint2*>(codes)[k] =
+          make_uint2(cc[0] | (cc[1] << 8) | (cc[2] << 16) | (cc[3] << 24),
+                     cc[4] | (cc[5] << 8) | (cc[6] << 16) | (cc[7] << 24));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Dequantize.  value = fp(s * (q - z)) (kvmanager.py:154).  8 values per thread.
+//   ROWS: row = element / row_len; CHANNEL/HEAD: native planes as above.
+// OUT: uint16_t (fp16, rounded once from the float64 product) or double (exact reference).
+// ---------------------------------------------------------------------------------
+template <typename OUT, int BITS, bool PACK>
+__global__ void __launch_bounds__(256)
+k_dequant(int kind, const uint8_t* __restrict__ codes, const double* __restrict__ scale,
+          const void* __restrict__ zero, bool zf32, int64_t n, int64_t row_len, int64_t T,
+          int64_t Hd, int64_t D, OUT* __restrict__ out) {
+  const int64_t nvec = n / 8;  // host guarantees n % 8 == 0
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nvec;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t q[8];
+    if (PACK) {
+      const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(codes) + k);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q[j] = (w >> (4 * j)) & 15u;
+    } else {
+      const uint2 w = __ldcs(reinterpret_cast<const uint2*>(codes) + k);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { q[j] = (w.x >> (8 * j)) & 255u; q[4 + j] = (w.y >> (8 * j)) & 255u; }
+    }
+    const int64_t e0 = k * 8;
+    int64_t r0;
+    bool uniform;
+    if (kind == KIND_ROWS) {
+      r0 = e0 / row_len;
+      uniform = (row_len % 8) == 0;
+    } else {
+      const int64_t line = e0 / Hd, c = e0 - line * Hd, plane = line / T;
+      if (kind == KIND_HEAD) { r0 = plane * (Hd / D) + c / D; uniform = (D % 8) == 0; }
+      else { r0 = plane * Hd + c; uniform = false; }
+    }
+    OUT o[8];
+    if (uniform) {
+      const double s = scale[r0];
+      const double z = zf32 ? (double)reinterpret_cast<const float*>(zero)[r0]
+                            : reinterpret_cast<const double*>(zero)[r0];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double v = __dmul_rn(s, __dsub_rn((double)q[j], z));
+        if constexpr (sizeof(OUT) == 2) o[j] = __half_as_ushort(__double2half(v));
+        else o[j] = v;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        int64_t r;
+        if (kind == KIND_ROWS) r = (e0 + j) / row_len;
+        else if (kind == KIND_CHANNEL) r = r0 + j;
+        else { const int64_t line = (e0 + j) / Hd, c = e0 + j - line * Hd; r = (line / T) * (Hd / D) + c / D; }
+        const double s = scale[r];
+        const double z = zf32 ? (double)reinterpret_cast<const float*>(zero)[r]
+                              : reinterpret_cast<const double*>(zero)[r];
+        const double v = __dmul_rn(s, __dsub_rn((double)q[j], z));
+        if constexpr (sizeof(OUT) == 2) o[j] = __half_as_ushort(__double2half(v));
+        else o[j] = v;
+      }
+    }
+    if constexpr (sizeof(OUT) == 2) {
+      uint4 w;
+      w.x = (uint32_t)o[0] | ((uint32_t)o[1] << 16);
+      w.y = (uint32_t)o[2] | ((uint32_t)o[3] << 16);
+      w.z = (uint32_t)o[4] | ((uint32_t)o[5] << 16);
+      w.w = (uint32_t)o[6] | ((uint32_t)o[7] << 16);
+      __stcs(reinterpret_cast<uint4*>(out) + k, w);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) out[e0 + j] = o[j];
+    }
+  }
+}
+
+// Dequantize for arbitrary n (tail-safe scalar version), ROWS kind only.
+template <typename OUT, int BITS, bool PACK>
+__global__ void k_dequant_tail(const uint8_t* __restrict__ codes, const double* __restrict__ scale,
+                               const void* __restrict__ zero, bool zf32, int64_t e_begin, int64_t n,
+                               int64_t row_len, OUT* __restrict__ out) {
+  const int64_t e = e_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const uint32_t q = PACK ? ((codes[e >> 1] >> (4 * (e & 1))) & 15u) : codes[e];
+  const int64_t r = e / row_len;
+  const double s = scale[r];
+  const double z = zf32 ? (double)reinterpret_cast<const float*>(zero)[r]
+                        : reinterpret_cast<const double*>(zero)[r];
+  const double v = __dmul_rn(s, __dsub_rn((double)q, z));
+  if constexpr (sizeof(OUT) == 2) out[e] = __half_as_ushort(__double2half(v));
+  else out[e] = v;
+}
+
+}  // namespace alise

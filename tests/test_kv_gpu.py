@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA quantizer / dequantizer / swap path vs the oracle and the
+reference golden vectors.  Bar: codes, scale, zero bit-exact; dequantized float64
+bit-exact; fp16 dequant = fp16(reference float64) (0 ulp)."""
+import numpy as np
+import pytest
+
+from oracle import kv_oracle as ko
+from tests.conftest import c_quantize, have_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a CUDA device")]
+
+C1_CASES = [("contig", 32), ("contig", 64), ("channel", 0), ("head", 0)]
+
+
+@pytest.fixture(scope="module")
+def km():
+    from paper_2410_23537_b200 import kvmanager
+    return kvmanager
+
+
+def _layout(km, kv, kind, group, bits, packed=False, ppc=0):
+    L, _, T, Hd = kv.shape
+    k = "rows" if kind == "contig" else kind
+    return km.KVLayout(L, T, Hd, 32, kind=k, group=group or 128, bits=bits, packed=packed,
+                       planes_per_chunk=ppc)
+
+
+def _slab_to_rows(km, layout, slab, shape, kind, group, head_dim):
+    """Decode a host/device slab into (codes in reference row order, scale, zero)."""
+    import math
+    g = layout.geometry()
+    L, two, T, Hd = shape
+    planes = L * two
+    ppc = math.ceil(planes / g["n_chunks"]) if layout.planes_per_chunk <= 0 else min(layout.planes_per_chunk, planes)
+    rows_pp = g["rows"] // planes
+    per_plane_codes = T * Hd // (2 if layout.packed else 1)
+    a256 = lambda x: (x + 255) // 256 * 256
+    codes, scales, zeros = [], [], []
+    for c in range(g["n_chunks"]):
+        np_ = min(ppc, planes - c * ppc)
+        base = c * g["chunk_bytes"]
+        cs = a256(np_ * per_plane_codes)
+        ss = a256(np_ * rows_pp * 8)
+        codes.append(slab[base: base + np_ * per_plane_codes])
+        scales.append(slab[base + cs: base + cs + np_ * rows_pp * 8].view(np.float64))
+        zeros.append(slab[base + cs + ss: base + cs + ss + np_ * rows_pp * 4].view(np.float32))
+    native = np.concatenate(codes)
+    if layout.packed:
+        lo, hi = native & 15, native >> 4
+        native = np.stack([lo, hi], axis=1).reshape(-1)
+    native = native.reshape(shape)
+    rows = ko.view_rows(native, kind, group=group, head_dim=head_dim)
+    return rows, np.concatenate(scales)[:, None], np.concatenate(zeros).astype(np.float64)[:, None]
+
+
+# ----------------------------------------------------------------- drop-in API
+@pytest.mark.parametrize("kind,group", C1_CASES)
+@pytest.mark.parametrize("bits", [4, 8])
+def test_quantize_dropin_matches_reference_golden(km, kv_golden, kind, group, bits):
+    kv = kv_golden["c1_kv"]
+    view = ko.view_rows(kv, kind, group=group, head_dim=32)
+    qt = km.quantize(view, bits)
+    tag = f"c1_{kind}{group or ''}_b{bits}"
+    assert qt.values.dtype == np.uint8 and qt.scale.shape == (view.shape[0], 1)
+    assert np.array_equal(qt.values, kv_golden[tag + "_codes"])
+    assert np.array_equal(qt.scale, kv_golden[tag + "_scale"])
+    assert np.array_equal(qt.zero, kv_golden[tag + "_zero"])
+    assert np.array_equal(km.dequantize(qt), kv_golden[tag + "_deq"])
+
+
+def test_quantize_dropin_float64_cases(km, kv_golden):
+    for i in range(40):
+        x = kv_golden[f"f64_{i}_x"]
+        bits = int(kv_golden[f"f64_{i}_bits"])
+        qt = km.quantize(x, bits)
+        assert np.array_equal(qt.values, kv_golden[f"f64_{i}_codes"]), i
+        assert np.array_equal(qt.scale, kv_golden[f"f64_{i}_scale"]), i
+        assert np.array_equal(qt.zero, kv_golden[f"f64_{i}_zero"]), i
+        assert np.array_equal(km.dequantize(qt), kv_golden[f"f64_{i}_deq"]), i
+
+
+def test_reference_known_answers_through_gpu(km):
+    # pkg/tests/test_kvmanager.py:53-126, run through the CUDA path
+    qt = km.quantize(np.array([[0.0, 1.0]]), 8)
+    assert qt.scale[0, 0] == 1.0 / 255.0 and qt.zero[0, 0] == 0.0
+    assert qt.values[0].tolist() == [0, 255]
+    deq = km.dequantize(qt)
+    assert deq[0, 1] == 1.0 and deq[0, 0] == 0.0
+    gen = np.random.default_rng(5)
+    for _ in range(50):
+        c = float(gen.uniform(-750, 750))
+        x = np.full((1, int(gen.integers(1, 40))), c)
+        for bits in (4, 8):
+            assert np.array_equal(km.dequantize(km.quantize(x, bits)), x)
+    gen = np.random.default_rng(17)
+    for i in range(100):
+        bits = 4 if i % 2 else 8
+        length = int(gen.integers(1, 513))
+        sc = 10.0 ** gen.uniform(-2, 2)
+        x = gen.uniform(-sc, sc, size=(3, length))
+        if i % 3 == 1:
+            x = np.abs(x)
+        elif i % 3 == 2:
+            x = -np.abs(x)
+        qt = km.quantize(x, bits)
+        assert np.all(np.abs(x - km.dequantize(qt)) <= qt.scale / 2 + 1e-9)
+        ref = ko.quantize_rows(x, bits)
+        assert np.array_equal(qt.values, ref[0]) and np.array_equal(qt.scale, ref[1])
+    gen = np.random.default_rng(29)
+    for i in range(60):
+        bits = 4 if i % 2 else 8
+        x = gen.uniform(-1, 1, size=(2, int(gen.integers(2, 257))))
+        y1 = km.dequantize(km.quantize(x, bits))
+        qt2 = km.quantize(y1, bits)
+        assert np.array_equal(km.quantize(x, bits).values, qt2.values)
+        assert np.array_equal(y1, km.dequantize(qt2))
+    with pytest.raises(ValueError):
+        km.quantize(np.ones((1, 4)), 5)
+    with pytest.raises(ValueError):
+        km.quantize(np.ones((1, 0)), 8)
+    with pytest.raises(ValueError):
+        km.quantize(np.array([[1.0, np.nan]]), 8)
+    with pytest.raises(ValueError):
+        km.quantize(np.array([[1.0, np.inf]], dtype=np.float16), 8)
+
+
+@pytest.mark.parametrize("row_len", [8, 16, 24, 64, 96, 128, 200, 256, 264, 1000, 65536])
+@pytest.mark.parametrize("bits", [4, 8])
+def test_quantize_fp16_row_lengths_vs_c_oracle(km, c_oracle, row_len, bits):
+    g = np.random.default_rng(row_len * 10 + bits)
+    rows = max(3, min(4000, 400000 // row_len))
+    x = (g.standard_normal((rows, row_len)) * 10.0 ** g.uniform(-3, 3, size=(rows, 1))).astype(np.float16)
+    x[::5] = np.abs(x[::5]) + np.float16(200)
+    x[1::9] = -np.abs(x[1::9]) - np.float16(1000)
+    x[2::11] = x[2::11, :1]
+    qt = km.quantize(x, bits)
+    c, s, z = c_quantize(c_oracle, x, bits)
+    assert np.array_equal(qt.values, c)
+    assert np.array_equal(qt.scale, s)
+    assert np.array_equal(qt.zero, z)
+
+
+def test_quantize_1d_and_float32(km):
+    x = np.linspace(-3, 7, 1001).astype(np.float32)
+    qt = km.quantize(x, 8)
+    ref = ko.quantize_rows(x, 8)
+    assert qt.values.shape == (1, 1001)
+    assert np.array_equal(qt.values, ref[0]) and np.array_equal(qt.scale, ref[1])
+
+
+def test_dequantize_fp16_is_one_rounding_of_reference(km, kv_golden):
+    import torch
+    kv = kv_golden["c1_kv"]
+    view = ko.view_rows(kv, "contig", group=64, head_dim=32)
+    qt = km.quantize(view, 8)
+    out = km.dequantize_tensor(qt, out_dtype=torch.float16).cpu().numpy()
+    assert np.array_equal(out, km.dequantize(qt).astype(np.float16))
+
+
+# ----------------------------------------------------------------- KV data plane
+@pytest.mark.parametrize("kind,group", C1_CASES)
+@pytest.mark.parametrize("bits,packed", [(8, False), (4, False), (4, True)])
+def test_kv_device_slab_matches_reference(km, kv_golden, kind, group, bits, packed):
+    import torch
+    kv = kv_golden["c1_kv"]
+    layout = _layout(km, kv, kind, group, bits, packed, ppc=1)
+    g = layout.geometry()
+    src = torch.from_numpy(kv).cuda()
+    slab = torch.zeros(g["slab_bytes"], dtype=torch.uint8, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    km._lib.call("alise_kv_quantize", km._lib.C.byref(layout.desc()), km._lib.ptr(src), km._lib.ptr(slab),
+                 km._lib.ptr(flag), km._lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 0
+    rows, scale, zero = _slab_to_rows(km, layout, slab.cpu().numpy(), kv.shape, kind, group, 32)
+    tag = f"c1_{kind}{group or ''}_b{bits}"
+    assert np.array_equal(rows, kv_golden[tag + "_codes"])
+    assert np.array_equal(scale, kv_golden[tag + "_scale"])
+    assert np.array_equal(zero, kv_golden[tag + "_zero"])
+    out = torch.empty_like(src)
+    km._lib.call("alise_kv_dequantize", km._lib.C.byref(layout.desc()), km._lib.ptr(slab), km._lib.ptr(out),
+                 km._lib.stream_ptr())
+    ref = ko.rows_to_native(kv_golden[tag + "_deq"], kv.shape, kind, group=group, head_dim=32)
+    assert np.array_equal(out.cpu().numpy(), ref.astype(np.float16))
+
+
+@pytest.mark.parametrize("mode", ["staged", "zerocopy"])
+@pytest.mark.parametrize("kind,group,bits,packed", [("contig", 64, 8, False), ("contig", 32, 4, True),
+                                                    ("channel", 0, 8, False), ("head", 0, 4, False)])
+def test_swap_round_trip_through_host(km, kv_golden, mode, kind, group, bits, packed):
+    import torch
+    kv = kv_golden["c1_kv"]
+    layout = _layout(km, kv, kind, group, bits, packed, ppc=1)
+    g = layout.geometry()
+    pool = km.HostSlabPool(g["slab_bytes"] + 4096)
+    eng = km.KVSwapEngine(mode=mode)
+    try:
+        src = torch.from_numpy(kv).cuda()
+        addr = pool.alloc(g["slab_bytes"])
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        eng.offload(layout, src, addr, flag=flag)
+        torch.cuda.synchronize()
+        rows, scale, zero = _slab_to_rows(km, layout, pool.view(addr, g["slab_bytes"]).copy(), kv.shape,
+                                          kind, group, 32)
+        tag = f"c1_{kind}{group or ''}_b{bits}"
+        assert np.array_equal(rows, kv_golden[tag + "_codes"])
+        assert np.array_equal(scale, kv_golden[tag + "_scale"])
+        out = torch.zeros_like(src)
+        eng.upload(layout, addr, out)
+        torch.cuda.synchronize()
+        ref = ko.rows_to_native(kv_golden[tag + "_deq"], kv.shape, kind, group=group, head_dim=32)
+        assert np.array_equal(out.cpu().numpy(), ref.astype(np.float16))
+    finally:
+        eng.close()
+        pool.close()
+
+
+def test_device_memory_state_moves_real_bytes(km, kv_golden):
+    import torch
+    kv = kv_golden["c1_kv"]
+    layout = _layout(km, kv, "contig", 64, 8)
+    m = km.ModelConfig("toy", 4, 2, 128)
+    link = km.quantized_kv_bytes(m, 64, 8)
+    gpu_b = km.kv_bytes(m, 64)
+    ms = km.DeviceMemoryState(gpu_capacity=10 * gpu_b, cpu_capacity=10 * link, pcie_bytes_per_ms=25e6,
+                              host_pool_bytes=1 << 24)
+    src = torch.from_numpy(kv).cuda()
+    ms.bind(7, src, layout)
+    ms.reserve_gpu(gpu_b)
+    cmd = ms.start_offload(7, link, gpu_b, now_us=0)
+    assert cmd.complete_us == ms.transfer_us(link)
+    ms.complete(cmd)
+    assert ms.gpu_used == 0 and ms.cpu_used == link
+    src.zero_()
+    cmd = ms.start_upload(7, link, gpu_b, now_us=cmd.complete_us)
+    ms.complete(cmd)
+    assert ms.cpu_used == 0 and ms.gpu_used == gpu_b
+    ref = ko.rows_to_native(kv_golden["c1_contig64_b8_deq"], kv.shape, "contig", group=64)
+    assert np.array_equal(src.cpu().numpy(), ref.astype(np.float16))
+
+
+def test_nonfinite_kv_flagged_at_complete(km):
+    import torch
+    layout = km.KVLayout(1, 16, 64, 32, kind="rows", group=64, bits=8)
+    kv = torch.randn(1, 2, 16, 64, device="cuda").half()
+    kv[0, 1, 3, 5] = float("inf")
+    ms = km.DeviceMemoryState(gpu_capacity=1 << 30, cpu_capacity=1 << 30, pcie_bytes_per_ms=25e6,
+                              host_pool_bytes=1 << 20)
+    ms.bind(1, kv, layout)
+    ms.reserve_gpu(4096)
+    cmd = ms.start_offload(1, 2048, 4096, 0)
+    with pytest.raises(ValueError):
+        ms.complete(cmd)
+
+
+@pytest.mark.slow
+def test_llama7b_job_round_trip_properties(km):
+    """Full C2-size job (1 GiB fp16): bit-exact against the C oracle on sampled rows,
+    and the reference's error bound |x - deq| <= scale/2 on every element."""
+    import torch
+    from paper_2410_23537_b200 import synthetic
+    layout = km.KVLayout(32, 2048, 4096, 128, kind="rows", group=128, bits=8)
+    kv = synthetic.kv_job_torch(32, 2048, 4096, seed=0, job=3, group=128)
+    g = layout.geometry()
+    slab = torch.empty(g["slab_bytes"], dtype=torch.uint8, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    km._lib.call("alise_kv_quantize", km._lib.C.byref(layout.desc()), km._lib.ptr(kv), km._lib.ptr(slab),
+                 km._lib.ptr(flag), km._lib.stream_ptr())
+    out = torch.empty_like(kv)
+    km._lib.call("alise_kv_dequantize", km._lib.C.byref(layout.desc()), km._lib.ptr(slab), km._lib.ptr(out),
+                 km._lib.stream_ptr())
+    torch.cuda.synchronize()
+    err = (kv.float() - out.float()).abs().view(-1, 128).amax(dim=1)
+    span = (kv.float().view(-1, 128).amax(1) - kv.float().view(-1, 128).amin(1))
+    # |x - deq| <= scale/2 (+ fp16 output rounding of the dequantized value)
+    bound = span / 255 / 2 + kv.float().view(-1, 128).abs().amax(1) * 2 ** -11 + 1e-6
+    assert bool((err <= bound).all())
