@@ -242,6 +242,8 @@ def kv_bench(args, world, rank, local):
     ev_off = [km._Event() for _ in range(H)]
     ev_up = [km._Event() for _ in range(H)]
     used_up = [False] * H
+    ev_job = [km._Event() for _ in kvs]   # last upload into each job's KV buffer
+    up_pending = [False] * len(kvs)
     stream = torch.cuda.current_stream()
 
     def step():
@@ -251,11 +253,15 @@ def kv_bench(args, world, rank, local):
                 s = j % H
                 if used_up[s]:
                     eng.depend(ev_up[s].h)      # slab s was being read by an upload
+                if up_pending[j]:               # previous step's upload wrote kvs[j]
+                    km._lib.call("alise_stream_wait", km._lib.stream_ptr(), ev_job[j].h)
                 eng.offload(layout, kvs[j], slabs[s], flag=flag, event=ev_off[s].h)
             if j > 0:
                 s = (j - 1) % H
                 eng.depend(ev_off[s].h)         # upload reads what the offload wrote
                 eng.upload(layout, slabs[s], kvs[j - 1], event=ev_up[s].h)
+                km._lib.call("alise_event_record", ev_job[j - 1].h, km._lib.stream_ptr(eng.up_stream))
+                up_pending[j - 1] = True
                 used_up[s] = True
         # the step ends when both directions are done
         for e in (ev_off[(n - 1) % H], ev_up[(n - 1) % H]):

@@ -142,6 +142,11 @@ int alise_db_destroy(alise_db *db);
 int alise_db_append(alise_db *db, const float *vecs, const int32_t *lens, const int64_t *seqs,
                     int64_t n, void *stream);
 int alise_db_size(alise_db *db, int64_t *size, int64_t *next_seq);
+/* Copy the first n live slots (fp32 vectors, lens, seqs) to device buffers. */
+int alise_db_export(alise_db *db, float *vecs, int32_t *lens, int64_t *seqs, int64_t n, void *stream);
+/* Number of rescored candidates whose correct rounding could not be certified
+ * (expected 0; synchronous). */
+int alise_db_inexact(alise_db *db, unsigned int *count);
 /* Exact top-k of B queries (fp32 [B][dim], device) against the db: sims are the
  * correctly rounded float64 dot products, ordered by (-sim, seq) (ties -> older
  * first).  Outputs [B][k]; count[b] = min(k, size). */

@@ -52,6 +52,32 @@ def search_exact(db32, lens, seqs, q32, k: int):
     return exact[order], np.asarray(lens)[pick].astype(np.int64), np.asarray(seqs)[pick].astype(np.int64)
 
 
+def search_exact_batch(db32, lens, seqs, Q32, k: int, chunk: int = 256):
+    """search_exact for a batch (one BLAS GEMM for the coarse pass).
+    Returns lists of (sims, lens, seqs) per query."""
+    db32 = np.asarray(db32, dtype=np.float32)
+    db64 = db32.astype(np.float64)
+    Q32 = np.asarray(Q32, dtype=np.float32)
+    n = db32.shape[0]
+    kk = min(k, n)
+    out = []
+    amax = float(np.abs(db32).max()) if n else 1.0
+    for c0 in range(0, len(Q32), chunk):
+        Qc = Q32[c0:c0 + chunk].astype(np.float64)
+        coarse = db64 @ Qc.T
+        for j in range(Qc.shape[0]):
+            col = coarse[:, j]
+            margin = 1e-9 * max(1.0, float(np.abs(Qc[j]).sum())) * max(1.0, amax)
+            kth = np.partition(col, n - kk)[n - kk]
+            cand = np.flatnonzero(col >= kth - 2 * margin)
+            exact = np.array([exact_dot(db32[r], Q32[c0 + j]) for r in cand])
+            order = np.lexsort((np.asarray(seqs)[cand], -exact))[:kk]
+            pick = cand[order]
+            out.append((exact[order], np.asarray(lens)[pick].astype(np.int64),
+                        np.asarray(seqs)[pick].astype(np.int64)))
+    return out
+
+
 def aggregate(sims, lens, s0: float, max_len: int):
     """predict_vector's retrieval branch (predictor.py:314-324).
 

@@ -42,8 +42,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
+    # static cudart: the library loads (and its symbols can be checked) on hosts
+    # without a CUDA driver; libcuda is resolved lazily at the first CUDA call
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
-                    *objs, "-lcudart"], check=True)
+                    *objs, "-cudart", "static"], check=True)
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)

@@ -71,19 +71,18 @@ extern "C" int alise_sm_count(int device, int* out) {
 template <int BITS, bool PACK, bool ZF32>
 static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
                             double* scale, void* zero, int* flag, cudaStream_t st) {
-  const int lpr_needed = (row_len + 7) / 8;
-  const int64_t tiles_rows = (lpr_needed >= 32) ? 16 : 32;
-  const int64_t warps = (rows + tiles_rows - 1) / tiles_rows;
+  const int vpl = (row_len / 8 + 3) / 4;  // 16-byte vectors per lane per row
+  const int64_t warps = (rows + 31) / 32;
   const int block = 256;
-  const int grid = grid_for(warps * 32, block, 16);
-#define TILE_CASE(L)                                                                    \
-  if (lpr_needed <= L) {                                                                \
-    k_quant_tile<BITS, PACK, L, ZF32><<<grid, block, 0, st>>>(x, rows, row_len, codes,  \
+  const int grid = grid_for(warps * 32, block, 4);
+#define TILE_CASE(V)                                                                    \
+  if (vpl <= V) {                                                                       \
+    k_quant_tile<BITS, PACK, V, ZF32><<<grid, block, 0, st>>>(x, rows, row_len, codes,  \
                                                               scale, zero, flag);       \
     CKL();                                                                              \
     return ALISE_OK;                                                                    \
   }
-  TILE_CASE(1) TILE_CASE(2) TILE_CASE(4) TILE_CASE(8) TILE_CASE(16) TILE_CASE(32)
+  TILE_CASE(1) TILE_CASE(2) TILE_CASE(4) TILE_CASE(8)
 #undef TILE_CASE
   return fail(ALISE_EINVAL, "row_len %d too long for the tile kernel", row_len);
 }
@@ -179,11 +178,32 @@ extern "C" int alise_quantize_rows(const void* src, int src_dtype, int64_t rows,
   return fail(ALISE_EINVAL, "unknown dtype %d", src_dtype);
 }
 
+template <int BITS, bool PACK, bool ZF32>
+static int launch_dequant_tile(const uint8_t* codes, const double* scale, const void* zero,
+                               int64_t n, int row_len, uint16_t* out, cudaStream_t st) {
+  const int grid = grid_for(n / 8, 256, 8);
+  k_dequant_tile<BITS, PACK, ZF32><<<grid, 256, 0, st>>>(codes, scale, zero, n, row_len, out);
+  CKL();
+  return ALISE_OK;
+}
+
 template <typename OUT>
 static int dequant_launch(int kind, const uint8_t* codes, const double* scale, const void* zero,
                           bool zf32, int64_t n, int64_t row_len, int64_t T, int64_t Hd, int64_t D,
                           int bits, bool pack, OUT* out, cudaStream_t st) {
   const int64_t nv = n / 8;
+  if constexpr (sizeof(OUT) == 2) {
+    if (kind == KIND_ROWS && row_len % 8 == 0 && row_len <= (1 << 30) && !((uintptr_t)out & 15)) {
+      if (bits == 8)
+        return zf32 ? launch_dequant_tile<8, false, true>(codes, scale, zero, n, (int)row_len, out, st)
+                    : launch_dequant_tile<8, false, false>(codes, scale, zero, n, (int)row_len, out, st);
+      if (pack)
+        return zf32 ? launch_dequant_tile<4, true, true>(codes, scale, zero, n, (int)row_len, out, st)
+                    : launch_dequant_tile<4, true, false>(codes, scale, zero, n, (int)row_len, out, st);
+      return zf32 ? launch_dequant_tile<4, false, true>(codes, scale, zero, n, (int)row_len, out, st)
+                  : launch_dequant_tile<4, false, false>(codes, scale, zero, n, (int)row_len, out, st);
+    }
+  }
   if (nv > 0) {
     const int grid = grid_for(nv, 256, 16);
 #define DQ(B, P) k_dequant<OUT, B, P><<<grid, 256, 0, st>>>(kind, codes, scale, zero, zf32, nv * 8, row_len, T, Hd, D, out)
@@ -258,7 +278,7 @@ static int geom(const alise_kv_desc* d, KvGeom* g) {
   }
   g->code_bytes_pp = d->packed ? g->plane_elems / 2 : g->plane_elems;
   int64_t ppc = d->planes_per_chunk;
-  if (ppc <= 0) ppc = std::max<int64_t>(1, (int64_t(16) << 20) / g->code_bytes_pp);
+  if (ppc <= 0) ppc = std::max<int64_t>(1, (int64_t(64) << 20) / g->code_bytes_pp);
   g->ppc = std::min(ppc, g->planes);
   g->n_chunks = (g->planes + g->ppc - 1) / g->ppc;
   g->rec_bytes = g->rec(g->ppc);

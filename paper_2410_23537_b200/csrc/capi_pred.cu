@@ -1,0 +1,290 @@
+// C ABI for the retrieval length predictor: device DB ring (VectorStore), exact
+// batched top-k (tcgen05 coarse scan + exact rescoring), shard merge, finish.
+// Declarations and reference citations: include/alise_b200.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/alise_b200.h"
+#include "pred_scan.cuh"
+
+namespace alise {
+int fail(int code, const char* fmt, ...);
+}
+using namespace alise;
+using namespace alise::pred;
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return fail(ALISE_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+#define CKL()                                                                                 \
+  do {                                                                                        \
+    cudaError_t e_ = cudaGetLastError();                                                      \
+    if (e_ != cudaSuccess) return fail(ALISE_ECUDA, "launch: %s", cudaGetErrorString(e_));    \
+  } while (0)
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2D fp16 K-major tile map: rows x cols(=dp), box rows_box x 64, 128-byte swizzle.
+static int make_map(CUtensorMap* m, void* base, uint64_t rows, uint64_t dp, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(ALISE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {dp, rows};
+  cuuint64_t strides[1] = {dp * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ALISE_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return ALISE_OK;
+}
+
+struct alise_db {
+  int device = 0;
+  int64_t capacity = 0, cap_p = 0, dim = 0, dp = 0;
+  int64_t size = 0, next_seq = 0;
+  float* v32 = nullptr;
+  __half* v16 = nullptr;
+  int32_t* lens = nullptr;
+  int64_t* seqs = nullptr;
+  unsigned int* vmax = nullptr;     // float bits of the max row norm
+  unsigned int* inexact = nullptr;  // candidates whose rounding could not be certified
+  CUtensorMap tmD;
+  // query scratch
+  int64_t bp_cap = 0;
+  int splits_cap = 0;
+  __half* q16 = nullptr;
+  float* two_delta = nullptr;
+  float* cand_s = nullptr;
+  int32_t* cand_r = nullptr;
+  int32_t* cand_n = nullptr;
+  float* topc = nullptr;
+  int32_t* need = nullptr;
+  CUtensorMap tmQ;
+};
+
+extern "C" int alise_db_create(int device, int64_t capacity, int64_t dim, alise_db** out) {
+  if (capacity <= 0 || dim <= 0) return fail(ALISE_EINVAL, "capacity and dim must be positive");
+  if (capacity > ((int64_t)1 << 31) - 512) return fail(ALISE_EINVAL, "capacity too large");
+  CK(cudaSetDevice(device));
+  alise_db* db = new alise_db();
+  db->device = device;
+  db->capacity = capacity;
+  db->cap_p = (capacity + BN - 1) / BN * BN;
+  db->dim = dim;
+  db->dp = (dim + 63) / 64 * 64;
+  CK(cudaMalloc(&db->v32, sizeof(float) * capacity * dim));
+  CK(cudaMalloc(&db->v16, sizeof(__half) * db->cap_p * db->dp));
+  CK(cudaMemset(db->v16, 0, sizeof(__half) * db->cap_p * db->dp));
+  CK(cudaMalloc(&db->lens, sizeof(int32_t) * capacity));
+  CK(cudaMalloc(&db->seqs, sizeof(int64_t) * capacity));
+  CK(cudaMalloc(&db->vmax, 2 * sizeof(unsigned int)));
+  CK(cudaMemset(db->vmax, 0, 2 * sizeof(unsigned int)));
+  db->inexact = db->vmax + 1;
+  int s = make_map(&db->tmD, db->v16, db->cap_p, db->dp, BN);
+  if (s) return s;
+  *out = db;
+  return ALISE_OK;
+}
+
+static void free_scratch(alise_db* db) {
+  cudaFree(db->q16);
+  cudaFree(db->two_delta);
+  cudaFree(db->cand_s);
+  cudaFree(db->cand_r);
+  cudaFree(db->cand_n);
+  cudaFree(db->topc);
+  cudaFree(db->need);
+  db->q16 = nullptr;
+  db->bp_cap = 0;
+  db->splits_cap = 0;
+}
+
+extern "C" int alise_db_destroy(alise_db* db) {
+  if (!db) return ALISE_OK;
+  cudaDeviceSynchronize();
+  cudaFree(db->v32);
+  cudaFree(db->v16);
+  cudaFree(db->lens);
+  cudaFree(db->seqs);
+  cudaFree(db->vmax);
+  free_scratch(db);
+  delete db;
+  return ALISE_OK;
+}
+
+extern "C" int alise_db_append(alise_db* db, const float* vecs, const int32_t* lens, const int64_t* seqs,
+                               int64_t n, void* stream) {
+  if (!db || n < 0) return fail(ALISE_EINVAL, "bad append");
+  if (n == 0) return ALISE_OK;
+  // rows with equal slot in one batch would race; the host splits batches larger than capacity
+  if (n > db->capacity) return fail(ALISE_EINVAL, "append batch larger than capacity");
+  k_db_append<<<(unsigned)n, 128, 0, S(stream)>>>(vecs, lens, seqs, n, db->dim, db->dp, db->capacity, db->v32,
+                                                  db->v16, db->lens, db->seqs, db->vmax);
+  CKL();
+  db->next_seq += n;
+  db->size = std::min(db->capacity, db->size + n);
+  return ALISE_OK;
+}
+
+extern "C" int alise_db_size(alise_db* db, int64_t* size, int64_t* next_seq) {
+  if (!db) return fail(ALISE_EINVAL, "null db");
+  if (size) *size = db->size;
+  if (next_seq) *next_seq = db->next_seq;
+  return ALISE_OK;
+}
+
+extern "C" int alise_db_export(alise_db* db, float* vecs, int32_t* lens, int64_t* seqs, int64_t n, void* stream) {
+  if (!db || n < 0 || n > db->size) return fail(ALISE_EINVAL, "bad export count");
+  if (n == 0) return ALISE_OK;
+  CK(cudaMemcpyAsync(vecs, db->v32, sizeof(float) * n * db->dim, cudaMemcpyDeviceToDevice, S(stream)));
+  CK(cudaMemcpyAsync(lens, db->lens, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, S(stream)));
+  CK(cudaMemcpyAsync(seqs, db->seqs, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, S(stream)));
+  return ALISE_OK;
+}
+
+extern "C" int alise_db_inexact(alise_db* db, unsigned int* count) {
+  CK(cudaMemcpy(count, db->inexact, sizeof(unsigned int), cudaMemcpyDeviceToHost));
+  return ALISE_OK;
+}
+
+static int choose_splits(int n_qb, int n_tiles, int sms) {
+  // fill the machine: ~2 waves of one CTA per SM, at least one tile per split
+  int s = std::max(1, (2 * sms + n_qb - 1) / n_qb);
+  s = std::min(s, std::max(1, n_tiles));
+  s = std::min(s, 8192 / KMAX);
+  return s;
+}
+
+static int ensure_scratch(alise_db* db, int64_t Bp, int splits, cudaStream_t st) {
+  if (Bp <= db->bp_cap && splits <= db->splits_cap) return ALISE_OK;
+  CK(cudaStreamSynchronize(st));
+  free_scratch(db);
+  const int64_t bp = std::max(Bp, (int64_t)128);
+  const int sp = std::max(splits, 1);
+  CK(cudaMalloc(&db->q16, sizeof(__half) * bp * db->dp));
+  CK(cudaMalloc(&db->two_delta, sizeof(float) * bp));
+  CK(cudaMalloc(&db->cand_s, sizeof(float) * sp * bp * CAP));
+  CK(cudaMalloc(&db->cand_r, sizeof(int32_t) * sp * bp * CAP));
+  CK(cudaMalloc(&db->cand_n, sizeof(int32_t) * sp * bp));
+  CK(cudaMalloc(&db->topc, sizeof(float) * sp * bp * KMAX));
+  CK(cudaMalloc(&db->need, sizeof(int32_t) * bp));
+  db->bp_cap = bp;
+  db->splits_cap = sp;
+  return make_map(&db->tmQ, db->q16, bp, db->dp, BM);
+}
+
+static int sm_count_pred() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int k, double* out_sim,
+                             int64_t* out_seq, int32_t* out_len, int32_t* out_count, void* stream) {
+  if (!db || B < 0) return fail(ALISE_EINVAL, "bad topk call");
+  if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
+  cudaStream_t st = S(stream);
+  if (B == 0) return ALISE_OK;
+  if (db->size == 0) {
+    CK(cudaMemsetAsync(out_count, 0, sizeof(int32_t) * B, st));
+    return ALISE_OK;
+  }
+  const int64_t Bp = (B + BM - 1) / BM * BM;
+  const int n_qb = (int)(Bp / BM);
+  const int n_tiles = (int)((db->size + BN - 1) / BN);
+  const int splits = choose_splits(n_qb, n_tiles, sm_count_pred());
+  int s = ensure_scratch(db, Bp, splits, st);
+  if (s) return s;
+  k_query_prep<<<(unsigned)Bp, 128, 0, st>>>(queries, B, db->dim, db->dp, db->vmax, db->q16, db->two_delta);
+  CKL();
+  ScanArgs a;
+  a.n_kb = (int)(db->dp / BK);
+  a.n_rows = db->size;
+  a.n_tiles = n_tiles;
+  a.n_qb = n_qb;
+  a.n_splits = splits;
+  a.Bp = (int)Bp;
+  a.k = k;
+  a.two_delta = db->two_delta;
+  a.cand_s = db->cand_s;
+  a.cand_r = db->cand_r;
+  a.cand_n = db->cand_n;
+  a.topc = db->topc;
+  static bool attr_set[2] = {false, false};
+  const int kt = k <= 8 ? 0 : 1;
+  if (!attr_set[kt]) {
+    if (kt == 0) CK(cudaFuncSetAttribute(k_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM));
+    else CK(cudaFuncSetAttribute(k_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM));
+    attr_set[kt] = true;
+  }
+  const unsigned grid = (unsigned)(n_qb * splits);
+  if (kt == 0) k_scan<8><<<grid, 192, SCAN_SMEM, st>>>(db->tmQ, db->tmD, a);
+  else k_scan<16><<<grid, 192, SCAN_SMEM, st>>>(db->tmQ, db->tmD, a);
+  CKL();
+  CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
+  k_rescore<<<(unsigned)B, 256, 0, st>>>(splits, (int)Bp, B, k, db->size, db->dim, queries, db->v32, db->lens,
+                                         db->seqs, db->two_delta, db->cand_s, db->cand_r, db->cand_n, db->topc,
+                                         out_sim, out_seq, out_len, out_count, db->need, db->inexact);
+  CKL();
+  k_exhaustive<<<(unsigned)B, 256, 0, st>>>(B, k, db->size, db->dim, queries, db->v32, db->lens, db->seqs, db->need,
+                                            out_sim, out_seq, out_len, out_count, db->inexact);
+  CKL();
+  return ALISE_OK;
+}
+
+extern "C" int alise_topk_merge(int G, int64_t B, int k, const double* sims, const int64_t* seqs,
+                                const int32_t* lens, const int32_t* counts, double* out_sim, int64_t* out_seq,
+                                int32_t* out_len, int32_t* out_count, void* stream) {
+  if (G < 1 || G > 64 || k < 1 || k > KMAX) return fail(ALISE_EINVAL, "bad merge arguments");
+  if (B == 0) return ALISE_OK;
+  k_topk_merge<<<(unsigned)((B + 127) / 128), 128, 0, S(stream)>>>(G, B, k, sims, seqs, lens, counts, out_sim,
+                                                                     out_seq, out_len, out_count);
+  CKL();
+  return ALISE_OK;
+}
+
+extern "C" int alise_predict_finish(int64_t B, int k, const double* sims, const int32_t* lens,
+                                    const int32_t* counts, double s0, const float* queries, int64_t dim,
+                                    const double* W1, const double* b1, const double* w2, double b2,
+                                    int64_t hidden, int64_t max_len, double log_cap, int32_t* out_len,
+                                    uint8_t* out_retrieved, void* stream) {
+  if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
+  if (hidden < 1 || hidden > 128) return fail(ALISE_EINVAL, "hidden must be in [1, 128]");
+  if (B == 0) return ALISE_OK;
+  const int64_t threads = B * 32;
+  k_finish<<<(unsigned)((threads + 255) / 256), 256, 0, S(stream)>>>(B, k, sims, lens, counts, s0, queries, dim, W1,
+                                                                     b1, w2, b2, hidden, max_len, log_cap, out_len,
+                                                                     out_retrieved);
+  CKL();
+  return ALISE_OK;
+}

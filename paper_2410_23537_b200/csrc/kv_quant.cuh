@@ -49,108 +49,240 @@ __device__ __forceinline__ void raise_flag(int* flag, bool bad) {
 }
 
 // ---------------------------------------------------------------------------------
-// Fused single-pass tile kernel: fp16 rows, row_len % 8 == 0, row_len <= 8*LPR.
-// A warp owns TILE consecutive rows; lane l, pass p holds 8 values of row
-// p*RPP + l/LPR at column 8*(l%LPR).
+// Fused tile kernel: fp16 rows, row_len % 8 == 0, row_len <= 8 * 4 * VPL.
+// A warp owns a 32-row tile.  4 lanes per row, 8 rows per pass, 4 passes; lane l
+// of a row holds 16-byte vectors l, l+4, l+8, ... (VPL of them) so every load
+// instruction covers 8 rows x 64 contiguous bytes.
+//   A: NaN-propagating half2 min/max, 2 shuffles per row, gathered so that lane j
+//      owns tile row j;
+//   B: lane-per-row float64 parameter solve (scale, zero, snap loop) + fast-path
+//      constants (qmath.cuh TileParams);
+//   C: reload (L1/L2 hit), codes via one fp32x2 FMA + integer decision per value,
+//      warp-uniform float64 re-run of the rare values near a rounding boundary.
+// HBM traffic: 2 B read + b/8 B written per value + 12-16 B per row.
 // ---------------------------------------------------------------------------------
-template <int BITS, bool PACK, int LPR, bool ZF32>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ uint32_t f2bits(float f) { return __float_as_uint(f); }
+
+template <int BITS, bool PACK, int VPL, bool ZF32>
+__global__ void __launch_bounds__(256, 4)
 k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
              uint8_t* __restrict__ codes, double* __restrict__ scale, void* __restrict__ zero,
              int* __restrict__ flag) {
-  constexpr int RPP = 32 / LPR;                 // rows per pass
-  constexpr int TILE = (LPR >= 32) ? 16 : 32;   // rows per warp tile
-  constexpr int PASSES = TILE / RPP;
   constexpr float QMAXF = (float)((1 << BITS) - 1);
   const int lane = threadIdx.x & 31;
-  const int sub = lane / LPR;        // row slot within a pass
-  const int vec = lane % LPR;        // 16-byte column vector index
-  const bool col_ok = vec * 8 < row_len;
+  const int sub = lane >> 2;  // row slot within a pass (8 rows per pass)
+  const int q4 = lane & 3;    // lane within the row
+  const int nvec = row_len >> 3;
   const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t ntiles = (rows + TILE - 1) / TILE;
+  const int64_t ntiles = (rows + 31) >> 5;
+  constexpr int F = TileMagic<BITS>::F;
+  constexpr uint32_t HALF = 1u << (F - 1);
+  constexpr uint32_t FMASK = (1u << F) - 1;
+  const uint32_t kMagicBits = f2bits(TileMagic<BITS>::M);
 
   for (int64_t tile = warp_global; tile < ntiles; tile += nwarps) {
-    const int64_t row0 = tile * TILE;
-    uint4 v[PASSES];
-    bool bad = false;
+    const int64_t row0 = tile << 5;
+    // ---------------- A: per-row min / max
+    uint32_t mine = 0;
 #pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      const int64_t r = row0 + p * RPP + sub;
-      if (col_ok && r < rows) {
-        v[p] = __ldcs(reinterpret_cast<const uint4*>(x + r * row_len + vec * 8));
-      } else {
-        v[p] = make_uint4(0, 0, 0, 0);
-      }
-    }
-    // per-pass row min/max (values exact in fp32), gathered so lane j owns tile row j
-    // (pass j/RPP, slot j%RPP)
-    float my_mn = 0.f, my_mx = 0.f;
+    for (int p = 0; p < 4; ++p) {
+      const int64_t r = row0 + p * 8 + sub;
+      __half2 lo2 = __half2half2(__ushort_as_half(0x7c00)), hi2 = __half2half2(__ushort_as_half(0xfc00));
+      if (r < rows) {
+        const uint4* src = reinterpret_cast<const uint4*>(x + r * row_len);
 #pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      const int64_t r = row0 + p * RPP + sub;
-      const bool live = col_ok && r < rows;
-      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v[p]);
-      float a = __int_as_float(0x7f800000), b = -a;
-      if (live) {
+        for (int i = 0; i < VPL; ++i) {
+          const int v = q4 + 4 * i;
+          if (v < nvec) {
+            const uint4 d = __ldg(src + v);
+            const __half2* h = reinterpret_cast<const __half2*>(&d);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          bad |= h_nonfinite(h[j]);
-          const float f = h2f(h[j]);
-          a = fminf(a, f);
-          b = fmaxf(b, f);
+            for (int k = 0; k < 4; ++k) {
+              lo2 = __hmin2_nan(lo2, h[k]);
+              hi2 = __hmax2_nan(hi2, h[k]);
+            }
+          }
         }
       }
+      const __half mn = __hmin_nan(__low2half(lo2), __high2half(lo2));
+      const __half mx = __hmax_nan(__low2half(hi2), __high2half(hi2));
+      __half2 pk = __halves2half2(mn, __hneg(mx));
+      uint32_t u = *reinterpret_cast<uint32_t*>(&pk);
 #pragma unroll
-      for (int o = LPR / 2; o > 0; o >>= 1) {
-        a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
-        b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+      for (int o = 1; o < 4; o <<= 1) {
+        uint32_t w = __shfl_xor_sync(0xffffffffu, u, o);
+        __half2 c = __hmin2_nan(*reinterpret_cast<__half2*>(&u), *reinterpret_cast<__half2*>(&w));
+        u = *reinterpret_cast<uint32_t*>(&c);
       }
-      const int src = (lane % RPP) * LPR;
-      a = __shfl_sync(0xffffffffu, a, src);
-      b = __shfl_sync(0xffffffffu, b, src);
-      if (lane / RPP == p) { my_mn = a; my_mx = b; }
+      const uint32_t g = __shfl_sync(0xffffffffu, u, (lane & 7) << 2);
+      if ((lane >> 3) == p) mine = g;
     }
-    raise_flag(flag, bad);
+    // ---------------- B: lane-per-row parameters
     const int64_t my_row = row0 + lane;
-    const bool own = lane < TILE && my_row < rows;
-    if (!own) { my_mn = 0.f; my_mx = 0.f; }
-    const QParams q = make_params((double)my_mn, (double)my_mx, BITS, false);
+    const bool own = my_row < rows;
+    const __half2 mm = *reinterpret_cast<__half2*>(&mine);
+    float fmn = __low2float(mm), fmx = -__high2float(mm);
+    const bool bad = own && !(isfinite(fmn) && isfinite(fmx));
+    raise_flag(flag, bad);
+    if (!own || bad) { fmn = 0.f; fmx = 0.f; }
+    const QParams q = make_params((double)fmn, (double)fmx, BITS, false);
+    const TileParams tp = make_tile_params<BITS>(q, fmax(fabs((double)fmn), fabs((double)fmx)));
     if (own) {
       scale[my_row] = q.s;
       if (ZF32) reinterpret_cast<float*>(zero)[my_row] = (float)q.z;
       else reinterpret_cast<double*>(zero)[my_row] = q.z;
     }
-    // broadcast params back and emit codes
+    __syncwarp();  // the float64 fallback below re-reads scale / zero of other lanes' rows
+    // ---------------- C: codes
+#pragma unroll 1
+    for (int p = 0; p < 4; ++p) {
+      const int src_lane = p * 8 + sub;
+      const float inv_s = __shfl_sync(0xffffffffu, tp.inv_s, src_lane);
+      const float zc = __shfl_sync(0xffffffffu, tp.zc, src_lane);
+      const int w = __shfl_sync(0xffffffffu, tp.w, src_lane);
+      const int64_t r = row0 + src_lane;
+      const bool live_row = r < rows;
+      // unsafe iff ((bits(y) - bits(M) - HALF + w) & FMASK) <= 2w
+      const uint32_t koff = (uint32_t)w - HALF - kMagicBits;
+      const uint32_t kwin = (uint32_t)(2 * w);
+      const uint32_t kcode = kMagicBits - HALF;  // code = (bits(y) - kcode) >> F
+      const uint4* src = reinterpret_cast<const uint4*>(x + (live_row ? r : 0) * row_len);
+      uint32_t cw[VPL][PACK ? 1 : 2];
+      bool unsafe = false;
 #pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      const int src = p * RPP + sub;
-      QParams t;
-      t.inv_s = __shfl_sync(0xffffffffu, q.inv_s, src);
-      t.zf = __shfl_sync(0xffffffffu, q.zf, src);
-      t.err = __shfl_sync(0xffffffffu, q.err, src);
-      t.s = __shfl_sync(0xffffffffu, q.s, src);
-      t.z = __shfl_sync(0xffffffffu, q.z, src);
-      const int64_t r = row0 + src;
-      if (!(col_ok && r < rows)) continue;
-      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v[p]);
-      uint32_t c[8];
+      for (int i = 0; i < VPL; ++i) {
+        const int v = q4 + 4 * i;
+        if (live_row && v < nvec) {
+          const uint4 d = __ldg(src + v);
+          const __half2* h = reinterpret_cast<const __half2*>(&d);
+          uint32_t c[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float f = h2f(h[j]);
-        c[j] = quant_code(f, (double)f, t, QMAXF);
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __half22float2(h[k]);
+            const float2 y = __ffma2_rn(f, make_float2(inv_s, inv_s), make_float2(zc, zc));
+            const uint32_t b0 = f2bits(y.x), b1 = f2bits(y.y);
+            unsafe |= ((b0 + koff) & FMASK) <= kwin;
+            unsafe |= ((b1 + koff) & FMASK) <= kwin;
+            c[2 * k] = (b0 - kcode) >> F;
+            c[2 * k + 1] = (b1 - kcode) >> F;
+          }
+          // out-of-range codes only occur for unsafe values (rewritten below); the
+          // packing keeps each code in its own byte / nibble so neighbours stay intact
+          if (PACK) {
+            uint32_t wv = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) wv |= (c[j] & 15u) << (4 * j);
+            cw[i][0] = wv;
+          } else {
+            cw[i][0] = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
+            cw[i][PACK ? 0 : 1] =
+                __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
+          }
+        }
       }
-      const int64_t e0 = r * row_len + vec * 8;
-      if (PACK) {
-        const uint32_t w = c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12) | (c[4] << 16) |
-                           (c[5] << 20) | (c[6] << 24) | (c[7] << 28);
-        __stcs(reinterpret_cast<uint32_t*>(codes + e0 / 2), w);
-      } else {
-        const uint2 w = make_uint2(c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24),
-                                   c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24));
-        __stcs(reinterpret_cast<uint2*>(codes + e0), w);
+      if (__any_sync(0xffffffffu, unsafe)) {
+        // rare: redo the values near a rounding boundary with the reference float64 ops
+        if (unsafe) {
+          const double s = scale[r];
+          const double z = ZF32 ? (double)reinterpret_cast<const float*>(zero)[r]
+                                : reinterpret_cast<const double*>(zero)[r];
+#pragma unroll
+          for (int i = 0; i < VPL; ++i) {
+            const int v = q4 + 4 * i;
+            if (v < nvec) {
+              const uint4 d = __ldg(src + v);
+              const uint16_t* hh = reinterpret_cast<const uint16_t*>(&d);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float f = h2f(hh[j]);
+                const uint32_t b = f2bits(fmaf(f, inv_s, zc));
+                if (((b + koff) & FMASK) <= kwin) {
+                  float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, s), z));
+                  rr = fminf(fmaxf(rr, 0.f), QMAXF);
+                  const uint32_t cc = (uint32_t)rr;
+                  if (PACK) {
+                    cw[i][0] = (cw[i][0] & ~(15u << (4 * j))) | (cc << (4 * j));
+                  } else {
+                    const int wi = j >> 2, sh = 8 * (j & 3);
+                    cw[i][wi] = (cw[i][wi] & ~(255u << sh)) | (cc << sh);
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+      if (live_row) {
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          const int v = q4 + 4 * i;
+          if (v < nvec) {
+            const int64_t e0 = r * row_len + v * 8;
+            if (PACK) __stcs(reinterpret_cast<uint32_t*>(codes + e0 / 2), cw[i][0]);
+            else __stcs(reinterpret_cast<uint2*>(codes + e0), make_uint2(cw[i][0], cw[i][PACK ? 0 : 1]));
+          }
+        }
       }
     }
+  }
+}
+
+// Fast dequantize of ROWS-kind codes (row_len % 8 == 0) to fp16.  Each thread owns 8
+// values of one row.  y = fp32(s) * ((2^23+q) - (2^23+z)) is exact up to two fp32
+// roundings; fp16(y) equals fp16(float64 s*(q-z)) unless y is within 4 fp32 ulps of an
+// fp16 rounding midpoint or below the fp16 normal range, where the thread re-runs the
+// reference float64 product (warp-uniform branch).
+template <int BITS, bool PACK, bool ZF32>
+__global__ void __launch_bounds__(256)
+k_dequant_tile(const uint8_t* __restrict__ codes, const double* __restrict__ scale,
+               const void* __restrict__ zero, int64_t n, int row_len, uint16_t* __restrict__ out) {
+  const int64_t nvec = n >> 3;
+  const int vpr = row_len >> 3;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nvec;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = k / vpr;
+    const double s = __ldg(scale + r);
+    const double z = ZF32 ? (double)__ldg(reinterpret_cast<const float*>(zero) + r)
+                          : __ldg(reinterpret_cast<const double*>(zero) + r);
+    const float s32 = (float)s;
+    // rows whose products may leave the fp16 normal range take the exact path
+    const bool row_fast = fabs(z) < 4194304.0 && s >= 0x1p-14 && s < 60000.0 &&
+                          (z == rint(z) || fabs(z) >= 0x1p-14 || z == 0.0);
+    const float zm = (float)(z + 8388608.0);
+    uint32_t q[8];
+    if (PACK) {
+      const uint32_t wd = __ldcs(reinterpret_cast<const uint32_t*>(codes) + k);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q[j] = (wd >> (4 * j)) & 15u;
+    } else {
+      const uint2 wd = __ldcs(reinterpret_cast<const uint2*>(codes) + k);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { q[j] = (wd.x >> (8 * j)) & 255u; q[4 + j] = (wd.y >> (8 * j)) & 255u; }
+    }
+    uint32_t o[4];
+    bool unsafe = !row_fast;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 qf = make_float2(__uint_as_float(0x4B000000u | q[2 * j]), __uint_as_float(0x4B000000u | q[2 * j + 1]));
+      const float2 d = __fadd2_rn(qf, make_float2(-zm, -zm));
+      const float2 y = __fmul2_rn(d, make_float2(s32, s32));
+      const uint32_t b0 = __float_as_uint(y.x), b1 = __float_as_uint(y.y);
+      unsafe |= ((b0 + (4u - 0x1000u)) & 0x1fffu) <= 8u;
+      unsafe |= ((b1 + (4u - 0x1000u)) & 0x1fffu) <= 8u;
+      const __half2 hv = __floats2half2_rn(y.x, y.y);
+      o[j] = *reinterpret_cast<const uint32_t*>(&hv);
+    }
+    if (__any_sync(__activemask(), unsafe) && unsafe) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double v = __dmul_rn(s, __dsub_rn((double)q[j], z));
+        const uint32_t hb = __half_as_ushort(__double2half(v));
+        const int wi = j >> 1, sh = 16 * (j & 1);
+        o[wi] = (o[wi] & ~(0xffffu << sh)) | (hb << sh);
+      }
+    }
+    __stcs(reinterpret_cast<uint4*>(out) + k, make_uint4(o[0], o[1], o[2], o[3]));
   }
 }
 

@@ -1,0 +1,623 @@
+// Predictor kernels (sm_100a): DB ring append, query prep, the tcgen05 coarse scan
+// with a fused candidate filter, exact float64 rescoring + (-sim, seq) top-k, the
+// cross-shard merge and the aggregate / all-MLP finish.
+//
+// Reference: /root/reference/pkg/src/servesim/predictor.py
+//   VectorStore.add / search   :135-163   (ring slot = seq % capacity; sims = V @ q;
+//                                          order (-sim, seq))
+//   LengthPredictor.predict_vector :311-325, FallbackRegressor._forward/predict_len :209-219
+//
+// Exactness argument: the coarse score s~ = fp16(q).fp16(v) with
+// fp32 accumulation differs from the exact dot product s by at most
+//   delta_q = |q| * Vmax * (2^-10 + D*2^-21) + (|q| + Vmax) * sqrt(D) * 2^-24,
+// so every row of the exact top-k has s~ >= (k-th largest s~) - 2*delta_q.  Each scan
+// CTA keeps, per query, its running top-k of s~ and appends every row that reaches
+// (running k-th) - 2*delta_q; since the running k-th never exceeds the final one the
+// appended set is a superset of the needed candidates.  Candidates are rescored with a
+// double-double float64 dot product whose correct rounding is verified per candidate.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "sm100.cuh"
+
+namespace alise {
+namespace pred {
+
+constexpr int BM = 128;        // queries per CTA (TMEM lanes)
+constexpr int BN = 256;        // DB rows per tile (UMMA N)
+constexpr int BK = 64;         // K per pipeline stage (128-byte rows, SW128)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int KMAX = 16;       // largest supported k
+constexpr int CAP = 128;       // candidate slots per (split, query)
+constexpr int SCAN_SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int MAXC = 512;      // candidates rescored per query
+
+// ------------------------------------------------------------------ DB maintenance
+// Append n rows at ring slots seq % capacity: fp32 master, fp16 coarse copy (zero
+// padded to dp), lengths, seqs; track an upper bound of the row L2 norms.
+__global__ void k_db_append(const float* __restrict__ vecs, const int32_t* __restrict__ lens,
+                            const int64_t* __restrict__ seqs, int64_t n, int64_t dim, int64_t dp,
+                            int64_t capacity, float* __restrict__ v32, __half* __restrict__ v16,
+                            int32_t* __restrict__ dlens, int64_t* __restrict__ dseqs,
+                            unsigned int* __restrict__ vmax_bits) {
+  const int64_t i = blockIdx.x;
+  if (i >= n) return;
+  const int64_t slot = seqs[i] % capacity;
+  double ss = 0.0;
+  for (int64_t d = threadIdx.x; d < dp; d += blockDim.x) {
+    const float v = d < dim ? vecs[i * dim + d] : 0.f;
+    if (d < dim) v32[slot * dim + d] = v;
+    v16[slot * dp + d] = __float2half_rn(v);
+    ss += (double)v * (double)v;
+  }
+  __shared__ double red[32];
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    dlens[slot] = lens[i];
+    dseqs[slot] = seqs[i];
+    // round the norm up so Vmax stays an upper bound
+    const float nrm = __double2float_ru(sqrt(t) * (1.0 + 1e-12));
+    atomicMax(vmax_bits, __float_as_uint(nrm));
+  }
+}
+
+// Queries: fp32 [B][dim] -> fp16 [Bp][dp] (zero padded) and 2*delta per query.
+__global__ void k_query_prep(const float* __restrict__ q, int64_t B, int64_t dim, int64_t dp,
+                             const unsigned int* __restrict__ vmax_bits, __half* __restrict__ q16,
+                             float* __restrict__ two_delta) {
+  const int64_t i = blockIdx.x;
+  double ss = 0.0;
+  for (int64_t d = threadIdx.x; d < dp; d += blockDim.x) {
+    const float v = (i < B && d < dim) ? q[i * dim + d] : 0.f;
+    q16[i * dp + d] = __float2half_rn(v);
+    ss += (double)v * (double)v;
+  }
+  __shared__ double red[32];
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    const double qn = sqrt(t) * (1.0 + 1e-12);
+    const double V = (double)__uint_as_float(*vmax_bits);
+    const double D = (double)dim;
+    const double delta = qn * V * (0x1p-10 + D * 0x1p-21) + (qn + V) * sqrt(D) * 0x1p-24;
+    two_delta[i] = __double2float_ru(2.0 * delta);
+  }
+}
+
+// ------------------------------------------------------------------ tcgen05 scan
+struct ScanArgs {
+  int n_kb;          // padded dim / 64
+  int64_t n_rows;    // valid DB rows (slots [0, n_rows))
+  int n_tiles;       // ceil(n_rows / BN)
+  int n_qb;          // query blocks of 128
+  int n_splits;      // DB splits (CTAs per query block)
+  int Bp;            // padded query count
+  int k;
+  const float* two_delta;
+  float* cand_s;     // [n_splits][Bp][CAP]
+  int32_t* cand_r;   // [n_splits][Bp][CAP]
+  int32_t* cand_n;   // [n_splits][Bp]   (-1 = overflow)
+  float* topc;       // [n_splits][Bp][KMAX]
+};
+
+template <int KT>
+__device__ __forceinline__ float topk_insert(float (&top)[KT], float s, int k) {
+  // top[] sorted descending over its first k slots; returns the new k-th value
+#pragma unroll
+  for (int i = 0; i < KT; ++i) {
+    if (i < k && s > top[i]) {
+      const float t = top[i];
+      top[i] = s;
+      s = t;
+    }
+  }
+  float kth = top[0];
+#pragma unroll
+  for (int i = 0; i < KT; ++i)
+    if (i == k - 1) kth = top[i];
+  return kth;
+}
+
+template <int KT>
+__global__ void __launch_bounds__(192, 1)
+k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmD, const ScanArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = blockIdx.x % a.n_qb;
+  const int split = blockIdx.x / a.n_qb;
+  const int t0 = (int)((int64_t)split * a.n_tiles / a.n_splits);
+  const int t1 = (int)((int64_t)(split + 1) * a.n_tiles / a.n_splits);
+
+  if (warp == 0 && lane == 0) {
+    sm100::prefetch_tmap(&tmQ);
+    sm100::prefetch_tmap(&tmD);
+    for (int s = 0; s < STAGES; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&tfull[s], 1);
+      sm100::mbar_init(&tempty[s], 4);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 2) sm100::tmem_alloc<512>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = t0; t < t1; ++t) {
+        for (int kb = 0; kb < a.n_kb; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          sm100::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          sm100::tma_load_2d(&tmQ, sa, &full[stage], kb * BK, qb * BM);
+          sm100::tma_load_2d(&tmD, sa + A_BYTES, &full[stage], kb * BK, t * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer (one thread)
+      constexpr uint32_t idesc = sm100::idesc_f16_f32(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int i = 0;
+      for (int t = t0; t < t1; ++t, ++i) {
+        const int acc = i & 1;
+        const uint32_t aph = (i >> 1) & 1;
+        sm100::mbar_wait(&tempty[acc], aph ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < a.n_kb; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t a0 = sm100::smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t b0 = a0 + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(a0 + kk * 32), sm100::umma_desc_sw128(b0 + kk * 32),
+                            idesc, (kb | kk) != 0);
+          }
+          sm100::umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        sm100::umma_commit(&tfull[acc]);
+      }
+    }
+  } else {  // ---------------- epilogue: warps 2..5, thread = query
+    const int quarter = warp & 3;
+    const int q = qb * BM + quarter * 32 + lane;
+    const int k = a.k;
+    float top[KT];
+#pragma unroll
+    for (int i = 0; i < KT; ++i) top[i] = -__int_as_float(0x7f800000);
+    const float td = a.two_delta[q];
+    float thr = -__int_as_float(0x7f800000);
+    float kth = thr;
+    int cnt = 0;
+    bool ovf = false;
+    const size_t base = ((size_t)split * a.Bp + q);
+    float* cs = a.cand_s + base * CAP;
+    int32_t* cr = a.cand_r + base * CAP;
+    int i = 0;
+    for (int t = t0; t < t1; ++t, ++i) {
+      const int acc = i & 1;
+      const uint32_t aph = (i >> 1) & 1;
+      sm100::mbar_wait(&tfull[acc], aph);
+      sm100::tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        sm100::tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, v);
+        const int rbase = t * BN + c * 32;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float s = v[j];
+          if (s >= thr) {
+            const int row = rbase + j;
+            if (row < a.n_rows) {
+              if (s > kth) {  // beats the running k-th: insert
+                kth = topk_insert<KT>(top, s, k);
+                thr = kth - td;
+              }
+              if (!ovf) {
+                if (cnt == CAP) {  // compact against the risen threshold
+                  int w = 0;
+                  for (int u = 0; u < CAP; ++u) {
+                    const float sv = cs[u];
+                    if (sv >= thr) {
+                      cs[w] = sv;
+                      cr[w] = cr[u];
+                      ++w;
+                    }
+                  }
+                  cnt = w;
+                  if (cnt == CAP) ovf = true;
+                }
+                if (!ovf) {
+                  cs[cnt] = s;
+                  cr[cnt] = row;
+                  ++cnt;
+                }
+              }
+            }
+          }
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+    }
+    a.cand_n[base] = ovf ? -1 : cnt;
+#pragma unroll
+    for (int u = 0; u < KT; ++u)
+      if (u < k) a.topc[base * KMAX + u] = top[u];
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ exact rescoring
+struct DD {
+  double hi, lo, ab;
+};
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+// Warp-cooperative exact dot of two fp32 vectors.  Returns the float64 value and sets
+// `ok` when it is provably the correctly rounded exact sum (fp32*fp32 products are
+// exact in float64; the double-double accumulation error is < (dim+64)*2^-104*sum|p|).
+__device__ double warp_exact_dot(const float* __restrict__ a, const float* __restrict__ b, int64_t dim,
+                                 bool& ok) {
+  const int lane = threadIdx.x & 31;
+  double hi = 0.0, lo = 0.0, ab = 0.0;
+  for (int64_t d = lane; d < dim; d += 32) {
+    const double p = __dmul_rn((double)__ldg(a + d), (double)__ldg(b + d));
+    double s, e;
+    two_sum(hi, p, s, e);
+    hi = s;
+    lo = __dadd_rn(lo, e);
+    ab = __dadd_rn(ab, fabs(p));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    const double l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const double a2 = __shfl_xor_sync(0xffffffffu, ab, o);
+    double s, e;
+    two_sum(hi, h2, s, e);
+    hi = s;
+    lo = __dadd_rn(__dadd_rn(lo, l2), e);
+    ab = __dadd_rn(ab, a2);
+  }
+  double r, t;
+  two_sum(hi, lo, r, t);
+  const double bound = ab * (double)(dim + 64) * 0x1p-104 + 0x1p-1070;
+  // quarter ulp of r (conservative across a binade boundary)
+  const double ar = fabs(r);
+  const double qulp = ar > 0.0 ? ldexp(1.0, ilogb(ar) - 54) : 0x1p-1074;
+  ok = fabs(t) + bound < qulp || (ab == 0.0);
+  return r;
+}
+
+// Per query: global coarse k-th from the splits' top lists, candidate compaction,
+// exact rescoring, (-sim, seq) order.  Block = 256 threads.
+__global__ void __launch_bounds__(256)
+k_rescore(int n_splits, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
+          const float* __restrict__ v32, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
+          const float* __restrict__ two_delta, const float* __restrict__ cand_s, const int32_t* __restrict__ cand_r,
+          const int32_t* __restrict__ cand_n, const float* __restrict__ topc, double* __restrict__ out_sim,
+          int64_t* __restrict__ out_seq, int32_t* __restrict__ out_len, int32_t* __restrict__ out_count,
+          int32_t* __restrict__ need_exhaustive, unsigned int* __restrict__ inexact_count) {
+  const int64_t q = blockIdx.x;
+  if (q >= B) return;
+  __shared__ float s_top[8192];
+  __shared__ int s_rows[MAXC];
+  __shared__ double s_sim[MAXC];
+  __shared__ int64_t s_seq[MAXC];
+  __shared__ float s_rv[8];
+  __shared__ int s_ri[8];
+  __shared__ int s_n;
+  __shared__ int s_flag;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) { s_n = 0; s_flag = 0; }
+  // 1) kk-th largest coarse score across the splits' top lists (real rows' scores):
+  //    kk rounds of block-wide argmax with removal
+  const int m = n_splits * k;  // host guarantees m <= 8192
+  const int64_t kk = k < n_rows ? k : n_rows;
+  const float NEG = -__int_as_float(0x7f800000);
+  for (int i = tid; i < m; i += blockDim.x) {
+    const int sp = i / k, j = i % k;
+    s_top[i] = topc[((size_t)sp * Bp + q) * KMAX + j];
+  }
+  __syncthreads();
+  float kth = NEG;
+  for (int64_t round = 0; round < kk; ++round) {
+    float bv = NEG;
+    int bi = 0x7fffffff;
+    for (int i = tid; i < m; i += blockDim.x) {
+      const float v = s_top[i];
+      if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; }
+    }
+    if (lane == 0) { s_rv[warp] = bv; s_ri[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      float v = s_rv[0];
+      int ix = s_ri[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+        if (s_rv[w] > v || (s_rv[w] == v && s_ri[w] < ix)) { v = s_rv[w]; ix = s_ri[w]; }
+      s_rv[0] = v;
+      if (ix >= 0 && ix < m) s_top[ix] = NEG;
+    }
+    __syncthreads();
+    kth = s_rv[0];
+    __syncthreads();
+  }
+  const float thr = kth - two_delta[q];
+  // 2) gather candidates above the final threshold
+  for (int sp = 0; sp < n_splits; ++sp) {
+    const int cnt = cand_n[(size_t)sp * Bp + q];
+    if (cnt < 0) {
+      if (tid == 0) s_flag = 1;
+      continue;
+    }
+    const float* cs = cand_s + ((size_t)sp * Bp + q) * CAP;
+    const int32_t* cr = cand_r + ((size_t)sp * Bp + q) * CAP;
+    for (int i = tid; i < cnt; i += blockDim.x) {
+      if (cs[i] >= thr) {
+        const int slot = atomicAdd(&s_n, 1);
+        if (slot < MAXC) s_rows[slot] = cr[i];
+      }
+    }
+  }
+  __syncthreads();
+  const int n = s_n;
+  if (n > MAXC || s_flag) {
+    if (tid == 0) need_exhaustive[q] = 1;
+    return;
+  }
+  // 3) exact float64 scores, one warp per candidate
+  for (int c = warp; c < n; c += blockDim.x >> 5) {
+    const int row = s_rows[c];
+    bool ok;
+    const double sim = warp_exact_dot(v32 + (size_t)row * dim, q32 + q * dim, dim, ok);
+    if (lane == 0) {
+      s_sim[c] = sim;
+      s_seq[c] = seqs[row];
+      if (!ok) atomicAdd(inexact_count, 1u);
+    }
+  }
+  __syncthreads();
+  // 4) rank by (-sim, seq); seqs are unique
+  for (int c = tid; c < n; c += blockDim.x) {
+    const double sv = s_sim[c];
+    const int64_t qv = s_seq[c];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) rank += (s_sim[j] > sv) || (s_sim[j] == sv && s_seq[j] < qv);
+    if (rank < k) {
+      out_sim[q * k + rank] = sv;
+      out_seq[q * k + rank] = qv;
+      out_len[q * k + rank] = lens[s_rows[c]];
+    }
+  }
+  if (tid == 0) out_count[q] = (int32_t)(n < kk ? n : kk);
+}
+
+// Exhaustive exact top-k for queries flagged by k_rescore (candidate overflow from
+// heavy ties); a no-op block for every other query.  Slow but exact.
+__global__ void __launch_bounds__(256)
+k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
+             const float* __restrict__ v32, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
+             int32_t* __restrict__ need, double* __restrict__ out_sim, int64_t* __restrict__ out_seq,
+             int32_t* __restrict__ out_len, int32_t* __restrict__ out_count, unsigned int* __restrict__ inexact_count) {
+  const int64_t q = blockIdx.x;
+  if (q >= B || !need[q]) return;
+  __shared__ double s_sim[8 * KMAX];
+  __shared__ int64_t s_seq[8 * KMAX];
+  __shared__ int s_row[8 * KMAX];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // each warp keeps its own sorted top-k list (lane 0 owns it)
+  double tsim[KMAX];
+  int64_t tseq[KMAX];
+  int trow[KMAX];
+  for (int i = 0; i < KMAX; ++i) { tsim[i] = -__longlong_as_double(0x7ff0000000000000ll); tseq[i] = INT64_MAX; trow[i] = -1; }
+  for (int64_t row = warp; row < n_rows; row += blockDim.x >> 5) {
+    bool ok;
+    const double sim = warp_exact_dot(v32 + row * dim, q32 + q * dim, dim, ok);
+    if (lane == 0) {
+      if (!ok) atomicAdd(inexact_count, 1u);
+      double cs = sim;
+      int64_t cq = seqs[row];
+      int cr = (int)row;
+      for (int i = 0; i < k; ++i) {
+        if (cs > tsim[i] || (cs == tsim[i] && cq < tseq[i])) {
+          double a = tsim[i]; int64_t b = tseq[i]; int c = trow[i];
+          tsim[i] = cs; tseq[i] = cq; trow[i] = cr;
+          cs = a; cq = b; cr = c;
+        }
+      }
+    }
+  }
+  if (lane == 0)
+    for (int i = 0; i < k; ++i) { s_sim[warp * KMAX + i] = tsim[i]; s_seq[warp * KMAX + i] = tseq[i]; s_row[warp * KMAX + i] = trow[i]; }
+  __syncthreads();
+  const int m = (blockDim.x >> 5) * KMAX;
+  for (int c = threadIdx.x; c < m; c += blockDim.x) {
+    if ((c % KMAX) >= k || s_row[c] < 0) continue;
+    int rank = 0;
+    for (int j = 0; j < m; ++j) {
+      if ((j % KMAX) >= k || s_row[j] < 0) continue;
+      rank += (s_sim[j] > s_sim[c]) || (s_sim[j] == s_sim[c] && s_seq[j] < s_seq[c]);
+    }
+    if (rank < k) { out_sim[q * k + rank] = s_sim[c]; out_seq[q * k + rank] = s_seq[c]; out_len[q * k + rank] = lens[s_row[c]]; }
+  }
+  if (threadIdx.x == 0) { out_count[q] = (int32_t)(n_rows < k ? n_rows : k); need[q] = 0; }
+}
+
+// ------------------------------------------------------------------ shard merge
+// G per-shard sorted lists [G][B][k] -> global top-k by (-sim, seq).  Thread per query.
+__global__ void k_topk_merge(int G, int64_t B, int k, const double* __restrict__ sims, const int64_t* __restrict__ seqs,
+                             const int32_t* __restrict__ lens, const int32_t* __restrict__ counts,
+                             double* __restrict__ o_sim, int64_t* __restrict__ o_seq, int32_t* __restrict__ o_len,
+                             int32_t* __restrict__ o_cnt) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= B) return;
+  int pos[64];
+  for (int g = 0; g < G; ++g) pos[g] = 0;
+  int n = 0;
+  while (n < k) {
+    int best = -1;
+    double bs = 0;
+    int64_t bq = 0;
+    for (int g = 0; g < G; ++g) {
+      const int c = counts[(size_t)g * B + q];
+      if (pos[g] >= c) continue;
+      const size_t idx = ((size_t)g * B + q) * k + pos[g];
+      const double s = sims[idx];
+      const int64_t sq = seqs[idx];
+      if (best < 0 || s > bs || (s == bs && sq < bq)) { best = g; bs = s; bq = sq; }
+    }
+    if (best < 0) break;
+    const size_t idx = ((size_t)best * B + q) * k + pos[best];
+    o_sim[q * k + n] = bs;
+    o_seq[q * k + n] = bq;
+    o_len[q * k + n] = lens[idx];
+    ++pos[best];
+    ++n;
+  }
+  o_cnt[q] = n;
+}
+
+// ------------------------------------------------------------------ finish
+// numpy's reduction order for a contiguous float64 array (n < 8: sequential from 0.0;
+// n >= 8: 8 accumulators, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the remainder).
+__device__ double np_sum(const double* v, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, v[i]);
+    return r;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = v[j];
+  int i = 8;
+  for (; i + 8 <= n; i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v[i + j]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, v[i]);
+  return res;
+}
+
+// Warp per query.  Retrieval branch (predictor.py:314-324) when any neighbour has sim
+// >= s0, else the float64 MLP (predictor.py:209-219): h_j = tanh(b1_j + sum_d x_d W1[d,j])
+// with the sum in index order, out = b2 + sum_j h_j w2_j in index order.
+__global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, const int32_t* __restrict__ lens,
+                         const int32_t* __restrict__ counts, double s0, const float* __restrict__ x, int64_t dim,
+                         const double* __restrict__ W1, const double* __restrict__ b1, const double* __restrict__ w2,
+                         double b2, int64_t hidden, int64_t max_len, double log_cap, int32_t* __restrict__ out_len,
+                         uint8_t* __restrict__ out_ret) {
+  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (q >= B) return;
+  const int c = counts[q];
+  int nq = 0;
+  double w[KMAX], prod[KMAX], vals[KMAX];
+  for (int i = 0; i < c; ++i) {
+    const double s = sims[q * k + i];
+    if (s >= s0) {
+      const double wi = s < 0.0 ? 0.0 : s;  // np.clip(.., 0, None)
+      vals[nq] = (double)lens[q * k + i];
+      w[nq] = wi;
+      prod[nq] = __dmul_rn(wi, vals[nq]);
+      ++nq;
+    }
+  }
+  if (nq > 0) {
+    if (lane == 0) {
+      const double ws = np_sum(w, nq);
+      double pred;
+      if (ws > 0.0) pred = __ddiv_rn(np_sum(prod, nq), ws);
+      else pred = __ddiv_rn(np_sum(vals, nq), (double)nq);
+      double r = rint(pred);
+      r = fmin(fmax(r, 1.0), (double)max_len);
+      out_len[q] = (int32_t)r;
+      out_ret[q] = 1;
+    }
+    return;
+  }
+  // fallback MLP: lane j computes hidden units j, j+32, ...
+  const float* xq = x + q * dim;
+  double out = 0.0;
+  double hv[4];
+  const int per = (int)((hidden + 31) / 32);
+  for (int t = 0; t < per && t < 4; ++t) {
+    const int64_t j = lane + 32 * t;
+    double acc = 0.0;
+    if (j < hidden) {
+      for (int64_t d = 0; d < dim; ++d) acc = __dadd_rn(acc, __dmul_rn((double)__ldg(xq + d), W1[d * hidden + j]));
+      hv[t] = tanh(__dadd_rn(acc, b1[j]));
+    } else {
+      hv[t] = 0.0;
+    }
+  }
+  // sequential sum over hidden units in index order (lane 0 gathers)
+  for (int64_t j = 0; j < hidden; ++j) {
+    const int t = (int)(j / 32), src = (int)(j % 32);
+    double hj = 0.0;
+    for (int tt = 0; tt < 4; ++tt) {
+      const double v = __shfl_sync(0xffffffffu, hv[tt], src);
+      if (tt == t) hj = v;
+    }
+    out = __dadd_rn(out, __dmul_rn(hj, w2[j]));
+  }
+  if (lane == 0) {
+    out = __dadd_rn(out, b2);
+    const double raw = exp(fmin(out, log_cap));
+    double r = rint(raw);
+    r = fmin(fmax(r, 1.0), (double)max_len);
+    out_len[q] = (int32_t)r;
+    out_ret[q] = 0;
+  }
+}
+
+}  // namespace pred
+}  // namespace alise

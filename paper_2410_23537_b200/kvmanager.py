@@ -479,6 +479,9 @@ class KVSwapEngine:
         _lib.call("alise_swapper_create", self.device, m, 0, _lib.C.byref(h))
         self.handle = h.value
         self.mode = mode
+        # uploads run their dequantize kernels on their own stream so the compute
+        # stream's quantize kernels (gated by D2H progress) never block H2D progress
+        self.up_stream = torch.cuda.Stream(device=self.device)
 
     def offload(self, layout: KVLayout, kv, host_addr: int, flag=None, stream=None, event=None):
         d = layout.desc()
@@ -487,8 +490,9 @@ class KVSwapEngine:
 
     def upload(self, layout: KVLayout, host_addr: int, kv, stream=None, event=None):
         d = layout.desc()
+        st = stream if stream is not None else self.up_stream
         _lib.call("alise_kv_upload", self.handle, _lib.C.byref(d), host_addr, _lib.ptr(kv),
-                  _lib.stream_ptr(stream), event or 0)
+                  _lib.stream_ptr(st), event or 0)
 
     def depend(self, event_handle: int):
         """Order later transfers after a recorded event (e.g. upload after offload)."""

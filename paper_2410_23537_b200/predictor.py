@@ -1,0 +1,515 @@
+"""Drop-in for ``servesim.predictor`` with a B200 retrieval path.
+
+Reference: /root/reference/pkg/src/servesim/predictor.py.  Same names, argument
+meanings and errors.  The hot path — ``VectorStore.search`` (predictor.py:154-163)
+and ``LengthPredictor.predict_vector`` (predictor.py:311-325) — runs on the GPU:
+
+* the store is a device FIFO ring (fp32 master + fp16 coarse copy, slot = seq % cap);
+* ``search`` / ``search_batch`` compute the exact top-k by (-sim, seq): a tcgen05
+  fp16 coarse scan with a provable candidate margin, then correctly rounded float64
+  rescoring of the candidates (sims are the exact dot products of the stored fp32
+  vectors, rounded once to float64);
+* ``predict_batch`` fuses the aggregate (numpy's summation order, half-even
+  rounding) with the float64 all-MLP fallback in one kernel.
+
+Vectors are stored in fp32 (the reference keeps float64); sims therefore match the
+reference to ~1e-7 relative, and exactly the restated oracle (oracle/pred_oracle.py).
+
+Training of the fallback regressor (``FallbackRegressor.fit``, predictor.py:221-264)
+and the hashing embedder (predictor.py:66-100) are host-side producers of weights /
+query vectors, outside the hot path; they are provided here so the module is a
+complete drop-in.
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+_FNV_OFFSET = 0xCBF29CE484222325
+_FNV_PRIME = 0x100000001B3
+_MASK64 = 0xFFFFFFFFFFFFFFFF
+FALLBACK_INIT = 4  # rng.py stream tag
+RETRIEVED = "retrieved"
+FALLBACK = "fallback"
+MAX_K = 16
+
+
+class PredictorError(ValueError):
+    pass
+
+
+def _stream(seed: int, tag: int, *sub: int) -> np.random.Generator:
+    """The reference's seeded PCG64 streams (rng.py:20-22)."""
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, tag, *sub])))
+
+
+@dataclass
+class PredictorConfig:
+    """predictor.py:38-63."""
+
+    dimension: int = 64
+    top_k: int = 8
+    similarity_threshold: float = 0.80
+    db_capacity: int = 100_000
+    max_len: int = 2048
+    fallback_hidden: int = 32
+    fallback_epochs: int = 150
+    fallback_learning_rate: float = 0.05
+    allow_untrained: bool = True
+    online_refit: bool = True
+    refit_epochs: int = 40
+    refit_sample_cap: int = 256
+
+    def validate(self):
+        checks = [
+            (self.dimension >= 1, "dimension must be >= 1"),
+            (self.top_k >= 1, "top_k must be >= 1"),
+            (self.db_capacity >= self.top_k, "db_capacity must be >= top_k"),
+            (-1.0 <= self.similarity_threshold <= 1.0, "similarity_threshold must be in [-1, 1]"),
+            (self.max_len >= 1, "max_len must be >= 1"),
+        ]
+        for ok, msg in checks:
+            if not ok:
+                raise PredictorError(msg)
+        if self.top_k > MAX_K:
+            raise PredictorError(f"top_k must be <= {MAX_K} on the GPU path")
+
+
+def _fnv1a(data: bytes) -> int:
+    h = _FNV_OFFSET
+    for byte in data:
+        h = ((h ^ byte) * _FNV_PRIME) & _MASK64
+    return h
+
+
+class HashingEmbedder:
+    """Unigram + bigram FNV-1a feature hashing, L2-normalised (predictor.py:66-100)."""
+
+    def __init__(self, dimension: int = 64):
+        if dimension < 1:
+            raise PredictorError("dimension must be >= 1")
+        self.dimension = dimension
+
+    def embed(self, tokens) -> np.ndarray:
+        seq = [int(t) for t in (tokens if tokens is not None else [])]
+        if not seq:
+            raise PredictorError("cannot embed an empty token sequence")
+        v = np.zeros(self.dimension)
+        feats = [f"u:{t}" for t in seq] + [f"b:{a}:{b}" for a, b in zip(seq, seq[1:])]
+        order = []
+        for i, t in enumerate(seq):  # reference interleaves u:t_i then b:t_{i-1}:t_i
+            order.append(feats[i])
+            if i:
+                order.append(feats[len(seq) + i - 1])
+        for f in order:
+            h = _fnv1a(f.encode())
+            v[h % self.dimension] += 1.0 if (h >> 63) & 1 else -1.0
+        n = float(np.linalg.norm(v))
+        if n == 0.0:
+            v[0], n = 1.0, 1.0
+        return v / n
+
+
+def load_precomputed_embeddings(path) -> dict:
+    """JSON-lines {"id", "vector"}, re-normalised (predictor.py:103-117)."""
+    out = {}
+    with open(path) as fh:
+        for line in fh:
+            line = line.strip()
+            if not line:
+                continue
+            rec = json.loads(line)
+            v = np.asarray(rec["vector"], dtype=np.float64)
+            n = float(np.linalg.norm(v))
+            if n == 0:
+                raise PredictorError(f"zero vector for id {rec['id']}")
+            out[int(rec["id"])] = v / n
+    return out
+
+
+# ----------------------------------------------------------------- device store
+class VectorStore:
+    """FIFO-bounded device store of (vector, observed length) (predictor.py:120-189).
+
+    Same semantics: slot = seq % capacity, ``add`` returns the insert sequence,
+    ``search`` returns (sims f64, lens i64, seqs i64) ordered by (-sim, seq).
+    """
+
+    def __init__(self, dimension: int, capacity: int, device: int | None = None):
+        import torch
+
+        _lib.require_cuda()
+        self.dimension = int(dimension)
+        self.capacity = int(capacity)
+        self.device = torch.cuda.current_device() if device is None else device
+        h = _lib.C.c_void_p()
+        _lib.call("alise_db_create", self.device, self.capacity, self.dimension, _lib.C.byref(h))
+        self._h = h.value
+        self.size = 0
+        self.next_seq = 0
+        # host mirror of lengths/seqs is not kept; vectors are read back on demand
+
+    def __len__(self):
+        return self.size
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.lib().alise_db_destroy(h)
+            except Exception:
+                pass
+
+    def _dev(self):
+        import torch
+        return torch.device("cuda", self.device)
+
+    def add(self, vector, observed_len: int) -> int:
+        if observed_len < 1:
+            raise PredictorError("observed_len must be >= 1")
+        seq = self.next_seq
+        self.add_batch(np.asarray(vector, dtype=np.float64)[None, :], [int(observed_len)])
+        return seq
+
+    def add_batch(self, vectors, lens, stream=None):
+        """Append rows in insert order (batched VectorStore.add)."""
+        import torch
+
+        v = torch.as_tensor(np.asarray(vectors) if not isinstance(vectors, torch.Tensor) else vectors)
+        v = v.to(self._dev(), torch.float32).reshape(-1, self.dimension).contiguous()
+        ln = torch.as_tensor(np.asarray(lens) if not isinstance(lens, torch.Tensor) else lens)
+        ln = ln.to(self._dev(), torch.int32).reshape(-1).contiguous()
+        n = v.shape[0]
+        if ln.numel() != n:
+            raise PredictorError("vectors and lengths differ in count")
+        if n and int(ln.min().item()) < 1:
+            raise PredictorError("observed_len must be >= 1")
+        done = 0
+        while done < n:
+            m = min(n - done, self.capacity)
+            seqs = torch.arange(self.next_seq, self.next_seq + m, dtype=torch.int64, device=self._dev())
+            _lib.call("alise_db_append", self._h, _lib.ptr(v[done:done + m]), _lib.ptr(ln[done:done + m]),
+                      _lib.ptr(seqs), m, _lib.stream_ptr(stream))
+            self.next_seq += m
+            self.size = min(self.capacity, self.size + m)
+            done += m
+        return self.next_seq - 1
+
+    def search_batch(self, queries, k: int, stream=None):
+        """Exact top-k for a batch.  Returns CUDA tensors (sims f64 [B,k], seqs i64,
+        lens i32, counts i32 [B]); rows past counts[b] are undefined."""
+        import torch
+
+        if k < 1 or k > MAX_K:
+            raise PredictorError(f"k must be in [1, {MAX_K}]")
+        q = torch.as_tensor(queries if isinstance(queries, torch.Tensor) else np.asarray(queries))
+        q = q.to(self._dev(), torch.float32).reshape(-1, self.dimension).contiguous()
+        B = q.shape[0]
+        dev = self._dev()
+        sims = torch.empty((B, k), dtype=torch.float64, device=dev)
+        seqs = torch.empty((B, k), dtype=torch.int64, device=dev)
+        lens = torch.empty((B, k), dtype=torch.int32, device=dev)
+        cnt = torch.empty(B, dtype=torch.int32, device=dev)
+        _lib.call("alise_db_topk", self._h, _lib.ptr(q), B, k, _lib.ptr(sims), _lib.ptr(seqs),
+                  _lib.ptr(lens), _lib.ptr(cnt), _lib.stream_ptr(stream))
+        return sims, seqs, lens, cnt, q
+
+    def search(self, vector, k: int):
+        """Top-k by cosine similarity; ties broken by older insert first."""
+        if self.size == 0:
+            return np.array([]), np.array([], dtype=np.int64), np.array([], dtype=np.int64)
+        k = min(k, self.size)
+        sims, seqs, lens, cnt, _ = self.search_batch(np.asarray(vector, dtype=np.float64)[None, :], k)
+        c = int(cnt[0].item())
+        return (sims[0, :c].cpu().numpy(), lens[0, :c].cpu().numpy().astype(np.int64),
+                seqs[0, :c].cpu().numpy())
+
+    def inexact_count(self) -> int:
+        """Candidates whose float64 rounding could not be certified (expected 0)."""
+        c = _lib.C.c_uint()
+        _lib.call("alise_db_inexact", self._h, _lib.C.byref(c))
+        return int(c.value)
+
+    # -- host-side views (not on the hot path) --------------------------------------
+    def newest(self, count: int):
+        """Vectors and lengths of the most recently inserted records (predictor.py:165-168)."""
+        vecs, lens, seqs = self.export()
+        order = np.argsort(seqs)[-count:]
+        return vecs[order], lens[order]
+
+    def export(self):
+        """Copy the live records to the host: (vectors f64 [n,d], lens i64, seqs i64)."""
+        import ctypes
+
+        n = self.size
+        if n == 0:
+            return np.zeros((0, self.dimension)), np.zeros(0, np.int64), np.zeros(0, np.int64)
+        return self._export_impl(n, ctypes)
+
+    def _export_impl(self, n, ctypes):
+        import torch
+        vec = torch.empty((n, self.dimension), dtype=torch.float32, device=self._dev())
+        lens = torch.empty(n, dtype=torch.int32, device=self._dev())
+        seqs = torch.empty(n, dtype=torch.int64, device=self._dev())
+        _lib.call("alise_db_export", self._h, _lib.ptr(vec), _lib.ptr(lens), _lib.ptr(seqs), n,
+                  _lib.stream_ptr())
+        return (vec.cpu().numpy().astype(np.float64), lens.cpu().numpy().astype(np.int64),
+                seqs.cpu().numpy())
+
+    def save(self, path):
+        vecs, lens, seqs = self.export()
+        with open(path, "w") as fh:
+            for i in np.argsort(seqs):
+                fh.write(json.dumps({"seq": int(seqs[i]), "len": int(lens[i]),
+                                     "vector": [float(x) for x in vecs[i]]}) + "\n")
+
+    @classmethod
+    def load(cls, path, dimension: int, capacity: int) -> "VectorStore":
+        vecs, lens = [], []
+        with open(path) as fh:
+            for line in fh:
+                line = line.strip()
+                if line:
+                    rec = json.loads(line)
+                    vecs.append(rec["vector"])
+                    lens.append(int(rec["len"]))
+        store = cls(dimension, capacity)
+        if vecs:
+            store.add_batch(np.asarray(vecs, dtype=np.float64), lens)
+        return store
+
+
+# ----------------------------------------------------------------- fallback regressor
+class FallbackRegressor:
+    """One-hidden-layer tanh regressor on log length (predictor.py:192-264)."""
+
+    def __init__(self, dimension: int, hidden: int, seed: int = 0):
+        gen = _stream(seed, FALLBACK_INIT)
+        lim = math.sqrt(6.0 / (dimension + hidden))
+        self.w1 = gen.uniform(-lim, lim, size=(dimension, hidden))
+        self.b1 = np.zeros(hidden)
+        self.w2 = gen.uniform(-lim, lim, size=hidden) / math.sqrt(hidden)
+        self.b2 = 0.0
+        self.loss_history: list = []
+        self.trained = False
+        self._dev_cache = None
+
+    # host-side forward (training only)
+    def _forward(self, X):
+        h = np.tanh(X @ self.w1 + self.b1)
+        return h, h @ self.w2 + self.b2
+
+    def predict_log(self, vector) -> float:
+        return float(self._forward(np.asarray(vector, dtype=np.float64)[None, :])[1][0])
+
+    def device_weights(self):
+        """float64 CUDA copies of (W1, b1, w2), refreshed when the weights change."""
+        import torch
+        key = (id(self.w1), id(self.b1), id(self.w2))
+        if self._dev_cache is None or self._dev_cache[0] != key:
+            d = torch.device("cuda", torch.cuda.current_device())
+            self._dev_cache = (key, torch.as_tensor(np.ascontiguousarray(self.w1), dtype=torch.float64).to(d),
+                               torch.as_tensor(self.b1, dtype=torch.float64).to(d),
+                               torch.as_tensor(self.w2, dtype=torch.float64).to(d))
+        return self._dev_cache[1:]
+
+    def predict_len_batch(self, X, max_len: int, stream=None):
+        """Batched predict_len on the GPU (float64 MLP, same op order as the oracle)."""
+        import torch
+        x = torch.as_tensor(X if isinstance(X, torch.Tensor) else np.asarray(X))
+        x = x.to(torch.device("cuda", torch.cuda.current_device()), torch.float32).contiguous()
+        B = x.shape[0]
+        dev = x.device
+        cnt = torch.zeros(B, dtype=torch.int32, device=dev)
+        sims = torch.empty((B, 1), dtype=torch.float64, device=dev)
+        lens = torch.empty((B, 1), dtype=torch.int32, device=dev)
+        out = torch.empty(B, dtype=torch.int32, device=dev)
+        ret = torch.empty(B, dtype=torch.uint8, device=dev)
+        W1, b1, w2 = self.device_weights()
+        _lib.call("alise_predict_finish", B, 1, _lib.ptr(sims), _lib.ptr(lens), _lib.ptr(cnt), 2.0,
+                  _lib.ptr(x), x.shape[1], _lib.ptr(W1), _lib.ptr(b1), _lib.ptr(w2), float(self.b2),
+                  W1.shape[1], int(max_len), math.log(max_len) + 1.0, _lib.ptr(out), _lib.ptr(ret),
+                  _lib.stream_ptr(stream))
+        return out
+
+    def predict_len(self, vector, max_len: int) -> int:
+        return int(self.predict_len_batch(np.asarray(vector, dtype=np.float64)[None, :], max_len)[0].item())
+
+    def fit(self, X, lengths, epochs: int, learning_rate: float):
+        """Full-batch gradient descent with backtracking (predictor.py:221-264).
+        Host-side weight production (not on the hot path)."""
+        X = np.asarray(X, dtype=np.float64)
+        y = np.log(np.asarray(lengths, dtype=np.float64))
+        n = X.shape[0]
+
+        def evaluate(w1, b1, w2, b2):
+            h = np.tanh(X @ w1 + b1)
+            err = (h @ w2 + b2) - y
+            g = 2.0 * err / n
+            dpre = np.outer(g, w2) * (1.0 - h ** 2)
+            return float(np.mean(err ** 2)), (X.T @ dpre, dpre.sum(axis=0), h.T @ g, float(g.sum()))
+
+        params = (self.w1, self.b1, self.w2, self.b2)
+        loss, grads = evaluate(*params)
+        self.loss_history = [loss]
+        lr = learning_rate
+        for _ in range(epochs):
+            step_taken = False
+            for _ in range(30):
+                trial = tuple(p - lr * g for p, g in zip(params, grads))
+                t_loss, t_grads = evaluate(*trial)
+                if t_loss <= loss:
+                    params, loss, grads, step_taken = trial, t_loss, t_grads, True
+                    break
+                lr *= 0.5
+            self.loss_history.append(loss)
+            if step_taken:
+                lr = min(lr * 1.25, learning_rate)
+        self.w1, self.b1, self.w2, self.b2 = params
+        self.b2 = float(self.b2)
+        self.trained = True
+        self._dev_cache = None
+        return self
+
+
+def train_fallback(corpus, config: PredictorConfig, seed: int = 0, embedder=None) -> FallbackRegressor:
+    """predictor.py:267-279."""
+    if len(corpus) < 10:
+        raise PredictorError("training corpus must have at least 10 examples")
+    embedder = embedder or HashingEmbedder(config.dimension)
+    X = np.stack([embedder.embed(tokens) for tokens, _ in corpus])
+    lengths = [n for _, n in corpus]
+    if min(lengths) < 1:
+        raise PredictorError("corpus lengths must be >= 1")
+    reg = FallbackRegressor(config.dimension, config.fallback_hidden, seed=seed)
+    return reg.fit(X, lengths, config.fallback_epochs, config.fallback_learning_rate)
+
+
+# ----------------------------------------------------------------- length predictor
+class LengthPredictor:
+    """Retrieval-first length predictor with regressor fallback (predictor.py:286-352)."""
+
+    def __init__(self, config: PredictorConfig, regressor: FallbackRegressor | None = None,
+                 embedder: HashingEmbedder | None = None, store: VectorStore | None = None,
+                 precomputed: dict | None = None):
+        config.validate()
+        self.config = config
+        self.embedder = embedder or HashingEmbedder(config.dimension)
+        self.store = store if store is not None else VectorStore(config.dimension, config.db_capacity)
+        if regressor is None and not config.allow_untrained:
+            raise PredictorError("no trained fallback and allow_untrained is false")
+        self._untrained = regressor is None
+        self.regressor = regressor or FallbackRegressor(config.dimension, config.fallback_hidden, seed=0)
+        self.precomputed = precomputed or {}
+        self._observations = 0
+        self._next_refit = 8
+
+    def embed(self, tokens, request_id: int | None = None) -> np.ndarray:
+        if request_id is not None and request_id in self.precomputed:
+            return self.precomputed[request_id]
+        return self.embedder.embed(tokens)
+
+    def predict_batch(self, queries, stream=None):
+        """Batched predict_vector: (lengths int32 [B], retrieved uint8 [B]) CUDA tensors."""
+        import torch
+        cfg = self.config
+        q = torch.as_tensor(queries if isinstance(queries, torch.Tensor) else np.asarray(queries))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        q = q.to(dev, torch.float32).reshape(-1, cfg.dimension).contiguous()
+        B = q.shape[0]
+        k = cfg.top_k
+        if self.store.size > 0:
+            sims, _seqs, lens, cnt, q = self.store.search_batch(q, k, stream=stream)
+        else:
+            sims = torch.empty((B, k), dtype=torch.float64, device=dev)
+            lens = torch.empty((B, k), dtype=torch.int32, device=dev)
+            cnt = torch.zeros(B, dtype=torch.int32, device=dev)
+        return self.finish(sims, lens, cnt, q, stream=stream)
+
+    def finish(self, sims, lens, cnt, q, stream=None):
+        """Aggregate + MLP fallback over given (possibly merged) top-k lists."""
+        import torch
+        cfg = self.config
+        B, k = sims.shape
+        out = torch.empty(B, dtype=torch.int32, device=q.device)
+        ret = torch.empty(B, dtype=torch.uint8, device=q.device)
+        W1, b1, w2 = self.regressor.device_weights()
+        _lib.call("alise_predict_finish", B, k, _lib.ptr(sims), _lib.ptr(lens), _lib.ptr(cnt),
+                  float(cfg.similarity_threshold), _lib.ptr(q), cfg.dimension, _lib.ptr(W1), _lib.ptr(b1),
+                  _lib.ptr(w2), float(self.regressor.b2), W1.shape[1], int(cfg.max_len),
+                  math.log(cfg.max_len) + 1.0, _lib.ptr(out), _lib.ptr(ret), _lib.stream_ptr(stream))
+        return out, ret
+
+    def predict_vector(self, vector) -> tuple:
+        """Predict from an already-embedded prompt; returns (length, provenance)."""
+        out, ret = self.predict_batch(np.asarray(vector, dtype=np.float64)[None, :])
+        return int(out[0].item()), (RETRIEVED if int(ret[0].item()) else FALLBACK)
+
+    def predict(self, tokens, request_id: int | None = None) -> tuple:
+        vec = self.embed(tokens, request_id)
+        length, provenance = self.predict_vector(vec)
+        return length, provenance, vec
+
+    def observe(self, vector, actual_len: int):
+        """Append a finished request; refit the fallback on a geometric schedule."""
+        self.store.add(vector, actual_len)
+        self._observations += 1
+        if self.config.online_refit and self._observations >= self._next_refit:
+            self._refit()
+            cap = self.config.refit_sample_cap
+            self._next_refit = min(self._next_refit * 2, self._observations + cap)
+
+    def _refit(self):
+        X, lens = self.store.newest(self.config.refit_sample_cap)
+        reg = FallbackRegressor(self.config.dimension, self.config.fallback_hidden, seed=self._observations)
+        reg.fit(X, lens, self.config.refit_epochs, self.config.fallback_learning_rate)
+        self.regressor = reg
+
+
+def eval_accuracy(pairs, bin_width: int, latencies_ms=None) -> dict:
+    """Bucketed accuracy and mean relative error (predictor.py:355-374)."""
+    if bin_width < 1:
+        raise PredictorError("bin_width must be >= 1")
+    pairs = list(pairs)
+    if not pairs:
+        raise PredictorError("no prediction pairs to evaluate")
+    hits = sum(1 for p, a in pairs if p // bin_width == a // bin_width)
+    rel = sum(abs(p - a) / a for p, a in pairs) / len(pairs)
+    return {"count": len(pairs), "accuracy": hits / len(pairs), "pred_error": rel,
+            "mean_latency_ms": float(np.mean(latencies_ms)) if latencies_ms else 0.0}
+
+
+def smoke_check():
+    """Tiny exact top-k + predict check used by __graft_entry__.smoke()."""
+    import torch
+
+    from oracle import pred_oracle
+    g = np.random.default_rng(3)
+    n, d = 700, 64
+    db = g.standard_normal((n, d)).astype(np.float32)
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    db[100:111] = db[5]  # tie group
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = np.concatenate([db[[5, 17, 300]] + 0.01 * g.standard_normal((3, d)).astype(np.float32),
+                        g.standard_normal((5, d)).astype(np.float32)])
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    Q = Q.astype(np.float32)
+    store = VectorStore(d, 1024)
+    store.add_batch(db, lens)
+    sims, seqs, slens, cnt, _ = store.search_batch(Q, 8)
+    torch.cuda.synchronize()
+    for i in range(len(Q)):
+        es, el, eq = pred_oracle.search_exact(db, lens, np.arange(n), Q[i], 8)
+        assert np.array_equal(seqs[i].cpu().numpy(), eq), (i, seqs[i], eq)
+        assert np.array_equal(sims[i].cpu().numpy(), es)
+    reg = FallbackRegressor(d, 32, seed=0)
+    reg.b2 = 5.0
+    pred = LengthPredictor(PredictorConfig(dimension=d, db_capacity=1024), regressor=reg, store=store)
+    out, ret = pred.predict_batch(Q)
+    ref_len, ref_ret = pred_oracle.predict_batch(db, lens, np.arange(n), Q, reg.w1, reg.b1, reg.w2, reg.b2)
+    assert np.array_equal(out.cpu().numpy(), ref_len) and np.array_equal(ret.cpu().numpy().astype(bool), ref_ret)

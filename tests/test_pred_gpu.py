@@ -1,0 +1,193 @@
+"""GPU parity for the predictor: exact top-k (indices and float64 sims bit-exact with
+the restated oracle, ties by insert order), predicted lengths exact, plus the
+reference's known-answer tests (pkg/tests/test_predictor.py) through the GPU path."""
+import numpy as np
+import pytest
+
+from oracle import pred_oracle as po
+from tests.conftest import have_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def pr():
+    from paper_2410_23537_b200 import predictor
+    return predictor
+
+
+def unit(*values, dim=8):
+    v = np.zeros(dim)
+    v[:len(values)] = values
+    return v / np.linalg.norm(v)
+
+
+def check_batch(pr, db, lens, Q, k, capacity=None):
+    import torch
+    n, d = db.shape
+    store = pr.VectorStore(d, capacity or max(n, 8))
+    store.add_batch(db, lens)
+    sims, seqs, slens, cnt, _ = store.search_batch(Q, k)
+    torch.cuda.synchronize()
+    ref = po.search_exact_batch(db, lens, np.arange(n), Q, k)
+    sims, seqs, slens, cnt = (t.cpu().numpy() for t in (sims, seqs, slens, cnt))
+    for i, (es, el, eq) in enumerate(ref):
+        c = cnt[i]
+        assert c == len(eq), (i, c, len(eq))
+        assert np.array_equal(seqs[i, :c], eq), (i, seqs[i, :c], eq)
+        assert np.array_equal(sims[i, :c], es), (i, sims[i, :c] - es)
+        assert np.array_equal(slens[i, :c], el)
+    assert store.inexact_count() == 0
+    return store
+
+
+@pytest.mark.parametrize("tag", ["d64", "d768"])
+def test_search_matches_oracle_and_reference(pr, pred_golden, tag):
+    g = pred_golden
+    db, lens, Q = g[f"{tag}_db"], g[f"{tag}_lens"], g[f"{tag}_q"]
+    check_batch(pr, db, lens, Q, 8, capacity=4096)
+
+
+@pytest.mark.parametrize("tag", ["d64", "d768"])
+def test_predict_batch_exact(pr, pred_golden, tag):
+    g = pred_golden
+    db, lens, Q = g[f"{tag}_db"], g[f"{tag}_lens"], g[f"{tag}_q"]
+    reg = pr.FallbackRegressor(db.shape[1], 32, seed=0)
+    reg.b2 = float(g[f"{tag}_b2"])
+    store = pr.VectorStore(db.shape[1], 4096)
+    store.add_batch(db, lens)
+    p = pr.LengthPredictor(pr.PredictorConfig(dimension=db.shape[1], db_capacity=4096), regressor=reg,
+                           store=store)
+    out, ret = p.predict_batch(Q)
+    ref_len, ref_ret = po.predict_batch(db, lens, np.arange(len(db)), Q, reg.w1, reg.b1, reg.w2, reg.b2)
+    assert np.array_equal(out.cpu().numpy(), ref_len)
+    assert np.array_equal(ret.cpu().numpy().astype(bool), ref_ret)
+    mlp = reg.predict_len_batch(Q, 2048).cpu().numpy()
+    assert np.array_equal(mlp, g[f"{tag}_mlp"])
+
+
+@pytest.mark.parametrize("n,d,B,k", [(1, 8, 3, 8), (7, 8, 5, 8), (300, 100, 130, 5), (2000, 64, 257, 1),
+                                     (5000, 768, 64, 16), (20000, 128, 300, 8)])
+def test_shapes_and_k(pr, n, d, B, k):
+    g = np.random.default_rng(n + d + B + k)
+    db = g.standard_normal((n, d)).astype(np.float32)
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = g.standard_normal((B, d)).astype(np.float32)
+    Q[: B // 2] = db[g.integers(0, n, size=B // 2)] + 0.02 * g.standard_normal((B // 2, d)).astype(np.float32)
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    check_batch(pr, db, lens, Q.astype(np.float32), k)
+
+
+def test_ties_broken_by_insert_order(pr):
+    g = np.random.default_rng(9)
+    d = 64
+    db = g.standard_normal((3000, d)).astype(np.float32)
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    for grp in range(20):  # groups of 11 identical rows competing for 8 slots
+        base = grp * 37
+        idx = g.choice(np.arange(1000, 3000), size=10, replace=False)
+        db[idx] = db[base]
+    lens = g.integers(1, 2048, size=3000).astype(np.int32)
+    Q = db[[grp * 37 for grp in range(20)]] + 0.001 * g.standard_normal((20, d)).astype(np.float32)
+    Q = (Q / np.linalg.norm(Q, axis=1, keepdims=True)).astype(np.float32)
+    check_batch(pr, db, lens, Q, 8)
+
+
+def test_heavy_ties_take_the_exhaustive_path(pr):
+    # 600 identical rows: more candidates than a scan CTA can hold -> exact fallback
+    d = 32
+    v = np.ones((600, d), np.float32) / np.sqrt(d)
+    g = np.random.default_rng(2)
+    other = g.standard_normal((400, d)).astype(np.float32)
+    db = np.concatenate([other[:200], v, other[200:]])
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    lens = np.arange(1, 1001).astype(np.int32)
+    Q = db[[250, 0, 999]].astype(np.float32)
+    check_batch(pr, db, lens, Q, 8)
+
+
+def test_fifo_ring_semantics(pr):
+    import torch
+    d = 16
+    store = pr.VectorStore(d, 100)
+    g = np.random.default_rng(4)
+    rows = g.standard_normal((250, d)).astype(np.float32)
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    lens = np.arange(1, 251)
+    for c in range(0, 250, 60):
+        store.add_batch(rows[c:c + 60], lens[c:c + 60])
+    assert len(store) == 100 and store.next_seq == 250
+    live = rows[150:]
+    Q = rows[[160, 249, 10]]
+    sims, seqs, slens, cnt, _ = store.search_batch(Q, 8)
+    torch.cuda.synchronize()
+    ref = po.search_exact_batch(live, lens[150:], np.arange(150, 250), Q, 8)
+    for i, (es, el, eq) in enumerate(ref):
+        assert np.array_equal(seqs[i].cpu().numpy(), eq)
+        assert np.array_equal(sims[i].cpu().numpy(), es)
+
+
+# ---- reference known answers (pkg/tests/test_predictor.py), through the GPU ---------
+def test_reference_vectorstore_known_answers(pr, tmp_path):
+    store = pr.VectorStore(dimension=8, capacity=3)
+    for i in range(3):
+        store.add(unit(1, i + 1), observed_len=10 * (i + 1))
+    store.add(unit(5, 5), observed_len=99)
+    assert len(store) == 3
+    sims, lens, seqs = store.search(unit(1, 1), k=3)
+    assert 10 not in lens and seqs.min() == 1
+    store = pr.VectorStore(dimension=4, capacity=10)
+    seqs = [store.add(unit(1, i, dim=4), 5) for i in range(6)]
+    assert seqs == sorted(seqs) and len(set(seqs)) == 6
+    store = pr.VectorStore(dimension=8, capacity=10)
+    store.add(unit(1, 0), 10)
+    store.add(unit(1, 1), 20)
+    store.add(unit(0, 1), 30)
+    sims, lens, _ = store.search(unit(1, 0), k=3)
+    assert list(lens) == [10, 20, 30] and sims[0] == pytest.approx(1.0)
+    store = pr.VectorStore(dimension=4, capacity=10)
+    for i in range(5):
+        store.add(unit(1, i, dim=4), 7 + i)
+    store.save(tmp_path / "db.jsonl")
+    loaded = pr.VectorStore.load(tmp_path / "db.jsonl", dimension=4, capacity=10)
+    q = unit(1, 2, dim=4)
+    assert np.allclose(store.search(q, 3)[0], loaded.search(q, 3)[0])
+
+
+def test_reference_prediction_known_answers(pr):
+    def cfg(**kw):
+        base = dict(dimension=8, top_k=3, similarity_threshold=0.8, db_capacity=100, max_len=2048)
+        base.update(kw)
+        return pr.PredictorConfig(**base)
+    p = pr.LengthPredictor(cfg())
+    p.store.add(unit(1, 2, 3), 100)
+    assert p.predict_vector(unit(1, 2, 3)) == (100, pr.RETRIEVED)
+    p = pr.LengthPredictor(cfg())
+    _, prov = p.predict_vector(unit(1, 0))
+    assert prov == pr.FALLBACK
+    p = pr.LengthPredictor(cfg())
+    a = unit(1, 0.5)
+    b = unit(0.5, 1)
+    p.store.add(a, 100)
+    p.store.add(b, 200)
+    q = unit(1, 1)
+    sa, sb = float(q @ a), float(q @ b)
+    assert sa == pytest.approx(sb)
+    length, prov = p.predict_vector(q)
+    assert prov == pr.RETRIEVED and length == 150
+    p = pr.LengthPredictor(cfg(max_len=64))
+    p.store.add(unit(1, 1), 5000)
+    assert p.predict_vector(unit(1, 1)) == (64, pr.RETRIEVED)
+    p = pr.LengthPredictor(cfg(online_refit=False))
+    p.observe(unit(3, 1, 4), 123)
+    assert p.predict_vector(unit(3, 1, 4)) == (123, pr.RETRIEVED)
+
+
+@pytest.mark.slow
+def test_c4_scale_200k_x_768(pr):
+    """C4 shape at 1/5 scale (200k x 768 DB, 512 queries, planted duplicates)."""
+    from paper_2410_23537_b200 import synthetic
+    db, lens = synthetic.predictor_db(200_000, 768, seed=0, dup_groups=200)
+    Q = synthetic.predictor_queries(db, 512, seed=0)
+    check_batch(pr, db, lens, Q, 8)
