@@ -53,6 +53,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-planes", type=int, default=16)
+    ap.add_argument("--no-pred", action="store_true")
+    ap.add_argument("--pred-n", type=int, default=1_000_000)
+    ap.add_argument("--pred-b", type=int, default=4096)
+    ap.add_argument("--pred-dim", type=int, default=768)
+    ap.add_argument("--pred-cpu-queries", type=int, default=16)
     return ap.parse_args()
 
 
@@ -347,6 +352,119 @@ def kv_bench(args, world, rank, local):
     return res
 
 
+# ----------------------------------------------------------------- predictor bench (config 4)
+def pred_bench(args, world, rank, local):
+    """BASELINE config 4: 1M x 768 fp32 DB (sharded seq % G over the ranks), B = 4096
+    queries, exact top-8 + aggregate / all-MLP finish.  Step = one batch."""
+    import math
+
+    import torch
+
+    from paper_2410_23537_b200 import _lib
+    from paper_2410_23537_b200 import predictor as pr
+    from paper_2410_23537_b200 import sharding, synthetic
+
+    dev = torch.device("cuda", local)
+    N, D, B, K = args.pred_n, args.pred_dim, args.pred_b, 8
+    db, lens = synthetic.predictor_db_torch(N, D, seed=0, dup_groups=1000, device=dev)
+    Q = synthetic.predictor_queries_torch(db, B, seed=1)
+    cfg = pr.PredictorConfig(dimension=D, top_k=K, db_capacity=N)
+    reg = pr.FallbackRegressor(D, 32, seed=0)
+    reg.b2 = 5.0
+    if world > 1:
+        store = sharding.ShardedVectorStore(D, N)
+        store.add_batch(db, lens.cpu().numpy())
+        local_store = store.local
+    else:
+        store = pr.VectorStore(D, N)
+        store.add_batch(db, lens)
+        local_store = store
+    del db
+    torch.cuda.empty_cache()
+    predictor = pr.LengthPredictor(cfg, regressor=reg, store=local_store)
+    sl = slice(rank * B // world, (rank + 1) * B // world)
+
+    def step(q):
+        if world > 1:
+            sims, _sq, ln, cnt, qd = store.search_batch(q, K)
+            return predictor.finish(sims[sl], ln[sl], cnt[sl], qd[sl])
+        return predictor.predict_batch(q)
+
+    for _ in range(args.warmup):
+        step(Q)
+    torch.cuda.synchronize()
+    local_store.kernel_stats()
+    local_store.set_timing(True)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        out = step(Q)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    local_store.set_timing(False)
+    scan_ms, scan_n, scan_flops = local_store.kernel_stats()
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    res = {"ms_per_step": ms / args.steps, "qps": B * args.steps / (ms / 1e3),
+           "scan_ms_avg": scan_ms / max(1, scan_n), "scan_flops_per_launch": scan_flops / max(1, scan_n),
+           "scan_launches": scan_n, "inexact": local_store.inexact_count(),
+           "retrieved_frac": float(out[1].float().mean().item())}
+    # e2e through the public API: host (pinned) queries in, host lengths out
+    hq = Q.cpu().pin_memory()
+    for _ in range(2):
+        step(hq.to(dev, non_blocking=True))
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o_len, o_ret = step(hq.to(dev, non_blocking=True))
+        host_len = o_len.cpu()
+        host_ret = o_ret.cpu()
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    res["e2e"] = {"value": B * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": B * D * 4,
+                  "d2h_bytes_per_step": int(host_len.numel() * 4 + host_ret.numel()),
+                  "api": "LengthPredictor.predict_batch(host queries) -> host lengths"}
+    res["shard_rows"] = local_store.size
+    del store, local_store, predictor
+    torch.cuda.empty_cache()
+    return res
+
+
+def cpu_pred_sample(args, n_queries: int):
+    """The reference predictor's CPU path on a bounded sample: float64 brute-force
+    search (predictor.py:158, BLAS gemv over the whole DB) + exact ordering +
+    aggregate/MLP (oracle port), all host cores via BLAS threads."""
+    import numpy as np
+
+    from oracle import pred_oracle
+    g = np.random.default_rng(0)
+    N, D = args.pred_n, args.pred_dim
+    db = g.standard_normal((N, D), dtype=np.float32)
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    db64 = db.astype(np.float64)
+    lens = g.integers(1, 2048, size=N)
+    Q = g.standard_normal((n_queries, D)).astype(np.float32)
+    Q[: n_queries // 2] = db[: n_queries // 2] + 0.015 * g.standard_normal((n_queries // 2, D)).astype(np.float32)
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    W1 = g.uniform(-0.08, 0.08, size=(D, 32))
+    b1 = np.zeros(32)
+    w2 = g.uniform(-0.08, 0.08, size=32)
+    t0 = time.perf_counter()
+    for q in Q:
+        sims = db64 @ q.astype(np.float64)              # the reference's scan
+        kth = np.partition(sims, N - 8)[N - 8]
+        cand = np.flatnonzero(sims >= kth)
+        order = np.lexsort((cand, -sims[cand]))[:8]
+        a = pred_oracle.aggregate(sims[cand][order], lens[cand][order], 0.8, 2048)
+        if a is None:
+            pred_oracle.mlp_predict_len(q[None].astype(np.float64), W1, b1, w2, 5.0, 2048)
+    wall = time.perf_counter() - t0
+    return {"qps": n_queries / wall, "wall_s": wall, "cores": os.cpu_count() or 1}
+
+
 # ----------------------------------------------------------------- main
 def main():
     args = parse()
@@ -362,9 +480,12 @@ def main():
     hbm_peak, bf16_peak, peak_src = load_peaks()
     links = link_peaks(local)
     kv = kv_bench(args, world, rank, local)
-    cpu = None
+    pred = None if args.no_pred else pred_bench(args, world, rank, local)
+    cpu = cpu_pred = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_kv_sample(args, args.cpu_planes)
+        if pred is not None:
+            cpu_pred = cpu_pred_sample(args, args.pred_cpu_queries)
     if rank == 0:
         layout_elems = args.layers * 2 * args.tokens * args.hidden
         geo = kv["geo"]
@@ -424,6 +545,28 @@ def main():
         }
         if "e2e" in kv:
             out["e2e"] = kv["e2e"]
+        if pred is not None:
+            ach = pred["scan_flops_per_launch"] / (pred["scan_ms_avg"] / 1e3) / 1e12 if pred["scan_ms_avg"] else None
+            out["predictor"] = {
+                "metric": "predictor queries/s (exact top-8 + aggregate/MLP)",
+                "value": round(pred["qps"], 1), "unit": "queries/s", "ms_per_step": round(pred["ms_per_step"], 3),
+                "config": {"workload": f"C4: {args.pred_n} x {args.pred_dim} fp32 DB (sharded seq % {world}),"
+                                       f" B={args.pred_b} queries, k=8, s0=0.80, MLP 768-32-1 float64",
+                           "rows_per_gpu": pred["shard_rows"]},
+                "roofline": {"bound": "tensor", "kernel": "k_scan (tcgen05 fp16 coarse scan + fused filter)",
+                             "achieved": round(ach, 1) if ach else None, "peak": bf16_peak, "unit": "TFLOP/s",
+                             "frac": round(ach / bf16_peak, 4) if ach else None, "peak_source": peak_src,
+                             "flops_per_launch": pred["scan_flops_per_launch"],
+                             "avg_launch_ms": pred["scan_ms_avg"], "traffic": None},
+                "e2e": pred["e2e"], "inexact_candidates": pred["inexact"],
+                "retrieved_frac": round(pred["retrieved_frac"], 4),
+                "gpu_launches_per_step": 5 + (2 if world > 1 else 0),
+            }
+            if cpu_pred is not None:
+                out["predictor"]["cpu_baseline"] = {
+                    "value": round(cpu_pred["qps"], 3), "unit": "queries/s", "cores": cpu_pred["cores"],
+                    "kind": "port", "sample": f"{args.pred_cpu_queries} queries vs the full {args.pred_n} x "
+                                              f"{args.pred_dim} float64 DB (BLAS gemv scan, predictor.py:158)"}
         if cpu is not None:
             out["cpu_baseline"] = {"value": round(cpu["GBps"], 4), "unit": "GB/s", "cores": cpu["cores"],
                                    "kind": "port",

@@ -138,20 +138,28 @@ typedef struct alise_db alise_db;
 int alise_db_create(int device, int64_t capacity, int64_t dim, alise_db **out);
 int alise_db_destroy(alise_db *db);
 /* Append n rows (device pointers): vecs fp32 [n][dim], lens int32 [n], seqs int64 [n]
- * (seqs must be consecutive from the db's next sequence number). */
+ * (the store's next sequence numbers, in order; slot = (seq / stride) % capacity). */
 int alise_db_append(alise_db *db, const float *vecs, const int32_t *lens, const int64_t *seqs,
                     int64_t n, void *stream);
 int alise_db_size(alise_db *db, int64_t *size, int64_t *next_seq);
+/* Shard of a G-way sequence-sharded store: this db receives every G-th sequence number
+ * (seq % G == rank) and places it at slot (seq / G) % capacity, so per-shard FIFO
+ * eviction equals the global FIFO when the global capacity is G * capacity. */
+int alise_db_set_seq_stride(alise_db *db, int64_t stride);
 /* Copy the first n live slots (fp32 vectors, lens, seqs) to device buffers. */
 int alise_db_export(alise_db *db, float *vecs, int32_t *lens, int64_t *seqs, int64_t n, void *stream);
-/* Number of rescored candidates whose correct rounding could not be certified
- * (expected 0; synchronous). */
+/* Number of rescored candidates whose double-double sum could not certify the float64
+ * rounding and were recomputed with the exact 640-bit accumulator (synchronous). */
 int alise_db_inexact(alise_db *db, unsigned int *count);
 /* Exact top-k of B queries (fp32 [B][dim], device) against the db: sims are the
  * correctly rounded float64 dot products, ordered by (-sim, seq) (ties -> older
  * first).  Outputs [B][k]; count[b] = min(k, size). */
 int alise_db_topk(alise_db *db, const float *queries, int64_t B, int k, double *out_sim,
                   int64_t *out_seq, int32_t *out_len, int32_t *out_count, void *stream);
+/* Bench instrumentation: CUDA events around every coarse-scan launch; kernel_stats
+ * returns the summed scan time, launch count and algorithmic flops (2*B*size*dim). */
+int alise_db_timing(alise_db *db, int enable);
+int alise_db_kernel_stats(alise_db *db, double *scan_ms, int64_t *launches, double *flops);
 /* Merge G per-shard top-k lists ([G][B][k] each) into a global top-k by (-sim, seq). */
 int alise_topk_merge(int G, int64_t B, int k, const double *sims, const int64_t *seqs,
                      const int32_t *lens, const int32_t *counts, double *out_sim,

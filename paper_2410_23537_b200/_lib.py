@@ -58,6 +58,9 @@ _SIGS = {
     "alise_db_append": [vp, vp, vp, vp, i64, vp],
     "alise_db_size": [vp, vp, vp],
     "alise_db_inexact": [vp, vp],
+    "alise_db_set_seq_stride": [vp, i64],
+    "alise_db_timing": [vp, i32],
+    "alise_db_kernel_stats": [vp, vp, vp, vp],
     "alise_db_export": [vp, vp, vp, vp, i64, vp],
     "alise_db_topk": [vp, vp, i64, i32, vp, vp, vp, vp, vp],
     "alise_topk_merge": [i32, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp],

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <string>
+#include <vector>
 
 #include "../../include/alise_b200.h"
 #include "pred_scan.cuh"
@@ -67,6 +68,7 @@ struct alise_db {
   int device = 0;
   int64_t capacity = 0, cap_p = 0, dim = 0, dp = 0;
   int64_t size = 0, next_seq = 0;
+  int64_t seq_stride = 1;  // sharded stores hold every G-th sequence: slot = (seq / G) % capacity
   float* v32 = nullptr;
   __half* v16 = nullptr;
   int32_t* lens = nullptr;
@@ -85,6 +87,10 @@ struct alise_db {
   float* topc = nullptr;
   int32_t* need = nullptr;
   CUtensorMap tmQ;
+  // optional kernel timing (bench roofline): event pairs around each scan launch
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  double scan_flops = 0.0;
 };
 
 extern "C" int alise_db_create(int device, int64_t capacity, int64_t dim, alise_db** out) {
@@ -143,11 +149,19 @@ extern "C" int alise_db_append(alise_db* db, const float* vecs, const int32_t* l
   if (n == 0) return ALISE_OK;
   // rows with equal slot in one batch would race; the host splits batches larger than capacity
   if (n > db->capacity) return fail(ALISE_EINVAL, "append batch larger than capacity");
-  k_db_append<<<(unsigned)n, 128, 0, S(stream)>>>(vecs, lens, seqs, n, db->dim, db->dp, db->capacity, db->v32,
-                                                  db->v16, db->lens, db->seqs, db->vmax);
+  k_db_append<<<(unsigned)n, 128, 0, S(stream)>>>(vecs, lens, seqs, n, db->dim, db->dp, db->capacity,
+                                                  db->seq_stride, db->v32, db->v16, db->lens, db->seqs,
+                                                  db->vmax);
   CKL();
   db->next_seq += n;
   db->size = std::min(db->capacity, db->size + n);
+  return ALISE_OK;
+}
+
+extern "C" int alise_db_set_seq_stride(alise_db* db, int64_t stride) {
+  if (!db || stride < 1) return fail(ALISE_EINVAL, "stride must be >= 1");
+  if (db->next_seq) return fail(ALISE_EINVAL, "set the stride before the first append");
+  db->seq_stride = stride;
   return ALISE_OK;
 }
 
@@ -173,11 +187,12 @@ extern "C" int alise_db_inexact(alise_db* db, unsigned int* count) {
 }
 
 static int choose_splits(int n_qb, int n_tiles, int sms) {
-  // fill the machine: ~2 waves of one CTA per SM, at least one tile per split
-  int s = std::max(1, (2 * sms + n_qb - 1) / n_qb);
-  s = std::min(s, std::max(1, n_tiles));
-  s = std::min(s, 8192 / KMAX);
-  return s;
+  // tile groups: one persistent CTA per (query block, group), as many groups as fit
+  // on the SMs alongside the query blocks
+  int g = std::max(1, sms / std::max(1, n_qb));
+  g = std::min(g, std::max(1, n_tiles));
+  g = std::min(g, 8192 / KMAX);
+  return g;
 }
 
 static int ensure_scratch(alise_db* db, int64_t Bp, int splits, cudaStream_t st) {
@@ -233,6 +248,7 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   a.n_tiles = n_tiles;
   a.n_qb = n_qb;
   a.n_splits = splits;
+  a.B = (int)B;
   a.Bp = (int)Bp;
   a.k = k;
   a.two_delta = db->two_delta;
@@ -247,10 +263,22 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
     else CK(cudaFuncSetAttribute(k_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM));
     attr_set[kt] = true;
   }
-  const unsigned grid = (unsigned)(n_qb * splits);
+  const unsigned grid = (unsigned)std::min(n_qb * splits, sm_count_pred());
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (db->timing) {
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    db->scan_flops += 2.0 * (double)B * (double)db->size * (double)db->dim;
+  }
   if (kt == 0) k_scan<8><<<grid, 192, SCAN_SMEM, st>>>(db->tmQ, db->tmD, a);
   else k_scan<16><<<grid, 192, SCAN_SMEM, st>>>(db->tmQ, db->tmD, a);
   CKL();
+  if (db->timing) {
+    CK(cudaEventRecord(e1, st));
+    db->ev.push_back(e0);
+    db->ev.push_back(e1);
+  }
   CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
   k_rescore<<<(unsigned)B, 256, 0, st>>>(splits, (int)Bp, B, k, db->size, db->dim, queries, db->v32, db->lens,
                                          db->seqs, db->two_delta, db->cand_s, db->cand_r, db->cand_n, db->topc,
@@ -259,6 +287,29 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   k_exhaustive<<<(unsigned)B, 256, 0, st>>>(B, k, db->size, db->dim, queries, db->v32, db->lens, db->seqs, db->need,
                                             out_sim, out_seq, out_len, out_count, db->inexact);
   CKL();
+  return ALISE_OK;
+}
+
+extern "C" int alise_db_timing(alise_db* db, int enable) {
+  db->timing = enable != 0;
+  return ALISE_OK;
+}
+
+// Sums the scan kernel time (ms) and algorithmic flops since the last call (synchronises).
+extern "C" int alise_db_kernel_stats(alise_db* db, double* scan_ms, int64_t* launches, double* flops) {
+  CK(cudaDeviceSynchronize());
+  double tot = 0;
+  for (size_t i = 0; i + 1 < db->ev.size(); i += 2) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, db->ev[i], db->ev[i + 1]));
+    tot += ms;
+  }
+  *scan_ms = tot;
+  *launches = (int64_t)(db->ev.size() / 2);
+  *flops = db->scan_flops;
+  for (auto e : db->ev) cudaEventDestroy(e);
+  db->ev.clear();
+  db->scan_flops = 0.0;
   return ALISE_OK;
 }
 

@@ -247,8 +247,9 @@ k_dequant_tile(const uint8_t* __restrict__ codes, const double* __restrict__ sca
                           : __ldg(reinterpret_cast<const double*>(zero) + r);
     const float s32 = (float)s;
     // rows whose products may leave the fp16 normal range take the exact path
-    const bool row_fast = fabs(z) < 4194304.0 && s >= 0x1p-14 && s < 60000.0 &&
-                          (z == rint(z) || fabs(z) >= 0x1p-14 || z == 0.0);
+    // fast rows: integer zero (so 2^23 + z is exact in fp32) and products in the
+    // fp16 normal range; constant rows (real-valued zero) take the exact path
+    const bool row_fast = z == rint(z) && fabs(z) < 4194304.0 && s >= 0x1p-14 && s < 60000.0;
     const float zm = (float)(z + 8388608.0);
     uint32_t q[8];
     if (PACK) {

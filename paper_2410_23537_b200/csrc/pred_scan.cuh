@@ -34,7 +34,7 @@ constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int KMAX = 16;       // largest supported k
 constexpr int CAP = 128;       // candidate slots per (split, query)
-constexpr int SCAN_SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int SCAN_SMEM = STAGES * STAGE_BYTES + 1024 + 256 + BM * 33 * 4;
 constexpr int MAXC = 512;      // candidates rescored per query
 
 // ------------------------------------------------------------------ DB maintenance
@@ -42,12 +42,12 @@ constexpr int MAXC = 512;      // candidates rescored per query
 // padded to dp), lengths, seqs; track an upper bound of the row L2 norms.
 __global__ void k_db_append(const float* __restrict__ vecs, const int32_t* __restrict__ lens,
                             const int64_t* __restrict__ seqs, int64_t n, int64_t dim, int64_t dp,
-                            int64_t capacity, float* __restrict__ v32, __half* __restrict__ v16,
+                            int64_t capacity, int64_t stride, float* __restrict__ v32, __half* __restrict__ v16,
                             int32_t* __restrict__ dlens, int64_t* __restrict__ dseqs,
                             unsigned int* __restrict__ vmax_bits) {
   const int64_t i = blockIdx.x;
   if (i >= n) return;
-  const int64_t slot = seqs[i] % capacity;
+  const int64_t slot = (seqs[i] / stride) % capacity;
   double ss = 0.0;
   for (int64_t d = threadIdx.x; d < dp; d += blockDim.x) {
     const float v = d < dim ? vecs[i * dim + d] : 0.f;
@@ -102,7 +102,8 @@ struct ScanArgs {
   int64_t n_rows;    // valid DB rows (slots [0, n_rows))
   int n_tiles;       // ceil(n_rows / BN)
   int n_qb;          // query blocks of 128
-  int n_splits;      // DB splits (CTAs per query block)
+  int n_splits;      // tile groups G: group g scans tiles g, g+G, ...
+  int B;             // real query count
   int Bp;            // padded query count
   int k;
   const float* two_delta;
@@ -130,6 +131,24 @@ __device__ __forceinline__ float topk_insert(float (&top)[KT], float s, int k) {
   return kth;
 }
 
+// Compaction of a full candidate buffer against the risen threshold (rare).
+__device__ __noinline__ int compact_candidates(float* __restrict__ cs, int32_t* __restrict__ cr, float thr) {
+  int w = 0;
+  for (int u = 0; u < CAP; ++u) {
+    const float sv = cs[u];
+    if (sv >= thr) {
+      cs[w] = sv;
+      cr[w] = cr[u];
+      ++w;
+    }
+  }
+  return w;
+}
+
+// Persistent CTAs.  Work item w = (query block qb, tile group g): the CTA keeps one
+// running top-k per query across all tiles t = g, g+G, g+2G, ... (so the threshold
+// warms up once), and the n_qb CTAs of a group walk the same tile sequence in lock
+// step, so each DB tile is read from HBM once and from L2 by the other query blocks.
 template <int KT>
 __global__ void __launch_bounds__(192, 1)
 k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmD, const ScanArgs a) {
@@ -140,12 +159,11 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stage32 = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);  // [128][33]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qb = blockIdx.x % a.n_qb;
-  const int split = blockIdx.x / a.n_qb;
-  const int t0 = (int)((int64_t)split * a.n_tiles / a.n_splits);
-  const int t1 = (int)((int64_t)(split + 1) * a.n_tiles / a.n_splits);
+  const int G = a.n_splits;
+  const int n_work = a.n_qb * G;
 
   if (warp == 0 && lane == 0) {
     sm100::prefetch_tmap(&tmQ);
@@ -170,14 +188,17 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = t0; t < t1; ++t) {
-        for (int kb = 0; kb < a.n_kb; ++kb) {
-          sm100::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * STAGE_BYTES;
-          sm100::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          sm100::tma_load_2d(&tmQ, sa, &full[stage], kb * BK, qb * BM);
-          sm100::tma_load_2d(&tmD, sa + A_BYTES, &full[stage], kb * BK, t * BN);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int qb = w % a.n_qb, g = w / a.n_qb;
+        for (int t = g; t < a.n_tiles; t += G) {
+          for (int kb = 0; kb < a.n_kb; ++kb) {
+            sm100::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * STAGE_BYTES;
+            sm100::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+            sm100::tma_load_2d(&tmQ, sa, &full[stage], kb * BK, qb * BM);
+            sm100::tma_load_2d(&tmD, sa + A_BYTES, &full[stage], kb * BK, t * BN);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
         }
       }
     }
@@ -187,96 +208,109 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
-      for (int t = t0; t < t1; ++t, ++i) {
-        const int acc = i & 1;
-        const uint32_t aph = (i >> 1) & 1;
-        sm100::mbar_wait(&tempty[acc], aph ^ 1);
-        sm100::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < a.n_kb; ++kb) {
-          sm100::mbar_wait(&full[stage], phase);
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int g = w / a.n_qb;
+        for (int t = g; t < a.n_tiles; t += G, ++i) {
+          const int acc = i & 1;
+          const uint32_t aph = (i >> 1) & 1;
+          sm100::mbar_wait(&tempty[acc], aph ^ 1);
           sm100::tc_fence_after();
-          const uint32_t a0 = sm100::smem_u32(smem + stage * STAGE_BYTES);
-          const uint32_t b0 = a0 + A_BYTES;
+          const uint32_t d_tmem = tmem_base + acc * BN;
+          for (int kb = 0; kb < a.n_kb; ++kb) {
+            sm100::mbar_wait(&full[stage], phase);
+            sm100::tc_fence_after();
+            const uint32_t a0 = sm100::smem_u32(smem + stage * STAGE_BYTES);
+            const uint32_t b0 = a0 + A_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(a0 + kk * 32), sm100::umma_desc_sw128(b0 + kk * 32),
-                            idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(a0 + kk * 32),
+                              sm100::umma_desc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+            }
+            sm100::umma_commit(&empty[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          sm100::umma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          sm100::umma_commit(&tfull[acc]);
         }
-        sm100::umma_commit(&tfull[acc]);
       }
     }
   } else {  // ---------------- epilogue: warps 2..5, thread = query
     const int quarter = warp & 3;
-    const int q = qb * BM + quarter * 32 + lane;
+    const int tq = quarter * 32 + lane;
+    float* my_stage = stage32 + tq * 33;
     const int k = a.k;
-    float top[KT];
-#pragma unroll
-    for (int i = 0; i < KT; ++i) top[i] = -__int_as_float(0x7f800000);
-    const float td = a.two_delta[q];
-    float thr = -__int_as_float(0x7f800000);
-    float kth = thr;
-    int cnt = 0;
-    bool ovf = false;
-    const size_t base = ((size_t)split * a.Bp + q);
-    float* cs = a.cand_s + base * CAP;
-    int32_t* cr = a.cand_r + base * CAP;
     int i = 0;
-    for (int t = t0; t < t1; ++t, ++i) {
-      const int acc = i & 1;
-      const uint32_t aph = (i >> 1) & 1;
-      sm100::mbar_wait(&tfull[acc], aph);
-      sm100::tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        float v[32];
-        sm100::tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, v);
-        const int rbase = t * BN + c * 32;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const int qb = w % a.n_qb, g = w / a.n_qb;
+      const int q = qb * BM + tq;
+      float top[KT];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float s = v[j];
-          if (s >= thr) {
-            const int row = rbase + j;
-            if (row < a.n_rows) {
-              if (s > kth) {  // beats the running k-th: insert
-                kth = topk_insert<KT>(top, s, k);
+      for (int x = 0; x < KT; ++x) top[x] = -__int_as_float(0x7f800000);
+      const float td = a.two_delta[q];
+      // padding queries (q >= B) never pass
+      float thr = q < a.B ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
+      float kth = -__int_as_float(0x7f800000);
+      int cnt = 0;
+      bool ovf = false;
+      const size_t base = ((size_t)g * a.Bp + q);
+      float* cs = a.cand_s + base * CAP;
+      int32_t* cr = a.cand_r + base * CAP;
+      for (int t = g; t < a.n_tiles; t += G, ++i) {
+        const int acc = i & 1;
+        const uint32_t aph = (i >> 1) & 1;
+        sm100::mbar_wait(&tfull[acc], aph);
+        sm100::tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          sm100::tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, v);
+          // hot path: one max-reduction and one compare per 32 scores
+          float m8[8];
+#pragma unroll
+          for (int x = 0; x < 8; ++x) m8[x] = fmaxf(fmaxf(v[4 * x], v[4 * x + 1]), fmaxf(v[4 * x + 2], v[4 * x + 3]));
+          const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+          const bool hit = mx >= thr;
+          if (__any_sync(0xffffffffu, hit)) {
+            uint32_t mask = 0;
+#pragma unroll
+            for (int x = 0; x < 32; ++x) {
+              my_stage[x] = v[x];
+              mask |= (v[x] >= thr ? 1u : 0u) << x;
+            }
+            const int rbase = t * BN + c * 32;
+            if (rbase + 32 > a.n_rows) mask &= (a.n_rows > rbase) ? (0xffffffffu >> (32 - (a.n_rows - rbase))) : 0u;
+            while (mask) {
+              const int j = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const float sc = my_stage[j];
+              if (!(sc >= thr)) continue;
+              if (sc > kth) {  // beats the running k-th: insert
+                kth = topk_insert<KT>(top, sc, k);
                 thr = kth - td;
               }
-              if (!ovf) {
-                if (cnt == CAP) {  // compact against the risen threshold
-                  int w = 0;
-                  for (int u = 0; u < CAP; ++u) {
-                    const float sv = cs[u];
-                    if (sv >= thr) {
-                      cs[w] = sv;
-                      cr[w] = cr[u];
-                      ++w;
-                    }
-                  }
-                  cnt = w;
-                  if (cnt == CAP) ovf = true;
-                }
-                if (!ovf) {
-                  cs[cnt] = s;
-                  cr[cnt] = row;
-                  ++cnt;
+              if (ovf) continue;
+              if (cnt == CAP) {
+                cnt = compact_candidates(cs, cr, thr);
+                if (cnt == CAP) {
+                  ovf = true;
+                  continue;
                 }
               }
+              cs[cnt] = sc;
+              cr[cnt] = rbase + j;
+              ++cnt;
             }
           }
         }
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
       }
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
-    }
-    a.cand_n[base] = ovf ? -1 : cnt;
+      a.cand_n[base] = ovf ? -1 : cnt;
 #pragma unroll
-    for (int u = 0; u < KT; ++u)
-      if (u < k) a.topc[base * KMAX + u] = top[u];
+      for (int x = 0; x < KT; ++x)
+        if (x < k) a.topc[base * KMAX + x] = top[x];
+    }
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -325,12 +359,102 @@ __device__ double warp_exact_dot(const float* __restrict__ a, const float* __res
   }
   double r, t;
   two_sum(hi, lo, r, t);
+  // r = RN(hi + lo); exact sum S = r + t + e with |e| <= bound.  RN(S) == r iff S stays
+  // strictly inside r's rounding interval: half an ulp above/below, except that just
+  // below a power of two the ulp halves.
   const double bound = ab * (double)(dim + 64) * 0x1p-104 + 0x1p-1070;
-  // quarter ulp of r (conservative across a binade boundary)
   const double ar = fabs(r);
-  const double qulp = ar > 0.0 ? ldexp(1.0, ilogb(ar) - 54) : 0x1p-1074;
-  ok = fabs(t) + bound < qulp || (ab == 0.0);
+  bool exact_sum = (ab == 0.0);
+  if (!exact_sum && ar > 0.0) {
+    const int e2 = ilogb(ar);
+    double half = ldexp(1.0, e2 - 53);
+    const bool pow2 = ar == ldexp(1.0, e2);
+    const bool toward_zero = (t != 0.0) && ((t < 0.0) != (r < 0.0));
+    if (pow2 && toward_zero) half *= 0.5;
+    exact_sum = fabs(t) + bound < half;
+  }
+  ok = exact_sum;
   return r;
+}
+
+// Exact correctly rounded float64 dot product of two fp32 vectors with a 640-bit
+// fixed-point accumulator (LSB weight 2^-320; fp32 x fp32 products have integer
+// significands < 2^48 at weights >= 2^-298).  Single thread; used only when the
+// double-double certificate cannot decide the rounding (exact ties at a float64
+// midpoint are common for fp32 inputs).
+__device__ __noinline__ double exact_dot_super(const float* __restrict__ a, const float* __restrict__ b,
+                                               int64_t dim) {
+  constexpr int L = 10;
+  constexpr int BASE = -320;
+  uint64_t acc[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) acc[i] = 0;
+  for (int64_t d = 0; d < dim; ++d) {
+    const uint32_t bx = __float_as_uint(__ldg(a + d)), by = __float_as_uint(__ldg(b + d));
+    uint32_t mx = bx & 0x7fffffu, my = by & 0x7fffffu;
+    int ex = (bx >> 23) & 255, ey = (by >> 23) & 255;
+    if ((!ex && !mx) || (!ey && !my)) continue;  // a zero factor
+    if (ex) mx |= 0x800000u; else ex = 1;
+    if (ey) my |= 0x800000u; else ey = 1;
+    const uint64_t m = (uint64_t)mx * my;          // < 2^48
+    const int e = (ex - 150) + (ey - 150) - BASE;  // >= 22
+    const int li = e >> 6, sh = e & 63;
+    const uint64_t lo = m << sh;
+    const uint64_t hi = sh ? (m >> (64 - sh)) : 0;
+    if (((bx ^ by) >> 31) == 0) {
+      uint64_t s0 = acc[li] + lo;
+      uint64_t carry = s0 < lo;
+      acc[li] = s0;
+      uint64_t s1 = acc[li + 1] + hi;
+      uint64_t c2 = s1 < hi;
+      s1 += carry;
+      c2 |= (s1 < carry);
+      acc[li + 1] = s1;
+      for (int j = li + 2; j < L && c2; ++j) { acc[j] += 1; c2 = acc[j] == 0; }
+    } else {
+      const uint64_t d0 = acc[li] - lo;
+      uint64_t borrow = acc[li] < lo;
+      acc[li] = d0;
+      const uint64_t t1 = acc[li + 1];
+      uint64_t d1 = t1 - hi;
+      uint64_t b2 = t1 < hi;
+      b2 |= (d1 < borrow);
+      d1 -= borrow;
+      acc[li + 1] = d1;
+      for (int j = li + 2; j < L && b2; ++j) { b2 = acc[j] == 0; acc[j] -= 1; }
+    }
+  }
+  const bool neg = (acc[L - 1] >> 63) != 0;
+  if (neg) {  // two's complement magnitude
+    uint64_t c = 1;
+    for (int i = 0; i < L; ++i) {
+      acc[i] = ~acc[i] + c;
+      c = (c && acc[i] == 0) ? 1 : 0;
+    }
+  }
+  int top = L - 1;
+  while (top >= 0 && acc[top] == 0) --top;
+  if (top < 0) return 0.0;
+  const int msb = top * 64 + (63 - __clzll(acc[top]));
+  auto bit = [&](int p) -> uint64_t { return p < 0 ? 0ull : (acc[p >> 6] >> (p & 63)) & 1ull; };
+  uint64_t mant = 0;
+  for (int p = msb; p > msb - 53; --p) mant = (mant << 1) | bit(p);
+  const uint64_t guard = bit(msb - 53);
+  bool sticky = false;
+  const int sp = msb - 54;  // bits [0, sp] are sticky
+  if (sp >= 0) {
+    for (int i = 0; i < (sp >> 6); ++i) sticky |= acc[i] != 0;
+    const int r = sp & 63;
+    const uint64_t maskp = (r == 63) ? ~0ull : ((1ull << (r + 1)) - 1);
+    sticky |= (acc[sp >> 6] & maskp) != 0;
+  }
+  int exp2 = msb - 52 + BASE;
+  if (guard && (sticky || (mant & 1))) {
+    ++mant;
+    if (mant == (1ull << 53)) { mant >>= 1; ++exp2; }
+  }
+  const double v = ldexp((double)mant, exp2);
+  return neg ? -v : v;
 }
 
 // Per query: global coarse k-th from the splits' top lists, candidate compaction,
@@ -419,11 +543,14 @@ k_rescore(int n_splits, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, c
   for (int c = warp; c < n; c += blockDim.x >> 5) {
     const int row = s_rows[c];
     bool ok;
-    const double sim = warp_exact_dot(v32 + (size_t)row * dim, q32 + q * dim, dim, ok);
+    double sim = warp_exact_dot(v32 + (size_t)row * dim, q32 + q * dim, dim, ok);
     if (lane == 0) {
+      if (!ok) {
+        sim = exact_dot_super(v32 + (size_t)row * dim, q32 + q * dim, dim);
+        atomicAdd(inexact_count, 1u);
+      }
       s_sim[c] = sim;
       s_seq[c] = seqs[row];
-      if (!ok) atomicAdd(inexact_count, 1u);
     }
   }
   __syncthreads();
@@ -462,9 +589,12 @@ k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restr
   for (int i = 0; i < KMAX; ++i) { tsim[i] = -__longlong_as_double(0x7ff0000000000000ll); tseq[i] = INT64_MAX; trow[i] = -1; }
   for (int64_t row = warp; row < n_rows; row += blockDim.x >> 5) {
     bool ok;
-    const double sim = warp_exact_dot(v32 + row * dim, q32 + q * dim, dim, ok);
+    double sim = warp_exact_dot(v32 + row * dim, q32 + q * dim, dim, ok);
     if (lane == 0) {
-      if (!ok) atomicAdd(inexact_count, 1u);
+      if (!ok) {
+        sim = exact_dot_super(v32 + row * dim, q32 + q * dim, dim);
+        atomicAdd(inexact_count, 1u);
+      }
       double cs = sim;
       int64_t cq = seqs[row];
       int cr = (int)row;

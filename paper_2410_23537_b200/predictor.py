@@ -229,6 +229,16 @@ class VectorStore:
         return (sims[0, :c].cpu().numpy(), lens[0, :c].cpu().numpy().astype(np.int64),
                 seqs[0, :c].cpu().numpy())
 
+    def set_timing(self, on: bool):
+        _lib.call("alise_db_timing", self._h, int(on))
+
+    def kernel_stats(self):
+        """(scan_ms, launches, algorithmic flops) since the last call (synchronises)."""
+        ms, fl = _lib.C.c_double(), _lib.C.c_double()
+        n = _lib.C.c_int64()
+        _lib.call("alise_db_kernel_stats", self._h, _lib.C.byref(ms), _lib.C.byref(n), _lib.C.byref(fl))
+        return ms.value, n.value, fl.value
+
     def inexact_count(self) -> int:
         """Candidates whose float64 rounding could not be certified (expected 0)."""
         c = _lib.C.c_uint()

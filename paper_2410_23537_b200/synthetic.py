@@ -106,3 +106,36 @@ def predictor_queries(db: np.ndarray, b: int, seed: int = 0, near_frac: float = 
     q[:nn] = db[src] + noise * g.standard_normal((nn, dim), dtype=np.float32)
     q /= np.linalg.norm(q, axis=1, keepdims=True)
     return q.astype(np.float32)
+
+
+def predictor_db_torch(n: int, dim: int, seed: int = 0, dup_groups: int = 0, dup_size: int = 11,
+                       device="cuda"):
+    """Device-side twin of predictor_db for GiB-scale benches (same distribution
+    family, torch generator): unit-norm fp32 rows with planted duplicate groups and
+    ShareGPT-like lengths."""
+    import torch
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed * 7919 + 77)
+    v = torch.randn((n, dim), generator=gen, device=device, dtype=torch.float32)
+    v /= v.norm(dim=1, keepdim=True)
+    if dup_groups:
+        src = torch.randint(0, n, (dup_groups,), generator=gen, device=device)
+        dst = torch.randint(0, n, (dup_groups, dup_size - 1), generator=gen, device=device)
+        v[dst.reshape(-1)] = v[src].repeat_interleave(dup_size - 1, dim=0)
+    ln = torch.exp(SHAREGPT["output_mu"] + SHAREGPT["output_sigma"] *
+                   torch.randn(n, generator=gen, device=device, dtype=torch.float64))
+    lens = ln.round().clamp(1, SHAREGPT["max_len"]).to(torch.int32)
+    return v, lens
+
+
+def predictor_queries_torch(db, b: int, seed: int = 0, near_frac: float = 0.5, noise: float = 0.015):
+    import torch
+    gen = torch.Generator(device=db.device)
+    gen.manual_seed(seed * 7919 + 78)
+    n, dim = db.shape
+    nn = int(b * near_frac)
+    q = torch.randn((b, dim), generator=gen, device=db.device, dtype=torch.float32)
+    src = torch.randint(0, n, (nn,), generator=gen, device=db.device)
+    q[:nn] = db[src] + noise * torch.randn((nn, dim), generator=gen, device=db.device)
+    q /= q.norm(dim=1, keepdim=True)
+    return q
