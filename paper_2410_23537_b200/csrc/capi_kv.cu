@@ -320,6 +320,15 @@ static int quant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, cons
   const int64_t rows = np * g.rows_pp;
   if (d->kind == ALISE_KIND_ROWS)
     return launch_tile(d->bits, d->packed != 0, true, kv, rows, d->group, codes, scale, zero, flag, st);
+  const int cpr = d->kind == ALISE_KIND_CHANNEL ? 1 : (int)d->head_dim;
+  if (d->hidden % 128 == 0 && cpr <= 128 && 128 % cpr == 0) {
+    dim3 grid((unsigned)(d->hidden / 128), (unsigned)np);
+    if (d->bits == 8) k_quant_cols<8, false><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, scale, zero, flag);
+    else if (d->packed) k_quant_cols<4, true><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, scale, zero, flag);
+    else k_quant_cols<4, false><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, scale, zero, flag);
+    CKL();
+    return ALISE_OK;
+  }
   int nch;
   int64_t tchunk;
   cols_workspace(d, g, &nch, &tchunk);
@@ -353,6 +362,15 @@ static int dequant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, co
   const double* scale = reinterpret_cast<const double*>(rec + g.codes_sec(np));
   const float* zero = reinterpret_cast<const float*>(rec + g.codes_sec(np) + g.scale_sec(np));
   const int64_t D = d->head_dim > 0 ? d->head_dim : 1;
+  const int cpr = d->kind == ALISE_KIND_CHANNEL ? 1 : (int)D;
+  if (d->kind != ALISE_KIND_ROWS && d->hidden % 128 == 0 && cpr <= 128 && 128 % cpr == 0) {
+    dim3 grid((unsigned)(d->hidden / 128), (unsigned)np);
+    if (d->bits == 8) k_dequant_cols<8, false><<<grid, 256, 0, st>>>(codes, scale, zero, d->tokens, d->hidden, cpr, g.rows_pp, kv);
+    else if (d->packed) k_dequant_cols<4, true><<<grid, 256, 0, st>>>(codes, scale, zero, d->tokens, d->hidden, cpr, g.rows_pp, kv);
+    else k_dequant_cols<4, false><<<grid, 256, 0, st>>>(codes, scale, zero, d->tokens, d->hidden, cpr, g.rows_pp, kv);
+    CKL();
+    return ALISE_OK;
+  }
   return dequant_launch<uint16_t>(d->kind, codes, scale, zero, true, np * g.plane_elems,
                                   d->kind == ALISE_KIND_ROWS ? d->group : 1, d->tokens, d->hidden,
                                   D, d->bits, d->packed != 0, kv, st);

@@ -288,6 +288,197 @@ k_dequant_tile(const uint8_t* __restrict__ codes, const double* __restrict__ sca
 }
 
 // ---------------------------------------------------------------------------------
+// Fused column kernel for the CHANNEL / HEAD kinds (rows run along tokens).
+// Block = 256 threads = 16 column vectors (128 columns) x 16 token lanes over one
+// plane [T][Hd].  Pass 1: NaN-propagating half2 min/max down the tokens, reduced
+// across token lanes in shared memory, then one thread per group (column, or head
+// of `cpr` columns) solves the float64 parameters.  Pass 2: the strip is re-read
+// (L2) and each thread quantizes its 8 columns with per-column fp32 constants held
+// in registers.  Codes stay in native [T][Hd] order.
+// ---------------------------------------------------------------------------------
+template <int BITS, bool PACK>
+__global__ void __launch_bounds__(256)
+k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int64_t rows_per_plane,
+             uint8_t* __restrict__ codes, double* __restrict__ scale, float* __restrict__ zero,
+             int* __restrict__ flag) {
+  constexpr int F = TileMagic<BITS>::F;
+  constexpr uint32_t HALF = 1u << (F - 1);
+  constexpr uint32_t FMASK = (1u << F) - 1;
+  constexpr float QMAXF = (float)((1 << BITS) - 1);
+  __shared__ __half2 s_mm[16][128];      // (min, -max) per token lane and column
+  __shared__ float s_inv[128], s_zc[128];
+  __shared__ int s_w[128];
+  const int tid = threadIdx.x;
+  const int cv = tid & 15, tl = tid >> 4;
+  const int64_t plane = blockIdx.y;
+  const int64_t col0 = (int64_t)blockIdx.x * 128;
+  const uint16_t* base = x + plane * T * Hd + col0 + cv * 8;
+  // ---- pass 1
+  __half2 lo[4], hi[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    lo[j] = __half2half2(__ushort_as_half(0x7c00));
+    hi[j] = __half2half2(__ushort_as_half(0xfc00));
+  }
+  for (int64_t t = tl; t < T; t += 16) {
+    const uint4 d = __ldg(reinterpret_cast<const uint4*>(base + t * Hd));
+    const __half2* h = reinterpret_cast<const __half2*>(&d);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      lo[j] = __hmin2_nan(lo[j], h[j]);
+      hi[j] = __hmax2_nan(hi[j], h[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    s_mm[tl][cv * 8 + 2 * j] = __halves2half2(__low2half(lo[j]), __hneg(__low2half(hi[j])));
+    s_mm[tl][cv * 8 + 2 * j + 1] = __halves2half2(__high2half(lo[j]), __hneg(__high2half(hi[j])));
+  }
+  __syncthreads();
+  if (tid < 128) {
+    __half2 m = s_mm[0][tid];
+    for (int u = 1; u < 16; ++u) m = __hmin2_nan(m, s_mm[u][tid]);
+    s_mm[0][tid] = m;
+  }
+  __syncthreads();
+  // one thread per group of cpr columns
+  const int groups = 128 / cpr;
+  if (tid < groups) {
+    __half2 m = s_mm[0][tid * cpr];
+    for (int u = 1; u < cpr; ++u) m = __hmin2_nan(m, s_mm[0][tid * cpr + u]);
+    float fmn = __low2float(m), fmx = -__high2float(m);
+    const bool bad = !(isfinite(fmn) && isfinite(fmx));
+    if (bad) { atomicOr(flag, 1); fmn = 0.f; fmx = 0.f; }
+    const QParams q = make_params((double)fmn, (double)fmx, BITS, false);
+    const TileParams tp = make_tile_params<BITS>(q, fmax(fabs((double)fmn), fabs((double)fmx)));
+    const int64_t r = plane * rows_per_plane + (col0 / cpr) + tid;
+    scale[r] = q.s;
+    zero[r] = (float)q.z;
+    for (int u = 0; u < cpr; ++u) {
+      s_inv[tid * cpr + u] = tp.inv_s;
+      s_zc[tid * cpr + u] = tp.zc;
+      s_w[tid * cpr + u] = tp.w;
+    }
+  }
+  __syncthreads();
+  // ---- pass 2
+  float inv[8], zc[8];
+  uint32_t koff[8], kwin[8];
+  const uint32_t kMagicBits = f2bits(TileMagic<BITS>::M);
+  const uint32_t kcode = kMagicBits - HALF;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    inv[j] = s_inv[cv * 8 + j];
+    zc[j] = s_zc[cv * 8 + j];
+    const int w = s_w[cv * 8 + j];
+    koff[j] = (uint32_t)w - HALF - kMagicBits;
+    kwin[j] = (uint32_t)(2 * w);
+  }
+  uint8_t* cbase = codes + (plane * T * Hd + col0 + cv * 8) / (PACK ? 2 : 1);
+  for (int64_t t = tl; t < T; t += 16) {
+    const uint4 d = __ldg(reinterpret_cast<const uint4*>(base + t * Hd));
+    const __half2* h = reinterpret_cast<const __half2*>(&d);
+    uint32_t c[8];
+    bool unsafe = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __half22float2(h[j]);
+      const float2 y = __ffma2_rn(f, make_float2(inv[2 * j], inv[2 * j + 1]), make_float2(zc[2 * j], zc[2 * j + 1]));
+      const uint32_t b0 = f2bits(y.x), b1 = f2bits(y.y);
+      unsafe |= ((b0 + koff[2 * j]) & FMASK) <= kwin[2 * j];
+      unsafe |= ((b1 + koff[2 * j + 1]) & FMASK) <= kwin[2 * j + 1];
+      c[2 * j] = (b0 - kcode) >> F;
+      c[2 * j + 1] = (b1 - kcode) >> F;
+    }
+    if (unsafe) {  // rare: the reference float64 ops for the values near a boundary
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float f = __half2float(reinterpret_cast<const __half*>(&d)[j]);
+        const uint32_t b = f2bits(fmaf(f, inv[j], zc[j]));
+        if (((b + koff[j]) & FMASK) <= kwin[j]) {
+          const int64_t r = plane * rows_per_plane + (col0 + cv * 8 + j) / cpr;
+          const double sd = scale[r], zd = (double)zero[r];
+          float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, sd), zd));
+          c[j] = (uint32_t)fminf(fmaxf(rr, 0.f), QMAXF);
+        }
+      }
+    }
+    if (PACK) {
+      uint32_t wv = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) wv |= (c[j] & 15u) << (4 * j);
+      __stcs(reinterpret_cast<uint32_t*>(cbase + t * Hd / 2), wv);
+    } else {
+      const uint32_t w0 = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
+      const uint32_t w1 = __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
+      __stcs(reinterpret_cast<uint2*>(cbase + t * Hd), make_uint2(w0, w1));
+    }
+  }
+}
+
+// Column dequantize for CHANNEL / HEAD kinds: each thread owns 8 columns of a strip
+// and walks the tokens with per-column constants in registers (fast path + exact
+// re-run as in k_dequant_tile).
+template <int BITS, bool PACK>
+__global__ void __launch_bounds__(256)
+k_dequant_cols(const uint8_t* __restrict__ codes, const double* __restrict__ scale, const float* __restrict__ zero,
+               int64_t T, int64_t Hd, int cpr, int64_t rows_per_plane, uint16_t* __restrict__ out) {
+  const int tid = threadIdx.x;
+  const int cv = tid & 15, tl = tid >> 4;
+  const int64_t plane = blockIdx.y;
+  const int64_t col0 = (int64_t)blockIdx.x * 128 + cv * 8;
+  double sd[8], zd[8];
+  float s32[8], zm[8];
+  bool fast = true;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t r = plane * rows_per_plane + (col0 + j) / cpr;
+    sd[j] = scale[r];
+    zd[j] = (double)zero[r];
+    s32[j] = (float)sd[j];
+    zm[j] = (float)(zd[j] + 8388608.0);
+    fast &= zd[j] == rint(zd[j]) && fabs(zd[j]) < 4194304.0 && sd[j] >= 0x1p-14 && sd[j] < 60000.0;
+  }
+  const uint8_t* cb = codes + (plane * T * Hd + col0) / (PACK ? 2 : 1);
+  uint16_t* ob = out + plane * T * Hd + col0;
+  for (int64_t t = tl; t < T; t += 16) {
+    uint32_t q[8];
+    if (PACK) {
+      const uint32_t wd = __ldcs(reinterpret_cast<const uint32_t*>(cb + t * Hd / 2));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q[j] = (wd >> (4 * j)) & 15u;
+    } else {
+      const uint2 wd = __ldcs(reinterpret_cast<const uint2*>(cb + t * Hd));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { q[j] = (wd.x >> (8 * j)) & 255u; q[4 + j] = (wd.y >> (8 * j)) & 255u; }
+    }
+    uint32_t o[4];
+    bool unsafe = !fast;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 qf = make_float2(__uint_as_float(0x4B000000u | q[2 * j]), __uint_as_float(0x4B000000u | q[2 * j + 1]));
+      const float2 d = __fadd2_rn(qf, make_float2(-zm[2 * j], -zm[2 * j + 1]));
+      const float2 y = __fmul2_rn(d, make_float2(s32[2 * j], s32[2 * j + 1]));
+      const uint32_t b0 = __float_as_uint(y.x), b1 = __float_as_uint(y.y);
+      unsafe |= ((b0 + (4u - 0x1000u)) & 0x1fffu) <= 8u;
+      unsafe |= ((b1 + (4u - 0x1000u)) & 0x1fffu) <= 8u;
+      const __half2 hv = __floats2half2_rn(y.x, y.y);
+      o[j] = *reinterpret_cast<const uint32_t*>(&hv);
+    }
+    if (unsafe) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double v = __dmul_rn(sd[j], __dsub_rn((double)q[j], zd[j]));
+        const uint32_t hb = __half_as_ushort(__double2half(v));
+        const int wi = j >> 1, sh = 16 * (j & 1);
+        o[wi] = (o[wi] & ~(0xffffu << sh)) | (hb << sh);
+      }
+    }
+    __stcs(reinterpret_cast<uint4*>(ob + t * Hd), make_uint4(o[0], o[1], o[2], o[3]));
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // Generic path, phase 1a: partial min/max of strided rows (any dtype), block per
 // (row, chunk).  partials are float64 [rows][nch].
 // ---------------------------------------------------------------------------------
