@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-planes", type=int, default=16)
     ap.add_argument("--no-pred", action="store_true")
+    ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--pred-n", type=int, default=1_000_000)
     ap.add_argument("--pred-b", type=int, default=4096)
     ap.add_argument("--pred-dim", type=int, default=768)
@@ -222,7 +223,8 @@ def link_peaks(dev_index: int):
 
 
 # ----------------------------------------------------------------- KV bench
-def kv_bench(args, world, rank, local):
+def kv_bench(args, world, rank, local, layouts=None, e2e=True):
+    """Swap pipeline over a job list (one KVLayout per job); jobs LPT-assigned to ranks."""
     import torch
 
     from paper_2410_23537_b200 import kvmanager as km
@@ -230,15 +232,18 @@ def kv_bench(args, world, rank, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    layout = km.KVLayout(args.layers, args.tokens, args.hidden, args.head_dim, kind=args.kind,
-                         group=args.group, bits=args.bits, packed=args.packed)
-    geo = layout.geometry()
-    job_bytes = layout.elements * 2
-    sizes = [job_bytes] * args.jobs
+    if layouts is None:
+        layouts = [km.KVLayout(args.layers, args.tokens, args.hidden, args.head_dim, kind=args.kind,
+                               group=args.group, bits=args.bits, packed=args.packed)] * args.jobs
+    sizes = [lay.elements * 2 for lay in layouts]
     mine = synthetic.lpt_assign(sizes, world)[rank]
-    kvs = [synthetic.kv_job_torch(args.layers, args.tokens, args.hidden, seed=0, job=j,
-                                  group=args.group if args.kind == "rows" else 64, device=dev)
-           for j in mine]
+    my_layouts = [layouts[j] for j in mine]
+    geos = [lay.geometry() for lay in my_layouts]
+    layout = my_layouts[0] if my_layouts else layouts[0]
+    geo = max(geos, key=lambda g: g["slab_bytes"]) if geos else layout.geometry()
+    kvs = [synthetic.kv_job_torch(lay.layers, lay.tokens, lay.hidden, seed=0, job=j,
+                                  group=lay.group if lay.kind == "rows" else 64, device=dev)
+           for j, lay in zip(mine, my_layouts)]
     H = max(2, args.host_slabs)
     pool = km.HostSlabPool(H * ((geo["slab_bytes"] + 255) // 256 * 256))
     slabs = [pool.alloc(geo["slab_bytes"]) for _ in range(H)]
@@ -260,17 +265,18 @@ def kv_bench(args, world, rank, local):
                     eng.depend(ev_up[s].h)      # slab s was being read by an upload
                 if up_pending[j]:               # previous step's upload wrote kvs[j]
                     km._lib.call("alise_stream_wait", km._lib.stream_ptr(), ev_job[j].h)
-                eng.offload(layout, kvs[j], slabs[s], flag=flag, event=ev_off[s].h)
+                eng.offload(my_layouts[j], kvs[j], slabs[s], flag=flag, event=ev_off[s].h)
             if j > 0:
                 s = (j - 1) % H
                 eng.depend(ev_off[s].h)         # upload reads what the offload wrote
-                eng.upload(layout, slabs[s], kvs[j - 1], event=ev_up[s].h)
+                eng.upload(my_layouts[j - 1], slabs[s], kvs[j - 1], event=ev_up[s].h)
                 km._lib.call("alise_event_record", ev_job[j - 1].h, km._lib.stream_ptr(eng.up_stream))
                 up_pending[j - 1] = True
                 used_up[s] = True
         # the step ends when both directions are done
-        for e in (ev_off[(n - 1) % H], ev_up[(n - 1) % H]):
-            km._lib.call("alise_stream_wait", km._lib.stream_ptr(), e.h)
+        if n:
+            for e in (ev_off[(n - 1) % H], ev_up[(n - 1) % H]):
+                km._lib.call("alise_stream_wait", km._lib.stream_ptr(), e.h)
 
     for _ in range(args.warmup):
         step()
@@ -295,17 +301,37 @@ def kv_bench(args, world, rank, local):
     ms = t0.elapsed_time(t1)
     ms_max = max_over_ranks(ms, world)
     bad = int(flag.item())
-    fp16_bytes_all = 2 * job_bytes * args.jobs  # out + in, every job, one step
+    fp16_bytes_all = 2 * sum(sizes)  # out + in, every job, one step
     value = fp16_bytes_all * args.steps / (ms_max / 1e3) / 1e9
-    link_bytes_rank = 2 * geo["slab_bytes"] * len(kvs) * args.steps
+    link_bytes_rank = 2 * sum(g["slab_bytes"] for g in geos) * args.steps
     link_total = sum_over_ranks(link_bytes_rank, world)
-    res = {"ms_per_step": ms_max / args.steps, "value": value, "nonfinite": bad,
+    # the same quantize kernel timed alone, device to device (no concurrent DMA / dequant)
+    iso = {}
+    if kvs:
+        d = my_layouts[0].desc()
+        dslab = torch.empty(geos[0]["slab_bytes"], dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            km._lib.call("alise_kv_quantize", km._lib.C.byref(d), km._lib.ptr(kvs[0]), km._lib.ptr(dslab),
+                         km._lib.ptr(flag), km._lib.stream_ptr())
+        torch.cuda.synchronize()
+        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        i0.record()
+        for _ in range(5):
+            km._lib.call("alise_kv_quantize", km._lib.C.byref(d), km._lib.ptr(kvs[0]), km._lib.ptr(dslab),
+                         km._lib.ptr(flag), km._lib.stream_ptr())
+        i1.record()
+        torch.cuda.synchronize()
+        iso = {"quant_ms_per_job": i0.elapsed_time(i1) / 5, "job_bytes": my_layouts[0].elements * 2,
+               "slab_bytes": geos[0]["slab_bytes"], "launches_per_job": geos[0]["n_chunks"]}
+        del dslab
+    res = {"ms_per_step": ms_max / args.steps, "value": value, "nonfinite": bad, "isolated": iso,
+           "link_bytes_per_step": link_total / args.steps,
            "link_GBs_total": link_total / (ms_max / 1e3) / 1e9,
            "quant_ms_total": qms, "quant_launches": qn, "deq_ms_total": dms, "deq_launches": dn,
            "clocks": ck, "geo": geo, "kernels_per_step": (qn + dn) / max(1, args.steps)}
 
     # e2e through the drop-in API (DeviceMemoryState), host slabs from its own pool
-    if not args.no_e2e:
+    if e2e and not args.no_e2e:
         m = km.ModelConfig("llama-2-7b", args.hidden // args.head_dim, args.layers, args.hidden)
         link_acc = km.quantized_kv_bytes(m, args.tokens, args.bits)
         gpu_b = km.kv_bytes(m, args.tokens)
@@ -480,6 +506,15 @@ def main():
     hbm_peak, bf16_peak, peak_src = load_peaks()
     links = link_peaks(local)
     kv = kv_bench(args, world, rank, local)
+    kv3 = None
+    if not args.no_c3:
+        from paper_2410_23537_b200 import kvmanager as km
+        from paper_2410_23537_b200 import synthetic
+        ctx = synthetic.sharegpt_job_tokens(256, seed=0)
+        lays = [km.KVLayout(args.layers, int(t), args.hidden, args.head_dim, kind="rows", group=64, bits=4,
+                            packed=True) for t in ctx]
+        kv3 = kv_bench(args, world, rank, local, layouts=lays, e2e=False)
+        kv3["tokens_total"] = int(ctx.sum())
     pred = None if args.no_pred else pred_bench(args, world, rank, local)
     cpu = cpu_pred = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -545,6 +580,22 @@ def main():
         }
         if "e2e" in kv:
             out["e2e"] = kv["e2e"]
+        iso = kv.get("isolated") or {}
+        if iso:
+            iso_ach = (iso["job_bytes"] + iso["slab_bytes"]) / (iso["quant_ms_per_job"] / 1e3) / 1e9
+            out["roofline_isolated"] = {"bound": "hbm", "kernel": "k_quant_tile, one 1 GiB job D2D, 5 reps",
+                                        "achieved": round(iso_ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                                        "frac": round(iso_ach / hbm_peak, 4),
+                                        "ms_per_job": round(iso["quant_ms_per_job"], 4)}
+        if kv3 is not None:
+            out["kv_c3"] = {"workload": f"C3: 256 ShareGPT-mix jobs ({kv3['tokens_total']} ctx tokens), Llama-2-7B"
+                                        f" KV, INT4 g=64 packed, LPT over {world} GPU(s)",
+                            "value": round(kv3["value"], 3), "unit": "GB/s (fp16 KV swapped out+in per s)",
+                            "ms_per_step": round(kv3["ms_per_step"], 3),
+                            "link_GBs_per_gpu": round(kv3["link_GBs_total"] / world, 2),
+                            "link_frac": round(kv3["link_GBs_total"] / world / link_peak, 4),
+                            "quant_launch_ms_avg": kv3["quant_ms_total"] / max(1, kv3["quant_launches"]),
+                            "gpu_launches": int(kv3["quant_launches"] + kv3["deq_launches"])}
         if pred is not None:
             ach = pred["scan_flops_per_launch"] / (pred["scan_ms_avg"] / 1e3) / 1e12 if pred["scan_ms_avg"] else None
             out["predictor"] = {

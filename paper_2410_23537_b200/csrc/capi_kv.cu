@@ -5,6 +5,7 @@
 #include <stdint.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -68,23 +69,47 @@ extern "C" int alise_sm_count(int device, int* out) {
 }
 
 // ------------------------------------------------------------------ fast tile launch
-template <int BITS, bool PACK, bool ZF32>
-static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
-                            double* scale, void* zero, int* flag, cudaStream_t st) {
+// Tile-kernel variant (tuning knob, ALISE_QUANT_VARIANT): 0 = values kept in
+// registers, 4 CTAs/SM; 1 = kept, 3 CTAs/SM; 2 = re-read, 4 CTAs/SM.
+static int quant_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ALISE_QUANT_VARIANT");
+    v = e ? atoi(e) : 2;
+    if (v < 0 || v > 2) v = 2;
+  }
+  return v;
+}
+
+template <int BITS, bool PACK, bool ZF32, bool KEEP, int MINB>
+static int launch_tile_var(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
+                           double* scale, void* zero, int* flag, cudaStream_t st) {
   const int vpl = (row_len / 8 + 3) / 4;  // 16-byte vectors per lane per row
-  const int64_t warps = (rows + 31) / 32;
+  const int tile_rows = !KEEP ? 32 : (vpl <= 2 ? 32 : (vpl <= 4 ? 16 : 8));
+  const int64_t warps = (rows + tile_rows - 1) / tile_rows;
   const int block = 256;
-  const int grid = grid_for(warps * 32, block, 4);
-#define TILE_CASE(V)                                                                    \
-  if (vpl <= V) {                                                                       \
-    k_quant_tile<BITS, PACK, V, ZF32><<<grid, block, 0, st>>>(x, rows, row_len, codes,  \
-                                                              scale, zero, flag);       \
-    CKL();                                                                              \
-    return ALISE_OK;                                                                    \
+  const int grid = grid_for(warps * 32, block, MINB);
+#define TILE_CASE(V)                                                                          \
+  if (vpl <= V) {                                                                             \
+    k_quant_tile<BITS, PACK, V, ZF32, KEEP, MINB><<<grid, block, 0, st>>>(x, rows, row_len,   \
+                                                                        codes, scale, zero,   \
+                                                                        flag);                \
+    CKL();                                                                                    \
+    return ALISE_OK;                                                                          \
   }
   TILE_CASE(1) TILE_CASE(2) TILE_CASE(4) TILE_CASE(8)
 #undef TILE_CASE
   return fail(ALISE_EINVAL, "row_len %d too long for the tile kernel", row_len);
+}
+
+template <int BITS, bool PACK, bool ZF32>
+static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
+                            double* scale, void* zero, int* flag, cudaStream_t st) {
+  switch (quant_variant()) {
+    case 0: return launch_tile_var<BITS, PACK, ZF32, true, 4>(x, rows, row_len, codes, scale, zero, flag, st);
+    case 1: return launch_tile_var<BITS, PACK, ZF32, true, 3>(x, rows, row_len, codes, scale, zero, flag, st);
+    default: return launch_tile_var<BITS, PACK, ZF32, false, 4>(x, rows, row_len, codes, scale, zero, flag, st);
+  }
 }
 
 static int launch_tile(int bits, bool pack, bool zf32, const uint16_t* x, int64_t rows,

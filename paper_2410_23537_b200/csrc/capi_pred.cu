@@ -186,13 +186,20 @@ extern "C" int alise_db_inexact(alise_db* db, unsigned int* count) {
   return ALISE_OK;
 }
 
-static int choose_splits(int n_qb, int n_tiles, int sms) {
-  // tile groups: one persistent CTA per (query block, group), as many groups as fit
-  // on the SMs alongside the query blocks
-  int g = std::max(1, sms / std::max(1, n_qb));
-  g = std::min(g, std::max(1, n_tiles));
-  g = std::min(g, 8192 / KMAX);
-  return g;
+// Tile groups: one persistent CTA per (query block, group).  Every SM gets a CTA:
+// query block qb owns base + (qb < extra) groups.  Returns the max groups per block.
+static int choose_groups(int n_qb, int n_tiles, int sms, int* base, int* extra) {
+  if (n_qb >= sms) {
+    *base = 1;
+    *extra = 0;
+    return 1;
+  }
+  int b = sms / n_qb, e = sms % n_qb;
+  const int cap = std::max(1, std::min(n_tiles, 8192 / KMAX));
+  if (b >= cap) { b = cap; e = 0; }
+  *base = b;
+  *extra = e;
+  return b + (e ? 1 : 0);
 }
 
 static int ensure_scratch(alise_db* db, int64_t Bp, int splits, cudaStream_t st) {
@@ -237,7 +244,8 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   const int64_t Bp = (B + BM - 1) / BM * BM;
   const int n_qb = (int)(Bp / BM);
   const int n_tiles = (int)((db->size + BN - 1) / BN);
-  const int splits = choose_splits(n_qb, n_tiles, sm_count_pred());
+  int base_g, extra_g;
+  const int splits = choose_groups(n_qb, n_tiles, sm_count_pred(), &base_g, &extra_g);
   int s = ensure_scratch(db, Bp, splits, st);
   if (s) return s;
   k_query_prep<<<(unsigned)Bp, 128, 0, st>>>(queries, B, db->dim, db->dp, db->vmax, db->q16, db->two_delta);
@@ -248,6 +256,8 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   a.n_tiles = n_tiles;
   a.n_qb = n_qb;
   a.n_splits = splits;
+  a.base_g = base_g;
+  a.extra_g = extra_g;
   a.B = (int)B;
   a.Bp = (int)Bp;
   a.k = k;
@@ -263,7 +273,7 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
     else CK(cudaFuncSetAttribute(k_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM));
     attr_set[kt] = true;
   }
-  const unsigned grid = (unsigned)std::min(n_qb * splits, sm_count_pred());
+  const unsigned grid = (unsigned)std::min(n_qb * base_g + extra_g, sm_count_pred());
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (db->timing) {
     CK(cudaEventCreate(&e0));
@@ -280,7 +290,7 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
     db->ev.push_back(e1);
   }
   CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
-  k_rescore<<<(unsigned)B, 256, 0, st>>>(splits, (int)Bp, B, k, db->size, db->dim, queries, db->v32, db->lens,
+  k_rescore<<<(unsigned)B, 256, 0, st>>>(base_g, extra_g, (int)Bp, B, k, db->size, db->dim, queries, db->v32, db->lens,
                                          db->seqs, db->two_delta, db->cand_s, db->cand_r, db->cand_n, db->topc,
                                          out_sim, out_seq, out_len, out_count, db->need, db->inexact);
   CKL();

@@ -63,11 +63,19 @@ __device__ __forceinline__ void raise_flag(int* flag, bool bad) {
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t f2bits(float f) { return __float_as_uint(f); }
 
-template <int BITS, bool PACK, int VPL, bool ZF32>
-__global__ void __launch_bounds__(256, 4)
+template <int BITS, bool PACK, int VPL, bool ZF32, bool KEEP, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
              uint8_t* __restrict__ codes, double* __restrict__ scale, void* __restrict__ zero,
              int* __restrict__ flag) {
+  // KEEP: rows per warp tile chosen so a lane holds 8 x 16 B of values (32 rows for
+  // g <= 64, 16 for g = 128, 8 for g = 256) kept in registers from load to code.
+  // !KEEP: 32-row tiles, values re-read (L1/L2) for the code pass.
+  constexpr int PASSES = !KEEP ? 4 : (VPL <= 2 ? 4 : (VPL == 4 ? 2 : 1));
+  constexpr int TILE = 8 * PASSES;
+  constexpr int F = TileMagic<BITS>::F;
+  constexpr uint32_t HALF = 1u << (F - 1);
+  constexpr uint32_t FMASK = (1u << F) - 1;
   constexpr float QMAXF = (float)((1 << BITS) - 1);
   const int lane = threadIdx.x & 31;
   const int sub = lane >> 2;  // row slot within a pass (8 rows per pass)
@@ -75,33 +83,46 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
   const int nvec = row_len >> 3;
   const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t ntiles = (rows + 31) >> 5;
-  constexpr int F = TileMagic<BITS>::F;
-  constexpr uint32_t HALF = 1u << (F - 1);
-  constexpr uint32_t FMASK = (1u << F) - 1;
+  const int64_t ntiles = (rows + TILE - 1) / TILE;
   const uint32_t kMagicBits = f2bits(TileMagic<BITS>::M);
 
   for (int64_t tile = warp_global; tile < ntiles; tile += nwarps) {
-    const int64_t row0 = tile << 5;
-    // ---------------- A: per-row min / max
-    uint32_t mine = 0;
+    const int64_t row0 = tile * TILE;
+    // ---------------- A: load the tile, per-row min / max
+    uint4 v[PASSES][VPL];
+    if (KEEP) {
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int64_t r = row0 + p * 8 + sub;
-      __half2 lo2 = __half2half2(__ushort_as_half(0x7c00)), hi2 = __half2half2(__ushort_as_half(0xfc00));
-      if (r < rows) {
-        const uint4* src = reinterpret_cast<const uint4*>(x + r * row_len);
+      for (int p = 0; p < PASSES; ++p) {
+        const int64_t r = row0 + p * 8 + sub;
+        const uint4* src = reinterpret_cast<const uint4*>(x + (r < rows ? r : 0) * row_len);
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
-          const int v = q4 + 4 * i;
-          if (v < nvec) {
-            const uint4 d = __ldg(src + v);
-            const __half2* h = reinterpret_cast<const __half2*>(&d);
+          const int vv = q4 + 4 * i;
+          v[p][i] = (r < rows && vv < nvec) ? __ldcs(src + vv) : make_uint4(0, 0, 0, 0);
+        }
+      }
+    }
+    uint32_t mine = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              lo2 = __hmin2_nan(lo2, h[k]);
-              hi2 = __hmax2_nan(hi2, h[k]);
-            }
+    for (int p = 0; p < PASSES; ++p) {
+      const int64_t r = row0 + p * 8 + sub;
+      if (!KEEP) {  // load pass by pass; the code pass re-reads
+        const uint4* src = reinterpret_cast<const uint4*>(x + (r < rows ? r : 0) * row_len);
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          const int vv = q4 + 4 * i;
+          v[p][i] = (r < rows && vv < nvec) ? __ldg(src + vv) : make_uint4(0, 0, 0, 0);
+        }
+      }
+      __half2 lo2 = __half2half2(__ushort_as_half(0x7c00)), hi2 = __half2half2(__ushort_as_half(0xfc00));
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        if (r < rows && q4 + 4 * i < nvec) {
+          const __half2* h = reinterpret_cast<const __half2*>(&v[p][i]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            lo2 = __hmin2_nan(lo2, h[k]);
+            hi2 = __hmax2_nan(hi2, h[k]);
           }
         }
       }
@@ -118,9 +139,9 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
       const uint32_t g = __shfl_sync(0xffffffffu, u, (lane & 7) << 2);
       if ((lane >> 3) == p) mine = g;
     }
-    // ---------------- B: lane-per-row parameters
+    // ---------------- B: lane-per-row parameters (lanes < TILE)
     const int64_t my_row = row0 + lane;
-    const bool own = my_row < rows;
+    const bool own = lane < TILE && my_row < rows;
     const __half2 mm = *reinterpret_cast<__half2*>(&mine);
     float fmn = __low2float(mm), fmx = -__high2float(mm);
     const bool bad = own && !(isfinite(fmn) && isfinite(fmx));
@@ -134,10 +155,19 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
       else reinterpret_cast<double*>(zero)[my_row] = q.z;
     }
     __syncwarp();  // the float64 fallback below re-reads scale / zero of other lanes' rows
-    // ---------------- C: codes
-#pragma unroll 1
-    for (int p = 0; p < 4; ++p) {
+    // ---------------- C: codes from the registers (KEEP) or a re-read (!KEEP)
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p) {
       const int src_lane = p * 8 + sub;
+      if (!KEEP) {
+        const int64_t rr0 = row0 + p * 8 + sub;
+        const uint4* src = reinterpret_cast<const uint4*>(x + (rr0 < rows ? rr0 : 0) * row_len);
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          const int vv = q4 + 4 * i;
+          v[p][i] = (rr0 < rows && vv < nvec) ? __ldg(src + vv) : make_uint4(0, 0, 0, 0);
+        }
+      }
       const float inv_s = __shfl_sync(0xffffffffu, tp.inv_s, src_lane);
       const float zc = __shfl_sync(0xffffffffu, tp.zc, src_lane);
       const int w = __shfl_sync(0xffffffffu, tp.w, src_lane);
@@ -147,80 +177,70 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
       const uint32_t koff = (uint32_t)w - HALF - kMagicBits;
       const uint32_t kwin = (uint32_t)(2 * w);
       const uint32_t kcode = kMagicBits - HALF;  // code = (bits(y) - kcode) >> F
-      const uint4* src = reinterpret_cast<const uint4*>(x + (live_row ? r : 0) * row_len);
       uint32_t cw[VPL][PACK ? 1 : 2];
       bool unsafe = false;
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
-        const int v = q4 + 4 * i;
-        if (live_row && v < nvec) {
-          const uint4 d = __ldg(src + v);
-          const __half2* h = reinterpret_cast<const __half2*>(&d);
-          uint32_t c[8];
+        const __half2* h = reinterpret_cast<const __half2*>(&v[p][i]);
+        uint32_t c[8];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float2 f = __half22float2(h[k]);
-            const float2 y = __ffma2_rn(f, make_float2(inv_s, inv_s), make_float2(zc, zc));
-            const uint32_t b0 = f2bits(y.x), b1 = f2bits(y.y);
-            unsafe |= ((b0 + koff) & FMASK) <= kwin;
-            unsafe |= ((b1 + koff) & FMASK) <= kwin;
-            c[2 * k] = (b0 - kcode) >> F;
-            c[2 * k + 1] = (b1 - kcode) >> F;
-          }
-          // out-of-range codes only occur for unsafe values (rewritten below); the
-          // packing keeps each code in its own byte / nibble so neighbours stay intact
-          if (PACK) {
-            uint32_t wv = 0;
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __half22float2(h[k]);
+          const float2 y = __ffma2_rn(f, make_float2(inv_s, inv_s), make_float2(zc, zc));
+          const uint32_t b0 = f2bits(y.x), b1 = f2bits(y.y);
+          unsafe |= ((b0 + koff) & FMASK) <= kwin;
+          unsafe |= ((b1 + koff) & FMASK) <= kwin;
+          c[2 * k] = (b0 - kcode) >> F;
+          c[2 * k + 1] = (b1 - kcode) >> F;
+        }
+        // out-of-range codes only occur for unsafe values (rewritten below); the
+        // packing keeps each code in its own byte / nibble so neighbours stay intact
+        if (PACK) {
+          uint32_t wv = 0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) wv |= (c[j] & 15u) << (4 * j);
-            cw[i][0] = wv;
-          } else {
-            cw[i][0] = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
-            cw[i][PACK ? 0 : 1] =
-                __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
-          }
+          for (int j = 0; j < 8; ++j) wv |= (c[j] & 15u) << (4 * j);
+          cw[i][0] = wv;
+        } else {
+          cw[i][0] = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
+          cw[i][PACK ? 0 : 1] =
+              __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
         }
       }
-      if (__any_sync(0xffffffffu, unsafe)) {
-        // rare: redo the values near a rounding boundary with the reference float64 ops
-        if (unsafe) {
-          const double s = scale[r];
-          const double z = ZF32 ? (double)reinterpret_cast<const float*>(zero)[r]
-                                : reinterpret_cast<const double*>(zero)[r];
-#pragma unroll
-          for (int i = 0; i < VPL; ++i) {
-            const int v = q4 + 4 * i;
-            if (v < nvec) {
-              const uint4 d = __ldg(src + v);
-              const uint16_t* hh = reinterpret_cast<const uint16_t*>(&d);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float f = h2f(hh[j]);
-                const uint32_t b = f2bits(fmaf(f, inv_s, zc));
-                if (((b + koff) & FMASK) <= kwin) {
-                  float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, s), z));
-                  rr = fminf(fmaxf(rr, 0.f), QMAXF);
-                  const uint32_t cc = (uint32_t)rr;
-                  if (PACK) {
-                    cw[i][0] = (cw[i][0] & ~(15u << (4 * j))) | (cc << (4 * j));
-                  } else {
-                    const int wi = j >> 2, sh = 8 * (j & 3);
-                    cw[i][wi] = (cw[i][wi] & ~(255u << sh)) | (cc << sh);
-                  }
-                }
-              }
-            }
-          }
-        }
-      }
+      unsafe = unsafe && live_row;
       if (live_row) {
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
-          const int v = q4 + 4 * i;
-          if (v < nvec) {
-            const int64_t e0 = r * row_len + v * 8;
+          const int vv = q4 + 4 * i;
+          if (vv < nvec) {
+            const int64_t e0 = r * row_len + vv * 8;
             if (PACK) __stcs(reinterpret_cast<uint32_t*>(codes + e0 / 2), cw[i][0]);
             else __stcs(reinterpret_cast<uint2*>(codes + e0), make_uint2(cw[i][0], cw[i][PACK ? 0 : 1]));
+          }
+        }
+      }
+      if (unsafe) {
+        // rare: the values near a rounding boundary get the reference float64 ops; a
+        // compact loop (small code) re-reads the value and patches its code in place
+        // (this lane owns all of its bytes, so the read-modify-write is race free)
+        const double sd = scale[r];
+        const double zd = ZF32 ? (double)reinterpret_cast<const float*>(zero)[r]
+                               : reinterpret_cast<const double*>(zero)[r];
+#pragma unroll 1
+        for (int e = 0; e < 8 * VPL; ++e) {
+          const int vv = q4 + 4 * (e >> 3);
+          if (vv >= nvec) continue;
+          const int64_t idx = r * row_len + vv * 8 + (e & 7);
+          const float f = h2f(x[idx]);
+          const uint32_t b = f2bits(fmaf(f, inv_s, zc));
+          if (((b + koff) & FMASK) > kwin) continue;
+          float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, sd), zd));
+          const uint32_t cc = (uint32_t)fminf(fmaxf(rr, 0.f), QMAXF);
+          if (PACK) {
+            uint8_t* pb = codes + (idx >> 1);
+            const uint32_t sh = 4 * (uint32_t)(idx & 1);
+            *pb = (uint8_t)((*pb & ~(15u << sh)) | (cc << sh));
+          } else {
+            codes[idx] = (uint8_t)cc;
           }
         }
       }

@@ -102,7 +102,9 @@ struct ScanArgs {
   int64_t n_rows;    // valid DB rows (slots [0, n_rows))
   int n_tiles;       // ceil(n_rows / BN)
   int n_qb;          // query blocks of 128
-  int n_splits;      // tile groups G: group g scans tiles g, g+G, ...
+  int n_splits;      // max tile groups per query block (candidate-list slots)
+  int base_g;        // query block qb owns G(qb) = base_g + (qb < extra_g) tile groups;
+  int extra_g;       //   group g of qb scans tiles g, g + G(qb), ...
   int B;             // real query count
   int Bp;            // padded query count
   int k;
@@ -162,8 +164,8 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
   float* stage32 = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);  // [128][33]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = a.n_splits;
-  const int n_work = a.n_qb * G;
+  // work item w -> (qb = w % n_qb, g = w / n_qb); n_work = sum over qb of G(qb)
+  const int n_work = a.n_qb * a.base_g + a.extra_g;
 
   if (warp == 0 && lane == 0) {
     sm100::prefetch_tmap(&tmQ);
@@ -190,6 +192,7 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
       uint32_t phase = 0;
       for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
         const int qb = w % a.n_qb, g = w / a.n_qb;
+        const int G = a.base_g + (qb < a.extra_g ? 1 : 0);
         for (int t = g; t < a.n_tiles; t += G) {
           for (int kb = 0; kb < a.n_kb; ++kb) {
             sm100::mbar_wait(&empty[stage], phase ^ 1);
@@ -209,7 +212,8 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
       uint32_t phase = 0;
       int i = 0;
       for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        const int g = w / a.n_qb;
+        const int qb = w % a.n_qb, g = w / a.n_qb;
+        const int G = a.base_g + (qb < a.extra_g ? 1 : 0);
         for (int t = g; t < a.n_tiles; t += G, ++i) {
           const int acc = i & 1;
           const uint32_t aph = (i >> 1) & 1;
@@ -241,6 +245,7 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
     int i = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
       const int qb = w % a.n_qb, g = w / a.n_qb;
+      const int G = a.base_g + (qb < a.extra_g ? 1 : 0);
       const int q = qb * BM + tq;
       float top[KT];
 #pragma unroll
@@ -460,7 +465,7 @@ __device__ __noinline__ double exact_dot_super(const float* __restrict__ a, cons
 // Per query: global coarse k-th from the splits' top lists, candidate compaction,
 // exact rescoring, (-sim, seq) order.  Block = 256 threads.
 __global__ void __launch_bounds__(256)
-k_rescore(int n_splits, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
+k_rescore(int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
           const float* __restrict__ v32, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
           const float* __restrict__ two_delta, const float* __restrict__ cand_s, const int32_t* __restrict__ cand_r,
           const int32_t* __restrict__ cand_n, const float* __restrict__ topc, double* __restrict__ out_sim,
@@ -481,6 +486,7 @@ k_rescore(int n_splits, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, c
   if (tid == 0) { s_n = 0; s_flag = 0; }
   // 1) kk-th largest coarse score across the splits' top lists (real rows' scores):
   //    kk rounds of block-wide argmax with removal
+  const int n_splits = base_g + ((q / BM) < extra_g ? 1 : 0);
   const int m = n_splits * k;  // host guarantees m <= 8192
   const int64_t kk = k < n_rows ? k : n_rows;
   const float NEG = -__int_as_float(0x7f800000);

@@ -64,8 +64,11 @@ def all_gather_records(local, group=None):
         buf = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
         if nccl:
             dist.all_gather_into_tensor(buf, t, group=group)
-        else:  # gloo (CPU multi-process tests)
-            dist.all_gather(list(buf.unbind(0)), t, group=group)
+        else:  # gloo (multi-process tests; CUDA tensors are staged through the host)
+            tc = t.cpu()
+            parts = [torch.empty_like(tc) for _ in range(world)]
+            dist.all_gather(parts, tc, group=group)
+            buf.copy_(torch.stack(parts))
         out.append(buf)
     return out
 

@@ -192,3 +192,52 @@ def test_c4_scale_200k_x_768(pr):
     db, lens = synthetic.predictor_db(200_000, 768, seed=0, dup_groups=200)
     Q = synthetic.predictor_queries(db, 512, seed=0)
     check_batch(pr, db, lens, Q, 8)
+
+
+def _sharded_worker(rank, world, port, result_dir):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_23537_b200 import sharding
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)  # both ranks share the one GPU; gloo carries the exchange
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = np.random.default_rng(21)
+    n, d, B, k = 6000, 96, 200, 8
+    db = g.standard_normal((n, d)).astype(np.float32)
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    db[3000:3011] = db[7]                       # tie group spanning both shards
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = np.concatenate([db[[7, 100, 4000]], g.standard_normal((B - 3, d)).astype(np.float32)])
+    Q = (Q / np.linalg.norm(Q, axis=1, keepdims=True)).astype(np.float32)
+    cap = 5000                                  # ring eviction: the oldest 1000 rows drop out
+    store = sharding.ShardedVectorStore(d, cap)
+    store.add_batch(db[:2500], lens[:2500])
+    store.add_batch(db[2500:], lens[2500:])
+    sims, seqs, slens, cnt, _ = store.search_batch(Q, k)
+    torch.cuda.synchronize()
+    live = np.arange(n - cap, n)
+    ref = po.search_exact_batch(db[live], lens[live], live, Q, k)
+    ok = all(np.array_equal(seqs[i].cpu().numpy(), r[2]) and np.array_equal(sims[i].cpu().numpy(), r[0])
+             and np.array_equal(slens[i].cpu().numpy(), r[1]) for i, r in enumerate(ref))
+    with open(os.path.join(result_dir, f"r{rank}"), "w") as fh:
+        fh.write("ok" if ok else "bad")
+    dist.destroy_process_group()
+
+
+def test_sharded_store_two_ranks_one_gpu(tmp_path):
+    """ShardedVectorStore end to end (seq % 2 shards, per-shard GPU top-k, all-gather,
+    GPU merge, FIFO eviction across shards) against the single-store oracle."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_sharded_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        assert (tmp_path / f"r{r}").read_text() == "ok"
