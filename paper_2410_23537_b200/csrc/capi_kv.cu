@@ -70,13 +70,14 @@ extern "C" int alise_sm_count(int device, int* out) {
 
 // ------------------------------------------------------------------ fast tile launch
 // Tile-kernel variant (tuning knob, ALISE_QUANT_VARIANT): 0 = values kept in
-// registers, 4 CTAs/SM; 1 = kept, 3 CTAs/SM; 2 = re-read, 4 CTAs/SM.
+// registers, 4 CTAs/SM; 1 = kept, 3 CTAs/SM; 2 = re-read, 4 CTAs/SM; 3 = cp.async
+// double-buffered shared-memory tiles (k_quant_tile_pf).
 static int quant_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("ALISE_QUANT_VARIANT");
     v = e ? atoi(e) : 2;
-    if (v < 0 || v > 2) v = 2;
+    if (v < 0 || v > 3) v = 2;
   }
   return v;
 }
@@ -103,9 +104,38 @@ static int launch_tile_var(const uint16_t* x, int64_t rows, int row_len, uint8_t
 }
 
 template <int BITS, bool PACK, bool ZF32>
+static int launch_tile_pf(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
+                          double* scale, void* zero, int* flag, cudaStream_t st) {
+  const int vpl = (row_len / 8 + 3) / 4;
+  const int tile_rows = vpl <= 2 ? 32 : (vpl <= 4 ? 16 : 8);
+  const int64_t warps = (rows + tile_rows - 1) / tile_rows;
+  const int block = 256;
+  const int grid = grid_for(warps * 32, block, 3);
+#define PF_CASE(V)                                                                            \
+  if (vpl <= V) {                                                                             \
+    constexpr int P = V <= 2 ? 4 : (V == 4 ? 2 : 1);                                          \
+    const int smem = 8 * 2 * (8 * P) * (64 * V + 16);                                         \
+    static bool attr = false;                                                                 \
+    if (!attr) {                                                                              \
+      CK(cudaFuncSetAttribute(k_quant_tile_pf<BITS, PACK, V, ZF32>,                           \
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));            \
+      attr = true;                                                                            \
+    }                                                                                         \
+    k_quant_tile_pf<BITS, PACK, V, ZF32><<<grid, block, smem, st>>>(x, rows, row_len, codes,  \
+                                                                    scale, zero, flag);       \
+    CKL();                                                                                    \
+    return ALISE_OK;                                                                          \
+  }
+  PF_CASE(1) PF_CASE(2) PF_CASE(4) PF_CASE(8)
+#undef PF_CASE
+  return fail(ALISE_EINVAL, "row_len %d too long for the tile kernel", row_len);
+}
+
+template <int BITS, bool PACK, bool ZF32>
 static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
                             double* scale, void* zero, int* flag, cudaStream_t st) {
   switch (quant_variant()) {
+    case 3: return launch_tile_pf<BITS, PACK, ZF32>(x, rows, row_len, codes, scale, zero, flag, st);
     case 0: return launch_tile_var<BITS, PACK, ZF32, true, 4>(x, rows, row_len, codes, scale, zero, flag, st);
     case 1: return launch_tile_var<BITS, PACK, ZF32, true, 3>(x, rows, row_len, codes, scale, zero, flag, st);
     default: return launch_tile_var<BITS, PACK, ZF32, false, 4>(x, rows, row_len, codes, scale, zero, flag, st);

@@ -248,6 +248,190 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
   }
 }
 
+// Prefetching variant of k_quant_tile: each warp double-buffers its tiles in shared
+// memory with cp.async (16-byte LDGSTS, rows padded by 16 B so the 4 lanes x 8 rows
+// of a load phase hit distinct banks); tile i+1 streams in while tile i is reduced,
+// solved and coded.  Same arithmetic and outputs as k_quant_tile.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int sz = pred ? 16 : 0;  // zero-fill when out of range
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int BITS, bool PACK, int VPL, bool ZF32>
+__global__ void __launch_bounds__(256, 3)
+k_quant_tile_pf(const uint16_t* __restrict__ x, int64_t rows, int row_len,
+                uint8_t* __restrict__ codes, double* __restrict__ scale, void* __restrict__ zero,
+                int* __restrict__ flag) {
+  constexpr int PASSES = VPL <= 2 ? 4 : (VPL == 4 ? 2 : 1);
+  constexpr int TILE = 8 * PASSES;
+  constexpr int ROWB = 64 * VPL + 16;  // padded smem row (bytes): 4 lanes x VPL x 16 B + 16
+  constexpr int F = TileMagic<BITS>::F;
+  constexpr uint32_t HALF = 1u << (F - 1);
+  constexpr uint32_t FMASK = (1u << F) - 1;
+  constexpr float QMAXF = (float)((1 << BITS) - 1);
+  extern __shared__ uint8_t smem_pf[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  uint8_t* wbuf = smem_pf + wib * (2 * TILE * ROWB);
+  const int sub = lane >> 2;
+  const int q4 = lane & 3;
+  const int nvec = row_len >> 3;
+  const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ntiles = (rows + TILE - 1) / TILE;
+  const uint32_t kMagicBits = f2bits(TileMagic<BITS>::M);
+
+  auto prefetch = [&](int64_t tile, int slot) {
+    uint8_t* b = wbuf + slot * (TILE * ROWB);
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p) {
+      const int rl = p * 8 + sub;
+      const int64_t r = tile * TILE + rl;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int vv = q4 + 4 * i;
+        const bool ok = tile < ntiles && r < rows && vv < nvec;
+        const uint16_t* g = x + (ok ? r * row_len + vv * 8 : 0);
+        cp_async16(b + rl * ROWB + (q4 + 4 * i) * 16, g, ok);
+      }
+    }
+    cp_async_commit();
+  };
+
+  int slot = 0;
+  prefetch(warp_global, 0);
+  for (int64_t tile = warp_global; tile < ntiles; tile += nwarps, slot ^= 1) {
+    prefetch(tile + nwarps, slot ^ 1);
+    cp_async_wait<1>();
+    __syncwarp();
+    const uint8_t* b = wbuf + slot * (TILE * ROWB);
+    const int64_t row0 = tile * TILE;
+    // ---------------- A: per-row min / max from shared memory
+    uint32_t mine = 0;
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p) {
+      const int rl = p * 8 + sub;
+      const int64_t r = row0 + rl;
+      __half2 lo2 = __half2half2(__ushort_as_half(0x7c00)), hi2 = __half2half2(__ushort_as_half(0xfc00));
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        if (r < rows && q4 + 4 * i < nvec) {
+          const uint4 d = *reinterpret_cast<const uint4*>(b + rl * ROWB + (q4 + 4 * i) * 16);
+          const __half2* h = reinterpret_cast<const __half2*>(&d);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            lo2 = __hmin2_nan(lo2, h[k]);
+            hi2 = __hmax2_nan(hi2, h[k]);
+          }
+        }
+      }
+      const __half mn = __hmin_nan(__low2half(lo2), __high2half(lo2));
+      const __half mx = __hmax_nan(__low2half(hi2), __high2half(hi2));
+      __half2 pk = __halves2half2(mn, __hneg(mx));
+      uint32_t u = *reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        uint32_t w = __shfl_xor_sync(0xffffffffu, u, o);
+        __half2 c = __hmin2_nan(*reinterpret_cast<__half2*>(&u), *reinterpret_cast<__half2*>(&w));
+        u = *reinterpret_cast<uint32_t*>(&c);
+      }
+      const uint32_t g = __shfl_sync(0xffffffffu, u, (lane & 7) << 2);
+      if ((lane >> 3) == p) mine = g;
+    }
+    // ---------------- B: lane-per-row parameters (lanes < TILE)
+    const int64_t my_row = row0 + lane;
+    const bool own = lane < TILE && my_row < rows;
+    const __half2 mm = *reinterpret_cast<__half2*>(&mine);
+    float fmn = __low2float(mm), fmx = -__high2float(mm);
+    const bool bad = own && !(isfinite(fmn) && isfinite(fmx));
+    raise_flag(flag, bad);
+    if (!own || bad) { fmn = 0.f; fmx = 0.f; }
+    const QParams q = make_params((double)fmn, (double)fmx, BITS, false);
+    const TileParams tp = make_tile_params<BITS>(q, fmax(fabs((double)fmn), fabs((double)fmx)));
+    if (own) {
+      scale[my_row] = q.s;
+      if (ZF32) reinterpret_cast<float*>(zero)[my_row] = (float)q.z;
+      else reinterpret_cast<double*>(zero)[my_row] = q.z;
+    }
+    __syncwarp();
+    // ---------------- C: codes from shared memory
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p) {
+      const int rl = p * 8 + sub;
+      const float inv_s = __shfl_sync(0xffffffffu, tp.inv_s, rl);
+      const float zc = __shfl_sync(0xffffffffu, tp.zc, rl);
+      const int w = __shfl_sync(0xffffffffu, tp.w, rl);
+      const int64_t r = row0 + rl;
+      const bool live_row = r < rows;
+      const uint32_t koff = (uint32_t)w - HALF - kMagicBits;
+      const uint32_t kwin = (uint32_t)(2 * w);
+      const uint32_t kcode = kMagicBits - HALF;
+      bool unsafe = false;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int vv = q4 + 4 * i;
+        if (!(live_row && vv < nvec)) continue;
+        const uint4 d = *reinterpret_cast<const uint4*>(b + rl * ROWB + vv * 16);
+        const __half2* h = reinterpret_cast<const __half2*>(&d);
+        uint32_t c[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __half22float2(h[k]);
+          const float2 y = __ffma2_rn(f, make_float2(inv_s, inv_s), make_float2(zc, zc));
+          const uint32_t b0 = f2bits(y.x), b1 = f2bits(y.y);
+          unsafe |= ((b0 + koff) & FMASK) <= kwin;
+          unsafe |= ((b1 + koff) & FMASK) <= kwin;
+          c[2 * k] = (b0 - kcode) >> F;
+          c[2 * k + 1] = (b1 - kcode) >> F;
+        }
+        const int64_t e0 = r * row_len + vv * 8;
+        if (PACK) {
+          uint32_t wv = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) wv |= (c[j] & 15u) << (4 * j);
+          __stcs(reinterpret_cast<uint32_t*>(codes + e0 / 2), wv);
+        } else {
+          const uint32_t w0 = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
+          const uint32_t w1 = __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
+          __stcs(reinterpret_cast<uint2*>(codes + e0), make_uint2(w0, w1));
+        }
+      }
+      if (unsafe) {
+        // rare: float64 reference ops for values near a rounding boundary; this lane
+        // owns every byte it patches
+        const double sd = scale[r];
+        const double zd = ZF32 ? (double)reinterpret_cast<const float*>(zero)[r]
+                               : reinterpret_cast<const double*>(zero)[r];
+#pragma unroll 1
+        for (int e = 0; e < 8 * VPL; ++e) {
+          const int vv = q4 + 4 * (e >> 3);
+          if (vv >= nvec) continue;
+          const uint16_t hv = *reinterpret_cast<const uint16_t*>(b + rl * ROWB + vv * 16 + 2 * (e & 7));
+          const float f = h2f(hv);
+          const uint32_t bb = f2bits(fmaf(f, inv_s, zc));
+          if (((bb + koff) & FMASK) > kwin) continue;
+          const float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, sd), zd));
+          const uint32_t cc = (uint32_t)fminf(fmaxf(rr, 0.f), QMAXF);
+          const int64_t idx = r * row_len + vv * 8 + (e & 7);
+          if (PACK) {
+            uint8_t* pb = codes + (idx >> 1);
+            const uint32_t sh = 4 * (uint32_t)(idx & 1);
+            *pb = (uint8_t)((*pb & ~(15u << sh)) | (cc << sh));
+          } else {
+            codes[idx] = (uint8_t)cc;
+          }
+        }
+      }
+    }
+    __syncwarp();  // all lanes are done with this slot before it is refilled
+  }
+  cp_async_wait<0>();
+}
+
 // Fast dequantize of ROWS-kind codes (row_len % 8 == 0) to fp16.  Each thread owns 8
 // values of one row.  y = fp32(s) * ((2^23+q) - (2^23+z)) is exact up to two fp32
 // roundings; fp16(y) equals fp16(float64 s*(q-z)) unless y is within 4 fp32 ulps of an

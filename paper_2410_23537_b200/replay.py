@@ -1,0 +1,140 @@
+"""Config-5 trace replay: drive the real KV data plane with the swap-call stream of the
+reference simulator.
+
+``tests/golden/record_c5.py`` runs the reference ``servesim.simcore.run`` (speculative
+policy, Alpaca arrivals, Llama-2-13B, INT8 KV, 8 replicas) with a recording
+``MemoryState`` and stores every ``start_offload`` / ``start_upload`` / ``complete``
+call with the ledger after it.  ``replay`` re-issues those calls, in order, on a
+``DeviceMemoryState`` whose jobs are bound to real fp16 KV tensors in HBM, so each
+offload quantizes a job and streams it to pinned host memory and each upload brings
+it back dequantized.  It checks after every call that the ledger (GPU/CPU bytes,
+swap counts and bytes) equals the reference's, and that every job's KV after its
+first round trip equals the device-to-device quantize/dequantize of its original.
+"""
+from __future__ import annotations
+
+import gzip
+import json
+import time
+
+from . import kvmanager as km
+
+
+def load(path):
+    with gzip.open(path, "rt") as fh:
+        return json.load(fh)
+
+
+def tokens_of(link_bytes: int, layers: int, hidden: int, bits: int) -> int:
+    """Invert quantized_kv_bytes (kvmanager.py:69-82) for the job's token count."""
+    ch = 2 * layers * hidden
+    per = (bits + 7) // 8
+    t, rem = divmod(link_bytes - ch * km.SCALE_ZP_BYTES, ch * per)
+    if rem or t <= 0:
+        raise ValueError(f"link bytes {link_bytes} are not a quantized KV footprint")
+    return t
+
+
+def replay(rec: dict, replica: int = 0, group: int = 128, check_data: bool = True, seed: int = 0,
+           max_events: int | None = None):
+    """Replay one replica's swap calls; returns a summary dict."""
+    import torch
+
+    from . import synthetic
+
+    layers, hidden, heads = rec["model"]
+    bits = rec["bits"]
+    events = rec["replicas"][replica]["events"]
+    if max_events:
+        events = events[:max_events]
+    f = {name: i for i, name in enumerate(rec["fields"])}
+    # pinned pool: the peak of concurrently held host slabs (+ alignment slack)
+    peak_cpu = max(e[f["cpu_used"]] for e in events) if events else 0
+    ms = km.DeviceMemoryState(gpu_capacity=rec["gpu_capacity"], cpu_capacity=rec["cpu_capacity"],
+                              pcie_bytes_per_ms=rec["pcie_bytes_per_ms"],
+                              host_pool_bytes=int(peak_cpu * 1.02) + (256 << 20))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    kv = {}          # job -> tensor
+    expect = {}      # job -> D2D round-trip reference (checked after the first upload)
+    inflight = {}    # job -> TransferCommand
+    mismatches = 0
+    data_checked = 0
+    moved = 0
+    # each job's KV is materialised at its first offloaded size (and its D2D round-trip
+    # reference computed) before the timed replay; jobs that decode while resident grow
+    # between swaps, which the replay applies outside the timed region
+    for e in events:
+        op, job, link = e[0], e[1], e[2]
+        if op != "o" or job in kv:
+            continue
+        T = tokens_of(link, layers, hidden, bits)
+        lay = km.KVLayout(layers, T, hidden, hidden // heads, kind="rows", group=group, bits=bits)
+        t = synthetic.kv_job_torch(layers, T, hidden, seed=seed, job=job, group=group, device=dev)
+        kv[job] = (t, lay)
+        if check_data:
+            g = lay.geometry()
+            slab = torch.empty(g["slab_bytes"], dtype=torch.uint8, device=dev)
+            flag = torch.zeros(1, dtype=torch.int32, device=dev)
+            ref = torch.empty_like(t)
+            km._lib.call("alise_kv_quantize", km._lib.C.byref(lay.desc()), km._lib.ptr(t),
+                         km._lib.ptr(slab), km._lib.ptr(flag), km._lib.stream_ptr())
+            km._lib.call("alise_kv_dequantize", km._lib.C.byref(lay.desc()), km._lib.ptr(slab),
+                         km._lib.ptr(ref), km._lib.stream_ptr())
+            expect[job] = ref
+        ms.bind(job, t, lay)
+    torch.cuda.synchronize()
+    paused = 0.0
+    t_start = time.perf_counter()
+    for e in events:
+        op, job, link, gpu_b, t0, t1 = e[0], e[1], e[2], e[3], e[4], e[5]
+        # the engine reserves / releases bytes directly between swap calls (KV growth,
+        # admissions, completions); adopt its ledger before each call, check after
+        ms.gpu_used, ms.cpu_used = e[f["gpu_before"]], e[f["cpu_before"]]
+        if op == "o":
+            T = tokens_of(link, layers, hidden, bits)
+            if T != kv[job][1].tokens:
+                # the job decoded while resident: grow its KV (engine work, not timed)
+                torch.cuda.synchronize()
+                tp = time.perf_counter()
+                old, lay0 = kv[job]
+                extra = synthetic.kv_job_torch(layers, T - lay0.tokens, hidden, seed=seed + 1, job=job,
+                                               group=group, device=dev)
+                t = torch.cat([old, extra], dim=2).contiguous()
+                lay = km.KVLayout(layers, T, hidden, hidden // heads, kind="rows", group=group, bits=bits)
+                kv[job] = (t, lay)
+                expect.pop(job, None)
+                ms.bind(job, t, lay)
+                torch.cuda.synchronize()
+                paused += time.perf_counter() - tp
+            inflight[job] = ms.start_offload(job, link, gpu_b, t0)
+            moved += 2 * kv[job][1].elements
+        elif op == "u":
+            inflight[job] = ms.start_upload(job, link, gpu_b, t0)
+            moved += 2 * kv[job][1].elements
+        else:
+            cmd = inflight.pop(job)
+            ms.complete(cmd)
+            if cmd.direction == "upload" and job in expect:
+                torch.cuda.synchronize()
+                if not torch.equal(kv[job][0], expect[job]):
+                    mismatches += 1
+                data_checked += 1
+                del expect[job]
+        got = (ms.gpu_used, ms.cpu_used, ms.swap_in_count, ms.swap_out_count, ms.swap_in_bytes,
+               ms.swap_out_bytes)
+        want = tuple(e[f[k]] for k in ("gpu_used", "cpu_used", "swap_in_count", "swap_out_count",
+                                       "swap_in_bytes", "swap_out_bytes"))
+        if got != want:
+            raise AssertionError(f"ledger diverged at {e}: got {got} want {want}")
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_start - paused
+    modeled_s = (max((e[5] for e in events), default=0) - min((e[4] for e in events), default=0)) / 1e6
+    link_total = ms.swap_in_bytes + ms.swap_out_bytes
+    out = {"replica": replica, "events": len(events), "swaps_out": ms.swap_out_count,
+           "swaps_in": ms.swap_in_count, "link_bytes": link_total, "fp16_bytes_moved": moved,
+           "wall_s": wall, "fp16_GBs": moved / wall / 1e9 if wall else None,
+           "link_GBs": link_total / wall / 1e9 if wall else None,
+           "modeled_span_s": modeled_s, "data_checked": data_checked, "data_mismatches": mismatches}
+    ms.host_pool.close()
+    ms.engine.close()
+    return out

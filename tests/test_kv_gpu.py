@@ -275,3 +275,19 @@ def test_llama7b_job_round_trip_properties(km):
     # |x - deq| <= scale/2 (+ fp16 output rounding of the dequantized value)
     bound = span / 255 / 2 + kv.float().view(-1, 128).abs().amax(1) * 2 ** -11 + 1e-6
     assert bool((err <= bound).all())
+
+
+@pytest.mark.slow
+def test_c5_replay_matches_reference_ledger():
+    """Config-5 replay (tests/golden/c5_swaps.json.gz, recorded from the reference
+    simulator): every swap call moves real quantized KV through DeviceMemoryState, the
+    ledger equals the reference after every call, and each job's KV after its first
+    round trip equals the device-to-device quantize/dequantize of its original."""
+    import os
+
+    from paper_2410_23537_b200 import replay
+    from tests.conftest import GOLDEN
+    rec = replay.load(os.path.join(GOLDEN, "c5_swaps.json.gz"))
+    out = replay.replay(rec, replica=3, max_events=1200)
+    assert out["swaps_out"] > 100 and out["data_checked"] > 10
+    assert out["data_mismatches"] == 0
