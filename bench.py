@@ -123,7 +123,8 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -133,7 +134,8 @@ def sum_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -142,6 +144,16 @@ def barrier(world: int):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
+
+
+def load_traffic():
+    """DRAM bytes per value / per flop measured by one ncu --set full capture of each
+    kernel (profiles/traffic.json, written from the committed ncu summaries)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
 
 
 def load_peaks():
@@ -499,12 +511,21 @@ def main():
     if args.impl == "reference":
         return reference_arm(args, world, rank)
     import torch
+    ndev = max(1, torch.cuda.device_count())
+    if local >= ndev:
+        # test mode only: more ranks than GPUs share devices (needs a non-NCCL backend)
+        local = local % ndev
+    backend = os.environ.get("ALISE_BENCH_BACKEND", "nccl")
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     hbm_peak, bf16_peak, peak_src = load_peaks()
+    traffic = load_traffic()
     links = link_peaks(local)
     kv = kv_bench(args, world, rank, local)
     kv3 = None
@@ -578,7 +599,9 @@ def main():
                          "unit": "GB/s", "frac": round(q_ach / hbm_peak, 4) if q_ach else None,
                          "peak_source": peak_src,
                          "bytes_per_launch": q_bytes, "avg_launch_ms": q_avg_ms,
-                         "traffic": None},
+                         "traffic": (round(traffic["k_quant_tile"]["dram_bytes_per_value"] * chunk_elems)
+                                     if "k_quant_tile" in traffic else None),
+                         "traffic_source": traffic.get("k_quant_tile", {}).get("source")},
             "roofline_dequant": {"bound": "hbm", "kernel": "k_dequant", "achieved":
                                  round(d_ach, 1) if d_ach else None, "peak": hbm_peak,
                                  "frac": round(d_ach / hbm_peak, 4) if d_ach else None,
@@ -630,7 +653,9 @@ def main():
                              "achieved": round(ach, 1) if ach else None, "peak": bf16_peak, "unit": "TFLOP/s",
                              "frac": round(ach / bf16_peak, 4) if ach else None, "peak_source": peak_src,
                              "flops_per_launch": pred["scan_flops_per_launch"],
-                             "avg_launch_ms": pred["scan_ms_avg"], "traffic": None},
+                             "avg_launch_ms": pred["scan_ms_avg"],
+                             "traffic": traffic.get("k_scan", {}).get("dram_bytes_per_launch"),
+                             "traffic_source": traffic.get("k_scan", {}).get("source")},
                 "e2e": pred["e2e"], "inexact_candidates": pred["inexact"],
                 "retrieved_frac": round(pred["retrieved_frac"], 4),
                 "gpu_launches_per_step": 5 + (2 if world > 1 else 0),

@@ -175,6 +175,13 @@ int alise_predict_finish(int64_t B, int k, const double *sims, const int32_t *le
                          int64_t hidden, int64_t max_len, double log_cap, int32_t *out_len,
                          uint8_t *out_retrieved, void *stream);
 
+/* Batched HashingEmbedder.embed (predictor.py:66-100): prompts are tokens[offsets[b] ..
+ * offsets[b+1]) (int64, device); writes float64 [B][dim] (bit-identical to the
+ * reference) and/or fp32 [B][dim] (either may be NULL).  Empty prompts are the
+ * caller's error (the reference raises PredictorError). */
+int alise_embed_batch(const int64_t *tokens, const int64_t *offsets, int64_t B, int64_t dim,
+                      double *out_f64, float *out_f32, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

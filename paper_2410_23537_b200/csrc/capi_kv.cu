@@ -69,77 +69,35 @@ extern "C" int alise_sm_count(int device, int* out) {
 }
 
 // ------------------------------------------------------------------ fast tile launch
-// Tile-kernel variant (tuning knob, ALISE_QUANT_VARIANT): 0 = values kept in
-// registers, 4 CTAs/SM; 1 = kept, 3 CTAs/SM; 2 = re-read, 4 CTAs/SM; 3 = cp.async
-// double-buffered shared-memory tiles (k_quant_tile_pf).
-static int quant_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("ALISE_QUANT_VARIANT");
-    v = e ? atoi(e) : 2;
-    if (v < 0 || v > 3) v = 2;
-  }
-  return v;
-}
-
-template <int BITS, bool PACK, bool ZF32, bool KEEP, int MINB>
-static int launch_tile_var(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
-                           double* scale, void* zero, int* flag, cudaStream_t st) {
-  const int vpl = (row_len / 8 + 3) / 4;  // 16-byte vectors per lane per row
-  const int tile_rows = !KEEP ? 32 : (vpl <= 2 ? 32 : (vpl <= 4 ? 16 : 8));
-  const int64_t warps = (rows + tile_rows - 1) / tile_rows;
+template <int BITS, bool PACK, bool ZF32, int V, int TP>
+static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes, double* scale,
+                         void* zero, int* flag, cudaStream_t st) {
   const int block = 256;
-  const int grid = grid_for(warps * 32, block, MINB);
-#define TILE_CASE(V)                                                                          \
-  if (vpl <= V) {                                                                             \
-    k_quant_tile<BITS, PACK, V, ZF32, KEEP, MINB><<<grid, block, 0, st>>>(x, rows, row_len,   \
-                                                                        codes, scale, zero,   \
-                                                                        flag);                \
-    CKL();                                                                                    \
-    return ALISE_OK;                                                                          \
+  const int smem = (block / 32) * 2 * (8 * TP) * (64 * V + 16);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_quant_tile<BITS, PACK, V, ZF32, TP>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
   }
-  TILE_CASE(1) TILE_CASE(2) TILE_CASE(4) TILE_CASE(8)
-#undef TILE_CASE
-  return fail(ALISE_EINVAL, "row_len %d too long for the tile kernel", row_len);
-}
-
-template <int BITS, bool PACK, bool ZF32>
-static int launch_tile_pf(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
-                          double* scale, void* zero, int* flag, cudaStream_t st) {
-  const int vpl = (row_len / 8 + 3) / 4;
-  const int tile_rows = vpl <= 2 ? 32 : (vpl <= 4 ? 16 : 8);
-  const int64_t warps = (rows + tile_rows - 1) / tile_rows;
-  const int block = 256;
-  const int grid = grid_for(warps * 32, block, 3);
-#define PF_CASE(V)                                                                            \
-  if (vpl <= V) {                                                                             \
-    constexpr int P = V <= 2 ? 4 : (V == 4 ? 2 : 1);                                          \
-    const int smem = 8 * 2 * (8 * P) * (64 * V + 16);                                         \
-    static bool attr = false;                                                                 \
-    if (!attr) {                                                                              \
-      CK(cudaFuncSetAttribute(k_quant_tile_pf<BITS, PACK, V, ZF32>,                           \
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));            \
-      attr = true;                                                                            \
-    }                                                                                         \
-    k_quant_tile_pf<BITS, PACK, V, ZF32><<<grid, block, smem, st>>>(x, rows, row_len, codes,  \
-                                                                    scale, zero, flag);       \
-    CKL();                                                                                    \
-    return ALISE_OK;                                                                          \
-  }
-  PF_CASE(1) PF_CASE(2) PF_CASE(4) PF_CASE(8)
-#undef PF_CASE
-  return fail(ALISE_EINVAL, "row_len %d too long for the tile kernel", row_len);
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quant_tile<BITS, PACK, V, ZF32, TP>, block, smem));
+  const int64_t warps = (rows + 8 * TP - 1) / (8 * TP);
+  const int grid = grid_for(warps * 32, block, std::max(1, per_sm));
+  k_quant_tile<BITS, PACK, V, ZF32, TP><<<grid, block, smem, st>>>(x, rows, row_len, codes, scale, zero, flag);
+  CKL();
+  return ALISE_OK;
 }
 
 template <int BITS, bool PACK, bool ZF32>
 static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
                             double* scale, void* zero, int* flag, cudaStream_t st) {
-  switch (quant_variant()) {
-    case 3: return launch_tile_pf<BITS, PACK, ZF32>(x, rows, row_len, codes, scale, zero, flag, st);
-    case 0: return launch_tile_var<BITS, PACK, ZF32, true, 4>(x, rows, row_len, codes, scale, zero, flag, st);
-    case 1: return launch_tile_var<BITS, PACK, ZF32, true, 3>(x, rows, row_len, codes, scale, zero, flag, st);
-    default: return launch_tile_var<BITS, PACK, ZF32, false, 4>(x, rows, row_len, codes, scale, zero, flag, st);
-  }
+  const int vpl = (row_len / 8 + 3) / 4;  // 16-byte vectors per lane per row
+  if (vpl <= 1) return launch_tile_v<BITS, PACK, ZF32, 1, 4>(x, rows, row_len, codes, scale, zero, flag, st);
+  if (vpl <= 2) return launch_tile_v<BITS, PACK, ZF32, 2, 4>(x, rows, row_len, codes, scale, zero, flag, st);
+  if (vpl <= 4) return launch_tile_v<BITS, PACK, ZF32, 4, 2>(x, rows, row_len, codes, scale, zero, flag, st);
+  if (vpl <= 8) return launch_tile_v<BITS, PACK, ZF32, 8, 1>(x, rows, row_len, codes, scale, zero, flag, st);
+  return fail(ALISE_EINVAL, "row_len %d too long for the tile kernel", row_len);
 }
 
 static int launch_tile(int bits, bool pack, bool zf32, const uint16_t* x, int64_t rows,

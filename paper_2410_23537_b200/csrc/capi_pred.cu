@@ -13,6 +13,7 @@
 
 #include "../../include/alise_b200.h"
 #include "pred_scan.cuh"
+#include "embed.cuh"
 
 namespace alise {
 int fail(int code, const char* fmt, ...);
@@ -346,6 +347,15 @@ extern "C" int alise_predict_finish(int64_t B, int k, const double* sims, const 
   k_finish<<<(unsigned)((threads + 255) / 256), 256, 0, S(stream)>>>(B, k, sims, lens, counts, s0, queries, dim, W1,
                                                                      b1, w2, b2, hidden, max_len, log_cap, out_len,
                                                                      out_retrieved);
+  CKL();
+  return ALISE_OK;
+}
+
+extern "C" int alise_embed_batch(const int64_t* tokens, const int64_t* offsets, int64_t B, int64_t dim,
+                                 double* out_f64, float* out_f32, void* stream) {
+  if (dim < 1 || dim > 8192) return fail(ALISE_EINVAL, "dimension must be in [1, 8192]");
+  if (B == 0) return ALISE_OK;
+  alise::emb::k_embed<<<(unsigned)B, 256, dim * sizeof(int), S(stream)>>>(tokens, offsets, dim, out_f64, out_f32);
   CKL();
   return ALISE_OK;
 }

@@ -12,10 +12,10 @@
 //   kind HEAD    : rows are (layer, k|v, head) over tokens x head_dim
 //
 // Hot path (ROWS, fp16, row_len <= 256): one fused single-pass kernel
-// (k_quant_tile) — 128-bit coalesced loads of a 32-row tile per warp,
-// warp-shuffle min/max, lane-per-row float64 parameter solve, codes from
-// registers, 64/32-bit coalesced stores.  HBM traffic = 2 B read + b/8 B written
-// per element + 12-16 B per row.
+// (k_quant_tile) — cp.async double-buffered warp tiles in shared memory,
+// half2 min/max + warp shuffles, lane-per-row float64 parameter solve, fp32x2
+// codes with a proven exactness window, 64/32-bit coalesced stores.  HBM traffic =
+// 2 B read + b/8 B written per element + 12-16 B per row.
 // Other shapes use a three-phase path: partial min/max -> per-row params -> codes.
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -63,195 +63,9 @@ __device__ __forceinline__ void raise_flag(int* flag, bool bad) {
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t f2bits(float f) { return __float_as_uint(f); }
 
-template <int BITS, bool PACK, int VPL, bool ZF32, bool KEEP, int MINB>
-__global__ void __launch_bounds__(256, MINB)
-k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
-             uint8_t* __restrict__ codes, double* __restrict__ scale, void* __restrict__ zero,
-             int* __restrict__ flag) {
-  // KEEP: rows per warp tile chosen so a lane holds 8 x 16 B of values (32 rows for
-  // g <= 64, 16 for g = 128, 8 for g = 256) kept in registers from load to code.
-  // !KEEP: 32-row tiles, values re-read (L1/L2) for the code pass.
-  constexpr int PASSES = !KEEP ? 4 : (VPL <= 2 ? 4 : (VPL == 4 ? 2 : 1));
-  constexpr int TILE = 8 * PASSES;
-  constexpr int F = TileMagic<BITS>::F;
-  constexpr uint32_t HALF = 1u << (F - 1);
-  constexpr uint32_t FMASK = (1u << F) - 1;
-  constexpr float QMAXF = (float)((1 << BITS) - 1);
-  const int lane = threadIdx.x & 31;
-  const int sub = lane >> 2;  // row slot within a pass (8 rows per pass)
-  const int q4 = lane & 3;    // lane within the row
-  const int nvec = row_len >> 3;
-  const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t ntiles = (rows + TILE - 1) / TILE;
-  const uint32_t kMagicBits = f2bits(TileMagic<BITS>::M);
-
-  for (int64_t tile = warp_global; tile < ntiles; tile += nwarps) {
-    const int64_t row0 = tile * TILE;
-    // ---------------- A: load the tile, per-row min / max
-    uint4 v[PASSES][VPL];
-    if (KEEP) {
-#pragma unroll
-      for (int p = 0; p < PASSES; ++p) {
-        const int64_t r = row0 + p * 8 + sub;
-        const uint4* src = reinterpret_cast<const uint4*>(x + (r < rows ? r : 0) * row_len);
-#pragma unroll
-        for (int i = 0; i < VPL; ++i) {
-          const int vv = q4 + 4 * i;
-          v[p][i] = (r < rows && vv < nvec) ? __ldcs(src + vv) : make_uint4(0, 0, 0, 0);
-        }
-      }
-    }
-    uint32_t mine = 0;
-#pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      const int64_t r = row0 + p * 8 + sub;
-      if (!KEEP) {  // load pass by pass; the code pass re-reads
-        const uint4* src = reinterpret_cast<const uint4*>(x + (r < rows ? r : 0) * row_len);
-#pragma unroll
-        for (int i = 0; i < VPL; ++i) {
-          const int vv = q4 + 4 * i;
-          v[p][i] = (r < rows && vv < nvec) ? __ldg(src + vv) : make_uint4(0, 0, 0, 0);
-        }
-      }
-      __half2 lo2 = __half2half2(__ushort_as_half(0x7c00)), hi2 = __half2half2(__ushort_as_half(0xfc00));
-#pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        if (r < rows && q4 + 4 * i < nvec) {
-          const __half2* h = reinterpret_cast<const __half2*>(&v[p][i]);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            lo2 = __hmin2_nan(lo2, h[k]);
-            hi2 = __hmax2_nan(hi2, h[k]);
-          }
-        }
-      }
-      const __half mn = __hmin_nan(__low2half(lo2), __high2half(lo2));
-      const __half mx = __hmax_nan(__low2half(hi2), __high2half(hi2));
-      __half2 pk = __halves2half2(mn, __hneg(mx));
-      uint32_t u = *reinterpret_cast<uint32_t*>(&pk);
-#pragma unroll
-      for (int o = 1; o < 4; o <<= 1) {
-        uint32_t w = __shfl_xor_sync(0xffffffffu, u, o);
-        __half2 c = __hmin2_nan(*reinterpret_cast<__half2*>(&u), *reinterpret_cast<__half2*>(&w));
-        u = *reinterpret_cast<uint32_t*>(&c);
-      }
-      const uint32_t g = __shfl_sync(0xffffffffu, u, (lane & 7) << 2);
-      if ((lane >> 3) == p) mine = g;
-    }
-    // ---------------- B: lane-per-row parameters (lanes < TILE)
-    const int64_t my_row = row0 + lane;
-    const bool own = lane < TILE && my_row < rows;
-    const __half2 mm = *reinterpret_cast<__half2*>(&mine);
-    float fmn = __low2float(mm), fmx = -__high2float(mm);
-    const bool bad = own && !(isfinite(fmn) && isfinite(fmx));
-    raise_flag(flag, bad);
-    if (!own || bad) { fmn = 0.f; fmx = 0.f; }
-    const QParams q = make_params((double)fmn, (double)fmx, BITS, false);
-    const TileParams tp = make_tile_params<BITS>(q, fmax(fabs((double)fmn), fabs((double)fmx)));
-    if (own) {
-      scale[my_row] = q.s;
-      if (ZF32) reinterpret_cast<float*>(zero)[my_row] = (float)q.z;
-      else reinterpret_cast<double*>(zero)[my_row] = q.z;
-    }
-    __syncwarp();  // the float64 fallback below re-reads scale / zero of other lanes' rows
-    // ---------------- C: codes from the registers (KEEP) or a re-read (!KEEP)
-#pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      const int src_lane = p * 8 + sub;
-      if (!KEEP) {
-        const int64_t rr0 = row0 + p * 8 + sub;
-        const uint4* src = reinterpret_cast<const uint4*>(x + (rr0 < rows ? rr0 : 0) * row_len);
-#pragma unroll
-        for (int i = 0; i < VPL; ++i) {
-          const int vv = q4 + 4 * i;
-          v[p][i] = (rr0 < rows && vv < nvec) ? __ldg(src + vv) : make_uint4(0, 0, 0, 0);
-        }
-      }
-      const float inv_s = __shfl_sync(0xffffffffu, tp.inv_s, src_lane);
-      const float zc = __shfl_sync(0xffffffffu, tp.zc, src_lane);
-      const int w = __shfl_sync(0xffffffffu, tp.w, src_lane);
-      const int64_t r = row0 + src_lane;
-      const bool live_row = r < rows;
-      // unsafe iff ((bits(y) - bits(M) - HALF + w) & FMASK) <= 2w
-      const uint32_t koff = (uint32_t)w - HALF - kMagicBits;
-      const uint32_t kwin = (uint32_t)(2 * w);
-      const uint32_t kcode = kMagicBits - HALF;  // code = (bits(y) - kcode) >> F
-      uint32_t cw[VPL][PACK ? 1 : 2];
-      bool unsafe = false;
-#pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        const __half2* h = reinterpret_cast<const __half2*>(&v[p][i]);
-        uint32_t c[8];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 f = __half22float2(h[k]);
-          const float2 y = __ffma2_rn(f, make_float2(inv_s, inv_s), make_float2(zc, zc));
-          const uint32_t b0 = f2bits(y.x), b1 = f2bits(y.y);
-          unsafe |= ((b0 + koff) & FMASK) <= kwin;
-          unsafe |= ((b1 + koff) & FMASK) <= kwin;
-          c[2 * k] = (b0 - kcode) >> F;
-          c[2 * k + 1] = (b1 - kcode) >> F;
-        }
-        // out-of-range codes only occur for unsafe values (rewritten below); the
-        // packing keeps each code in its own byte / nibble so neighbours stay intact
-        if (PACK) {
-          uint32_t wv = 0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) wv |= (c[j] & 15u) << (4 * j);
-          cw[i][0] = wv;
-        } else {
-          cw[i][0] = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
-          cw[i][PACK ? 0 : 1] =
-              __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
-        }
-      }
-      unsafe = unsafe && live_row;
-      if (live_row) {
-#pragma unroll
-        for (int i = 0; i < VPL; ++i) {
-          const int vv = q4 + 4 * i;
-          if (vv < nvec) {
-            const int64_t e0 = r * row_len + vv * 8;
-            if (PACK) __stcs(reinterpret_cast<uint32_t*>(codes + e0 / 2), cw[i][0]);
-            else __stcs(reinterpret_cast<uint2*>(codes + e0), make_uint2(cw[i][0], cw[i][PACK ? 0 : 1]));
-          }
-        }
-      }
-      if (unsafe) {
-        // rare: the values near a rounding boundary get the reference float64 ops; a
-        // compact loop (small code) re-reads the value and patches its code in place
-        // (this lane owns all of its bytes, so the read-modify-write is race free)
-        const double sd = scale[r];
-        const double zd = ZF32 ? (double)reinterpret_cast<const float*>(zero)[r]
-                               : reinterpret_cast<const double*>(zero)[r];
-#pragma unroll 1
-        for (int e = 0; e < 8 * VPL; ++e) {
-          const int vv = q4 + 4 * (e >> 3);
-          if (vv >= nvec) continue;
-          const int64_t idx = r * row_len + vv * 8 + (e & 7);
-          const float f = h2f(x[idx]);
-          const uint32_t b = f2bits(fmaf(f, inv_s, zc));
-          if (((b + koff) & FMASK) > kwin) continue;
-          float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, sd), zd));
-          const uint32_t cc = (uint32_t)fminf(fmaxf(rr, 0.f), QMAXF);
-          if (PACK) {
-            uint8_t* pb = codes + (idx >> 1);
-            const uint32_t sh = 4 * (uint32_t)(idx & 1);
-            *pb = (uint8_t)((*pb & ~(15u << sh)) | (cc << sh));
-          } else {
-            codes[idx] = (uint8_t)cc;
-          }
-        }
-      }
-    }
-  }
-}
-
-// Prefetching variant of k_quant_tile: each warp double-buffers its tiles in shared
-// memory with cp.async (16-byte LDGSTS, rows padded by 16 B so the 4 lanes x 8 rows
-// of a load phase hit distinct banks); tile i+1 streams in while tile i is reduced,
-// solved and coded.  Same arithmetic and outputs as k_quant_tile.
+// Each warp double-buffers its tiles in shared memory with cp.async (16-byte LDGSTS,
+// rows padded by 16 B so the 4 lanes x 8 rows of a load phase hit distinct banks):
+// tile i+1 streams in while tile i is reduced, solved and coded.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   const int sz = pred ? 16 : 0;  // zero-fill when out of range
@@ -261,12 +75,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int BITS, bool PACK, int VPL, bool ZF32>
+template <int BITS, bool PACK, int VPL, bool ZF32, int TP>
 __global__ void __launch_bounds__(256, 3)
-k_quant_tile_pf(const uint16_t* __restrict__ x, int64_t rows, int row_len,
+k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
                 uint8_t* __restrict__ codes, double* __restrict__ scale, void* __restrict__ zero,
                 int* __restrict__ flag) {
-  constexpr int PASSES = VPL <= 2 ? 4 : (VPL == 4 ? 2 : 1);
+  // TP = passes of 8 rows per warp tile: 32-row tiles for g <= 64, 16 for g = 128,
+  // 8 for g = 256 (a lane stages 8 x 16 B per tile; 3 CTAs x 8 warps per SM)
+  constexpr int PASSES = TP;
   constexpr int TILE = 8 * PASSES;
   constexpr int ROWB = 64 * VPL + 16;  // padded smem row (bytes): 4 lanes x VPL x 16 B + 16
   constexpr int F = TileMagic<BITS>::F;
@@ -359,6 +175,10 @@ k_quant_tile_pf(const uint16_t* __restrict__ x, int64_t rows, int row_len,
     }
     __syncwarp();
     // ---------------- C: codes from shared memory
+    // full tiles (every row live, every lane's vectors in range) take an unpredicated
+    // path with immediate offsets; the code byte comes straight from the mantissa of
+    // y + (1.5*2^23 - M) (round-to-nearest; exact ties are flagged unsafe anyway)
+    const bool full = (row0 + TILE <= rows) && (nvec == 4 * VPL);
 #pragma unroll
     for (int p = 0; p < PASSES; ++p) {
       const int rl = p * 8 + sub;
@@ -369,60 +189,71 @@ k_quant_tile_pf(const uint16_t* __restrict__ x, int64_t rows, int row_len,
       const bool live_row = r < rows;
       const uint32_t koff = (uint32_t)w - HALF - kMagicBits;
       const uint32_t kwin = (uint32_t)(2 * w);
-      const uint32_t kcode = kMagicBits - HALF;
+      const float2 inv2 = make_float2(inv_s, inv_s), zc2 = make_float2(zc, zc);
+      const float2 shift2 = make_float2(12582912.0f - TileMagic<BITS>::M, 12582912.0f - TileMagic<BITS>::M);
+      const uint8_t* srow = b + rl * ROWB + q4 * 16;
+      uint8_t* crow = codes + (r * row_len + q4 * 8) / (PACK ? 2 : 1);
       bool unsafe = false;
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
-        const int vv = q4 + 4 * i;
-        if (!(live_row && vv < nvec)) continue;
-        const uint4 d = *reinterpret_cast<const uint4*>(b + rl * ROWB + vv * 16);
+        if (!full && !(live_row && q4 + 4 * i < nvec)) continue;
+        const uint4 d = *reinterpret_cast<const uint4*>(srow + i * 64);
         const __half2* h = reinterpret_cast<const __half2*>(&d);
         uint32_t c[8];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float2 f = __half22float2(h[k]);
-          const float2 y = __ffma2_rn(f, make_float2(inv_s, inv_s), make_float2(zc, zc));
-          const uint32_t b0 = f2bits(y.x), b1 = f2bits(y.y);
-          unsafe |= ((b0 + koff) & FMASK) <= kwin;
-          unsafe |= ((b1 + koff) & FMASK) <= kwin;
-          c[2 * k] = (b0 - kcode) >> F;
-          c[2 * k + 1] = (b1 - kcode) >> F;
+          const float2 y = __ffma2_rn(f, inv2, zc2);
+          const float2 y2 = __fadd2_rn(y, shift2);
+          unsafe |= ((f2bits(y.x) + koff) & FMASK) <= kwin;
+          unsafe |= ((f2bits(y.y) + koff) & FMASK) <= kwin;
+          c[2 * k] = f2bits(y2.x);
+          c[2 * k + 1] = f2bits(y2.y);
         }
-        const int64_t e0 = r * row_len + vv * 8;
         if (PACK) {
           uint32_t wv = 0;
 #pragma unroll
           for (int j = 0; j < 8; ++j) wv |= (c[j] & 15u) << (4 * j);
-          __stcs(reinterpret_cast<uint32_t*>(codes + e0 / 2), wv);
+          __stcs(reinterpret_cast<uint32_t*>(crow + i * 16), wv);
         } else {
           const uint32_t w0 = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
           const uint32_t w1 = __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
-          __stcs(reinterpret_cast<uint2*>(codes + e0), make_uint2(w0, w1));
+          __stcs(reinterpret_cast<uint2*>(crow + i * 32), make_uint2(w0, w1));
         }
       }
       if (unsafe) {
-        // rare: float64 reference ops for values near a rounding boundary; this lane
+        // rare: float64 reference ops for values near a rounding boundary; vectors are
+        // re-checked 8 values at a time and only flagged values are redone; this lane
         // owns every byte it patches
         const double sd = scale[r];
         const double zd = ZF32 ? (double)reinterpret_cast<const float*>(zero)[r]
                                : reinterpret_cast<const double*>(zero)[r];
 #pragma unroll 1
-        for (int e = 0; e < 8 * VPL; ++e) {
-          const int vv = q4 + 4 * (e >> 3);
+        for (int i = 0; i < VPL; ++i) {
+          const int vv = q4 + 4 * i;
           if (vv >= nvec) continue;
-          const uint16_t hv = *reinterpret_cast<const uint16_t*>(b + rl * ROWB + vv * 16 + 2 * (e & 7));
-          const float f = h2f(hv);
-          const uint32_t bb = f2bits(fmaf(f, inv_s, zc));
-          if (((bb + koff) & FMASK) > kwin) continue;
-          const float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, sd), zd));
-          const uint32_t cc = (uint32_t)fminf(fmaxf(rr, 0.f), QMAXF);
-          const int64_t idx = r * row_len + vv * 8 + (e & 7);
-          if (PACK) {
-            uint8_t* pb = codes + (idx >> 1);
-            const uint32_t sh = 4 * (uint32_t)(idx & 1);
-            *pb = (uint8_t)((*pb & ~(15u << sh)) | (cc << sh));
-          } else {
-            codes[idx] = (uint8_t)cc;
+          const uint4 d = *reinterpret_cast<const uint4*>(srow + i * 64);
+          const uint16_t* hh = reinterpret_cast<const uint16_t*>(&d);
+          uint32_t m = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t bb = f2bits(fmaf(h2f(hh[j]), inv_s, zc));
+            m |= (((bb + koff) & FMASK) <= kwin ? 1u : 0u) << j;
+          }
+          while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const uint16_t hv = *reinterpret_cast<const uint16_t*>(srow + i * 64 + 2 * j);
+            const float rr = (float)rint(__dadd_rn(__ddiv_rn((double)h2f(hv), sd), zd));
+            const uint32_t cc = (uint32_t)fminf(fmaxf(rr, 0.f), QMAXF);
+            const int64_t idx = r * row_len + vv * 8 + j;
+            if (PACK) {
+              uint8_t* pb = codes + (idx >> 1);
+              const uint32_t sh = 4 * (uint32_t)(idx & 1);
+              *pb = (uint8_t)((*pb & ~(15u << sh)) | (cc << sh));
+            } else {
+              codes[idx] = (uint8_t)cc;
+            }
           }
         }
       }

@@ -114,6 +114,26 @@ class HashingEmbedder:
             v[0], n = 1.0, 1.0
         return v / n
 
+    def embed_batch(self, prompts, dtype=None, stream=None):
+        """Embed many prompts on the GPU (alise_embed_batch); bit-identical to ``embed``.
+        Returns a CUDA tensor [B, dimension] (float64 by default, or float32)."""
+        import torch
+        lens = [len(p) for p in prompts]
+        if any(n == 0 for n in lens):
+            raise PredictorError("cannot embed an empty token sequence")
+        _lib.require_cuda()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        flat = torch.tensor([int(t) for p in prompts for t in p], dtype=torch.int64)
+        offs = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int64)
+        flat, offs = flat.to(dev), offs.to(dev)
+        dtype = dtype or torch.float64
+        out = torch.empty((len(prompts), self.dimension), dtype=dtype, device=dev)
+        o64 = out if dtype == torch.float64 else None
+        o32 = out if dtype == torch.float32 else None
+        _lib.call("alise_embed_batch", _lib.ptr(flat), _lib.ptr(offs), len(prompts), self.dimension,
+                  _lib.ptr(o64), _lib.ptr(o32), _lib.stream_ptr(stream))
+        return out
+
 
 def load_precomputed_embeddings(path) -> dict:
     """JSON-lines {"id", "vector"}, re-normalised (predictor.py:103-117)."""
@@ -277,6 +297,23 @@ class VectorStore:
             for i in np.argsort(seqs):
                 fh.write(json.dumps({"seq": int(seqs[i]), "len": int(lens[i]),
                                      "vector": [float(x) for x in vecs[i]]}) + "\n")
+
+    def save_binary(self, path):
+        """Binary snapshot (npz: fp32 vectors, lengths, seqs in insert order) — the
+        GPU-native counterpart of the JSON-lines ``save`` (predictor.py:170-178)."""
+        vecs, lens, seqs = self.export()
+        order = np.argsort(seqs)
+        np.savez(path, vectors=vecs[order].astype(np.float32), lens=lens[order], seqs=seqs[order],
+                 dimension=self.dimension, capacity=self.capacity)
+
+    @classmethod
+    def load_binary(cls, path, capacity: int | None = None) -> "VectorStore":
+        """Re-adds the records in insert order (new seqs from 0, like ``load``)."""
+        z = np.load(path)
+        store = cls(int(z["dimension"]), int(capacity or z["capacity"]))
+        if len(z["lens"]):
+            store.add_batch(z["vectors"], z["lens"])
+        return store
 
     @classmethod
     def load(cls, path, dimension: int, capacity: int) -> "VectorStore":

@@ -241,3 +241,36 @@ def test_sharded_store_two_ranks_one_gpu(tmp_path):
     mp.spawn(_sharded_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     for r in range(2):
         assert (tmp_path / f"r{r}").read_text() == "ok"
+
+
+def test_gpu_embedder_bit_identical_to_reference_hashing(pr):
+    import torch
+    g = np.random.default_rng(8)
+    prompts = [g.integers(-5, 70000, size=int(g.integers(1, 300))).tolist() for _ in range(200)]
+    prompts += [[5], [9, 9, 9], list(range(50)), [-1, 0, 1]]
+    for dim in (64, 768):
+        emb = pr.HashingEmbedder(dim)
+        out = emb.embed_batch(prompts).cpu().numpy()
+        ref = np.stack([emb.embed(p) for p in prompts])
+        assert np.array_equal(out, ref)
+        o32 = emb.embed_batch(prompts, dtype=torch.float32).cpu().numpy()
+        assert np.array_equal(o32, ref.astype(np.float32))
+    with pytest.raises(pr.PredictorError):
+        pr.HashingEmbedder(8).embed_batch([[1, 2], []])
+
+
+def test_binary_snapshot_round_trip(pr, tmp_path):
+    import torch
+    g = np.random.default_rng(12)
+    d = 48
+    store = pr.VectorStore(d, 500)
+    rows = g.standard_normal((700, d)).astype(np.float32)
+    store.add_batch(rows, np.arange(1, 701))
+    store.save_binary(tmp_path / "db.npz")
+    loaded = pr.VectorStore.load_binary(tmp_path / "db.npz")
+    Q = rows[[650, 699, 100]]
+    a = store.search_batch(Q, 8)
+    b = loaded.search_batch(Q, 8)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[2], b[2])
+    assert torch.equal(a[1] - 200, b[1])  # re-added from seq 0 in the same order
