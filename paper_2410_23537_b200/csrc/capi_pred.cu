@@ -6,6 +6,7 @@
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <string>
@@ -77,6 +78,7 @@ struct alise_db {
   unsigned int* vmax = nullptr;     // float bits of the max row norm
   unsigned int* inexact = nullptr;  // candidates whose rounding could not be certified
   CUtensorMap tmD;
+  CUtensorMap tmD2;  // 128-row boxes for the 2-SM scan
   // query scratch
   int64_t bp_cap = 0;
   int splits_cap = 0;
@@ -113,6 +115,8 @@ extern "C" int alise_db_create(int device, int64_t capacity, int64_t dim, alise_
   CK(cudaMemset(db->vmax, 0, 2 * sizeof(unsigned int)));
   db->inexact = db->vmax + 1;
   int s = make_map(&db->tmD, db->v16, db->cap_p, db->dp, BN);
+  if (s) return s;
+  s = make_map(&db->tmD2, db->v16, db->cap_p, db->dp, BN / 2);
   if (s) return s;
   *out = db;
   return ALISE_OK;
@@ -242,11 +246,20 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
     CK(cudaMemsetAsync(out_count, 0, sizeof(int32_t) * B, st));
     return ALISE_OK;
   }
-  const int64_t Bp = (B + BM - 1) / BM * BM;
-  const int n_qb = (int)(Bp / BM);
+  // 2-SM (cta_group::2) scan for batches above one query block; 1-SM otherwise
+  static int force = -2;
+  if (force == -2) {
+    const char* e = getenv("ALISE_SCAN_2SM");
+    force = e ? atoi(e) : -1;
+  }
+  const bool two_sm = force == -1 ? (B > BM) : (force != 0);
+  const int qblk = two_sm ? 2 * BM : BM;
+  const int64_t Bp = (B + qblk - 1) / qblk * qblk;
+  const int n_qb = (int)(Bp / qblk);
   const int n_tiles = (int)((db->size + BN - 1) / BN);
+  const int units = two_sm ? sm_count_pred() / 2 : sm_count_pred();
   int base_g, extra_g;
-  const int splits = choose_groups(n_qb, n_tiles, sm_count_pred(), &base_g, &extra_g);
+  const int splits = choose_groups(n_qb, n_tiles, units, &base_g, &extra_g);
   int s = ensure_scratch(db, Bp, splits, st);
   if (s) return s;
   k_query_prep<<<(unsigned)Bp, 128, 0, st>>>(queries, B, db->dim, db->dp, db->vmax, db->q16, db->two_delta);
@@ -267,14 +280,19 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   a.cand_r = db->cand_r;
   a.cand_n = db->cand_n;
   a.topc = db->topc;
-  static bool attr_set[2] = {false, false};
-  const int kt = k <= 8 ? 0 : 1;
+  static bool attr_set[4] = {false, false, false, false};
+  const int kt = (k <= 8 ? 0 : 1) + (two_sm ? 2 : 0);
   if (!attr_set[kt]) {
-    if (kt == 0) CK(cudaFuncSetAttribute(k_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM));
-    else CK(cudaFuncSetAttribute(k_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM));
+    switch (kt) {
+      case 0: CK(cudaFuncSetAttribute(k_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM)); break;
+      case 1: CK(cudaFuncSetAttribute(k_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM)); break;
+      case 2: CK(cudaFuncSetAttribute(k_scan2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN2_SMEM)); break;
+      default: CK(cudaFuncSetAttribute(k_scan2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN2_SMEM)); break;
+    }
     attr_set[kt] = true;
   }
-  const unsigned grid = (unsigned)std::min(n_qb * base_g + extra_g, sm_count_pred());
+  const int work = n_qb * base_g + extra_g;
+  const unsigned grid = two_sm ? (unsigned)(2 * std::min(work, units)) : (unsigned)std::min(work, units);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (db->timing) {
     CK(cudaEventCreate(&e0));
@@ -282,8 +300,12 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
     CK(cudaEventRecord(e0, st));
     db->scan_flops += 2.0 * (double)B * (double)db->size * (double)db->dim;
   }
-  if (kt == 0) k_scan<8><<<grid, 192, SCAN_SMEM, st>>>(db->tmQ, db->tmD, a);
-  else k_scan<16><<<grid, 192, SCAN_SMEM, st>>>(db->tmQ, db->tmD, a);
+  switch (kt) {
+    case 0: k_scan<8><<<grid, 192, SCAN_SMEM, st>>>(db->tmQ, db->tmD, a); break;
+    case 1: k_scan<16><<<grid, 192, SCAN_SMEM, st>>>(db->tmQ, db->tmD, a); break;
+    case 2: k_scan2<8><<<grid, 192, SCAN2_SMEM, st>>>(db->tmQ, db->tmD2, a); break;
+    default: k_scan2<16><<<grid, 192, SCAN2_SMEM, st>>>(db->tmQ, db->tmD2, a); break;
+  }
   CKL();
   if (db->timing) {
     CK(cudaEventRecord(e1, st));
@@ -291,7 +313,7 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
     db->ev.push_back(e1);
   }
   CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
-  k_rescore<<<(unsigned)B, 256, 0, st>>>(base_g, extra_g, (int)Bp, B, k, db->size, db->dim, queries, db->v32, db->lens,
+  k_rescore<<<(unsigned)B, 256, 0, st>>>(qblk, base_g, extra_g, (int)Bp, B, k, db->size, db->dim, queries, db->v32, db->lens,
                                          db->seqs, db->two_delta, db->cand_s, db->cand_r, db->cand_n, db->topc,
                                          out_sim, out_seq, out_len, out_count, db->need, db->inexact);
   CKL();

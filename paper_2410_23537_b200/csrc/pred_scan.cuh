@@ -325,6 +325,197 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
   }
 }
 
+// ------------------------------------------------------------------ 2-SM scan
+// cta_group::2 variant: a CTA pair (cluster of 2 on one TPC) computes 256 queries x
+// 256 DB rows per tile with one UMMA M=256 stream issued by the leader; each CTA
+// stages its own 128 queries (A) and its half of the 256 DB rows (B), so shared-memory
+// and L2 traffic per MMA drop by a third versus the 1-SM kernel.  TMA of both CTAs
+// completes on the leader's full barrier; the leader's commits are multicast to both
+// CTAs (stage-free and accumulator-full); both CTAs' epilogues release the TMEM
+// accumulator to the leader.  Epilogue logic is the same as k_scan.
+constexpr int STAGES2 = 6;
+constexpr int A2_BYTES = BM * BK * 2;         // 16 KB: this CTA's 128 queries
+constexpr int B2_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's 128 DB rows
+constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
+constexpr int SCAN2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 256 + BM * 33 * 4;
+
+template <int KT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmD, const ScanArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tfull = empty + STAGES2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stage32 = reinterpret_cast<float*>(smem + STAGES2 * STAGE2_BYTES + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = sm100::cluster_ctarank();
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int n_work = a.n_qb * a.base_g + a.extra_g;  // n_qb counts query pairs (256 queries)
+
+  if (warp == 0 && lane == 0) {
+    sm100::prefetch_tmap(&tmQ);
+    sm100::prefetch_tmap(&tmD);
+    for (int s = 0; s < STAGES2; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&tfull[s], 1);
+      sm100::mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy used)
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 2) sm100::tmem_alloc_2sm<512>(tmem_slot);
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = pair; w < n_work; w += n_pairs) {
+        const int qp = w % a.n_qb, g = w / a.n_qb;
+        const int G = a.base_g + (qp < a.extra_g ? 1 : 0);
+        for (int t = g; t < a.n_tiles; t += G) {
+          for (int kb = 0; kb < a.n_kb; ++kb) {
+            sm100::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * STAGE2_BYTES;
+            if (rank == 0) sm100::mbar_arrive_expect_tx(&full[stage], 2 * STAGE2_BYTES);
+            const uint32_t fb = sm100::mapa(sm100::smem_u32(&full[stage]), 0);
+            sm100::tma_load_2d_2sm(&tmQ, sa, fb, kb * BK, qp * 2 * BM + (int)rank * BM);
+            sm100::tma_load_2d_2sm(&tmD, sa + A2_BYTES, fb, kb * BK, t * BN + (int)rank * (BN / 2));
+            if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader CTA, one thread)
+      constexpr uint32_t idesc = sm100::idesc_f16_f32(2 * BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int i = 0;
+      for (int w = pair; w < n_work; w += n_pairs) {
+        const int qp = w % a.n_qb, g = w / a.n_qb;
+        const int G = a.base_g + (qp < a.extra_g ? 1 : 0);
+        for (int t = g; t < a.n_tiles; t += G, ++i) {
+          const int acc = i & 1;
+          const uint32_t aph = (i >> 1) & 1;
+          sm100::mbar_wait(&tempty[acc], aph ^ 1);
+          sm100::tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * BN;
+          for (int kb = 0; kb < a.n_kb; ++kb) {
+            sm100::mbar_wait(&full[stage], phase);
+            sm100::tc_fence_after();
+            const uint32_t a0 = sm100::smem_u32(smem + stage * STAGE2_BYTES);
+            const uint32_t b0 = a0 + A2_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              sm100::umma_f16_2sm(d_tmem, sm100::umma_desc_sw128(a0 + kk * 32),
+                                  sm100::umma_desc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+            }
+            sm100::umma_commit_2sm(&empty[stage], 0x3);
+            if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+          }
+          sm100::umma_commit_2sm(&tfull[acc], 0x3);
+        }
+      }
+    }
+  } else {  // ---------------- epilogue: warps 2..5 of both CTAs, thread = query
+    const int quarter = warp & 3;
+    const int tq = quarter * 32 + lane;
+    float* my_stage = stage32 + tq * 33;
+    const int k = a.k;
+    const uint32_t tempty_leader0 = sm100::mapa(sm100::smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = sm100::mapa(sm100::smem_u32(&tempty[1]), 0);
+    int i = 0;
+    for (int w = pair; w < n_work; w += n_pairs) {
+      const int qp = w % a.n_qb, g = w / a.n_qb;
+      const int G = a.base_g + (qp < a.extra_g ? 1 : 0);
+      const int q = qp * 2 * BM + (int)rank * BM + tq;
+      float top[KT];
+#pragma unroll
+      for (int x = 0; x < KT; ++x) top[x] = -__int_as_float(0x7f800000);
+      const float td = a.two_delta[q];
+      float thr = q < a.B ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
+      float kth = -__int_as_float(0x7f800000);
+      int cnt = 0;
+      bool ovf = false;
+      const size_t base = ((size_t)g * a.Bp + q);
+      float* cs = a.cand_s + base * CAP;
+      int32_t* cr = a.cand_r + base * CAP;
+      for (int t = g; t < a.n_tiles; t += G, ++i) {
+        const int acc = i & 1;
+        const uint32_t aph = (i >> 1) & 1;
+        sm100::mbar_wait(&tfull[acc], aph);
+        sm100::tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          sm100::tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, v);
+          float m8[8];
+#pragma unroll
+          for (int x = 0; x < 8; ++x) m8[x] = fmaxf(fmaxf(v[4 * x], v[4 * x + 1]), fmaxf(v[4 * x + 2], v[4 * x + 3]));
+          const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+          const bool hit = mx >= thr;
+          if (__any_sync(0xffffffffu, hit)) {
+            uint32_t mask = 0;
+#pragma unroll
+            for (int x = 0; x < 32; ++x) {
+              my_stage[x] = v[x];
+              mask |= (v[x] >= thr ? 1u : 0u) << x;
+            }
+            const int rbase = t * BN + c * 32;
+            if (rbase + 32 > a.n_rows) mask &= (a.n_rows > rbase) ? (0xffffffffu >> (32 - (a.n_rows - rbase))) : 0u;
+            while (mask) {
+              const int j = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const float sc = my_stage[j];
+              if (!(sc >= thr)) continue;
+              if (sc > kth) {
+                kth = topk_insert<KT>(top, sc, k);
+                thr = kth - td;
+              }
+              if (ovf) continue;
+              if (cnt == CAP) {
+                cnt = compact_candidates(cs, cr, thr);
+                if (cnt == CAP) {
+                  ovf = true;
+                  continue;
+                }
+              }
+              cs[cnt] = sc;
+              cr[cnt] = rbase + j;
+              ++cnt;
+            }
+          }
+        }
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      }
+      a.cand_n[base] = ovf ? -1 : cnt;
+#pragma unroll
+      for (int x = 0; x < KT; ++x)
+        if (x < k) a.topc[base * KMAX + x] = top[x];
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::cluster_sync();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc_2sm<512>(tmem_base);
+  }
+}
+
 // ------------------------------------------------------------------ exact rescoring
 struct DD {
   double hi, lo, ab;
@@ -465,7 +656,7 @@ __device__ __noinline__ double exact_dot_super(const float* __restrict__ a, cons
 // Per query: global coarse k-th from the splits' top lists, candidate compaction,
 // exact rescoring, (-sim, seq) order.  Block = 256 threads.
 __global__ void __launch_bounds__(256)
-k_rescore(int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
+k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
           const float* __restrict__ v32, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
           const float* __restrict__ two_delta, const float* __restrict__ cand_s, const int32_t* __restrict__ cand_r,
           const int32_t* __restrict__ cand_n, const float* __restrict__ topc, double* __restrict__ out_sim,
@@ -486,7 +677,7 @@ k_rescore(int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n_rows, int
   if (tid == 0) { s_n = 0; s_flag = 0; }
   // 1) kk-th largest coarse score across the splits' top lists (real rows' scores):
   //    kk rounds of block-wide argmax with removal
-  const int n_splits = base_g + ((q / BM) < extra_g ? 1 : 0);
+  const int n_splits = base_g + ((q / qblk) < extra_g ? 1 : 0);
   const int m = n_splits * k;  // host guarantees m <= 8192
   const int64_t kk = k < n_rows ? k : n_rows;
   const float NEG = -__int_as_float(0x7f800000);
