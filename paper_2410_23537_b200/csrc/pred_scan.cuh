@@ -265,9 +265,19 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
         sm100::mbar_wait(&tfull[acc], aph);
         sm100::tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c2 = 0; c2 < BN / 64; ++c2) {
+          // two TMEM loads in flight per wait
+          uint32_t r0[32], r1[32];
+          const uint32_t ta = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c2 * 64;
+          sm100::tmem_ld32_async(ta, r0);
+          sm100::tmem_ld32_async(ta + 32, r1);
+          sm100::tmem_wait_ld();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+          const int c = 2 * c2 + h;
           float v[32];
-          sm100::tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, v);
+#pragma unroll
+          for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(h ? r1[x] : r0[x]);
           // hot path: one max-reduction and one compare per 32 scores
           float m8[8];
 #pragma unroll
@@ -305,6 +315,7 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
               cr[cnt] = rbase + j;
               ++cnt;
             }
+          }
           }
         }
         sm100::tc_fence_before();
@@ -456,9 +467,19 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
         sm100::mbar_wait(&tfull[acc], aph);
         sm100::tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c2 = 0; c2 < BN / 64; ++c2) {
+          // two TMEM loads in flight per wait
+          uint32_t r0[32], r1[32];
+          const uint32_t ta = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c2 * 64;
+          sm100::tmem_ld32_async(ta, r0);
+          sm100::tmem_ld32_async(ta + 32, r1);
+          sm100::tmem_wait_ld();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+          const int c = 2 * c2 + h;
           float v[32];
-          sm100::tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, v);
+#pragma unroll
+          for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(h ? r1[x] : r0[x]);
           float m8[8];
 #pragma unroll
           for (int x = 0; x < 8; ++x) m8[x] = fmaxf(fmaxf(v[4 * x], v[4 * x + 1]), fmaxf(v[4 * x + 2], v[4 * x + 3]));
@@ -495,6 +516,7 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
               cr[cnt] = rbase + j;
               ++cnt;
             }
+          }
           }
         }
         sm100::tc_fence_before();
