@@ -51,6 +51,10 @@ extern "C" {
 const char *alise_last_error(void);
 int alise_version(void);
 int alise_sm_count(int device, int *out);
+/* Self-test of the quantizer's constant-divisor division (qmath.cuh qdiv) against
+ * __ddiv_rn on n device doubles x: adds the count of bit mismatches of x/(2^bits-1)
+ * to *mismatches (device int64).  Test support, not part of the reference interface. */
+int alise_selftest_qdiv(const double *x, int64_t n, int bits, int64_t *mismatches, void *stream);
 
 /* ---------------------------------------------------------------- quantizer ---- */
 /* Drop-in for kvmanager.quantize: rows x row_len values (row i at src + i*row_stride

@@ -68,35 +68,79 @@ extern "C" int alise_sm_count(int device, int* out) {
   return ALISE_OK;
 }
 
-// ------------------------------------------------------------------ fast tile launch
-template <int BITS, bool PACK, bool ZF32, int V, int TP>
-static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes, double* scale,
-                         void* zero, int* flag, cudaStream_t st) {
-  const int block = 256;
-  const int smem = (block / 32) * 2 * (8 * TP) * (64 * V + 16);
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_quant_tile<BITS, PACK, V, ZF32, TP>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
+__global__ void k_selftest_qdiv(const double* __restrict__ x, int64_t n, double b,
+                                unsigned long long* __restrict__ bad) {
+  const QDiv dq = qdiv_make(b);
+  unsigned long long cnt = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double f = qdiv(x[i], dq), r = __ddiv_rn(x[i], b);
+    cnt += (__double_as_longlong(f) != __double_as_longlong(r)) ? 1 : 0;
   }
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quant_tile<BITS, PACK, V, ZF32, TP>, block, smem));
-  const int64_t warps = (rows + 8 * TP - 1) / (8 * TP);
-  const int grid = grid_for(warps * 32, block, std::max(1, per_sm));
-  k_quant_tile<BITS, PACK, V, ZF32, TP><<<grid, block, smem, st>>>(x, rows, row_len, codes, scale, zero, flag);
+  if (cnt) atomicAdd(bad, cnt);
+}
+
+extern "C" int alise_selftest_qdiv(const double* x, int64_t n, int bits, int64_t* mismatches, void* stream) {
+  if (bits != 4 && bits != 8) return fail(ALISE_EINVAL, "bits must be 4 or 8");
+  if (n <= 0) return ALISE_OK;
+  k_selftest_qdiv<<<grid_for(n, 256), 256, 0, S(stream)>>>(x, n, (double)((1 << bits) - 1),
+                                                         reinterpret_cast<unsigned long long*>(mismatches));
   CKL();
   return ALISE_OK;
+}
+
+// ------------------------------------------------------------------ fast tile launch
+template <int BITS, bool PACK, bool ZF32, int V, int TP, int WPB, int MINB = 1>
+static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes, double* scale,
+                         void* zero, int* flag, cudaStream_t st) {
+  constexpr int block = 32 * WPB;
+  constexpr int smem = WPB * 2 * (8 * TP) * (64 * V + 16);
+  auto kern = k_quant_tile<BITS, PACK, V, ZF32, TP, WPB, MINB>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem));
+    per_sm = std::max(1, per_sm);
+  }
+  const int64_t warps = (rows + 8 * TP - 1) / (8 * TP);
+  const int grid = grid_for(warps * 32, block, per_sm);
+  kern<<<grid, block, smem, st>>>(x, rows, row_len, codes, scale, zero, flag);
+  CKL();
+  return ALISE_OK;
+}
+
+// Tile shape per row length (V = 16-byte vectors per lane per row; TP passes of 8 rows
+// per warp tile; WPB warps per CTA; MINB = register cap via min CTAs per SM).
+// ALISE_QTILE selects tuning variants (tools/kv_kernel_bench.py sweeps them).
+static int qtile_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ALISE_QTILE");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 template <int BITS, bool PACK, bool ZF32>
 static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
                             double* scale, void* zero, int* flag, cudaStream_t st) {
   const int vpl = (row_len / 8 + 3) / 4;  // 16-byte vectors per lane per row
-  if (vpl <= 1) return launch_tile_v<BITS, PACK, ZF32, 1, 4>(x, rows, row_len, codes, scale, zero, flag, st);
-  if (vpl <= 2) return launch_tile_v<BITS, PACK, ZF32, 2, 4>(x, rows, row_len, codes, scale, zero, flag, st);
-  if (vpl <= 4) return launch_tile_v<BITS, PACK, ZF32, 4, 2>(x, rows, row_len, codes, scale, zero, flag, st);
-  if (vpl <= 8) return launch_tile_v<BITS, PACK, ZF32, 8, 1>(x, rows, row_len, codes, scale, zero, flag, st);
+  const int var = qtile_variant();
+#define QT(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB>(x, rows, row_len, codes, scale, zero, flag, st)
+  if (vpl <= 1) QT(1, 4, 8, 3);
+  if (vpl <= 2) {
+    if (var == 1) QT(2, 2, 8, 4);
+    if (var == 2) QT(2, 4, 4, 6);
+    if (var == 3) QT(2, 2, 8, 3);
+    QT(2, 4, 8, 3);
+  }
+  if (vpl <= 4) {
+    if (var == 1) QT(4, 2, 8, 4);
+    if (var == 2) QT(4, 2, 8, 3);
+    if (var == 3) QT(4, 1, 8, 4);
+    QT(4, 2, 4, 6);
+  }
+  if (vpl <= 8) QT(8, 2, 4, 3);
+#undef QT
   return fail(ALISE_EINVAL, "row_len %d too long for the tile kernel", row_len);
 }
 
@@ -194,6 +238,19 @@ extern "C" int alise_quantize_rows(const void* src, int src_dtype, int64_t rows,
 template <int BITS, bool PACK, bool ZF32>
 static int launch_dequant_tile(const uint8_t* codes, const double* scale, const void* zero,
                                int64_t n, int row_len, uint16_t* out, cudaStream_t st) {
+  constexpr int VALS = PACK ? 32 : 16;
+  const int64_t cpr = row_len / VALS;
+  if (row_len % VALS == 0 && !((uintptr_t)codes & 15) && n / VALS < (int64_t(1) << 31) && cpr < 512 &&
+      getenv("ALISE_DQ_NARROW") == nullptr) {
+    const uint32_t nchunks = (uint32_t)(n / VALS);
+    const int shift = (cpr & (cpr - 1)) ? -1 : __builtin_ctzll((unsigned long long)cpr);
+    const uint64_t recip = ((uint64_t(1) << 40) + cpr - 1) / cpr;
+    const int grid = grid_for(nchunks, 256, 8);
+    k_dequant_wide<BITS, PACK, ZF32><<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(codes), scale, zero,
+                                                           nchunks, shift, recip, reinterpret_cast<uint4*>(out));
+    CKL();
+    return ALISE_OK;
+  }
   const int grid = grid_for(n / 8, 256, 8);
   k_dequant_tile<BITS, PACK, ZF32><<<grid, 256, 0, st>>>(codes, scale, zero, n, row_len, out);
   CKL();

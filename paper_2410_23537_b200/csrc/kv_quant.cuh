@@ -20,6 +20,8 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "qmath.cuh"
 
 namespace alise {
@@ -75,19 +77,17 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int BITS, bool PACK, int VPL, bool ZF32, int TP>
-__global__ void __launch_bounds__(256, 3)
+template <int BITS, bool PACK, int VPL, bool ZF32, int TP, int WPB, int MINB>
+__global__ void __launch_bounds__(32 * WPB, MINB)
 k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
                 uint8_t* __restrict__ codes, double* __restrict__ scale, void* __restrict__ zero,
                 int* __restrict__ flag) {
-  // TP = passes of 8 rows per warp tile: 32-row tiles for g <= 64, 16 for g = 128,
-  // 8 for g = 256 (a lane stages 8 x 16 B per tile; 3 CTAs x 8 warps per SM)
+  // TP = passes of 8 rows per warp tile (TILE = 8 * TP rows; 32 keeps every lane busy
+  // in the parameter solve).  A lane stages TP x VPL 16-byte vectors per tile.
   constexpr int PASSES = TP;
   constexpr int TILE = 8 * PASSES;
+  constexpr int RL = 32 * VPL;         // row length of a full tile (elements)
   constexpr int ROWB = 64 * VPL + 16;  // padded smem row (bytes): 4 lanes x VPL x 16 B + 16
-  constexpr int F = TileMagic<BITS>::F;
-  constexpr uint32_t HALF = 1u << (F - 1);
-  constexpr uint32_t FMASK = (1u << F) - 1;
   constexpr float QMAXF = (float)((1 << BITS) - 1);
   extern __shared__ uint8_t smem_pf[];
   const int lane = threadIdx.x & 31;
@@ -96,23 +96,31 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
   const int sub = lane >> 2;
   const int q4 = lane & 3;
   const int nvec = row_len >> 3;
+  const bool wide_rows = nvec == 4 * VPL;  // every lane's vectors are in range
   const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t ntiles = (rows + TILE - 1) / TILE;
-  const uint32_t kMagicBits = f2bits(TileMagic<BITS>::M);
+  const QDiv dq = qdiv_make((double)((1 << BITS) - 1));
 
   auto prefetch = [&](int64_t tile, int slot) {
-    uint8_t* b = wbuf + slot * (TILE * ROWB);
+    uint8_t* b = wbuf + slot * (TILE * ROWB) + sub * ROWB + q4 * 16;
+    if (wide_rows && (tile + 1) * TILE <= rows) {
+      // full tile: unpredicated, compile-time offsets
+      const uint16_t* g = x + (tile * TILE + sub) * (int64_t)RL + q4 * 8;
 #pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      const int rl = p * 8 + sub;
-      const int64_t r = tile * TILE + rl;
+      for (int p = 0; p < PASSES; ++p)
 #pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        const int vv = q4 + 4 * i;
-        const bool ok = tile < ntiles && r < rows && vv < nvec;
-        const uint16_t* g = x + (ok ? r * row_len + vv * 8 : 0);
-        cp_async16(b + rl * ROWB + (q4 + 4 * i) * 16, g, ok);
+        for (int i = 0; i < VPL; ++i) cp_async16(b + p * 8 * ROWB + i * 64, g + p * 8 * RL + i * 32, true);
+    } else {
+#pragma unroll
+      for (int p = 0; p < PASSES; ++p) {
+        const int64_t r = tile * TILE + p * 8 + sub;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          const int vv = q4 + 4 * i;
+          const bool ok = tile < ntiles && r < rows && vv < nvec;
+          cp_async16(b + p * 8 * ROWB + i * 64, x + (ok ? r * row_len + vv * 8 : 0), ok);
+        }
       }
     }
     cp_async_commit();
@@ -126,7 +134,8 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
     __syncwarp();
     const uint8_t* b = wbuf + slot * (TILE * ROWB);
     const int64_t row0 = tile * TILE;
-    // ---------------- A: per-row min / max from shared memory
+    // ---------------- A: per-row min / max from shared memory (zero-filled vectors
+    // of a partial tile are skipped)
     uint32_t mine = 0;
 #pragma unroll
     for (int p = 0; p < PASSES; ++p) {
@@ -166,50 +175,49 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
     const bool bad = own && !(isfinite(fmn) && isfinite(fmx));
     raise_flag(flag, bad);
     if (!own || bad) { fmn = 0.f; fmx = 0.f; }
-    const QParams q = make_params((double)fmn, (double)fmx, BITS, false);
-    const TileParams tp = make_tile_params<BITS>(q, fmax(fabs((double)fmn), fabs((double)fmx)));
+    double s_row, z_row;
+    const TileParams tp = tile_params_f16(fmn, fmx, dq, s_row, z_row);
     if (own) {
-      scale[my_row] = q.s;
-      if (ZF32) reinterpret_cast<float*>(zero)[my_row] = (float)q.z;
-      else reinterpret_cast<double*>(zero)[my_row] = q.z;
+      scale[my_row] = s_row;
+      if (ZF32) reinterpret_cast<float*>(zero)[my_row] = (float)z_row;
+      else reinterpret_cast<double*>(zero)[my_row] = z_row;
     }
-    __syncwarp();
     // ---------------- C: codes from shared memory
     // full tiles (every row live, every lane's vectors in range) take an unpredicated
-    // path with immediate offsets; the code byte comes straight from the mantissa of
-    // y + (1.5*2^23 - M) (round-to-nearest; exact ties are flagged unsafe anyway)
-    const bool full = (row0 + TILE <= rows) && (nvec == 4 * VPL);
+    // path with compile-time offsets; the code is the low byte / nibble of
+    // y = fma(x, inv_s, z + 1.5*2^23), e = fma(x, inv_s, K - y) proves it (qmath.cuh)
+    const bool full = wide_rows && (row0 + TILE <= rows);
 #pragma unroll
     for (int p = 0; p < PASSES; ++p) {
       const int rl = p * 8 + sub;
       const float inv_s = __shfl_sync(0xffffffffu, tp.inv_s, rl);
       const float zc = __shfl_sync(0xffffffffu, tp.zc, rl);
-      const int w = __shfl_sync(0xffffffffu, tp.w, rl);
+      const float thr = __shfl_sync(0xffffffffu, tp.thr, rl);
       const int64_t r = row0 + rl;
       const bool live_row = r < rows;
-      const uint32_t koff = (uint32_t)w - HALF - kMagicBits;
-      const uint32_t kwin = (uint32_t)(2 * w);
       const float2 inv2 = make_float2(inv_s, inv_s), zc2 = make_float2(zc, zc);
-      const float2 shift2 = make_float2(12582912.0f - TileMagic<BITS>::M, 12582912.0f - TileMagic<BITS>::M);
+      const float2 nzc2 = make_float2(-zc, -zc);
       const uint8_t* srow = b + rl * ROWB + q4 * 16;
-      uint8_t* crow = codes + (r * row_len + q4 * 8) / (PACK ? 2 : 1);
-      bool unsafe = false;
+      uint8_t* crow = codes + (r * (full ? (int64_t)RL : (int64_t)row_len) + q4 * 8) / (PACK ? 2 : 1);
+      uint32_t umask = 0;  // vectors holding a value near a rounding boundary
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
         if (!full && !(live_row && q4 + 4 * i < nvec)) continue;
         const uint4 d = *reinterpret_cast<const uint4*>(srow + i * 64);
         const __half2* h = reinterpret_cast<const __half2*>(&d);
         uint32_t c[8];
+        float dmax = 0.f;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float2 f = __half22float2(h[k]);
-          const float2 y = __ffma2_rn(f, inv2, zc2);
-          const float2 y2 = __fadd2_rn(y, shift2);
-          unsafe |= ((f2bits(y.x) + koff) & FMASK) <= kwin;
-          unsafe |= ((f2bits(y.y) + koff) & FMASK) <= kwin;
-          c[2 * k] = f2bits(y2.x);
-          c[2 * k + 1] = f2bits(y2.y);
+          const float2 y = __ffma2_rn(f, inv2, zc2);                    // 1.5*2^23 + code
+          const float2 cc = __fadd2_rn(y, nzc2);                        // code - z, exact
+          const float2 e = __ffma2_rn(f, inv2, make_float2(-cc.x, -cc.y));  // RN(t32 - code)
+          dmax = fmaxf(dmax, fmaxf(fabsf(e.x), fabsf(e.y)));
+          c[2 * k] = f2bits(y.x);
+          c[2 * k + 1] = f2bits(y.y);
         }
+        umask |= (dmax >= thr ? 1u : 0u) << i;
         if (PACK) {
           uint32_t wv = 0;
 #pragma unroll
@@ -221,31 +229,25 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
           __stcs(reinterpret_cast<uint2*>(crow + i * 32), make_uint2(w0, w1));
         }
       }
-      if (unsafe) {
-        // rare: float64 reference ops for values near a rounding boundary; vectors are
-        // re-checked 8 values at a time and only flagged values are redone; this lane
-        // owns every byte it patches
+      if (umask) {
+        // rare: float64 reference ops for the values of the flagged vectors that are near
+        // a rounding boundary; this lane owns every byte it patches
         const double sd = scale[r];
         const double zd = ZF32 ? (double)reinterpret_cast<const float*>(zero)[r]
                                : reinterpret_cast<const double*>(zero)[r];
 #pragma unroll 1
-        for (int i = 0; i < VPL; ++i) {
+        while (umask) {
+          const int i = __ffs(umask) - 1;
+          umask &= umask - 1;
           const int vv = q4 + 4 * i;
-          if (vv >= nvec) continue;
-          const uint4 d = *reinterpret_cast<const uint4*>(srow + i * 64);
-          const uint16_t* hh = reinterpret_cast<const uint16_t*>(&d);
-          uint32_t m = 0;
-#pragma unroll
+#pragma unroll 1
           for (int j = 0; j < 8; ++j) {
-            const uint32_t bb = f2bits(fmaf(h2f(hh[j]), inv_s, zc));
-            m |= (((bb + koff) & FMASK) <= kwin ? 1u : 0u) << j;
-          }
-          while (m) {
-            const int j = __ffs(m) - 1;
-            m &= m - 1;
             const uint16_t hv = *reinterpret_cast<const uint16_t*>(srow + i * 64 + 2 * j);
-            const float rr = (float)rint(__dadd_rn(__ddiv_rn((double)h2f(hv), sd), zd));
-            const uint32_t cc = (uint32_t)fminf(fmaxf(rr, 0.f), QMAXF);
+            const float xf = h2f(hv);
+            const float y = fmaf(xf, inv_s, zc);
+            if (!(fabsf(fmaf(xf, inv_s, -__fadd_rn(y, -zc))) >= thr)) continue;
+            const float rc = (float)rint(__dadd_rn(__ddiv_rn((double)h2f(hv), sd), zd));
+            const uint32_t cc = (uint32_t)fminf(fmaxf(rc, 0.f), QMAXF);
             const int64_t idx = r * row_len + vv * 8 + j;
             if (PACK) {
               uint8_t* pb = codes + (idx >> 1);
@@ -322,6 +324,84 @@ k_dequant_tile(const uint8_t* __restrict__ codes, const double* __restrict__ sca
   }
 }
 
+// Wide dequantize of ROWS-kind codes to fp16: each thread owns one 16-byte word of
+// codes (16 INT8 or 32 packed INT4 values, inside one row), so a warp keeps 512 B of
+// reads in flight per instruction and the row's (scale, zero) are loaded and checked
+// once per 16/32 values.  Row index = chunk / chunks_per_row via shift or a 2^40
+// reciprocal (exact for chunk < 2^31, chunks_per_row < 2^9).  Values: y = fp32(s) *
+// ((2^23+q) - (2^23+z)) (one product rounding after an exact difference), fp16(y)
+// equals fp16(float64 s*(q-z)) unless y's 13 discarded bits are within 4 of the
+// fp16 rounding midpoint (checked two values at a time on 16-bit lanes, window 9
+// so a carry between the lanes can only widen it) or the row's products may leave
+// the fp16 normal range; those vectors re-run the reference float64 product.
+template <int BITS, bool PACK, bool ZF32>
+__global__ void __launch_bounds__(256)
+k_dequant_wide(const uint4* __restrict__ codes, const double* __restrict__ scale,
+               const void* __restrict__ zero, uint32_t nchunks, int cpr_shift, uint64_t cpr_recip,
+               uint4* __restrict__ out) {
+  constexpr int VALS = PACK ? 32 : 16;  // values per 16-byte chunk
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nchunks; k += gridDim.x * blockDim.x) {
+    const uint32_t r = cpr_shift >= 0 ? (k >> cpr_shift) : (uint32_t)(((uint64_t)k * cpr_recip) >> 40);
+    const uint4 w = __ldcs(codes + k);
+    const double s = __ldg(scale + r);
+    float zf;
+    double z;
+    if (ZF32) {
+      zf = __ldg(reinterpret_cast<const float*>(zero) + r);
+      z = (double)zf;
+    } else {
+      z = __ldg(reinterpret_cast<const double*>(zero) + r);
+      zf = (float)z;
+    }
+    const float s32 = (float)s;
+    // fast rows: integer zero (2^23 + z exact in fp32) and products in the fp16 normal
+    // range (s32 > 2^-14 implies s > 2^-14); constant rows (real-valued zero) go exact
+    const bool row_fast = (double)zf == z && zf == rintf(zf) && fabsf(zf) < 4194304.0f &&
+                          s32 > 0x1p-14f && s32 < 60000.0f;
+    const float zm = zf + 8388608.0f;
+    const float2 nz2 = make_float2(-zm, -zm), s2 = make_float2(s32, s32);
+    const uint32_t wd[4] = {w.x, w.y, w.z, w.w};
+    uint32_t o[VALS / 2];
+    uint32_t acc = 0xffffffffu;
+#pragma unroll
+    for (int p = 0; p < VALS / 2; ++p) {
+      // code -> float 2^23 + q with one byte permute: bytes (q, 0, 0, 0x4B)
+      uint32_t f0, f1;
+      if (PACK) {
+        const uint32_t wv = wd[p >> 2];
+        const int j = p & 3;
+        f0 = __byte_perm(wv & 0x0F0F0F0Fu, 0x4Bu, 0x4550 + j);
+        f1 = __byte_perm((wv >> 4) & 0x0F0F0F0Fu, 0x4Bu, 0x4550 + j);
+      } else {
+        const uint32_t wv = wd[p >> 1];
+        const int j = 2 * (p & 1);
+        f0 = __byte_perm(wv, 0x4Bu, 0x4550 + j);
+        f1 = __byte_perm(wv, 0x4Bu, 0x4551 + j);
+      }
+      const float2 qf = make_float2(__uint_as_float(f0), __uint_as_float(f1));
+      const float2 y = __fmul2_rn(__fadd2_rn(qf, nz2), s2);
+      const __half2 hv = __floats2half2_rn(y.x, y.y);
+      o[p] = *reinterpret_cast<const uint32_t*>(&hv);
+      const uint32_t lo = __byte_perm(__float_as_uint(y.x), __float_as_uint(y.y), 0x5410);
+      acc = __vminu2(acc, (lo + 0x10041004u) & 0x1fff1fffu);
+    }
+    const bool unsafe = !row_fast || (acc & 0xffffu) <= 9u || (acc >> 16) <= 9u;
+    if (unsafe) {
+#pragma unroll
+      for (int j = 0; j < VALS; ++j) {
+        const uint32_t q = PACK ? (wd[j >> 3] >> (4 * (j & 7))) & 15u : (wd[j >> 2] >> (8 * (j & 3))) & 255u;
+        const double v = __dmul_rn(s, __dsub_rn((double)q, z));
+        const uint32_t hb = __half_as_ushort(__double2half(v));
+        const int wi = j >> 1, sh = 16 * (j & 1);
+        o[wi] = (o[wi] & ~(0xffffu << sh)) | (hb << sh);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < VALS / 8; ++c)
+      __stcs(out + (size_t)k * (VALS / 8) + c, make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]));
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // Fused column kernel for the CHANNEL / HEAD kinds (rows run along tokens).
 // Block = 256 threads = 16 column vectors (128 columns) x 16 token lanes over one
@@ -332,17 +412,13 @@ k_dequant_tile(const uint8_t* __restrict__ codes, const double* __restrict__ sca
 // in registers.  Codes stay in native [T][Hd] order.
 // ---------------------------------------------------------------------------------
 template <int BITS, bool PACK>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int64_t rows_per_plane,
              uint8_t* __restrict__ codes, double* __restrict__ scale, float* __restrict__ zero,
              int* __restrict__ flag) {
-  constexpr int F = TileMagic<BITS>::F;
-  constexpr uint32_t HALF = 1u << (F - 1);
-  constexpr uint32_t FMASK = (1u << F) - 1;
   constexpr float QMAXF = (float)((1 << BITS) - 1);
   __shared__ __half2 s_mm[16][128];      // (min, -max) per token lane and column
-  __shared__ float s_inv[128], s_zc[128];
-  __shared__ int s_w[128];
+  __shared__ float s_inv[128], s_zc[128], s_thr[128];
   const int tid = threadIdx.x;
   const int cv = tid & 15, tl = tid >> 4;
   const int64_t plane = blockIdx.y;
@@ -355,15 +431,23 @@ k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int
     lo[j] = __half2half2(__ushort_as_half(0x7c00));
     hi[j] = __half2half2(__ushort_as_half(0xfc00));
   }
-  for (int64_t t = tl; t < T; t += 16) {
-    const uint4 d = __ldg(reinterpret_cast<const uint4*>(base + t * Hd));
+  auto mm_vec = [&](const uint4 d) {
     const __half2* h = reinterpret_cast<const __half2*>(&d);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       lo[j] = __hmin2_nan(lo[j], h[j]);
       hi[j] = __hmax2_nan(hi[j], h[j]);
     }
+  };
+  int64_t t1 = tl;
+  for (; t1 + 48 < T; t1 += 64) {
+    uint4 d[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d[u] = __ldg(reinterpret_cast<const uint4*>(base + (t1 + 16 * u) * Hd));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) mm_vec(d[u]);
   }
+  for (; t1 < T; t1 += 16) mm_vec(__ldg(reinterpret_cast<const uint4*>(base + t1 * Hd)));
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     s_mm[tl][cv * 8 + 2 * j] = __halves2half2(__low2half(lo[j]), __hneg(__low2half(hi[j])));
@@ -384,53 +468,48 @@ k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int
     float fmn = __low2float(m), fmx = -__high2float(m);
     const bool bad = !(isfinite(fmn) && isfinite(fmx));
     if (bad) { atomicOr(flag, 1); fmn = 0.f; fmx = 0.f; }
-    const QParams q = make_params((double)fmn, (double)fmx, BITS, false);
-    const TileParams tp = make_tile_params<BITS>(q, fmax(fabs((double)fmn), fabs((double)fmx)));
+    double sd, zd;
+    const TileParams tp = tile_params_f16(fmn, fmx, qdiv_make((double)((1 << BITS) - 1)), sd, zd);
     const int64_t r = plane * rows_per_plane + (col0 / cpr) + tid;
-    scale[r] = q.s;
-    zero[r] = (float)q.z;
+    scale[r] = sd;
+    zero[r] = (float)zd;
     for (int u = 0; u < cpr; ++u) {
       s_inv[tid * cpr + u] = tp.inv_s;
       s_zc[tid * cpr + u] = tp.zc;
-      s_w[tid * cpr + u] = tp.w;
+      s_thr[tid * cpr + u] = tp.thr;
     }
   }
   __syncthreads();
   // ---- pass 2
-  float inv[8], zc[8];
-  uint32_t koff[8], kwin[8];
-  const uint32_t kMagicBits = f2bits(TileMagic<BITS>::M);
-  const uint32_t kcode = kMagicBits - HALF;
+  float inv[8], zc[8], thr[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     inv[j] = s_inv[cv * 8 + j];
     zc[j] = s_zc[cv * 8 + j];
-    const int w = s_w[cv * 8 + j];
-    koff[j] = (uint32_t)w - HALF - kMagicBits;
-    kwin[j] = (uint32_t)(2 * w);
+    thr[j] = s_thr[cv * 8 + j];
   }
   uint8_t* cbase = codes + (plane * T * Hd + col0 + cv * 8) / (PACK ? 2 : 1);
-  for (int64_t t = tl; t < T; t += 16) {
-    const uint4 d = __ldg(reinterpret_cast<const uint4*>(base + t * Hd));
+  auto code_vec = [&](const uint4 d, int64_t t) {
     const __half2* h = reinterpret_cast<const __half2*>(&d);
     uint32_t c[8];
     bool unsafe = false;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float2 f = __half22float2(h[j]);
-      const float2 y = __ffma2_rn(f, make_float2(inv[2 * j], inv[2 * j + 1]), make_float2(zc[2 * j], zc[2 * j + 1]));
-      const uint32_t b0 = f2bits(y.x), b1 = f2bits(y.y);
-      unsafe |= ((b0 + koff[2 * j]) & FMASK) <= kwin[2 * j];
-      unsafe |= ((b1 + koff[2 * j + 1]) & FMASK) <= kwin[2 * j + 1];
-      c[2 * j] = (b0 - kcode) >> F;
-      c[2 * j + 1] = (b1 - kcode) >> F;
+      const float2 i2 = make_float2(inv[2 * j], inv[2 * j + 1]);
+      const float2 y = __ffma2_rn(f, i2, make_float2(zc[2 * j], zc[2 * j + 1]));
+      const float2 cc = __fadd2_rn(y, make_float2(-zc[2 * j], -zc[2 * j + 1]));
+      const float2 e = __ffma2_rn(f, i2, make_float2(-cc.x, -cc.y));
+      unsafe |= !(fabsf(e.x) < thr[2 * j]) || !(fabsf(e.y) < thr[2 * j + 1]);
+      c[2 * j] = f2bits(y.x) & ((1u << BITS) - 1);
+      c[2 * j + 1] = f2bits(y.y) & ((1u << BITS) - 1);
     }
     if (unsafe) {  // rare: the reference float64 ops for the values near a boundary
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float f = __half2float(reinterpret_cast<const __half*>(&d)[j]);
-        const uint32_t b = f2bits(fmaf(f, inv[j], zc[j]));
-        if (((b + koff[j]) & FMASK) <= kwin[j]) {
+        const float y = fmaf(f, inv[j], zc[j]);
+        if (!(fabsf(fmaf(f, inv[j], -__fadd_rn(y, -zc[j]))) < thr[j])) {
           const int64_t r = plane * rows_per_plane + (col0 + cv * 8 + j) / cpr;
           const double sd = scale[r], zd = (double)zero[r];
           float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, sd), zd));
@@ -448,7 +527,17 @@ k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int
       const uint32_t w1 = __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
       __stcs(reinterpret_cast<uint2*>(cbase + t * Hd), make_uint2(w0, w1));
     }
+  };
+  // four token rows in flight per thread (the loop is load-latency bound otherwise)
+  int64_t t = tl;
+  for (; t + 48 < T; t += 64) {
+    uint4 d[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d[u] = __ldg(reinterpret_cast<const uint4*>(base + (t + 16 * u) * Hd));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) code_vec(d[u], t + 16 * u);
   }
+  for (; t < T; t += 16) code_vec(__ldg(reinterpret_cast<const uint4*>(base + t * Hd)), t);
 }
 
 // Column dequantize for CHANNEL / HEAD kinds: each thread owns 8 columns of a strip
@@ -476,14 +565,13 @@ k_dequant_cols(const uint8_t* __restrict__ codes, const double* __restrict__ sca
   }
   const uint8_t* cb = codes + (plane * T * Hd + col0) / (PACK ? 2 : 1);
   uint16_t* ob = out + plane * T * Hd + col0;
-  for (int64_t t = tl; t < T; t += 16) {
+  using CodeWord = typename std::conditional<PACK, uint32_t, uint2>::type;
+  auto dq_vec = [&](const CodeWord wd, int64_t t) {
     uint32_t q[8];
-    if (PACK) {
-      const uint32_t wd = __ldcs(reinterpret_cast<const uint32_t*>(cb + t * Hd / 2));
+    if constexpr (PACK) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) q[j] = (wd >> (4 * j)) & 15u;
     } else {
-      const uint2 wd = __ldcs(reinterpret_cast<const uint2*>(cb + t * Hd));
 #pragma unroll
       for (int j = 0; j < 4; ++j) { q[j] = (wd.x >> (8 * j)) & 255u; q[4 + j] = (wd.y >> (8 * j)) & 255u; }
     }
@@ -510,7 +598,21 @@ k_dequant_cols(const uint8_t* __restrict__ codes, const double* __restrict__ sca
       }
     }
     __stcs(reinterpret_cast<uint4*>(ob + t * Hd), make_uint4(o[0], o[1], o[2], o[3]));
+  };
+  auto load = [&](int64_t t) -> CodeWord {
+    if constexpr (PACK) return __ldcs(reinterpret_cast<const uint32_t*>(cb + t * Hd / 2));
+    else return __ldcs(reinterpret_cast<const uint2*>(cb + t * Hd));
+  };
+  // four token rows of codes in flight per thread
+  int64_t t = tl;
+  for (; t + 48 < T; t += 64) {
+    CodeWord w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = load(t + 16 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dq_vec(w[u], t + 16 * u);
   }
+  for (; t < T; t += 16) dq_vec(load(t), t);
 }
 
 // ---------------------------------------------------------------------------------
@@ -624,7 +726,7 @@ __global__ void k_params(int kind, int64_t rows, int nch, const double* __restri
       }
     }
   }
-  const QParams q = make_params(mn, mx, bits, wide);
+  const QParams q = make_params(mn, mx, bits, wide, qdiv_make((double)((1 << bits) - 1)));
   scale[r] = q.s;
   if (ZF32) reinterpret_cast<float*>(zero)[r] = (float)q.z;
   else reinterpret_cast<double*>(zero)[r] = q.z;

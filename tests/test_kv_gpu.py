@@ -291,3 +291,30 @@ def test_c5_replay_matches_reference_ledger():
     out = replay.replay(rec, replica=3, max_events=1200)
     assert out["swaps_out"] > 100 and out["data_checked"] > 10
     assert out["data_mismatches"] == 0
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_constant_divisor_division_is_ddiv_rn(bits):
+    """qmath.cuh qdiv (hoisted reciprocal) == __ddiv_rn bit for bit: random doubles over
+    the whole exponent range, the snap loop's operands (s*(qmax-z) - s*(-z) for fp16
+    (min, max) pairs) and the special values."""
+    import torch
+    from paper_2410_23537_b200 import _lib
+    g = np.random.default_rng(bits)
+    qmax = float((1 << bits) - 1)
+    parts = [g.standard_normal(1 << 20) * np.exp2(g.integers(-1070, 1020, 1 << 20)),
+             g.integers(1, 1 << 62, 1 << 20, dtype=np.int64).view(np.float64)]
+    mn = g.standard_normal(1 << 20).astype(np.float16).astype(np.float64) * 100
+    mx = mn + np.abs(g.standard_normal(1 << 20).astype(np.float16).astype(np.float64)) * 100 + 2.0 ** -20
+    s = (mx - mn) / qmax
+    z = np.rint(-mn / s)
+    parts += [mx - mn, s * (qmax - z) - s * (0 - z)]
+    parts.append(np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 1.7e308, qmax, -qmax, 1.0]))
+    x = np.concatenate(parts)
+    x = x[np.isfinite(x) | np.isnan(x)]
+    xd = torch.from_numpy(x).cuda()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.call("alise_selftest_qdiv", _lib.ptr(xd), x.size, bits, _lib.ptr(bad), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    # NaN inputs compare by bits too (both paths return the canonical quiet NaN)
+    assert int(bad.item()) == 0

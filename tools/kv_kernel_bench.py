@@ -9,9 +9,12 @@ sys.path.insert(0, ".")
 from paper_2410_23537_b200 import kvmanager as km  # noqa: E402
 from paper_2410_23537_b200 import synthetic  # noqa: E402
 
+CASES = [("rows", 128, 8, False), ("rows", 64, 4, True), ("rows", 64, 8, False),
+         ("channel", 0, 8, False), ("head", 0, 8, False)]
+if len(sys.argv) > 1:  # e.g. "rows:128:8:0,rows:64:4:1"
+    CASES = [(k, int(g), int(b), bool(int(p))) for k, g, b, p in (c.split(":") for c in sys.argv[1].split(","))]
 res = []
-for kind, group, bits, packed in [("rows", 128, 8, False), ("rows", 64, 4, True), ("rows", 64, 8, False),
-                                  ("channel", 0, 8, False), ("head", 0, 8, False)]:
+for kind, group, bits, packed in CASES:
     lay = km.KVLayout(32, 2048, 4096, 128, kind=kind, group=group or 128, bits=bits, packed=packed,
                       planes_per_chunk=64)
     g = lay.geometry()
@@ -54,4 +57,6 @@ for kind, group, bits, packed in [("rows", 128, 8, False), ("rows", 64, 4, True)
     print(json.dumps(r))
     del kv, slab, out
     torch.cuda.empty_cache()
-json.dump(res, open("gpurun_out/kv_kernels.json", "w"), indent=1)
+import os  # noqa: E402
+os.makedirs("gpurun_out", exist_ok=True)
+json.dump(res, open("gpurun_out/kv_kernels%s.json" % os.environ.get("ALISE_QTILE", ""), "w"), indent=1)
