@@ -222,22 +222,39 @@ def link_peaks(dev_index: int):
         torch.cuda.synchronize()
         return (time.perf_counter() - t) / reps
 
-    d2h = n / timed(lambda: h.copy_(d, non_blocking=True)) / 1e9
-    h2d = n / timed(lambda: d.copy_(h, non_blocking=True)) / 1e9
+    # best of three trials each: the pinned-copy peak is noisy on a shared host
+    d2h = max(n / timed(lambda: h.copy_(d, non_blocking=True)) / 1e9 for _ in range(3))
+    h2d = max(n / timed(lambda: d.copy_(h, non_blocking=True)) / 1e9 for _ in range(3))
 
     def both():
         with torch.cuda.stream(s1):
             h.copy_(d, non_blocking=True)
         with torch.cuda.stream(s2):
             d2.copy_(h2, non_blocking=True)
-    duplex = 2 * n / timed(both) / 1e9
+    duplex = max(2 * n / timed(both) / 1e9 for _ in range(3))
     del d, d2, h, h2
     return {"d2h_GBs": d2h, "h2d_GBs": h2d, "duplex_total_GBs": duplex}
 
 
 # ----------------------------------------------------------------- KV bench
 def kv_bench(args, world, rank, local, layouts=None, e2e=True):
-    """Swap pipeline over a job list (one KVLayout per job); jobs LPT-assigned to ranks."""
+    """Swap pipeline over a job list (one KVLayout per job); jobs LPT-assigned to ranks.
+
+    The offload side (quantize kernels) runs on a high-priority stream so that its
+    CTAs are scheduled ahead of the concurrent upload-side dequantize kernels (the
+    step is host-link bound; the priority only decides which kernel waits for SMs)."""
+    import torch
+
+    torch.cuda.set_device(local)
+    hp = torch.cuda.Stream(device=local, priority=-1)
+    hp.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(hp):
+        res = _kv_bench(args, world, rank, local, layouts, e2e)
+    torch.cuda.synchronize()
+    return res
+
+
+def _kv_bench(args, world, rank, local, layouts=None, e2e=True):
     import torch
 
     from paper_2410_23537_b200 import kvmanager as km

@@ -245,7 +245,9 @@ static int launch_dequant_tile(const uint8_t* codes, const double* scale, const 
     const uint32_t nchunks = (uint32_t)(n / VALS);
     const int shift = (cpr & (cpr - 1)) ? -1 : __builtin_ctzll((unsigned long long)cpr);
     const uint64_t recip = ((uint64_t(1) << 40) + cpr - 1) / cpr;
-    const int grid = grid_for(nchunks, 256, 8);
+    // one 16-byte code word per thread, no grid-stride loop: CTAs retire continuously, so a
+    // concurrent higher-priority quantize launch gets SMs as soon as it is queued
+    const int grid = (int)((nchunks + 255) / 256);
     k_dequant_wide<BITS, PACK, ZF32><<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(codes), scale, zero,
                                                            nchunks, shift, recip, reinterpret_cast<uint4*>(out));
     CKL();
@@ -348,7 +350,9 @@ static int geom(const alise_kv_desc* d, KvGeom* g) {
   }
   g->code_bytes_pp = d->packed ? g->plane_elems / 2 : g->plane_elems;
   int64_t ppc = d->planes_per_chunk;
-  if (ppc <= 0) ppc = std::max<int64_t>(1, (int64_t(64) << 20) / g->code_bytes_pp);
+  // default transfer chunk: 128 MiB of codes (4 quantize launches per 1 GiB fp16 job at INT8:
+  // long enough that a launch's tail is small, short enough that the first copy starts early)
+  if (ppc <= 0) ppc = std::max<int64_t>(1, (int64_t(128) << 20) / g->code_bytes_pp);
   g->ppc = std::min(ppc, g->planes);
   g->n_chunks = (g->planes + g->ppc - 1) / g->ppc;
   g->rec_bytes = g->rec(g->ppc);

@@ -1,6 +1,7 @@
-"""Launch exactly the bench's kernel configurations once each (for ncu --set full):
-k_quant_tile on one 64 MiB-code chunk (8 planes, g=128, INT8) and k_scan at C4
-(B=4096 x 1M x 768).  Usage under ncu: -k regex:'k_quant_tile|k_scan' -c 2."""
+"""Launch exactly the bench's kernel configurations (for ncu --set full): one job's
+k_quant_tile / k_dequant_wide chunk launches (default 128 MiB-code chunks, g=128,
+INT8) and k_scan at C4 (B=4096 x 1M x 768).
+Usage under ncu: -k regex:'k_quant_tile|k_dequant_wide|k_scan' -c 3."""
 import sys
 
 import torch
@@ -17,9 +18,12 @@ slab = torch.empty(g["slab_bytes"], dtype=torch.uint8, device="cuda")
 flag = torch.zeros(1, dtype=torch.int32, device="cuda")
 km._lib.call("alise_kv_quantize", km._lib.C.byref(lay.desc()), km._lib.ptr(kv), km._lib.ptr(slab),
              km._lib.ptr(flag), km._lib.stream_ptr())
+out = torch.empty_like(kv)
+km._lib.call("alise_kv_dequantize", km._lib.C.byref(lay.desc()), km._lib.ptr(slab), km._lib.ptr(out),
+             km._lib.stream_ptr())
 torch.cuda.synchronize()
 print("quant chunks", g["n_chunks"], "values per chunk", lay.elements // g["n_chunks"])
-del kv, slab
+del kv, slab, out
 db, lens = synthetic.predictor_db_torch(1_000_000, 768, seed=0, dup_groups=1000)
 store = pr.VectorStore(768, 1_000_000)
 store.add_batch(db, lens)
