@@ -65,6 +65,18 @@ __device__ __forceinline__ void raise_flag(int* flag, bool bad) {
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t f2bits(float f) { return __float_as_uint(f); }
 
+// Pack the low bytes of eight fast-path words (bits = 1.5*2^23 + code, code < 2^BITS)
+// into codes: INT8 -> 8 bytes, INT4 -> 4 bytes (low nibble = even element).  Byte
+// permutes gather the low bytes; INT4 merges odd codes into the high nibbles.
+__device__ __forceinline__ uint32_t gather4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+__device__ __forceinline__ uint32_t pack_int4x8(const uint32_t (&c)[8]) {
+  const uint32_t even = gather4(c[0], c[2], c[4], c[6]);
+  const uint32_t odd = gather4(c[1], c[3], c[5], c[7]);
+  return even | (odd << 4);
+}
+
 // Each warp double-buffers its tiles in shared memory with cp.async (16-byte LDGSTS,
 // rows padded by 16 B so the 4 lanes x 8 rows of a load phase hit distinct banks):
 // tile i+1 streams in while tile i is reduced, solved and coded.
@@ -187,6 +199,7 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
     // path with compile-time offsets; the code is the low byte / nibble of
     // y = fma(x, inv_s, z + 1.5*2^23), e = fma(x, inv_s, K - y) proves it (qmath.cuh)
     const bool full = wide_rows && (row0 + TILE <= rows);
+    uint32_t pmask = 0;  // flagged vectors of this lane: bit p * VPL + i
 #pragma unroll
     for (int p = 0; p < PASSES; ++p) {
       const int rl = p * 8 + sub;
@@ -219,44 +232,52 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
         }
         umask |= (dmax >= thr ? 1u : 0u) << i;
         if (PACK) {
-          uint32_t wv = 0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) wv |= (c[j] & 15u) << (4 * j);
-          __stcs(reinterpret_cast<uint32_t*>(crow + i * 16), wv);
+          __stcs(reinterpret_cast<uint32_t*>(crow + i * 16), pack_int4x8(c));
         } else {
-          const uint32_t w0 = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
-          const uint32_t w1 = __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
-          __stcs(reinterpret_cast<uint2*>(crow + i * 32), make_uint2(w0, w1));
+          __stcs(reinterpret_cast<uint2*>(crow + i * 32),
+                 make_uint2(gather4(c[0], c[1], c[2], c[3]), gather4(c[4], c[5], c[6], c[7])));
         }
       }
-      if (umask) {
-        // rare: float64 reference ops for the values of the flagged vectors that are near
-        // a rounding boundary; this lane owns every byte it patches
-        const double sd = scale[r];
-        const double zd = ZF32 ? (double)reinterpret_cast<const float*>(zero)[r]
-                               : reinterpret_cast<const double*>(zero)[r];
+      pmask |= umask << (p * VPL);
+    }
+    // ---------------- D: rare fix-up of flagged vectors (a value near a rounding boundary),
+    // all lanes together: lane j recomputes the byte holding value j (INT8) or values
+    // 2j, 2j+1 (packed INT4) with the reference float64 ops where the check fails
+    __syncwarp();  // the vector stores above are visible to the whole warp
+    uint32_t pending = __ballot_sync(0xffffffffu, pmask != 0);
 #pragma unroll 1
-        while (umask) {
-          const int i = __ffs(umask) - 1;
-          umask &= umask - 1;
-          const int vv = q4 + 4 * i;
+    while (pending) {
+      const int src = __ffs(pending) - 1;
+      pending &= pending - 1;
+      uint32_t m = __shfl_sync(0xffffffffu, pmask, src);
 #pragma unroll 1
-          for (int j = 0; j < 8; ++j) {
-            const uint16_t hv = *reinterpret_cast<const uint16_t*>(srow + i * 64 + 2 * j);
-            const float xf = h2f(hv);
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        const int rl = (bit / VPL) * 8 + (src >> 2);
+        const int vv = (src & 3) + 4 * (bit % VPL);
+        const float inv_s = __shfl_sync(0xffffffffu, tp.inv_s, rl);
+        const float zc = __shfl_sync(0xffffffffu, tp.zc, rl);
+        const float thr = __shfl_sync(0xffffffffu, tp.thr, rl);
+        const double sd = __shfl_sync(0xffffffffu, s_row, rl);
+        const double zd = __shfl_sync(0xffffffffu, z_row, rl);
+        constexpr int PER = PACK ? 2 : 1;  // values per code byte
+        if (lane < 8 / PER) {
+          const int64_t r = row0 + rl;
+          const uint16_t* hv = reinterpret_cast<const uint16_t*>(b + rl * ROWB + vv * 16) + lane * PER;
+          uint32_t byte = 0;
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const float xf = h2f(hv[u]);
             const float y = fmaf(xf, inv_s, zc);
-            if (!(fabsf(fmaf(xf, inv_s, -__fadd_rn(y, -zc))) >= thr)) continue;
-            const float rc = (float)rint(__dadd_rn(__ddiv_rn((double)h2f(hv), sd), zd));
-            const uint32_t cc = (uint32_t)fminf(fmaxf(rc, 0.f), QMAXF);
-            const int64_t idx = r * row_len + vv * 8 + j;
-            if (PACK) {
-              uint8_t* pb = codes + (idx >> 1);
-              const uint32_t sh = 4 * (uint32_t)(idx & 1);
-              *pb = (uint8_t)((*pb & ~(15u << sh)) | (cc << sh));
-            } else {
-              codes[idx] = (uint8_t)cc;
+            uint32_t cc = f2bits(y) & ((1u << BITS) - 1);
+            if (!(fabsf(fmaf(xf, inv_s, -__fadd_rn(y, -zc))) < thr)) {
+              const float rc = (float)rint(__dadd_rn(__ddiv_rn((double)xf, sd), zd));
+              cc = (uint32_t)fminf(fmaxf(rc, 0.f), QMAXF);
             }
+            byte |= cc << (4 * u);
           }
+          codes[(r * row_len + vv * 8) / PER + lane] = (uint8_t)byte;
         }
       }
     }
@@ -518,14 +539,10 @@ k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int
       }
     }
     if (PACK) {
-      uint32_t wv = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) wv |= (c[j] & 15u) << (4 * j);
-      __stcs(reinterpret_cast<uint32_t*>(cbase + t * Hd / 2), wv);
+      __stcs(reinterpret_cast<uint32_t*>(cbase + t * Hd / 2), pack_int4x8(c));
     } else {
-      const uint32_t w0 = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
-      const uint32_t w1 = __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
-      __stcs(reinterpret_cast<uint2*>(cbase + t * Hd), make_uint2(w0, w1));
+      __stcs(reinterpret_cast<uint2*>(cbase + t * Hd),
+             make_uint2(gather4(c[0], c[1], c[2], c[3]), gather4(c[4], c[5], c[6], c[7])));
     }
   };
   // four token rows in flight per thread (the loop is load-latency bound otherwise)
