@@ -522,6 +522,38 @@ def cpu_pred_sample(args, n_queries: int):
 
 
 # ----------------------------------------------------------------- main
+def control_plane_bench(n: int = 16384, reps: int = 20):
+    """Host control plane: one rank -> EWT -> swap-plan step over n
+    live jobs, C++ (JobTable / alise_rank_and_plan) vs the Python restatement of the
+    reference (oracle/control_oracle.py, simcore.py:439-462 + kvmanager.py:276-322)."""
+    import numpy as np
+
+    from oracle import control_oracle as co
+    from paper_2410_23537_b200 import kvmanager as km
+    g = np.random.default_rng(0)
+    lev = np.sort(g.integers(0, 4, n)).astype(np.int32)
+    lp = g.integers(0, 10 ** 9, n)
+    rem = g.exponential(300.0, n)
+    res = g.integers(0, 5, n).astype(np.int32)
+    need = g.integers(1 << 20, 1 << 30, n)
+    budget = int(need.sum() // 3)
+    t = km.JobTable(n)
+    t.set_rank(np.arange(n), lev, lp, rem, res, need)
+    t.plan(5000.0, 10 ** 9, budget)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        order, act, _ = t.plan(5000.0, 10 ** 9, budget)
+    cpp_us = (time.perf_counter() - t0) / reps * 1e6
+    args = (lev.tolist(), lp.tolist(), rem.tolist(), res.tolist(), need.tolist(), 5000.0, 10 ** 9, budget)
+    t0 = time.perf_counter()
+    o2, a2, _ = co.rank_and_plan(*args)
+    py_us = (time.perf_counter() - t0) * 1e6
+    assert o2 == order.tolist() and a2 == act.tolist()
+    return {"workload": f"rank -> EWT -> swap plan over {n} live jobs (simcore.py:439-462)",
+            "cpp_us": round(cpp_us, 1), "python_port_us": round(py_us, 1),
+            "speedup": round(py_us / cpp_us, 1), "cores": 1}
+
+
 def main():
     args = parse()
     world, rank, local = dist_setup(args)
@@ -568,6 +600,7 @@ def main():
               "link_GBs": link / wall / 1e9, "swaps": int(swaps),
               "modeled_span_s": max(o["modeled_span_s"] for o in outs)}
     pred = None if args.no_pred else pred_bench(args, world, rank, local)
+    ctl = control_plane_bench() if rank == 0 else None
     cpu = cpu_pred = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_kv_sample(args, args.cpu_planes)
@@ -658,6 +691,8 @@ def main():
                 "value": round(c5["fp16_GBs"], 3), "unit": "GB/s (fp16 KV swapped)",
                 "link_GBs": round(c5["link_GBs"], 2), "swaps": c5["swaps"], "wall_s": round(c5["wall_s"], 3),
                 "reference_modeled_span_s": round(c5["modeled_span_s"], 3)}
+        if ctl is not None:
+            out["control_plane"] = ctl
         if pred is not None:
             ach = pred["scan_flops_per_launch"] / (pred["scan_ms_avg"] / 1e3) / 1e12 if pred["scan_ms_avg"] else None
             out["predictor"] = {

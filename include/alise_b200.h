@@ -56,6 +56,33 @@ int alise_sm_count(int device, int *out);
  * to *mismatches (device int64).  Test support, not part of the reference interface. */
 int alise_selftest_qdiv(const double *x, int64_t n, int bits, int64_t *mismatches, void *stream);
 
+/* ------------------------------------------------------- host control plane ---- */
+/* Residency codes (kvmanager.py:18-22: "gpu", "cpu", "none", "uploading", "offloading"). */
+#define ALISE_RES_GPU 0
+#define ALISE_RES_CPU 1
+#define ALISE_RES_NONE 2
+#define ALISE_RES_UPLOADING 3
+#define ALISE_RES_OFFLOADING 4
+/* Replaces kvmanager.py:276-294 ewt_ms: per job in global rank order, min(sum of the
+ * remaining ms of the jobs ahead, max(level*aging_ms - waited_ms, 0)); aging_ms = +inf
+ * disables the promote arm.  Host-only, float64 exactly as the reference computes it. */
+int alise_ewt_ms(int64_t n, const int32_t *level, const int64_t *last_promotion_us,
+                 const double *remaining_ms, double aging_ms, int64_t now_us, double *out_ewt_ms);
+/* Replaces kvmanager.py:297-322 plan_swaps over n entries in plan order, budget =
+ * gpu_capacity - in-flight gpu bytes.  out_action per entry: 0 denied, 1 granted,
+ * 2 granted + upload (entry on CPU), 3 denied + offload (entry on GPU). */
+int alise_plan_swaps(int64_t n, const int32_t *residency, const int64_t *need_gpu_bytes,
+                     int64_t budget_bytes, int8_t *out_action);
+/* Replaces simcore.py:439-462 _ranked_with_grants: EWT over the n jobs of the global
+ * rank, plan order = level ascending then (EWT, rank position), in-flight jobs
+ * (uploading/offloading) skipped, then plan_swaps.  out_order[0..*out_count) = rank
+ * positions of the planned entries, out_action as alise_plan_swaps. */
+int alise_rank_and_plan(int64_t n, const int32_t *level, const int64_t *last_promotion_us,
+                        const double *remaining_ms, const int32_t *residency,
+                        const int64_t *need_gpu_bytes, double aging_ms, int64_t now_us,
+                        int64_t budget_bytes, double *out_ewt_ms, int32_t *out_order,
+                        int64_t *out_count, int8_t *out_action);
+
 /* ---------------------------------------------------------------- quantizer ---- */
 /* Drop-in for kvmanager.quantize: rows x row_len values (row i at src + i*row_stride
  * elements, dtype ALISE_DT_*), bits in {4,8}.  codes: rows*row_len bytes (one code

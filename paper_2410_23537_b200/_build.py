@@ -11,6 +11,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libalise_b200.so")
 SOURCES = ["capi_kv.cu", "capi_pred.cu"]
+HOST_SOURCES = ["control.cpp"]  # host-only C++ (float64 semantics: no contraction)
+CXX = os.environ.get("CXX", "g++")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -40,6 +42,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.run(cmd, check=True)
+        objs.append(obj)
+    for src in HOST_SOURCES:
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(CSRC, src.replace(".cpp", ".o"))
+        subprocess.run([CXX, "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-I", os.path.join(ROOT, "include"),
+                        "-c", path, "-o", obj], check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
     # static cudart: the library loads (and its symbols can be checked) on hosts

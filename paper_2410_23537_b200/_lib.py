@@ -32,6 +32,9 @@ _SIGS = {
     "alise_version": [],
     "alise_sm_count": [i32, vp],
     "alise_selftest_qdiv": [vp, i64, i32, vp, vp],
+    "alise_ewt_ms": [i64, vp, vp, vp, dp, i64, vp],
+    "alise_plan_swaps": [i64, vp, vp, i64, vp],
+    "alise_rank_and_plan": [i64, vp, vp, vp, vp, vp, dp, i64, i64, vp, vp, vp, vp],
     "alise_quantize_rows_workspace": [i64, i64, i32, vp],
     "alise_quantize_rows": [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp, vp, vp],
     "alise_dequantize_rows": [vp, vp, vp, i64, i64, i32, vp, vp],

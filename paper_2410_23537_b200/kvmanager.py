@@ -334,42 +334,157 @@ class MemoryState:
         return min(c.complete_us for c in self.in_flight.values())
 
 
+_RES_CODE = {GPU: 0, CPU: 1, NONE: 2, UPLOADING: 3, OFFLOADING: 4}
+
+
+def _i64(values, n, what):
+    out = np.empty(n, dtype=np.int64)
+    for i, v in enumerate(values):
+        if i >= n:
+            break
+        if isinstance(v, (int, np.integer)):
+            out[i] = v
+        elif isinstance(v, float) and v.is_integer():
+            out[i] = int(v)
+        else:
+            raise TypeError(f"{what} must be integral, got {v!r}")
+    return out
+
+
 def ewt_ms(ranked_jobs, remaining_ms_list, aging_ms: float, now_us: int) -> list:
     """Estimated wait time per job in global rank order (kvmanager.py:276-294; Eq. 6-7):
-    min(total remaining time of the jobs ranked ahead, time until aging promotes it)."""
-    waits = []
-    queue_ahead = 0.0
-    aging_on = not math.isinf(aging_ms)
-    for job, rem in zip(ranked_jobs, remaining_ms_list):
-        if aging_on:
-            waited = (now_us - job.last_promotion_us) / 1000.0
-            until_top = max(job.level * aging_ms - waited, 0.0)
+    min(total remaining time of the jobs ranked ahead, time until aging promotes it).
+    Computed by the C++ control plane (csrc/control.cpp alise_ewt_ms)."""
+    ranked_jobs = list(ranked_jobs)
+    rems = list(remaining_ms_list)
+    n = min(len(ranked_jobs), len(rems))
+    if n == 0:
+        return []
+    lev = np.fromiter((j.level for j in ranked_jobs[:n]), dtype=np.int32, count=n)
+    lp = _i64((j.last_promotion_us for j in ranked_jobs[:n]), n, "last_promotion_us")
+    rem = np.asarray(rems[:n], dtype=np.float64)
+    out = np.empty(n, dtype=np.float64)
+    _lib.call("alise_ewt_ms", n, lev.ctypes.data, lp.ctypes.data, rem.ctypes.data, float(aging_ms),
+              int(now_us), out.ctypes.data)
+    return out.tolist()
+
+
+def _budget(memory: MemoryState) -> int:
+    return memory.gpu_capacity - sum(c.gpu_bytes for c in memory.in_flight.values())
+
+
+def _apply_actions(plan: SwapPlan, entries, actions, now_us: int):
+    for e, a in zip(entries, actions):
+        if a in (1, 2):
+            plan.granted.append(e.job_id)
+            if a == 2:
+                plan.commands.append(TransferCommand(e.job_id, "upload", e.link_bytes, e.data_gpu_bytes, now_us, -1))
         else:
-            until_top = math.inf
-        waits.append(min(queue_ahead, until_top))
-        queue_ahead += rem
-    return waits
+            plan.denied.append(e.job_id)
+            if a == 3:
+                plan.commands.append(TransferCommand(e.job_id, "offload", e.link_bytes, e.held_gpu_bytes, now_us, -1))
+    return plan
 
 
 def plan_swaps(entries, memory: MemoryState, now_us: int) -> SwapPlan:
-    """Greedy budgeted residency grant with first-fit skip (kvmanager.py:297-322; Alg. 2)."""
+    """Greedy budgeted residency grant with first-fit skip (kvmanager.py:297-322; Alg. 2),
+    computed by the C++ control plane (csrc/control.cpp alise_plan_swaps)."""
+    entries = list(entries)
+    n = len(entries)
     plan = SwapPlan()
-    budget = memory.gpu_capacity - sum(c.gpu_bytes for c in memory.in_flight.values())
-    used = 0
-    for e in entries:
-        fits = used + e.need_gpu_bytes <= budget
-        if fits:
-            used += e.need_gpu_bytes
-            plan.granted.append(e.job_id)
-            if e.residency == CPU:
-                plan.commands.append(TransferCommand(e.job_id, "upload", e.link_bytes,
-                                                     e.data_gpu_bytes, now_us, -1))
-        else:
-            plan.denied.append(e.job_id)
-            if e.residency == GPU:
-                plan.commands.append(TransferCommand(e.job_id, "offload", e.link_bytes,
-                                                     e.held_gpu_bytes, now_us, -1))
-    return plan
+    if n == 0:
+        return plan
+    res = np.fromiter((_RES_CODE.get(e.residency, 2) for e in entries), dtype=np.int32, count=n)
+    need = _i64((e.need_gpu_bytes for e in entries), n, "need_gpu_bytes")
+    act = np.empty(n, dtype=np.int8)
+    _lib.call("alise_plan_swaps", n, res.ctypes.data, need.ctypes.data, int(_budget(memory)), act.ctypes.data)
+    return _apply_actions(plan, entries, act.tolist(), now_us)
+
+
+def rank_and_plan(ranked_jobs, remaining_ms_list, aging_ms: float, now_us: int, memory: MemoryState,
+                  entry_of):
+    """The reference simulator's rank -> plan step (simcore.py:439-462
+    _ranked_with_grants) in one C++ call (alise_rank_and_plan): EWT over the global
+    rank, plan order = level then (EWT, rank position), in-flight jobs skipped, then the
+    swap planner.  `entry_of(job)` builds the PlanEntry of a planned job (the caller's
+    byte accounting, simcore.py:453-460).  Returns (SwapPlan, ewts)."""
+    ranked_jobs = list(ranked_jobs)
+    n = len(ranked_jobs)
+    plan = SwapPlan()
+    if n == 0:
+        return plan, []
+    lev = np.fromiter((j.level for j in ranked_jobs), dtype=np.int32, count=n)
+    lp = _i64((j.last_promotion_us for j in ranked_jobs), n, "last_promotion_us")
+    rem = np.asarray(list(remaining_ms_list)[:n], dtype=np.float64)
+    res = np.fromiter((_RES_CODE.get(j.residency, 2) for j in ranked_jobs), dtype=np.int32, count=n)
+    entries = [None] * n
+    need = np.zeros(n, dtype=np.int64)
+    for i, j in enumerate(ranked_jobs):
+        if res[i] not in (3, 4):
+            entries[i] = entry_of(j)
+            need[i] = entries[i].need_gpu_bytes
+    ewt = np.empty(n, dtype=np.float64)
+    order = np.empty(n, dtype=np.int32)
+    act = np.empty(n, dtype=np.int8)
+    cnt = np.zeros(1, dtype=np.int64)
+    _lib.call("alise_rank_and_plan", n, lev.ctypes.data, lp.ctypes.data, rem.ctypes.data, res.ctypes.data,
+              need.ctypes.data, float(aging_ms), int(now_us), int(_budget(memory)), ewt.ctypes.data,
+              order.ctypes.data, cnt.ctypes.data, act.ctypes.data)
+    m = int(cnt[0])
+    return _apply_actions(plan, [entries[i] for i in order[:m].tolist()], act[:m].tolist(), now_us), ewt.tolist()
+
+
+class JobTable:
+    """Structure-of-arrays view of the live jobs in global rank order, for engines that
+    plan every iteration over thousands of jobs: the rank -> EWT -> plan step is one
+    C++ call over resident numpy columns (no per-job Python marshalling).  Rows are
+    the rank positions; `set_rank` installs a new rank order."""
+
+    def __init__(self, capacity: int = 1024):
+        self.n = 0
+        self._alloc(max(1, capacity))
+
+    def _alloc(self, cap):
+        old = getattr(self, "job_id", None)
+        cols = {"job_id": np.int64, "level": np.int32, "last_promotion_us": np.int64,
+                "remaining_ms": np.float64, "residency": np.int32, "need_gpu_bytes": np.int64}
+        for name, dt in cols.items():
+            a = np.zeros(cap, dtype=dt)
+            if old is not None:
+                a[: self.n] = getattr(self, name)[: self.n]
+            setattr(self, name, a)
+        self.cap = cap
+        self._ewt = np.empty(cap, dtype=np.float64)
+        self._order = np.empty(cap, dtype=np.int32)
+        self._act = np.empty(cap, dtype=np.int8)
+
+    def set_rank(self, job_id, level, last_promotion_us, remaining_ms, residency, need_gpu_bytes):
+        """Install the live jobs (arrays or sequences in global rank order; residency as
+        strings or ALISE_RES_* codes)."""
+        n = len(job_id)
+        if n > self.cap:
+            self._alloc(max(n, 2 * self.cap))
+        self.n = n
+        self.job_id[:n] = job_id
+        self.level[:n] = level
+        self.last_promotion_us[:n] = last_promotion_us
+        self.remaining_ms[:n] = remaining_ms
+        res = np.asarray(residency)
+        self.residency[:n] = [_RES_CODE[r] for r in res] if res.dtype.kind in "UO" else res
+        self.need_gpu_bytes[:n] = need_gpu_bytes
+
+    def plan(self, aging_ms: float, now_us: int, budget_bytes: int):
+        """-> (order, action, ewt): rank positions of the planned jobs in plan order, their
+        actions (0 denied, 1 granted, 2 granted+upload, 3 denied+offload) and every job's
+        EWT (views valid until the next call)."""
+        n = self.n
+        cnt = np.zeros(1, dtype=np.int64)
+        _lib.call("alise_rank_and_plan", n, self.level.ctypes.data, self.last_promotion_us.ctypes.data,
+                  self.remaining_ms.ctypes.data, self.residency.ctypes.data, self.need_gpu_bytes.ctypes.data,
+                  float(aging_ms), int(now_us), int(budget_bytes), self._ewt.ctypes.data, self._order.ctypes.data,
+                  cnt.ctypes.data, self._act.ctypes.data)
+        m = int(cnt[0])
+        return self._order[:m], self._act[:m], self._ewt[:n]
 
 
 # ----------------------------------------------------------------- KV data plane
