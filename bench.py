@@ -598,7 +598,14 @@ def main():
         swaps = sum_over_ranks(sum(o["swaps_out"] + o["swaps_in"] for o in outs), world)
         c5 = {"replicas": len(rec["replicas"]) if world > 1 else 1, "wall_s": wall, "fp16_GBs": moved / wall / 1e9,
               "link_GBs": link / wall / 1e9, "swaps": int(swaps),
-              "modeled_span_s": max(o["modeled_span_s"] for o in outs)}
+              "modeled_span_s": max(o["modeled_span_s"] for o in outs),
+              "link_bytes_moved": sum_over_ranks(sum(o["link_bytes_moved"] for o in outs), world)}
+        # the same swap stream with incremental (delta) offload: only tokens generated since
+        # a job's host copy was written are re-quantized and moved
+        outs = [replay.replay(rec, replica=r, check_data=False, delta=True) for r in mine]
+        c5["delta"] = {"wall_s": max_over_ranks(sum(o["wall_s"] for o in outs), world),
+                       "link_bytes_moved": sum_over_ranks(sum(o["link_bytes_moved"] for o in outs), world),
+                       "fp16_bytes_moved": sum_over_ranks(sum(o["fp16_bytes_moved"] for o in outs), world)}
     pred = None if args.no_pred else pred_bench(args, world, rank, local)
     ctl = control_plane_bench() if rank == 0 else None
     cpu = cpu_pred = None
@@ -690,7 +697,13 @@ def main():
                             f"with real KV; ledger checked against the reference after every call",
                 "value": round(c5["fp16_GBs"], 3), "unit": "GB/s (fp16 KV swapped)",
                 "link_GBs": round(c5["link_GBs"], 2), "swaps": c5["swaps"], "wall_s": round(c5["wall_s"], 3),
-                "reference_modeled_span_s": round(c5["modeled_span_s"], 3)}
+                "reference_modeled_span_s": round(c5["modeled_span_s"], 3),
+                "link_bytes_moved": int(c5["link_bytes_moved"]),
+                "delta_offload": {"wall_s": round(c5["delta"]["wall_s"], 3),
+                                  "link_bytes_moved": int(c5["delta"]["link_bytes_moved"]),
+                                  "link_bytes_saved_frac": round(1 - c5["delta"]["link_bytes_moved"]
+                                                                 / max(1, c5["link_bytes_moved"]), 4),
+                                  "speedup_vs_full": round(c5["wall_s"] / max(1e-9, c5["delta"]["wall_s"]), 3)}}
         if ctl is not None:
             out["control_plane"] = ctl
         if pred is not None:

@@ -139,6 +139,18 @@ int alise_kv_offload(alise_swapper *sw, const alise_kv_desc *d, const uint16_t *
  * done_event fires (on `stream`) when kv is complete. */
 int alise_kv_upload(alise_swapper *sw, const alise_kv_desc *d, const void *host_slab,
                     uint16_t *kv, void *stream, void *done_event);
+/* Token-range transfers (ROWS kind, staged mode): d->tokens is the job's token capacity
+ * T_cap (HBM kv[L][2][T_cap][hidden], slab laid out for T_cap); only tokens [t0, t1) are
+ * quantized+offloaded into / uploaded+dequantized from their places in the slab.  A
+ * group never spans tokens, so the bytes equal that part of a full offload: re-offloading
+ * a job that grew from t0 to t1 tokens moves only the new tokens (incremental block-wise
+ * offload; the reference re-sends quantized_kv_bytes(kv_tokens) on every
+ * offload, simcore.py:338-339). */
+int alise_kv_offload_range(alise_swapper *sw, const alise_kv_desc *d, const uint16_t *kv,
+                           void *host_slab, int64_t t0, int64_t t1, int *nonfinite_flag, void *stream,
+                           void *done_event);
+int alise_kv_upload_range(alise_swapper *sw, const alise_kv_desc *d, const void *host_slab,
+                          uint16_t *kv, int64_t t0, int64_t t1, void *stream, void *done_event);
 
 /* Order every later transfer of this swapper after `event` (cudaEvent_t), e.g. an
  * upload that reads a host slab an earlier offload wrote. */

@@ -45,6 +45,8 @@ _SIGS = {
     "alise_swapper_destroy": [vp],
     "alise_kv_offload": [vp, vp, vp, vp, vp, vp, vp],
     "alise_kv_upload": [vp, vp, vp, vp, vp, vp],
+    "alise_kv_offload_range": [vp, vp, vp, vp, i64, i64, vp, vp, vp],
+    "alise_kv_upload_range": [vp, vp, vp, vp, i64, i64, vp, vp],
     "alise_swapper_depend": [vp, vp],
     "alise_swapper_timing": [vp, i32],
     "alise_swapper_kernel_stats": [vp, vp, vp, vp, vp],

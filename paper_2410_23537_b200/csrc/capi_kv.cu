@@ -61,6 +61,13 @@ static inline int grid_for(int64_t work, int block, int waves = 8) {
   return (int)std::max<int64_t>(1, std::min(g, cap));
 }
 
+// Segs for `per` work units per segment (per < 2^32): m = ceil(2^64 / per)
+static Segs make_segs(int64_t per, int64_t stride) {
+  Segs g{0, per, stride};
+  if (per > 1) g.m = (uint64_t)(((unsigned __int128)1 << 64) / (uint64_t)per) + 1;
+  return g;
+}
+
 extern "C" const char* alise_last_error(void) { return g_last_error.c_str(); }
 extern "C" int alise_version(void) { return 1; }
 extern "C" int alise_sm_count(int device, int* out) {
@@ -91,8 +98,15 @@ extern "C" int alise_selftest_qdiv(const double* x, int64_t n, int bits, int64_t
 // ------------------------------------------------------------------ fast tile launch
 template <int BITS, bool PACK, bool ZF32, int V, int TP, int WPB, int MINB = 1>
 static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes, double* scale,
-                         void* zero, int* flag, cudaStream_t st) {
+                         void* zero, int* flag, cudaStream_t st, int64_t seg_rows, int64_t seg_stride) {
   constexpr int block = 32 * WPB;
+  Segs seg{0, 0, 0};
+  if (seg_rows) {
+    // segmented sources (token-range transfers): full-width rows, whole rows per segment,
+    // and every tile full (a partial tile takes the contiguous path)
+    if (rows % seg_rows != 0) return fail(ALISE_EINVAL, "segmented quantize: rows must be whole segments");
+    seg = make_segs(seg_rows, seg_stride);
+  }
   constexpr int smem = WPB * 2 * (8 * TP) * (64 * V + 16);
   auto kern = k_quant_tile<BITS, PACK, V, ZF32, TP, WPB, MINB>;
   static int per_sm = 0;
@@ -103,7 +117,7 @@ static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* 
   }
   const int64_t warps = (rows + 8 * TP - 1) / (8 * TP);
   const int grid = grid_for(warps * 32, block, per_sm);
-  kern<<<grid, block, smem, st>>>(x, rows, row_len, codes, scale, zero, flag);
+  kern<<<grid, block, smem, st>>>(x, rows, row_len, codes, scale, zero, flag, seg);
   CKL();
   return ALISE_OK;
 }
@@ -122,10 +136,11 @@ static int qtile_variant() {
 
 template <int BITS, bool PACK, bool ZF32>
 static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
-                            double* scale, void* zero, int* flag, cudaStream_t st) {
+                            double* scale, void* zero, int* flag, cudaStream_t st, int64_t seg_rows,
+                            int64_t seg_stride) {
   const int vpl = (row_len / 8 + 3) / 4;  // 16-byte vectors per lane per row
   const int var = qtile_variant();
-#define QT(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB>(x, rows, row_len, codes, scale, zero, flag, st)
+#define QT(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride)
   if (vpl <= 1) QT(1, 4, 8, 3);
   if (vpl <= 2) {
     if (var == 1) QT(2, 2, 8, 4);
@@ -146,16 +161,16 @@ static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_
 
 static int launch_tile(int bits, bool pack, bool zf32, const uint16_t* x, int64_t rows,
                        int row_len, uint8_t* codes, double* scale, void* zero, int* flag,
-                       cudaStream_t st) {
+                       cudaStream_t st, int64_t seg_rows = 0, int64_t seg_stride = 0) {
   if (bits == 8) {
-    return zf32 ? launch_tile_bits<8, false, true>(x, rows, row_len, codes, scale, zero, flag, st)
-                : launch_tile_bits<8, false, false>(x, rows, row_len, codes, scale, zero, flag, st);
+    return zf32 ? launch_tile_bits<8, false, true>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride)
+                : launch_tile_bits<8, false, false>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride);
   }
   if (pack)
-    return zf32 ? launch_tile_bits<4, true, true>(x, rows, row_len, codes, scale, zero, flag, st)
-                : launch_tile_bits<4, true, false>(x, rows, row_len, codes, scale, zero, flag, st);
-  return zf32 ? launch_tile_bits<4, false, true>(x, rows, row_len, codes, scale, zero, flag, st)
-              : launch_tile_bits<4, false, false>(x, rows, row_len, codes, scale, zero, flag, st);
+    return zf32 ? launch_tile_bits<4, true, true>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride)
+                : launch_tile_bits<4, true, false>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride);
+  return zf32 ? launch_tile_bits<4, false, true>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride)
+              : launch_tile_bits<4, false, false>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride);
 }
 
 static bool tile_ok(int dtype, int64_t row_len, int64_t row_stride, const void* src,
@@ -237,11 +252,20 @@ extern "C" int alise_quantize_rows(const void* src, int src_dtype, int64_t rows,
 
 template <int BITS, bool PACK, bool ZF32>
 static int launch_dequant_tile(const uint8_t* codes, const double* scale, const void* zero,
-                               int64_t n, int row_len, uint16_t* out, cudaStream_t st) {
+                               int64_t n, int row_len, uint16_t* out, cudaStream_t st, int64_t seg_vals,
+                               int64_t seg_stride) {
   constexpr int VALS = PACK ? 32 : 16;
   const int64_t cpr = row_len / VALS;
-  if (row_len % VALS == 0 && !((uintptr_t)codes & 15) && n / VALS < (int64_t(1) << 31) && cpr < 512 &&
-      getenv("ALISE_DQ_NARROW") == nullptr) {
+  const bool wide = row_len % VALS == 0 && !((uintptr_t)codes & 15) && n / VALS < (int64_t(1) << 31) &&
+                    cpr < 512 && getenv("ALISE_DQ_NARROW") == nullptr;
+  Segs seg{0, 0, 0};
+  if (seg_vals) {
+    // segmented destination (token-range upload): whole 16-byte code words per segment
+    if (!wide || seg_vals % VALS || seg_stride % 8 || n % seg_vals)
+      return fail(ALISE_EINVAL, "segmented dequantize needs whole %d-value code words per segment", VALS);
+    seg = make_segs(seg_vals / VALS, seg_stride / 8);
+  }
+  if (wide) {
     const uint32_t nchunks = (uint32_t)(n / VALS);
     const int shift = (cpr & (cpr - 1)) ? -1 : __builtin_ctzll((unsigned long long)cpr);
     const uint64_t recip = ((uint64_t(1) << 40) + cpr - 1) / cpr;
@@ -249,7 +273,7 @@ static int launch_dequant_tile(const uint8_t* codes, const double* scale, const 
     // concurrent higher-priority quantize launch gets SMs as soon as it is queued
     const int grid = (int)((nchunks + 255) / 256);
     k_dequant_wide<BITS, PACK, ZF32><<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(codes), scale, zero,
-                                                           nchunks, shift, recip, reinterpret_cast<uint4*>(out));
+                                                           nchunks, shift, recip, reinterpret_cast<uint4*>(out), seg);
     CKL();
     return ALISE_OK;
   }
@@ -262,20 +286,19 @@ static int launch_dequant_tile(const uint8_t* codes, const double* scale, const 
 template <typename OUT>
 static int dequant_launch(int kind, const uint8_t* codes, const double* scale, const void* zero,
                           bool zf32, int64_t n, int64_t row_len, int64_t T, int64_t Hd, int64_t D,
-                          int bits, bool pack, OUT* out, cudaStream_t st) {
+                          int bits, bool pack, OUT* out, cudaStream_t st, int64_t seg_vals = 0,
+                          int64_t seg_stride = 0) {
   const int64_t nv = n / 8;
   if constexpr (sizeof(OUT) == 2) {
     if (kind == KIND_ROWS && row_len % 8 == 0 && row_len <= (1 << 30) && !((uintptr_t)out & 15)) {
-      if (bits == 8)
-        return zf32 ? launch_dequant_tile<8, false, true>(codes, scale, zero, n, (int)row_len, out, st)
-                    : launch_dequant_tile<8, false, false>(codes, scale, zero, n, (int)row_len, out, st);
-      if (pack)
-        return zf32 ? launch_dequant_tile<4, true, true>(codes, scale, zero, n, (int)row_len, out, st)
-                    : launch_dequant_tile<4, true, false>(codes, scale, zero, n, (int)row_len, out, st);
-      return zf32 ? launch_dequant_tile<4, false, true>(codes, scale, zero, n, (int)row_len, out, st)
-                  : launch_dequant_tile<4, false, false>(codes, scale, zero, n, (int)row_len, out, st);
+#define DQT(B, P, Z) launch_dequant_tile<B, P, Z>(codes, scale, zero, n, (int)row_len, out, st, seg_vals, seg_stride)
+      if (bits == 8) return zf32 ? DQT(8, false, true) : DQT(8, false, false);
+      if (pack) return zf32 ? DQT(4, true, true) : DQT(4, true, false);
+      return zf32 ? DQT(4, false, true) : DQT(4, false, false);
+#undef DQT
     }
   }
+  if (seg_vals) return fail(ALISE_EINVAL, "segmented dequantize: rows kind, fp16, 16-byte aligned only");
   if (nv > 0) {
     const int grid = grid_for(nv, 256, 16);
 #define DQ(B, P) k_dequant<OUT, B, P><<<grid, 256, 0, st>>>(kind, codes, scale, zero, zf32, nv * 8, row_len, T, Hd, D, out)
@@ -712,6 +735,130 @@ extern "C" int alise_kv_upload(alise_swapper* sw, const alise_kv_desc* d, const 
     CK(cudaStreamWaitEvent(st, sw->in_ready[slot], 0));
     TSTART(t_d);
     s = dequant_chunk(d, g, np, sw->ring_in[slot], kv + c * g.ppc * g.plane_elems, st);
+    TSTOP(t_d);
+    if (s) return s;
+    CK(cudaEventRecord(sw->in_free[slot], st));
+  }
+  if (done_event) CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(done_event), st));
+  return ALISE_OK;
+}
+
+// ------------------------------------------------------------------ token-range transfers
+// ROWS kind only (a quantization group never spans tokens, so the codes / params of a
+// token range equal that part of a full offload: a re-offload of a job that grew from t0
+// to t1 tokens moves only [t0, t1) -- incremental block-wise offload).  The desc's
+// `tokens` is the job's token capacity T_cap: HBM kv[L][2][T_cap][hidden] and the host
+// slab laid out for T_cap.  Per chunk of planes the range is quantized compactly into a
+// ring slot and scattered into the slab with 2D copies (one row per plane).
+struct RangeGeom {
+  int64_t R;          // quantization rows per plane in the range
+  int64_t run_vals;   // values per plane in the range
+  int64_t run_codes;  // code bytes per plane in the range
+  int64_t c_off, s_off, z_off;  // slab offsets of the range inside a plane's sections
+  int64_t ring_s(int64_t np) const { return align256(np * run_codes); }
+  int64_t ring_z(int64_t np) const { return ring_s(np) + align256(np * R * 8); }
+};
+
+static int range_geom(const alise_kv_desc* d, const KvGeom& g, int64_t t0, int64_t t1, RangeGeom* r) {
+  if (d->kind != ALISE_KIND_ROWS) return fail(ALISE_EINVAL, "token-range transfers need the rows group kind");
+  if (t0 < 0 || t1 > d->tokens || t0 >= t1) return fail(ALISE_EINVAL, "token range [%lld, %lld) outside [0, %lld)",
+                                                        (long long)t0, (long long)t1, (long long)d->tokens);
+  const int64_t pk = d->packed ? 2 : 1;
+  const int64_t rpt = d->hidden / d->group;
+  r->R = (t1 - t0) * rpt;
+  r->run_vals = (t1 - t0) * d->hidden;
+  r->run_codes = r->run_vals / pk;
+  r->c_off = t0 * d->hidden / pk;
+  r->s_off = t0 * rpt * 8;
+  r->z_off = t0 * rpt * 4;
+  (void)g;
+  return ALISE_OK;
+}
+
+extern "C" int alise_kv_offload_range(alise_swapper* sw, const alise_kv_desc* d, const uint16_t* kv,
+                                      void* host_slab, int64_t t0, int64_t t1, int* flag, void* stream,
+                                      void* done_event) {
+  if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
+  if (sw->mode != ALISE_SWAP_STAGED) return fail(ALISE_EINVAL, "token-range transfers use the staged mode");
+  KvGeom g;
+  int s = geom(d, &g);
+  if (s) return s;
+  RangeGeom rg;
+  s = range_geom(d, g, t0, t1, &rg);
+  if (s) return s;
+  s = sw_ensure(sw, g.rec_bytes, 0);
+  if (s) return s;
+  cudaStream_t st = S(stream);
+  uint8_t* host = reinterpret_cast<uint8_t*>(host_slab);
+  for (int64_t c = 0; c < g.n_chunks; ++c) {
+    const int slot = sw->next_out;
+    sw->next_out = (slot + 1) % kSlots;
+    const int64_t np = g.np_of(c);
+    uint8_t* ring = sw->ring_out[slot];
+    CK(cudaStreamWaitEvent(st, sw->out_free[slot], 0));
+    TSTART(t_q);
+    s = launch_tile(d->bits, d->packed != 0, true, kv + c * g.ppc * g.plane_elems + t0 * d->hidden, np * rg.R,
+                    d->group, ring, reinterpret_cast<double*>(ring + rg.ring_s(np)), ring + rg.ring_z(np), flag,
+                    st, rg.R, g.plane_elems);
+    TSTOP(t_q);
+    if (s) return s;
+    CK(cudaEventRecord(sw->out_ready[slot], st));
+    CK(cudaStreamWaitEvent(sw->s_out, sw->out_ready[slot], 0));
+    uint8_t* rec = host + c * g.rec_bytes;
+    CK(cudaMemcpy2DAsync(rec + rg.c_off, g.code_bytes_pp, ring, rg.run_codes, rg.run_codes, np,
+                         cudaMemcpyDeviceToHost, sw->s_out));
+    CK(cudaMemcpy2DAsync(rec + g.codes_sec(np) + rg.s_off, g.rows_pp * 8, ring + rg.ring_s(np), rg.R * 8,
+                         rg.R * 8, np, cudaMemcpyDeviceToHost, sw->s_out));
+    CK(cudaMemcpy2DAsync(rec + g.codes_sec(np) + g.scale_sec(np) + rg.z_off, g.rows_pp * 4,
+                         ring + rg.ring_z(np), rg.R * 4, rg.R * 4, np, cudaMemcpyDeviceToHost, sw->s_out));
+    CK(cudaEventRecord(sw->out_free[slot], sw->s_out));
+  }
+  if (done_event) CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(done_event), sw->s_out));
+  return ALISE_OK;
+}
+
+extern "C" int alise_kv_upload_range(alise_swapper* sw, const alise_kv_desc* d, const void* host_slab,
+                                     uint16_t* kv, int64_t t0, int64_t t1, void* stream, void* done_event) {
+  if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
+  if (sw->mode != ALISE_SWAP_STAGED) return fail(ALISE_EINVAL, "token-range transfers use the staged mode");
+  KvGeom g;
+  int s = geom(d, &g);
+  if (s) return s;
+  RangeGeom rg;
+  s = range_geom(d, g, t0, t1, &rg);
+  if (s) return s;
+  s = sw_ensure(sw, g.rec_bytes, 0);
+  if (s) return s;
+  cudaStream_t st = S(stream);
+  const uint8_t* host = reinterpret_cast<const uint8_t*>(host_slab);
+  for (int64_t c = 0; c < g.n_chunks; ++c) {
+    const int slot = sw->next_in;
+    sw->next_in = (slot + 1) % kSlots;
+    const int64_t np = g.np_of(c);
+    uint8_t* ring = sw->ring_in[slot];
+    const uint8_t* rec = host + c * g.rec_bytes;
+    CK(cudaStreamWaitEvent(sw->s_in, sw->in_free[slot], 0));
+    CK(cudaMemcpy2DAsync(ring, rg.run_codes, rec + rg.c_off, g.code_bytes_pp, rg.run_codes, np,
+                         cudaMemcpyHostToDevice, sw->s_in));
+    CK(cudaMemcpy2DAsync(ring + rg.ring_s(np), rg.R * 8, rec + g.codes_sec(np) + rg.s_off, g.rows_pp * 8,
+                         rg.R * 8, np, cudaMemcpyHostToDevice, sw->s_in));
+    CK(cudaMemcpy2DAsync(ring + rg.ring_z(np), rg.R * 4, rec + g.codes_sec(np) + g.scale_sec(np) + rg.z_off,
+                         g.rows_pp * 4, rg.R * 4, np, cudaMemcpyHostToDevice, sw->s_in));
+    CK(cudaEventRecord(sw->in_ready[slot], sw->s_in));
+    CK(cudaStreamWaitEvent(st, sw->in_ready[slot], 0));
+    TSTART(t_d);
+    uint16_t* dst = kv + c * g.ppc * g.plane_elems + t0 * d->hidden;
+    const double* rs = reinterpret_cast<const double*>(ring + rg.ring_s(np));
+    const float* rz = reinterpret_cast<const float*>(ring + rg.ring_z(np));
+    if (rg.run_vals % (d->packed ? 32 : 16) == 0 && rg.run_codes % 16 == 0) {
+      s = dequant_launch<uint16_t>(KIND_ROWS, ring, rs, rz, true, np * rg.run_vals, d->group, d->tokens,
+                                   d->hidden, 1, d->bits, d->packed != 0, dst, st, rg.run_vals, g.plane_elems);
+    } else {  // runs not made of whole 16-byte code words: one launch per plane
+      for (int64_t p = 0; p < np && !s; ++p)
+        s = dequant_launch<uint16_t>(KIND_ROWS, ring + p * rg.run_codes, rs + p * rg.R, rz + p * rg.R, true,
+                                     rg.run_vals, d->group, d->tokens, d->hidden, 1, d->bits, d->packed != 0,
+                                     dst + p * g.plane_elems, st);
+    }
     TSTOP(t_d);
     if (s) return s;
     CK(cudaEventRecord(sw->in_free[slot], st));

@@ -50,6 +50,21 @@ __device__ __forceinline__ void raise_flag(int* flag, bool bad) {
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
+// Segmented addressing of the full-precision side of a transfer: `per` work units
+// (rows / code words) per segment, segment starts `stride` elements apart; per == 0
+// means one contiguous run.  A token range [t0, t1) of a layer-major job
+// kv[layer][k|v][T_cap][hidden] is one segment per (layer, k|v) plane; the codes and
+// parameters stay compact.  m = ceil(2^64 / per): q = umulhi(n, m) is exact for
+// n, per < 2^32.
+struct Segs {
+  uint64_t m;
+  int64_t per;
+  int64_t stride;
+};
+__device__ __forceinline__ int64_t seg_of(int64_t n, const Segs& s) {
+  return s.per == 1 ? n : (int64_t)__umul64hi((uint64_t)n, s.m);
+}
+
 // ---------------------------------------------------------------------------------
 // Fused tile kernel: fp16 rows, row_len % 8 == 0, row_len <= 8 * 4 * VPL.
 // A warp owns a 32-row tile.  4 lanes per row, 8 rows per pass, 4 passes; lane l
@@ -93,7 +108,7 @@ template <int BITS, bool PACK, int VPL, bool ZF32, int TP, int WPB, int MINB>
 __global__ void __launch_bounds__(32 * WPB, MINB)
 k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
                 uint8_t* __restrict__ codes, double* __restrict__ scale, void* __restrict__ zero,
-                int* __restrict__ flag) {
+                int* __restrict__ flag, const Segs seg) {
   // TP = passes of 8 rows per warp tile (TILE = 8 * TP rows; 32 keeps every lane busy
   // in the parameter solve).  A lane stages TP x VPL 16-byte vectors per tile.
   constexpr int PASSES = TP;
@@ -117,12 +132,25 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
   auto prefetch = [&](int64_t tile, int slot) {
     uint8_t* b = wbuf + slot * (TILE * ROWB) + sub * ROWB + q4 * 16;
     if (wide_rows && (tile + 1) * TILE <= rows) {
-      // full tile: unpredicated, compile-time offsets
-      const uint16_t* g = x + (tile * TILE + sub) * (int64_t)RL + q4 * 8;
+      // full tile: unpredicated, compile-time offsets (segmented sources: whole tiles
+      // per segment, so a tile never straddles two segments)
+      if (seg.per) {
+        // segmented sources: segments of seg.per rows, seg.stride elements apart
 #pragma unroll
-      for (int p = 0; p < PASSES; ++p)
+        for (int p = 0; p < PASSES; ++p) {
+          const int64_t r = tile * TILE + p * 8 + sub;
+          const int64_t sg = seg_of(r, seg);
+          const uint16_t* g = x + sg * seg.stride + (r - sg * seg.per) * (int64_t)RL + q4 * 8;
 #pragma unroll
-        for (int i = 0; i < VPL; ++i) cp_async16(b + p * 8 * ROWB + i * 64, g + p * 8 * RL + i * 32, true);
+          for (int i = 0; i < VPL; ++i) cp_async16(b + p * 8 * ROWB + i * 64, g + i * 32, true);
+        }
+      } else {
+        const uint16_t* g = x + (tile * TILE + sub) * (int64_t)RL + q4 * 8;
+#pragma unroll
+        for (int p = 0; p < PASSES; ++p)
+#pragma unroll
+          for (int i = 0; i < VPL; ++i) cp_async16(b + p * 8 * ROWB + i * 64, g + p * 8 * RL + i * 32, true);
+      }
     } else {
 #pragma unroll
       for (int p = 0; p < PASSES; ++p) {
@@ -131,7 +159,12 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
         for (int i = 0; i < VPL; ++i) {
           const int vv = q4 + 4 * i;
           const bool ok = tile < ntiles && r < rows && vv < nvec;
-          cp_async16(b + p * 8 * ROWB + i * 64, x + (ok ? r * row_len + vv * 8 : 0), ok);
+          int64_t off = r * row_len;
+          if (seg.per && ok) {
+            const int64_t sg = seg_of(r, seg);
+            off = sg * seg.stride + (r - sg * seg.per) * row_len;
+          }
+          cp_async16(b + p * 8 * ROWB + i * 64, x + (ok ? off + vv * 8 : 0), ok);
         }
       }
     }
@@ -359,7 +392,7 @@ template <int BITS, bool PACK, bool ZF32>
 __global__ void __launch_bounds__(256)
 k_dequant_wide(const uint4* __restrict__ codes, const double* __restrict__ scale,
                const void* __restrict__ zero, uint32_t nchunks, int cpr_shift, uint64_t cpr_recip,
-               uint4* __restrict__ out) {
+               uint4* __restrict__ out, const Segs seg) {
   constexpr int VALS = PACK ? 32 : 16;  // values per 16-byte chunk
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nchunks; k += gridDim.x * blockDim.x) {
     const uint32_t r = cpr_shift >= 0 ? (k >> cpr_shift) : (uint32_t)(((uint64_t)k * cpr_recip) >> 40);
@@ -417,9 +450,14 @@ k_dequant_wide(const uint4* __restrict__ codes, const double* __restrict__ scale
         o[wi] = (o[wi] & ~(0xffffu << sh)) | (hb << sh);
       }
     }
+    uint4* dst = out + (size_t)k * (VALS / 8);
+    if (seg.per) {  // segmented destination (token-range upload); stride in uint4 units
+      const int64_t sg = seg_of(k, seg);
+      dst = out + sg * seg.stride + (k - sg * seg.per) * (VALS / 8);
+    }
 #pragma unroll
     for (int c = 0; c < VALS / 8; ++c)
-      __stcs(out + (size_t)k * (VALS / 8) + c, make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]));
+      __stcs(dst + c, make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]));
   }
 }
 

@@ -598,16 +598,27 @@ class KVSwapEngine:
         # stream's quantize kernels (gated by D2H progress) never block H2D progress
         self.up_stream = torch.cuda.Stream(device=self.device)
 
-    def offload(self, layout: KVLayout, kv, host_addr: int, flag=None, stream=None, event=None):
+    def offload(self, layout: KVLayout, kv, host_addr: int, flag=None, stream=None, event=None, tokens=None):
+        """Quantize + offload a job.  tokens=(t0, t1) moves only that token range into its
+        place in the slab (rows kind; layout.tokens is the job's token capacity)."""
         d = layout.desc()
-        _lib.call("alise_kv_offload", self.handle, _lib.C.byref(d), _lib.ptr(kv), host_addr,
-                  _lib.ptr(flag), _lib.stream_ptr(stream), event or 0)
+        if tokens is None:
+            _lib.call("alise_kv_offload", self.handle, _lib.C.byref(d), _lib.ptr(kv), host_addr,
+                      _lib.ptr(flag), _lib.stream_ptr(stream), event or 0)
+        else:
+            _lib.call("alise_kv_offload_range", self.handle, _lib.C.byref(d), _lib.ptr(kv), host_addr,
+                      int(tokens[0]), int(tokens[1]), _lib.ptr(flag), _lib.stream_ptr(stream), event or 0)
 
-    def upload(self, layout: KVLayout, host_addr: int, kv, stream=None, event=None):
+    def upload(self, layout: KVLayout, host_addr: int, kv, stream=None, event=None, tokens=None):
+        """Upload + dequantize a job (or only tokens=(t0, t1) of it, rows kind)."""
         d = layout.desc()
         st = stream if stream is not None else self.up_stream
-        _lib.call("alise_kv_upload", self.handle, _lib.C.byref(d), host_addr, _lib.ptr(kv),
-                  _lib.stream_ptr(st), event or 0)
+        if tokens is None:
+            _lib.call("alise_kv_upload", self.handle, _lib.C.byref(d), host_addr, _lib.ptr(kv),
+                      _lib.stream_ptr(st), event or 0)
+        else:
+            _lib.call("alise_kv_upload_range", self.handle, _lib.C.byref(d), host_addr, _lib.ptr(kv),
+                      int(tokens[0]), int(tokens[1]), _lib.stream_ptr(st), event or 0)
 
     def depend(self, event_handle: int):
         """Order later transfers after a recorded event (e.g. upload after offload)."""
@@ -661,13 +672,26 @@ class DeviceMemoryState(MemoryState):
     streams it back and dequantizes into the bound tensor, and ``complete`` waits for
     the job's transfer before applying the reference ledger update.  Unbound jobs
     are accounted exactly like the reference (no data to move).
+
+    ``delta=True`` (rows group kind): a job's host slab is kept after its upload, and a
+    later offload quantizes + moves only the tokens generated since the slab was written
+    (``set_tokens`` tracks the job's valid length inside its KV capacity
+    ``layout.tokens``).  The reference ledger and transfer-time model are unchanged;
+    ``link_bytes_moved`` counts the bytes that really crossed the host link.  Kept slabs
+    live outside the ledger's CPU budget and are dropped (oldest first) when the pinned
+    pool runs out.
     """
 
     host_pool_bytes: int = 0
+    delta: bool = False
     engine: object = None
     host_pool: object = None
+    link_bytes_moved: int = 0
     _bound: dict = field(default_factory=dict)
+    _tokens: dict = field(default_factory=dict)
     _slabs: dict = field(default_factory=dict)
+    _host_valid: dict = field(default_factory=dict)
+    _kept: dict = field(default_factory=dict)
     _pending: dict = field(default_factory=dict)
     _flags: dict = field(default_factory=dict)
     _last_offload: dict = field(default_factory=dict)
@@ -678,11 +702,20 @@ class DeviceMemoryState(MemoryState):
         if self.host_pool is None:
             self.host_pool = HostSlabPool(self.host_pool_bytes or self.cpu_capacity)
 
-    def bind(self, job_id: int, kv, layout: KVLayout):
+    def bind(self, job_id: int, kv, layout: KVLayout, tokens: int | None = None):
+        """Bind a job's HBM KV (capacity layout.tokens; `tokens` valid, default all)."""
         self._bound[job_id] = (kv, layout)
+        self._tokens[job_id] = layout.tokens if tokens is None else int(tokens)
+
+    def set_tokens(self, job_id: int, tokens: int):
+        """The job's KV now holds `tokens` valid tokens (it decoded while resident)."""
+        self._tokens[job_id] = int(tokens)
 
     def unbind(self, job_id: int):
         self._bound.pop(job_id, None)
+        self._tokens.pop(job_id, None)
+        self._host_valid.pop(job_id, None)
+        self._kept.pop(job_id, None)
         addr = self._slabs.pop(job_id, None)
         if addr is not None:
             self.host_pool.free(addr)
@@ -690,17 +723,50 @@ class DeviceMemoryState(MemoryState):
     def host_slab(self, job_id: int):
         return self._slabs.get(job_id)
 
+    def _range_bytes(self, layout: KVLayout, t0: int, t1: int) -> int:
+        pk = 2 if layout.packed else 1
+        rpt = layout.hidden // layout.group if layout.kind == "rows" else 0
+        return 2 * layout.layers * (t1 - t0) * (layout.hidden // pk + rpt * 12)
+
+    def _alloc_slab(self, nbytes: int) -> int:
+        while True:
+            try:
+                return self.host_pool.alloc(nbytes)
+            except MemoryAccountingError:
+                if not self._kept:
+                    raise
+                old = next(iter(self._kept))  # oldest kept slab
+                self._kept.pop(old)
+                self._host_valid.pop(old, None)
+                self.host_pool.free(self._slabs.pop(old))
+
     def start_offload(self, job_id, link_bytes, gpu_bytes, now_us):
         cmd = super().start_offload(job_id, link_bytes, gpu_bytes, now_us)
         if job_id in self._bound:
             import torch
             self._ensure()
             kv, layout = self._bound[job_id]
-            addr = self.host_pool.alloc(layout.geometry()["slab_bytes"])
-            self._slabs[job_id] = addr
+            T = self._tokens[job_id]
+            t0 = 0
+            if self.delta and layout.kind == "rows" and job_id in self._kept and self._host_valid[job_id] <= T:
+                self._kept.pop(job_id)          # the slab is live again (ledger-held)
+                t0 = self._host_valid[job_id]
+            else:
+                if job_id in self._kept:
+                    self._kept.pop(job_id)
+                    self.host_pool.free(self._slabs.pop(job_id))
+                self._slabs[job_id] = self._alloc_slab(layout.geometry()["slab_bytes"])
             flag = torch.zeros(1, dtype=torch.int32, device=kv.device)
             ev = _Event()
-            self.engine.offload(layout, kv, addr, flag=flag, event=ev.h)
+            if t0 < T:
+                full = t0 == 0 and T == layout.tokens
+                self.engine.offload(layout, kv, self._slabs[job_id], flag=flag, event=ev.h,
+                                    tokens=None if full else (t0, T))
+                self.link_bytes_moved += (layout.geometry()["slab_bytes"] if full
+                                          else self._range_bytes(layout, t0, T))
+            else:
+                _lib.call("alise_event_record", ev.h, _lib.stream_ptr())
+            self._host_valid[job_id] = T
             self._pending[job_id] = ev
             self._last_offload[job_id] = ev
             self._flags[job_id] = flag
@@ -714,8 +780,12 @@ class DeviceMemoryState(MemoryState):
             prior = self._last_offload.get(job_id)
             if prior is not None:
                 self.engine.depend(prior.h)
+            T = self._host_valid.get(job_id, self._tokens[job_id])
+            full = T == layout.tokens
             ev = _Event()
-            self.engine.upload(layout, self._slabs[job_id], kv, event=ev.h)
+            self.engine.upload(layout, self._slabs[job_id], kv, event=ev.h, tokens=None if full else (0, T))
+            self.link_bytes_moved += (layout.geometry()["slab_bytes"] if full else self._range_bytes(layout, 0, T))
+            self._tokens[job_id] = T
             self._pending[job_id] = ev
         return cmd
 
@@ -727,7 +797,12 @@ class DeviceMemoryState(MemoryState):
             if flag is not None and int(flag.item()):
                 raise ValueError("tensor contains non-finite values")
             if cmd.direction == "upload":
-                self.host_pool.free(self._slabs.pop(cmd.job_id))
+                _, layout = self._bound[cmd.job_id]
+                if self.delta and layout.kind == "rows":
+                    self._kept[cmd.job_id] = True     # clean host copy kept for a delta re-offload
+                else:
+                    self.host_pool.free(self._slabs.pop(cmd.job_id))
+                    self._host_valid.pop(cmd.job_id, None)
                 self._last_offload.pop(cmd.job_id, None)
         super().complete(cmd)
 

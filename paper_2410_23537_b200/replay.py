@@ -35,9 +35,27 @@ def tokens_of(link_bytes: int, layers: int, hidden: int, bits: int) -> int:
     return t
 
 
+def _round_trip(t, lay):
+    """Device-to-device quantize + dequantize of a whole job (the data-check reference)."""
+    import torch
+    g = lay.geometry()
+    slab = torch.empty(g["slab_bytes"], dtype=torch.uint8, device=t.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=t.device)
+    ref = torch.empty_like(t)
+    km._lib.call("alise_kv_quantize", km._lib.C.byref(lay.desc()), km._lib.ptr(t), km._lib.ptr(slab),
+                 km._lib.ptr(flag), km._lib.stream_ptr())
+    km._lib.call("alise_kv_dequantize", km._lib.C.byref(lay.desc()), km._lib.ptr(slab), km._lib.ptr(ref),
+                 km._lib.stream_ptr())
+    return ref
+
+
 def replay(rec: dict, replica: int = 0, group: int = 128, check_data: bool = True, seed: int = 0,
-           max_events: int | None = None):
-    """Replay one replica's swap calls; returns a summary dict."""
+           max_events: int | None = None, delta: bool = False, return_state: bool = False):
+    """Replay one replica's swap calls; returns a summary dict.
+
+    delta=True: jobs keep their KV in a tensor of their final (trace-maximum) token
+    capacity and DeviceMemoryState(delta=True) re-offloads only the tokens generated
+    since a job's host copy was written (same ledger, fewer bytes on the link)."""
     import torch
 
     from . import synthetic
@@ -50,11 +68,24 @@ def replay(rec: dict, replica: int = 0, group: int = 128, check_data: bool = Tru
     f = {name: i for i, name in enumerate(rec["fields"])}
     # pinned pool: the peak of concurrently held host slabs (+ alignment slack)
     peak_cpu = max(e[f["cpu_used"]] for e in events) if events else 0
+    cap = {}
+    for e in events:
+        if e[0] == "o":
+            cap[e[1]] = max(cap.get(e[1], 0), tokens_of(e[2], layers, hidden, bits))
+    # delta mode keeps clean host copies beyond the ledger: give the pool the room of
+    # every job's capacity slab (it still evicts oldest-first when full)
+    pool_bytes = int(peak_cpu * 1.02) + (256 << 20)
+    if delta:
+        pool_bytes = max(pool_bytes, sum(km.KVLayout(layers, T, hidden, hidden // heads, kind="rows", group=group,
+                                                     bits=bits).geometry()["slab_bytes"] + 256
+                                         for T in cap.values()) + (256 << 20))
     ms = km.DeviceMemoryState(gpu_capacity=rec["gpu_capacity"], cpu_capacity=rec["cpu_capacity"],
-                              pcie_bytes_per_ms=rec["pcie_bytes_per_ms"],
-                              host_pool_bytes=int(peak_cpu * 1.02) + (256 << 20))
+                              pcie_bytes_per_ms=rec["pcie_bytes_per_ms"], host_pool_bytes=pool_bytes,
+                              delta=delta)
     dev = torch.device("cuda", torch.cuda.current_device())
-    kv = {}          # job -> tensor
+    kv = {}          # job -> (tensor, layout)
+    orig = {}        # delta + check_data: job -> original (never re-quantized) KV
+    valid = {}       # job -> valid tokens
     expect = {}      # job -> D2D round-trip reference (checked after the first upload)
     inflight = {}    # job -> TransferCommand
     mismatches = 0
@@ -68,10 +99,17 @@ def replay(rec: dict, replica: int = 0, group: int = 128, check_data: bool = Tru
         if op != "o" or job in kv:
             continue
         T = tokens_of(link, layers, hidden, bits)
-        lay = km.KVLayout(layers, T, hidden, hidden // heads, kind="rows", group=group, bits=bits)
         t = synthetic.kv_job_torch(layers, T, hidden, seed=seed, job=job, group=group, device=dev)
+        if delta:
+            full = torch.zeros(layers, 2, cap[job], hidden, dtype=t.dtype, device=dev)
+            full[:, :, :T] = t
+            t = full
+        lay = km.KVLayout(layers, t.shape[2], hidden, hidden // heads, kind="rows", group=group, bits=bits)
         kv[job] = (t, lay)
-        if check_data:
+        valid[job] = T
+        if delta and check_data:
+            orig[job] = t.clone()
+        if check_data and not delta:
             g = lay.geometry()
             slab = torch.empty(g["slab_bytes"], dtype=torch.uint8, device=dev)
             flag = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -81,7 +119,8 @@ def replay(rec: dict, replica: int = 0, group: int = 128, check_data: bool = Tru
             km._lib.call("alise_kv_dequantize", km._lib.C.byref(lay.desc()), km._lib.ptr(slab),
                          km._lib.ptr(ref), km._lib.stream_ptr())
             expect[job] = ref
-        ms.bind(job, t, lay)
+        ms.bind(job, t, lay, tokens=T)
+    ms._ensure()  # engine + pinned pool created before the timed replay
     torch.cuda.synchronize()
     paused = 0.0
     t_start = time.perf_counter()
@@ -92,31 +131,51 @@ def replay(rec: dict, replica: int = 0, group: int = 128, check_data: bool = Tru
         ms.gpu_used, ms.cpu_used = e[f["gpu_before"]], e[f["cpu_before"]]
         if op == "o":
             T = tokens_of(link, layers, hidden, bits)
-            if T != kv[job][1].tokens:
+            if T != valid[job]:
                 # the job decoded while resident: grow its KV (engine work, not timed)
                 torch.cuda.synchronize()
                 tp = time.perf_counter()
                 old, lay0 = kv[job]
-                extra = synthetic.kv_job_torch(layers, T - lay0.tokens, hidden, seed=seed + 1, job=job,
+                extra = synthetic.kv_job_torch(layers, T - valid[job], hidden, seed=seed + 1, job=job,
                                                group=group, device=dev)
-                t = torch.cat([old, extra], dim=2).contiguous()
-                lay = km.KVLayout(layers, T, hidden, hidden // heads, kind="rows", group=group, bits=bits)
-                kv[job] = (t, lay)
+                if delta:
+                    old[:, :, valid[job]:T] = extra
+                    if check_data:
+                        orig[job][:, :, valid[job]:T] = extra
+                    ms.set_tokens(job, T)
+                else:
+                    t = torch.cat([old, extra], dim=2).contiguous()
+                    lay = km.KVLayout(layers, T, hidden, hidden // heads, kind="rows", group=group, bits=bits)
+                    kv[job] = (t, lay)
+                    ms.bind(job, t, lay)
+                valid[job] = T
                 expect.pop(job, None)
-                ms.bind(job, t, lay)
                 torch.cuda.synchronize()
                 paused += time.perf_counter() - tp
+            before = ms._host_valid.get(job, 0) if delta and job in ms._kept else 0
             inflight[job] = ms.start_offload(job, link, gpu_b, t0)
-            moved += 2 * kv[job][1].elements
+            moved += 2 * 2 * layers * hidden * (T - before)
         elif op == "u":
             inflight[job] = ms.start_upload(job, link, gpu_b, t0)
-            moved += 2 * kv[job][1].elements
+            moved += 2 * 2 * layers * hidden * valid[job]
         else:
             cmd = inflight.pop(job)
             ms.complete(cmd)
-            if cmd.direction == "upload" and job in expect:
+            if cmd.direction == "upload" and delta and check_data:
+                # delta mode quantizes every token once, from its original values: after
+                # any upload the job's KV is the D2D round trip of its original KV
                 torch.cuda.synchronize()
-                if not torch.equal(kv[job][0], expect[job]):
+                tp = time.perf_counter()
+                T = valid[job]
+                if not torch.equal(kv[job][0][:, :, :T], _round_trip(orig[job], kv[job][1])[:, :, :T]):
+                    mismatches += 1
+                data_checked += 1
+                torch.cuda.synchronize()
+                paused += time.perf_counter() - tp
+            elif cmd.direction == "upload" and job in expect:
+                torch.cuda.synchronize()
+                T = valid[job]
+                if not torch.equal(kv[job][0][:, :, :T], expect[job][:, :, :T]):
                     mismatches += 1
                 data_checked += 1
                 del expect[job]
@@ -132,9 +191,14 @@ def replay(rec: dict, replica: int = 0, group: int = 128, check_data: bool = Tru
     link_total = ms.swap_in_bytes + ms.swap_out_bytes
     out = {"replica": replica, "events": len(events), "swaps_out": ms.swap_out_count,
            "swaps_in": ms.swap_in_count, "link_bytes": link_total, "fp16_bytes_moved": moved,
+           "link_bytes_moved": ms.link_bytes_moved, "delta": delta,
            "wall_s": wall, "fp16_GBs": moved / wall / 1e9 if wall else None,
            "link_GBs": link_total / wall / 1e9 if wall else None,
            "modeled_span_s": modeled_s, "data_checked": data_checked, "data_mismatches": mismatches}
-    ms.host_pool.close()
-    ms.engine.close()
+    if return_state:  # every job's valid KV at the end (tests)
+        out["state"] = {j: kv[j][0][:, :, :valid[j]] for j in kv}
+    if ms.host_pool is not None:
+        ms.host_pool.close()
+    if ms.engine is not None:
+        ms.engine.close()
     return out

@@ -318,3 +318,80 @@ def test_constant_divisor_division_is_ddiv_rn(bits):
     torch.cuda.synchronize()
     # NaN inputs compare by bits too (both paths return the canonical quiet NaN)
     assert int(bad.item()) == 0
+
+
+# ----------------------------------------------------------------- token-range (delta) transfers
+@pytest.mark.parametrize("group,bits,packed,ppc", [(128, 8, False, 0), (64, 4, True, 3), (64, 8, False, 1)])
+def test_delta_offload_equals_full_offload(km, group, bits, packed, ppc):
+    """Offloading a job in token ranges (as it grows) writes exactly the bytes of one full
+    offload; uploading in ranges restores exactly the full upload (kvmanager.py:108-154
+    applied per (token, group) row)."""
+    import torch
+    from paper_2410_23537_b200 import synthetic
+    L, T, H = 3, 96, 4096
+    kv = synthetic.kv_job_torch(L, T, H, seed=0, job=5, group=group, device="cuda")
+    lay = km.KVLayout(L, T, H, 128, kind="rows", group=group, bits=bits, packed=packed, planes_per_chunk=ppc)
+    g = lay.geometry()
+    pool = km.HostSlabPool(2 * g["slab_bytes"] + 8192)
+    eng = km.KVSwapEngine()
+    try:
+        full, delta = pool.alloc(g["slab_bytes"]), pool.alloc(g["slab_bytes"])
+        pool.view(full, g["slab_bytes"])[:] = 0
+        pool.view(delta, g["slab_bytes"])[:] = 0
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        eng.offload(lay, kv, full, flag=flag)
+        for t0, t1 in [(0, 8), (8, 40), (40, 41), (41, 96)]:
+            eng.offload(lay, kv, delta, flag=flag, tokens=(t0, t1))
+        torch.cuda.synchronize()
+        assert np.array_equal(pool.view(full, g["slab_bytes"]), pool.view(delta, g["slab_bytes"]))
+        ref = torch.zeros_like(kv)
+        eng.upload(lay, full, ref)
+        out = torch.zeros_like(kv)
+        for t0, t1 in [(0, 33), (33, 96)]:
+            eng.upload(lay, delta, out, tokens=(t0, t1))
+        part = torch.zeros_like(kv)
+        eng.upload(lay, delta, part, tokens=(0, 50))
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+        assert torch.equal(part[:, :, :50], ref[:, :, :50]) and not part[:, :, 50:].any()
+        assert int(flag.item()) == 0
+    finally:
+        eng.close()
+        pool.close()
+
+
+def test_delta_transfer_errors(km):
+    import torch
+    lay = km.KVLayout(1, 32, 256, 64, kind="channel", bits=8)
+    eng = km.KVSwapEngine()
+    pool = km.HostSlabPool(1 << 20)
+    try:
+        kv = torch.zeros(1, 2, 32, 256, dtype=torch.float16, device="cuda")
+        addr = pool.alloc(lay.geometry()["slab_bytes"])
+        with pytest.raises(ValueError):
+            eng.offload(lay, kv, addr, tokens=(0, 8))     # groups span tokens
+        lay = km.KVLayout(1, 32, 256, 64, kind="rows", group=64, bits=8)
+        with pytest.raises(ValueError):
+            eng.offload(lay, kv, addr, tokens=(8, 40))    # beyond the token capacity
+        with pytest.raises(ValueError):
+            eng.upload(lay, addr, kv, tokens=(5, 5))      # empty range
+    finally:
+        eng.close()
+        pool.close()
+
+
+def test_c5_replay_delta_offload_same_ledger():
+    """Config-5 replay with incremental (delta) offload: the ledger still equals the
+    reference after every call, fewer bytes cross the link, and after every upload each
+    job's KV equals the device-to-device quantize/dequantize of its ORIGINAL values (each
+    token is quantized once; a full re-offload would re-quantize fp16-rounded
+    dequantized values)."""
+    import os
+
+    from paper_2410_23537_b200 import replay
+    from tests.conftest import GOLDEN
+    rec = replay.load(os.path.join(GOLDEN, "c5_swaps.json.gz"))
+    full = replay.replay(rec, replica=3, max_events=900, check_data=False)
+    dlt = replay.replay(rec, replica=3, max_events=900, delta=True)
+    assert dlt["data_mismatches"] == 0 and dlt["data_checked"] > 50
+    assert dlt["link_bytes_moved"] < full["link_bytes_moved"]
