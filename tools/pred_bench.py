@@ -22,7 +22,8 @@ reg = pr.FallbackRegressor(D, 32, seed=0)
 reg.b2 = 5.0
 p = pr.LengthPredictor(pr.PredictorConfig(dimension=D, db_capacity=N), regressor=reg, store=store)
 res = []
-for B in (4096, 1024, 256, 64, 1):
+BS = [int(b) for b in sys.argv[2].split(",")] if len(sys.argv) > 2 else [4096, 1024, 256, 64, 1]
+for B in BS:
     Q = torch.from_numpy(synthetic.predictor_queries(db, B, seed=1)).cuda()
     for _ in range(3):
         p.predict_batch(Q)
