@@ -89,6 +89,7 @@ struct alise_db {
   int32_t* cand_n = nullptr;
   float* topc = nullptr;
   int32_t* need = nullptr;
+  uint32_t* gkth = nullptr;  // shared running k-th per query (scan threshold sharing)
   CUtensorMap tmQ;
   // optional kernel timing (bench roofline): event pairs around each scan launch
   bool timing = false;
@@ -130,6 +131,8 @@ static void free_scratch(alise_db* db) {
   cudaFree(db->cand_n);
   cudaFree(db->topc);
   cudaFree(db->need);
+  cudaFree(db->gkth);
+  db->gkth = nullptr;
   db->q16 = nullptr;
   db->bp_cap = 0;
   db->splits_cap = 0;
@@ -220,6 +223,7 @@ static int ensure_scratch(alise_db* db, int64_t Bp, int splits, cudaStream_t st)
   CK(cudaMalloc(&db->cand_n, sizeof(int32_t) * sp * bp));
   CK(cudaMalloc(&db->topc, sizeof(float) * sp * bp * KMAX));
   CK(cudaMalloc(&db->need, sizeof(int32_t) * bp));
+  CK(cudaMalloc(&db->gkth, sizeof(uint32_t) * bp));
   db->bp_cap = bp;
   db->splits_cap = sp;
   return make_map(&db->tmQ, db->q16, bp, db->dp, BM);
@@ -280,6 +284,8 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   a.cand_r = db->cand_r;
   a.cand_n = db->cand_n;
   a.topc = db->topc;
+  a.gkth = db->gkth;
+  CK(cudaMemsetAsync(db->gkth, 0, sizeof(uint32_t) * Bp, st));
   static bool attr_set[4] = {false, false, false, false};
   const int kt = (k <= 8 ? 0 : 1) + (two_sm ? 2 : 0);
   if (!attr_set[kt]) {
@@ -366,9 +372,17 @@ extern "C" int alise_predict_finish(int64_t B, int k, const double* sims, const 
   if (hidden < 1 || hidden > 128) return fail(ALISE_EINVAL, "hidden must be in [1, 128]");
   if (B == 0) return ALISE_OK;
   const int64_t threads = B * 32;
-  k_finish<<<(unsigned)((threads + 255) / 256), 256, 0, S(stream)>>>(B, k, sims, lens, counts, s0, queries, dim, W1,
-                                                                     b1, w2, b2, hidden, max_len, log_cap, out_len,
-                                                                     out_retrieved);
+  // shared-memory staging of W1 + the block's 8 queries (fits for the C4 shape 768 x 32)
+  const int64_t smem = dim * hidden * 8 + 8 * dim * 4;
+  const bool stage = smem <= 220 * 1024;
+  static int64_t smem_set = 0;
+  if (stage && smem > smem_set) {
+    CK(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = smem;
+  }
+  k_finish<<<(unsigned)((threads + 255) / 256), 256, stage ? (size_t)smem : 0, S(stream)>>>(
+      B, k, sims, lens, counts, s0, queries, dim, W1, b1, w2, b2, hidden, max_len, log_cap, out_len, out_retrieved,
+      stage);
   CKL();
   return ALISE_OK;
 }

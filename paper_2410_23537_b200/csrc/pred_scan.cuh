@@ -113,7 +113,34 @@ struct ScanArgs {
   int32_t* cand_r;   // [n_splits][Bp][CAP]
   int32_t* cand_n;   // [n_splits][Bp]   (-1 = overflow)
   float* topc;       // [n_splits][Bp][KMAX]
+  uint32_t* gkth;    // [Bp] shared running k-th per query (ord_key; 0 = none yet)
 };
+
+// Order-preserving float <-> uint32 (atomicMax on the key = max on the float).
+__device__ __forceinline__ uint32_t ord_key(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord_val(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// Threshold sharing across the tile groups of a query: every group's running k-th
+// coarse score is a lower bound of the final k-th over all rows, so the largest
+// published one minus 2*delta is a valid candidate threshold for every group
+// (the candidate set stays a superset of the exact top-k).  Called once per tile.
+__device__ __forceinline__ void share_threshold(uint32_t* __restrict__ gk, float kth, float td, float& thr,
+                                                uint32_t& pub) {
+  if (kth > -__int_as_float(0x7f800000)) {
+    const uint32_t key = ord_key(kth);
+    if (key > pub) {
+      atomicMax(gk, key);
+      pub = key;
+    }
+  }
+  const float g = ord_val(*reinterpret_cast<volatile uint32_t*>(gk));
+  if (g - td > thr) thr = g - td;
+}
 
 template <int KT>
 __device__ __forceinline__ float topk_insert(float (&top)[KT], float s, int k) {
@@ -254,6 +281,7 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
       // padding queries (q >= B) never pass
       float thr = q < a.B ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
       float kth = -__int_as_float(0x7f800000);
+      uint32_t pub = 0;
       int cnt = 0;
       bool ovf = false;
       const size_t base = ((size_t)g * a.Bp + q);
@@ -321,6 +349,7 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+        if (q < a.B) share_threshold(a.gkth + q, kth, td, thr, pub);
       }
       a.cand_n[base] = ovf ? -1 : cnt;
 #pragma unroll
@@ -456,6 +485,7 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
       const float td = a.two_delta[q];
       float thr = q < a.B ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
       float kth = -__int_as_float(0x7f800000);
+      uint32_t pub = 0;
       int cnt = 0;
       bool ovf = false;
       const size_t base = ((size_t)g * a.Bp + q);
@@ -522,6 +552,7 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+        if (q < a.B) share_threshold(a.gkth + q, kth, td, thr, pub);
       }
       a.cand_n[base] = ovf ? -1 : cnt;
 #pragma unroll
@@ -736,16 +767,20 @@ k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n
     __syncthreads();
   }
   const float thr = kth - two_delta[q];
-  // 2) gather candidates above the final threshold
-  for (int sp = 0; sp < n_splits; ++sp) {
+  // 2) gather candidates above the final threshold: every split's count loaded in
+  //    parallel, then a warp per split (candidate order is irrelevant: step 4 ranks)
+  int* s_cnt = reinterpret_cast<int*>(s_top);  // the top lists are consumed
+  for (int sp = tid; sp < n_splits; sp += blockDim.x) {
     const int cnt = cand_n[(size_t)sp * Bp + q];
-    if (cnt < 0) {
-      if (tid == 0) s_flag = 1;
-      continue;
-    }
+    s_cnt[sp] = cnt;
+    if (cnt < 0) s_flag = 1;
+  }
+  __syncthreads();
+  for (int sp = warp; sp < n_splits; sp += blockDim.x >> 5) {
+    const int cnt = s_cnt[sp];
     const float* cs = cand_s + ((size_t)sp * Bp + q) * CAP;
     const int32_t* cr = cand_r + ((size_t)sp * Bp + q) * CAP;
-    for (int i = tid; i < cnt; i += blockDim.x) {
+    for (int i = lane; i < cnt; i += 32) {
       if (cs[i] >= thr) {
         const int slot = atomicAdd(&s_n, 1);
         if (slot < MAXC) s_rows[slot] = cr[i];
@@ -903,9 +938,30 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
                          const int32_t* __restrict__ counts, double s0, const float* __restrict__ x, int64_t dim,
                          const double* __restrict__ W1, const double* __restrict__ b1, const double* __restrict__ w2,
                          double b2, int64_t hidden, int64_t max_len, double log_cap, int32_t* __restrict__ out_len,
-                         uint8_t* __restrict__ out_ret) {
+                         uint8_t* __restrict__ out_ret, bool stage) {
   const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  // stage W1 (and each warp's query) in shared memory when some query of the block
+  // takes the MLP branch and the launch provided the space
+  extern __shared__ double smem_fin[];
+  const double* smem_w1 = nullptr;
+  if (stage) {
+    bool mlp = false;
+    if (q < B && lane == 0) {
+      mlp = true;
+      for (int i = 0; i < counts[q]; ++i)
+        if (sims[q * k + i] >= s0) mlp = false;
+    }
+    if (__syncthreads_or(mlp)) {
+      const int64_t nw = dim * hidden;
+      for (int64_t i = threadIdx.x; i < nw; i += blockDim.x) smem_fin[i] = W1[i];
+      float* xs = reinterpret_cast<float*>(smem_fin + nw) + (threadIdx.x >> 5) * dim;
+      if (q < B)
+        for (int64_t i = lane; i < dim; i += 32) xs[i] = x[q * dim + i];
+      __syncthreads();
+      smem_w1 = smem_fin;
+    }
+  }
   if (q >= B) return;
   const int c = counts[q];
   int nq = 0;
@@ -933,8 +989,15 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
     }
     return;
   }
-  // fallback MLP: lane j computes hidden units j, j+32, ...
+  // fallback MLP: lane j computes hidden units j, j+32, ...  The dependent index-order
+  // chain reads W1 and x from shared memory when the block staged them (one L2 round
+  // trip per block instead of one per term).
   const float* xq = x + q * dim;
+  const double* Wm = W1;
+  if (smem_w1) {
+    Wm = smem_w1;
+    xq = reinterpret_cast<const float*>(smem_w1 + dim * hidden) + (threadIdx.x >> 5) * dim;
+  }
   double out = 0.0;
   double hv[4];
   const int per = (int)((hidden + 31) / 32);
@@ -942,7 +1005,7 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
     const int64_t j = lane + 32 * t;
     double acc = 0.0;
     if (j < hidden) {
-      for (int64_t d = 0; d < dim; ++d) acc = __dadd_rn(acc, __dmul_rn((double)__ldg(xq + d), W1[d * hidden + j]));
+      for (int64_t d = 0; d < dim; ++d) acc = __dadd_rn(acc, __dmul_rn((double)xq[d], Wm[d * hidden + j]));
       hv[t] = tanh(__dadd_rn(acc, b1[j]));
     } else {
       hv[t] = 0.0;
