@@ -130,7 +130,7 @@ __device__ __forceinline__ float ord_val(uint32_t k) {
 // published one minus 2*delta is a valid candidate threshold for every group
 // (the candidate set stays a superset of the exact top-k).  Called once per tile.
 __device__ __forceinline__ void share_threshold(uint32_t* __restrict__ gk, float kth, float td, float& thr,
-                                                uint32_t& pub) {
+                                                uint32_t& pub, float& kfloor) {
   if (kth > -__int_as_float(0x7f800000)) {
     const uint32_t key = ord_key(kth);
     if (key > pub) {
@@ -140,6 +140,9 @@ __device__ __forceinline__ void share_threshold(uint32_t* __restrict__ gk, float
   }
   const float g = ord_val(*reinterpret_cast<volatile uint32_t*>(gk));
   if (g - td > thr) thr = g - td;
+  // a group's top list only has to hold values above the shared k-th: the group that
+  // published it holds k values >= it, so the union of the lists keeps its k-th
+  if (g > kfloor) kfloor = g;
 }
 
 template <int KT>
@@ -282,6 +285,7 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
       float thr = q < a.B ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
       float kth = -__int_as_float(0x7f800000);
       uint32_t pub = 0;
+      float kfloor = -__int_as_float(0x7f800000);  // shared k-th: lower values never enter top[]
       int cnt = 0;
       bool ovf = false;
       const size_t base = ((size_t)g * a.Bp + q);
@@ -327,9 +331,9 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
               mask &= mask - 1;
               const float sc = my_stage[j];
               if (!(sc >= thr)) continue;
-              if (sc > kth) {  // beats the running k-th: insert
+              if (sc > kth && sc > kfloor) {  // beats the running k-th: insert
                 kth = topk_insert<KT>(top, sc, k);
-                thr = kth - td;
+                thr = fmaxf(thr, kth - td);
               }
               if (ovf) continue;
               if (cnt == CAP) {
@@ -349,7 +353,7 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
-        if (q < a.B) share_threshold(a.gkth + q, kth, td, thr, pub);
+        if (q < a.B) share_threshold(a.gkth + q, kth, td, thr, pub, kfloor);
       }
       a.cand_n[base] = ovf ? -1 : cnt;
 #pragma unroll
@@ -486,6 +490,7 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
       float thr = q < a.B ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
       float kth = -__int_as_float(0x7f800000);
       uint32_t pub = 0;
+      float kfloor = -__int_as_float(0x7f800000);  // shared k-th: lower values never enter top[]
       int cnt = 0;
       bool ovf = false;
       const size_t base = ((size_t)g * a.Bp + q);
@@ -530,9 +535,9 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
               mask &= mask - 1;
               const float sc = my_stage[j];
               if (!(sc >= thr)) continue;
-              if (sc > kth) {
+              if (sc > kth && sc > kfloor) {
                 kth = topk_insert<KT>(top, sc, k);
-                thr = kth - td;
+                thr = fmaxf(thr, kth - td);
               }
               if (ovf) continue;
               if (cnt == CAP) {
@@ -552,7 +557,7 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-        if (q < a.B) share_threshold(a.gkth + q, kth, td, thr, pub);
+        if (q < a.B) share_threshold(a.gkth + q, kth, td, thr, pub, kfloor);
       }
       a.cand_n[base] = ovf ? -1 : cnt;
 #pragma unroll

@@ -35,12 +35,25 @@ __device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps in hardware (up to ~0.1 ms)
+// instead of re-issuing, leaving issue slots to the epilogue warps of the SM.
+__device__ __forceinline__ bool mbar_try_suspend(uint32_t a, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity), "r"(100000u)
+      : "memory");
+  return ok != 0;
+}
 // Wait for a phase; traps (kernel error instead of a hung GPU) after ~20 s.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try(a, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try(a, parity)) {
+  while (!mbar_try_suspend(a, parity)) {
     if (clock64() - t0 > 40000000000ll) __trap();
   }
 }
