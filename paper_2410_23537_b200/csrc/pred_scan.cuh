@@ -318,11 +318,22 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
                                  fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
           const bool hit = mx >= thr;
           if (__any_sync(0xffffffffu, hit)) {
+            // only the 4-value groups some lane hits are staged and tested (the warp
+            // executes the union of the lanes' groups, usually one or two of eight)
+            uint32_t gm = 0;
+#pragma unroll
+            for (int x = 0; x < 8; ++x) gm |= (m8[x] >= thr ? 1u : 0u) << x;
+            const uint32_t gu = __reduce_or_sync(0xffffffffu, gm);
             uint32_t mask = 0;
 #pragma unroll
-            for (int x = 0; x < 32; ++x) {
-              my_stage[x] = v[x];
-              mask |= (v[x] >= thr ? 1u : 0u) << x;
+            for (int g8 = 0; g8 < 8; ++g8) {
+              if (gu & (1u << g8)) {
+#pragma unroll
+                for (int x = 4 * g8; x < 4 * g8 + 4; ++x) {
+                  my_stage[x] = v[x];
+                  mask |= (v[x] >= thr ? 1u : 0u) << x;
+                }
+              }
             }
             const int rbase = t * BN + c * 32;
             if (rbase + 32 > a.n_rows) mask &= (a.n_rows > rbase) ? (0xffffffffu >> (32 - (a.n_rows - rbase))) : 0u;
@@ -522,11 +533,22 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
                                  fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
           const bool hit = mx >= thr;
           if (__any_sync(0xffffffffu, hit)) {
+            // only the 4-value groups some lane hits are staged and tested (the warp
+            // executes the union of the lanes' groups, usually one or two of eight)
+            uint32_t gm = 0;
+#pragma unroll
+            for (int x = 0; x < 8; ++x) gm |= (m8[x] >= thr ? 1u : 0u) << x;
+            const uint32_t gu = __reduce_or_sync(0xffffffffu, gm);
             uint32_t mask = 0;
 #pragma unroll
-            for (int x = 0; x < 32; ++x) {
-              my_stage[x] = v[x];
-              mask |= (v[x] >= thr ? 1u : 0u) << x;
+            for (int g8 = 0; g8 < 8; ++g8) {
+              if (gu & (1u << g8)) {
+#pragma unroll
+                for (int x = 4 * g8; x < 4 * g8 + 4; ++x) {
+                  my_stage[x] = v[x];
+                  mask |= (v[x] >= thr ? 1u : 0u) << x;
+                }
+              }
             }
             const int rbase = t * BN + c * 32;
             if (rbase + 32 > a.n_rows) mask &= (a.n_rows > rbase) ? (0xffffffffu >> (32 - (a.n_rows - rbase))) : 0u;
@@ -592,13 +614,25 @@ __device__ double warp_exact_dot(const float* __restrict__ a, const float* __res
                                  bool& ok) {
   const int lane = threadIdx.x & 31;
   double hi = 0.0, lo = 0.0, ab = 0.0;
-  for (int64_t d = lane; d < dim; d += 32) {
-    const double p = __dmul_rn((double)__ldg(a + d), (double)__ldg(b + d));
-    double s, e;
-    two_sum(hi, p, s, e);
-    hi = s;
-    lo = __dadd_rn(lo, e);
-    ab = __dadd_rn(ab, fabs(p));
+  // 8 elements per lane in flight per step (rows are random DB rows: DRAM latency);
+  // out-of-range elements are 0, which leaves hi, lo and ab unchanged
+  for (int64_t d0 = lane; d0 < dim; d0 += 256) {
+    float av[8], bv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t d = d0 + 32 * u;
+      av[u] = d < dim ? __ldg(a + d) : 0.f;
+      bv[u] = d < dim ? __ldg(b + d) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double p = __dmul_rn((double)av[u], (double)bv[u]);
+      double s, e;
+      two_sum(hi, p, s, e);
+      hi = s;
+      lo = __dadd_rn(lo, e);
+      ab = __dadd_rn(ab, fabs(p));
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -636,48 +670,49 @@ __device__ double warp_exact_dot(const float* __restrict__ a, const float* __res
 // significands < 2^48 at weights >= 2^-298).  Single thread; used only when the
 // double-double certificate cannot decide the rounding (exact ties at a float64
 // midpoint are common for fp32 inputs).
-__device__ __noinline__ double exact_dot_super(const float* __restrict__ a, const float* __restrict__ b,
-                                               int64_t dim) {
-  constexpr int L = 10;
-  constexpr int BASE = -320;
-  uint64_t acc[L];
-#pragma unroll
-  for (int i = 0; i < L; ++i) acc[i] = 0;
-  for (int64_t d = 0; d < dim; ++d) {
-    const uint32_t bx = __float_as_uint(__ldg(a + d)), by = __float_as_uint(__ldg(b + d));
-    uint32_t mx = bx & 0x7fffffu, my = by & 0x7fffffu;
-    int ex = (bx >> 23) & 255, ey = (by >> 23) & 255;
-    if ((!ex && !mx) || (!ey && !my)) continue;  // a zero factor
-    if (ex) mx |= 0x800000u; else ex = 1;
-    if (ey) my |= 0x800000u; else ey = 1;
-    const uint64_t m = (uint64_t)mx * my;          // < 2^48
-    const int e = (ex - 150) + (ey - 150) - BASE;  // >= 22
-    const int li = e >> 6, sh = e & 63;
-    const uint64_t lo = m << sh;
-    const uint64_t hi = sh ? (m >> (64 - sh)) : 0;
-    if (((bx ^ by) >> 31) == 0) {
-      uint64_t s0 = acc[li] + lo;
-      uint64_t carry = s0 < lo;
-      acc[li] = s0;
-      uint64_t s1 = acc[li + 1] + hi;
-      uint64_t c2 = s1 < hi;
-      s1 += carry;
-      c2 |= (s1 < carry);
-      acc[li + 1] = s1;
-      for (int j = li + 2; j < L && c2; ++j) { acc[j] += 1; c2 = acc[j] == 0; }
-    } else {
-      const uint64_t d0 = acc[li] - lo;
-      uint64_t borrow = acc[li] < lo;
-      acc[li] = d0;
-      const uint64_t t1 = acc[li + 1];
-      uint64_t d1 = t1 - hi;
-      uint64_t b2 = t1 < hi;
-      b2 |= (d1 < borrow);
-      d1 -= borrow;
-      acc[li + 1] = d1;
-      for (int j = li + 2; j < L && b2; ++j) { b2 = acc[j] == 0; acc[j] -= 1; }
-    }
+constexpr int SUPER_L = 10;
+constexpr int SUPER_BASE = -320;
+
+// Add the exact product a*b (fp32 x fp32) into a 640-bit two's complement accumulator.
+__device__ __forceinline__ void super_add(uint64_t (&acc)[SUPER_L], float fa, float fb) {
+  const uint32_t bx = __float_as_uint(fa), by = __float_as_uint(fb);
+  uint32_t mx = bx & 0x7fffffu, my = by & 0x7fffffu;
+  int ex = (bx >> 23) & 255, ey = (by >> 23) & 255;
+  if ((!ex && !mx) || (!ey && !my)) return;  // a zero factor
+  if (ex) mx |= 0x800000u; else ex = 1;
+  if (ey) my |= 0x800000u; else ey = 1;
+  const uint64_t m = (uint64_t)mx * my;                // < 2^48
+  const int e = (ex - 150) + (ey - 150) - SUPER_BASE;  // >= 22
+  const int li = e >> 6, sh = e & 63;
+  const uint64_t lo = m << sh;
+  const uint64_t hi = sh ? (m >> (64 - sh)) : 0;
+  if (((bx ^ by) >> 31) == 0) {
+    uint64_t s0 = acc[li] + lo;
+    uint64_t carry = s0 < lo;
+    acc[li] = s0;
+    uint64_t s1 = acc[li + 1] + hi;
+    uint64_t c2 = s1 < hi;
+    s1 += carry;
+    c2 |= (s1 < carry);
+    acc[li + 1] = s1;
+    for (int j = li + 2; j < SUPER_L && c2; ++j) { acc[j] += 1; c2 = acc[j] == 0; }
+  } else {
+    const uint64_t d0 = acc[li] - lo;
+    uint64_t borrow = acc[li] < lo;
+    acc[li] = d0;
+    const uint64_t t1 = acc[li + 1];
+    uint64_t d1 = t1 - hi;
+    uint64_t b2 = t1 < hi;
+    b2 |= (d1 < borrow);
+    d1 -= borrow;
+    acc[li + 1] = d1;
+    for (int j = li + 2; j < SUPER_L && b2; ++j) { b2 = acc[j] == 0; acc[j] -= 1; }
   }
+}
+
+// Round a 640-bit two's complement fixed-point value (LSB 2^-320) to float64 (RN-even).
+__device__ double super_round(uint64_t (&acc)[SUPER_L]) {
+  constexpr int L = SUPER_L;
   const bool neg = (acc[L - 1] >> 63) != 0;
   if (neg) {  // two's complement magnitude
     uint64_t c = 1;
@@ -702,13 +737,59 @@ __device__ __noinline__ double exact_dot_super(const float* __restrict__ a, cons
     const uint64_t maskp = (r == 63) ? ~0ull : ((1ull << (r + 1)) - 1);
     sticky |= (acc[sp >> 6] & maskp) != 0;
   }
-  int exp2 = msb - 52 + BASE;
+  int exp2 = msb - 52 + SUPER_BASE;
   if (guard && (sticky || (mant & 1))) {
     ++mant;
     if (mant == (1ull << 53)) { mant >>= 1; ++exp2; }
   }
   const double v = ldexp((double)mant, exp2);
   return neg ? -v : v;
+}
+
+// Single thread (reference implementation of the superaccumulator path).
+__device__ __noinline__ double exact_dot_super(const float* __restrict__ a, const float* __restrict__ b,
+                                               int64_t dim) {
+  uint64_t acc[SUPER_L];
+#pragma unroll
+  for (int i = 0; i < SUPER_L; ++i) acc[i] = 0;
+  for (int64_t d = 0; d < dim; ++d) super_add(acc, __ldg(a + d), __ldg(b + d));
+  return super_round(acc);
+}
+
+// Warp-cooperative: each lane accumulates dim/32 products, the 640-bit partial sums are
+// added across lanes (mod 2^640, carries propagated limb by limb), every lane rounds.
+// Called by all 32 lanes (warp-uniform branch).
+__device__ __noinline__ double warp_exact_dot_super(const float* __restrict__ a, const float* __restrict__ b,
+                                                    int64_t dim) {
+  const int lane = threadIdx.x & 31;
+  uint64_t acc[SUPER_L];
+#pragma unroll
+  for (int i = 0; i < SUPER_L; ++i) acc[i] = 0;
+  for (int64_t d0 = lane; d0 < dim; d0 += 256) {
+    float av[8], bv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t d = d0 + 32 * u;
+      av[u] = d < dim ? __ldg(a + d) : 0.f;
+      bv[u] = d < dim ? __ldg(b + d) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) super_add(acc, av[u], bv[u]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    uint64_t c = 0;
+#pragma unroll
+    for (int i = 0; i < SUPER_L; ++i) {
+      const uint64_t other = __shfl_xor_sync(0xffffffffu, acc[i], o);
+      const uint64_t s1 = acc[i] + other;
+      const uint64_t c1 = s1 < other;
+      const uint64_t s2 = s1 + c;
+      c = c1 | (s2 < c);
+      acc[i] = s2;
+    }
+  }
+  return super_round(acc);
 }
 
 // Per query: global coarse k-th from the splits' top lists, candidate compaction,
@@ -774,22 +855,42 @@ k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n
   const float thr = kth - two_delta[q];
   // 2) gather candidates above the final threshold: every split's count loaded in
   //    parallel, then a warp per split (candidate order is irrelevant: step 4 ranks)
-  int* s_cnt = reinterpret_cast<int*>(s_top);  // the top lists are consumed
+  //    and the (split, slot) entries flattened over the whole block through a prefix
+  //    sum of the counts, so every candidate load is in flight at once
+  int* s_off = reinterpret_cast<int*>(s_top);  // the top lists are consumed: [n_splits + 1]
   for (int sp = tid; sp < n_splits; sp += blockDim.x) {
     const int cnt = cand_n[(size_t)sp * Bp + q];
-    s_cnt[sp] = cnt;
+    s_off[sp + 1] = cnt < 0 ? 0 : cnt;
     if (cnt < 0) s_flag = 1;
   }
   __syncthreads();
-  for (int sp = warp; sp < n_splits; sp += blockDim.x >> 5) {
-    const int cnt = s_cnt[sp];
-    const float* cs = cand_s + ((size_t)sp * Bp + q) * CAP;
-    const int32_t* cr = cand_r + ((size_t)sp * Bp + q) * CAP;
-    for (int i = lane; i < cnt; i += 32) {
-      if (cs[i] >= thr) {
-        const int slot = atomicAdd(&s_n, 1);
-        if (slot < MAXC) s_rows[slot] = cr[i];
+  if (warp == 0) {  // inclusive scan of s_off[1..n_splits] (n_splits <= 512)
+    int carry = 0;
+    for (int base = 1; base <= n_splits; base += 32) {
+      const int i = base + lane;
+      int v = i <= n_splits ? s_off[i] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
       }
+      if (i <= n_splits) s_off[i] = v + carry;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) s_off[0] = 0;
+  }
+  __syncthreads();
+  const int total = s_off[n_splits];
+  for (int i = tid; i < total; i += blockDim.x) {
+    int lo = 0, hi = n_splits;  // largest sp with s_off[sp] <= i
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_off[mid] <= i) lo = mid; else hi = mid;
+    }
+    const size_t e = ((size_t)lo * Bp + q) * CAP + (i - s_off[lo]);
+    if (cand_s[e] >= thr) {
+      const int slot = atomicAdd(&s_n, 1);
+      if (slot < MAXC) s_rows[slot] = cand_r[e];
     }
   }
   __syncthreads();
@@ -803,11 +904,11 @@ k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n
     const int row = s_rows[c];
     bool ok;
     double sim = warp_exact_dot(v32 + (size_t)row * dim, q32 + q * dim, dim, ok);
+    if (!ok) {  // warp-uniform: the certificate is computed from butterfly-reduced sums
+      sim = warp_exact_dot_super(v32 + (size_t)row * dim, q32 + q * dim, dim);
+      if (lane == 0) atomicAdd(inexact_count, 1u);
+    }
     if (lane == 0) {
-      if (!ok) {
-        sim = exact_dot_super(v32 + (size_t)row * dim, q32 + q * dim, dim);
-        atomicAdd(inexact_count, 1u);
-      }
       s_sim[c] = sim;
       s_seq[c] = seqs[row];
     }
@@ -849,11 +950,11 @@ k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restr
   for (int64_t row = warp; row < n_rows; row += blockDim.x >> 5) {
     bool ok;
     double sim = warp_exact_dot(v32 + row * dim, q32 + q * dim, dim, ok);
+    if (!ok) {
+      sim = warp_exact_dot_super(v32 + row * dim, q32 + q * dim, dim);
+      if (lane == 0) atomicAdd(inexact_count, 1u);
+    }
     if (lane == 0) {
-      if (!ok) {
-        sim = exact_dot_super(v32 + row * dim, q32 + q * dim, dim);
-        atomicAdd(inexact_count, 1u);
-      }
       double cs = sim;
       int64_t cq = seqs[row];
       int cr = (int)row;
