@@ -881,16 +881,30 @@ k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n
   }
   __syncthreads();
   const int total = s_off[n_splits];
-  for (int i = tid; i < total; i += blockDim.x) {
-    int lo = 0, hi = n_splits;  // largest sp with s_off[sp] <= i
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (s_off[mid] <= i) lo = mid; else hi = mid;
+  for (int i0 = tid; i0 < total; i0 += 8 * blockDim.x) {
+    size_t ev[8];
+    float sv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {  // 8 candidate loads in flight per thread
+      const int i = i0 + u * (int)blockDim.x;
+      sv[u] = -__int_as_float(0x7f800000);
+      ev[u] = 0;
+      if (i < total) {
+        int lo = 0, hi = n_splits;  // largest sp with s_off[sp] <= i
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_off[mid] <= i) lo = mid; else hi = mid;
+        }
+        ev[u] = ((size_t)lo * Bp + q) * CAP + (i - s_off[lo]);
+        sv[u] = __ldg(cand_s + ev[u]);
+      }
     }
-    const size_t e = ((size_t)lo * Bp + q) * CAP + (i - s_off[lo]);
-    if (cand_s[e] >= thr) {
-      const int slot = atomicAdd(&s_n, 1);
-      if (slot < MAXC) s_rows[slot] = cand_r[e];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (sv[u] >= thr) {
+        const int slot = atomicAdd(&s_n, 1);
+        if (slot < MAXC) s_rows[slot] = cand_r[ev[u]];
+      }
     }
   }
   __syncthreads();
