@@ -179,6 +179,8 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
     __syncwarp();
     const uint8_t* b = wbuf + slot * (TILE * ROWB);
     const int64_t row0 = tile * TILE;
+    // full tiles (every row live, every lane's vectors in range) skip all range checks
+    const bool full = wide_rows && (row0 + TILE <= rows);
     // ---------------- A: per-row min / max from shared memory (zero-filled vectors
     // of a partial tile are skipped)
     uint32_t mine = 0;
@@ -189,7 +191,7 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
       __half2 lo2 = __half2half2(__ushort_as_half(0x7c00)), hi2 = __half2half2(__ushort_as_half(0xfc00));
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
-        if (r < rows && q4 + 4 * i < nvec) {
+        if (full || (r < rows && q4 + 4 * i < nvec)) {
           const uint4 d = *reinterpret_cast<const uint4*>(b + rl * ROWB + (q4 + 4 * i) * 16);
           const __half2* h = reinterpret_cast<const __half2*>(&d);
 #pragma unroll
@@ -231,7 +233,6 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
     // full tiles (every row live, every lane's vectors in range) take an unpredicated
     // path with compile-time offsets; the code is the low byte / nibble of
     // y = fma(x, inv_s, z + 1.5*2^23), e = fma(x, inv_s, K - y) proves it (qmath.cuh)
-    const bool full = wide_rows && (row0 + TILE <= rows);
     uint32_t pmask = 0;  // flagged vectors of this lane: bit p * VPL + i
 #pragma unroll
     for (int p = 0; p < PASSES; ++p) {
@@ -244,7 +245,7 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
       const float2 inv2 = make_float2(inv_s, inv_s), zc2 = make_float2(zc, zc);
       const float2 nzc2 = make_float2(-zc, -zc);
       const uint8_t* srow = b + rl * ROWB + q4 * 16;
-      uint8_t* crow = codes + (r * (full ? (int64_t)RL : (int64_t)row_len) + q4 * 8) / (PACK ? 2 : 1);
+      uint8_t* crow = codes + ((uint64_t)(r * (full ? (int64_t)RL : (int64_t)row_len) + q4 * 8) >> (PACK ? 1 : 0));
       uint32_t umask = 0;  // vectors holding a value near a rounding boundary
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
