@@ -96,7 +96,7 @@ extern "C" int alise_selftest_qdiv(const double* x, int64_t n, int bits, int64_t
 }
 
 // ------------------------------------------------------------------ fast tile launch
-template <int BITS, bool PACK, bool ZF32, int V, int TP, int WPB, int MINB = 1>
+template <int BITS, bool PACK, bool ZF32, int V, int TP, int WPB, int MINB = 1, int NBUF = 2>
 static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes, double* scale,
                          void* zero, int* flag, cudaStream_t st, int64_t seg_rows, int64_t seg_stride) {
   constexpr int block = 32 * WPB;
@@ -107,8 +107,8 @@ static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* 
     if (rows % seg_rows != 0) return fail(ALISE_EINVAL, "segmented quantize: rows must be whole segments");
     seg = make_segs(seg_rows, seg_stride);
   }
-  constexpr int smem = WPB * 2 * (8 * TP) * (64 * V + 16);
-  auto kern = k_quant_tile<BITS, PACK, V, ZF32, TP, WPB, MINB>;
+  constexpr int smem = WPB * NBUF * (8 * TP) * (64 * V + 16);
+  auto kern = k_quant_tile<BITS, PACK, V, ZF32, TP, WPB, MINB, NBUF>;
   static int per_sm = 0;
   if (!per_sm) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -123,7 +123,9 @@ static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* 
 }
 
 // Tile shape per row length (V = 16-byte vectors per lane per row; TP passes of 8 rows
-// per warp tile; WPB warps per CTA; MINB = register cap via min CTAs per SM).
+// per warp tile; WPB warps per CTA; MINB = register cap via min CTAs per SM; QT1 = one
+// smem slot per warp).  Measured: 32-row single-buffered tiles (every lane busy in the
+// float64 solve, 24 warps/SM) beat 16-row double-buffered ones by 10-13%.
 // ALISE_QTILE selects tuning variants (tools/kv_kernel_bench.py sweeps them).
 static int qtile_variant() {
   static int v = -1;
@@ -141,21 +143,27 @@ static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_
   const int vpl = (row_len / 8 + 3) / 4;  // 16-byte vectors per lane per row
   const int var = qtile_variant();
 #define QT(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride)
+#define QT1(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB, 1>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride)
   if (vpl <= 1) QT(1, 4, 8, 3);
   if (vpl <= 2) {
     if (var == 1) QT(2, 2, 8, 4);
     if (var == 2) QT(2, 4, 4, 6);
     if (var == 3) QT(2, 2, 8, 3);
-    QT(2, 4, 8, 3);
+    if (var == 4) QT1(2, 4, 8, 3);
+    if (var == 5) QT(2, 4, 8, 3);
+    QT1(2, 4, 8, 4);
   }
   if (vpl <= 4) {
     if (var == 1) QT(4, 2, 8, 4);
     if (var == 2) QT(4, 2, 8, 3);
     if (var == 3) QT(4, 1, 8, 4);
-    QT(4, 2, 4, 6);
+    if (var == 4) QT1(4, 4, 8, 3);
+    if (var == 5) QT(4, 2, 4, 6);
+    QT1(4, 4, 4, 6);
   }
   if (vpl <= 8) QT(8, 2, 4, 3);
 #undef QT
+#undef QT1
   return fail(ALISE_EINVAL, "row_len %d too long for the tile kernel", row_len);
 }
 

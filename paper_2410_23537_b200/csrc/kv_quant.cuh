@@ -104,7 +104,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int BITS, bool PACK, int VPL, bool ZF32, int TP, int WPB, int MINB>
+template <int BITS, bool PACK, int VPL, bool ZF32, int TP, int WPB, int MINB, int NBUF>
 __global__ void __launch_bounds__(32 * WPB, MINB)
 k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
                 uint8_t* __restrict__ codes, double* __restrict__ scale, void* __restrict__ zero,
@@ -119,7 +119,9 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
   extern __shared__ uint8_t smem_pf[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  uint8_t* wbuf = smem_pf + wib * (2 * TILE * ROWB);
+  // NBUF = 2: each warp double-buffers its tiles; NBUF = 1: one slot per warp, the next
+  // tile is loaded after this one is coded (latency hidden by the other warps)
+  uint8_t* wbuf = smem_pf + wib * (NBUF * TILE * ROWB);
   const int sub = lane >> 2;
   const int q4 = lane & 3;
   const int nvec = row_len >> 3;
@@ -173,9 +175,13 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
 
   int slot = 0;
   prefetch(warp_global, 0);
-  for (int64_t tile = warp_global; tile < ntiles; tile += nwarps, slot ^= 1) {
-    prefetch(tile + nwarps, slot ^ 1);
-    cp_async_wait<1>();
+  for (int64_t tile = warp_global; tile < ntiles; tile += nwarps, slot ^= (NBUF - 1)) {
+    if (NBUF == 2) {
+      prefetch(tile + nwarps, slot ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncwarp();
     const uint8_t* b = wbuf + slot * (TILE * ROWB);
     const int64_t row0 = tile * TILE;
@@ -316,6 +322,7 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
       }
     }
     __syncwarp();  // all lanes are done with this slot before it is refilled
+    if (NBUF == 1) prefetch(tile + nwarps, 0);
   }
   cp_async_wait<0>();
 }
