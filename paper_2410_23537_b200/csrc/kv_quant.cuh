@@ -132,6 +132,10 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
   const QDiv dq = qdiv_make((double)((1 << BITS) - 1));
 
   auto prefetch = [&](int64_t tile, int slot) {
+    if (tile >= ntiles) {  // past the end: an empty group keeps the wait counts uniform
+      cp_async_commit();
+      return;
+    }
     uint8_t* b = wbuf + slot * (TILE * ROWB) + sub * ROWB + q4 * 16;
     if (wide_rows && (tile + 1) * TILE <= rows) {
       // full tile: unpredicated, compile-time offsets (segmented sources: whole tiles
