@@ -388,11 +388,11 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
 // completes on the leader's full barrier; the leader's commits are multicast to both
 // CTAs (stage-free and accumulator-full); both CTAs' epilogues release the TMEM
 // accumulator to the leader.  Epilogue logic is the same as k_scan.
-constexpr int STAGES2 = 6;
+constexpr int STAGES2 = 7;  // 7 x 32 KB: the hit path needs no smem staging
 constexpr int A2_BYTES = BM * BK * 2;         // 16 KB: this CTA's 128 queries
 constexpr int B2_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's 128 DB rows
 constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
-constexpr int SCAN2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 256 + BM * 33 * 4;
+constexpr int SCAN2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 256;
 
 template <int KT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
@@ -404,7 +404,7 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
   uint64_t* tfull = empty + STAGES2;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* stage32 = reinterpret_cast<float*>(smem + STAGES2 * STAGE2_BYTES + 256);
+
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_ctarank();
@@ -485,7 +485,6 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
   } else {  // ---------------- epilogue: warps 2..5 of both CTAs, thread = query
     const int quarter = warp & 3;
     const int tq = quarter * 32 + lane;
-    float* my_stage = stage32 + tq * 33;
     const int k = a.k;
     const uint32_t tempty_leader0 = sm100::mapa(sm100::smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = sm100::mapa(sm100::smem_u32(&tempty[1]), 0);
@@ -545,7 +544,6 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
               if (gu & (1u << g8)) {
 #pragma unroll
                 for (int x = 4 * g8; x < 4 * g8 + 4; ++x) {
-                  my_stage[x] = v[x];
                   mask |= (v[x] >= thr ? 1u : 0u) << x;
                 }
               }
@@ -555,7 +553,10 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
             while (mask) {
               const int j = __ffs(mask) - 1;
               mask &= mask - 1;
-              const float sc = my_stage[j];
+              float sc = v[0];  // v[j] (rare path: a select chain instead of a smem stage)
+#pragma unroll
+              for (int x = 1; x < 32; ++x)
+                if (x == j) sc = v[x];
               if (!(sc >= thr)) continue;
               if (sc > kth && sc > kfloor) {
                 kth = topk_insert<KT>(top, sc, k);
