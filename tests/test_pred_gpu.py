@@ -274,3 +274,24 @@ def test_binary_snapshot_round_trip(pr, tmp_path):
     torch.cuda.synchronize()
     assert torch.equal(a[0], b[0]) and torch.equal(a[2], b[2])
     assert torch.equal(a[1] - 200, b[1])  # re-added from seq 0 in the same order
+
+
+@pytest.mark.parametrize("B", [1, 256, 700])
+def test_shared_thresholds_with_ties_across_tile_groups(pr, B):
+    """The scan's tile groups share their running k-th (atomic max per query) and keep
+    only values above it in their top lists; exact ties of the k-th spread over many
+    groups (copies of one row every ~2k rows) and near-ties must still give the exact
+    (-sim, seq) top-k."""
+    g = np.random.default_rng(B)
+    n, d = 120_000, 256
+    db = g.standard_normal((n, d)).astype(np.float32)
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    target = db[5].copy()
+    db[np.arange(1000, n, 2048)] = target              # ~58 exact copies in different groups
+    near = np.arange(1500, n, 4096)
+    db[near] = target + 1e-3 * g.standard_normal((near.size, d)).astype(np.float32)
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = np.repeat(target[None, :], B, axis=0)
+    Q[B // 2:] = g.standard_normal((B - B // 2, d)).astype(np.float32)
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    check_batch(pr, db, lens, Q.astype(np.float32), 8)
