@@ -1126,6 +1126,7 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
     const int64_t j = lane + 32 * t;
     double acc = 0.0;
     if (j < hidden) {
+#pragma unroll 8
       for (int64_t d = 0; d < dim; ++d) acc = __dadd_rn(acc, __dmul_rn((double)xq[d], Wm[d * hidden + j]));
       hv[t] = tanh(__dadd_rn(acc, b1[j]));
     } else {
