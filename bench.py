@@ -658,8 +658,12 @@ def main():
                          "bytes_per_launch": q_bytes, "avg_launch_ms": q_avg_ms,
                          "traffic": (round(traffic["k_quant_tile"]["dram_bytes_per_value"] * chunk_elems)
                                      if "k_quant_tile" in traffic else None),
-                         "traffic_source": traffic.get("k_quant_tile", {}).get("source")},
-            "roofline_dequant": {"bound": "hbm", "kernel": "k_dequant", "achieved":
+                         "traffic_source": traffic.get("k_quant_tile", {}).get("source"),
+                         "note": "launches timed inside the swap step, where the upload side's dequantize "
+                                 "kernels run concurrently on a second stream and share HBM and SMs "
+                                 "(the step itself is host-link bound: roofline_link); roofline_isolated is "
+                                 "the same kernel on the same chunks with nothing else running"},
+            "roofline_dequant": {"bound": "hbm", "kernel": "k_dequant_wide", "achieved":
                                  round(d_ach, 1) if d_ach else None, "peak": hbm_peak,
                                  "frac": round(d_ach / hbm_peak, 4) if d_ach else None,
                                  "avg_launch_ms": d_avg_ms},
