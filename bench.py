@@ -586,6 +586,13 @@ def main():
                             packed=True) for t in ctx]
         kv3 = kv_bench(args, world, rank, local, layouts=lays, e2e=False)
         kv3["tokens_total"] = int(ctx.sum())
+    kvch = None
+    if not args.no_c3:
+        # C2 in the reference's accounting layout: per (layer, k|v, hidden column) channel
+        # along tokens (kvmanager.py:72-75), 16 of the 64 jobs
+        from paper_2410_23537_b200 import kvmanager as km
+        lays = [km.KVLayout(args.layers, args.tokens, args.hidden, args.head_dim, kind="channel", bits=8)] * 16
+        kvch = kv_bench(args, world, rank, local, layouts=lays, e2e=False)
     c5 = None
     if not args.no_c5:
         from paper_2410_23537_b200 import replay
@@ -685,6 +692,15 @@ def main():
                                         "achieved": round(iso_ach, 1), "peak": hbm_peak, "unit": "GB/s",
                                         "frac": round(iso_ach / hbm_peak, 4),
                                         "ms_per_job": round(iso["quant_ms_per_job"], 4)}
+        if kvch is not None:
+            out["kv_c2_channel"] = {
+                "workload": f"C2 layout variant: 16 Llama-2-7B jobs x {args.tokens} tokens, INT8 per channel "
+                            f"(layer, k|v, hidden column) along tokens — the reference's accounting channel",
+                "value": round(kvch["value"], 3), "unit": "GB/s (fp16 KV swapped out+in per s)",
+                "ms_per_step": round(kvch["ms_per_step"], 3),
+                "link_GBs_per_gpu": round(kvch["link_GBs_total"] / world, 2),
+                "link_frac": round(kvch["link_GBs_total"] / world / link_peak, 4),
+                "quant_launch_ms_avg": kvch["quant_ms_total"] / max(1, kvch["quant_launches"])}
         if kv3 is not None:
             out["kv_c3"] = {"workload": f"C3: 256 ShareGPT-mix jobs ({kv3['tokens_total']} ctx tokens), Llama-2-7B"
                                         f" KV, INT4 g=64 packed, LPT over {world} GPU(s)",
