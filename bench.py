@@ -626,9 +626,9 @@ def main():
         chunk_elems = layout_elems / geo["n_chunks"]
         rows_per_chunk = geo["rows"] / geo["n_chunks"]
         q_bytes = chunk_elems * (2 + args.bits / 8 / (2 if args.packed else 1) * (2 if args.packed else 1)) \
-            + rows_per_chunk * 12
+            + rows_per_chunk * 4
         if args.packed:
-            q_bytes = chunk_elems * (2 + 0.5) + rows_per_chunk * 12
+            q_bytes = chunk_elems * (2 + 0.5) + rows_per_chunk * 4
         q_avg_ms = kv["quant_ms_total"] / max(1, kv["quant_launches"])
         d_avg_ms = kv["deq_ms_total"] / max(1, kv["deq_launches"])
         q_ach = q_bytes / (q_avg_ms / 1e3) / 1e9 if q_avg_ms > 0 else None

@@ -114,8 +114,11 @@ typedef struct {
 } alise_kv_desc;
 
 /* Host slab layout: ceil(planes/planes_per_chunk) chunk records, each
- *   [codes of its planes, native element order][scale f64 per row][zero f32 per row]
- * with every section 256-byte aligned.  rows = groups; link bytes = slab bytes. */
+ *   [codes of its planes, native element order][fp16 (min, -max) per group]
+ * with every section 256-byte aligned.  A group's float64 (scale, zero) are a function
+ * of its (min, max) (kvmanager.py:130-146) and are recomputed bit-exactly on upload, so
+ * the slab carries 4 bytes per group instead of 12.  rows = groups; link bytes = slab
+ * bytes. */
 int alise_kv_layout(const alise_kv_desc *d, int64_t *slab_bytes, int64_t *rows,
                     int64_t *chunk_bytes, int64_t *n_chunks);
 /* Device-to-device quantize of a whole job into a device slab (same layout). */

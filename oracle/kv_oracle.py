@@ -41,8 +41,18 @@ def quantize_rows(x, bits: int):
     if not np.isfinite(a).all():
         raise ValueError("tensor contains non-finite values")
     qmax = float(2 ** bits - 1)
-    lo = a.min(axis=1)
-    hi = a.max(axis=1)
+    s, z = params_from_minmax(a.min(axis=1), a.max(axis=1), bits)
+    codes = np.clip(np.rint(a / s[:, None] + z[:, None]), 0.0, qmax).astype(np.uint8)
+    return codes, s[:, None].copy(), z[:, None].copy()
+
+
+def params_from_minmax(lo, hi, bits: int):
+    """(scale, zero) per row from the row (min, max), kvmanager.py:130-146.  The data
+    plane's transfer slabs store only the fp16 (min, max) of each group and recompute
+    (scale, zero) with exactly this solve on upload."""
+    qmax = float(2 ** bits - 1)
+    lo = np.asarray(lo, dtype=np.float64).copy()
+    hi = np.asarray(hi, dtype=np.float64).copy()
     flat = hi == lo
     # kvmanager.py:135-136 (degenerate rows: scale 1, zero -min)
     with np.errstate(divide="ignore", invalid="ignore"):
@@ -59,8 +69,7 @@ def quantize_rows(x, bits: int):
         idx = np.flatnonzero(active)
         s[idx] = nxt
         active[idx[~moved]] = False
-    codes = np.clip(np.rint(a / s[:, None] + z[:, None]), 0.0, qmax).astype(np.uint8)
-    return codes, s[:, None].copy(), z[:, None].copy()
+    return s, z
 
 
 def dequantize_rows(codes, scale, zero):

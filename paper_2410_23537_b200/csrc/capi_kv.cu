@@ -98,7 +98,8 @@ extern "C" int alise_selftest_qdiv(const double* x, int64_t n, int bits, int64_t
 // ------------------------------------------------------------------ fast tile launch
 template <int BITS, bool PACK, bool ZF32, int V, int TP, int WPB, int MINB = 1, int NBUF = 2>
 static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes, double* scale,
-                         void* zero, int* flag, cudaStream_t st, int64_t seg_rows, int64_t seg_stride) {
+                         void* zero, uint32_t* mm, int* flag, cudaStream_t st, int64_t seg_rows,
+                         int64_t seg_stride) {
   constexpr int block = 32 * WPB;
   Segs seg{0, 0, 0};
   if (seg_rows) {
@@ -117,7 +118,7 @@ static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* 
   }
   const int64_t warps = (rows + 8 * TP - 1) / (8 * TP);
   const int grid = grid_for(warps * 32, block, per_sm);
-  kern<<<grid, block, smem, st>>>(x, rows, row_len, codes, scale, zero, flag, seg);
+  kern<<<grid, block, smem, st>>>(x, rows, row_len, codes, scale, zero, mm, flag, seg);
   CKL();
   return ALISE_OK;
 }
@@ -138,12 +139,12 @@ static int qtile_variant() {
 
 template <int BITS, bool PACK, bool ZF32>
 static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
-                            double* scale, void* zero, int* flag, cudaStream_t st, int64_t seg_rows,
-                            int64_t seg_stride) {
+                            double* scale, void* zero, uint32_t* mm, int* flag, cudaStream_t st,
+                            int64_t seg_rows, int64_t seg_stride) {
   const int vpl = (row_len / 8 + 3) / 4;  // 16-byte vectors per lane per row
   const int var = qtile_variant();
-#define QT(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride)
-#define QT1(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB, 1>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride)
+#define QT(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride)
+#define QT1(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB, 1>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride)
   if (vpl <= 1) QT(1, 4, 8, 3);
   if (vpl <= 2) {
     if (var == 1) QT(2, 2, 8, 4);
@@ -169,16 +170,16 @@ static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_
 
 static int launch_tile(int bits, bool pack, bool zf32, const uint16_t* x, int64_t rows,
                        int row_len, uint8_t* codes, double* scale, void* zero, int* flag,
-                       cudaStream_t st, int64_t seg_rows = 0, int64_t seg_stride = 0) {
+                       cudaStream_t st, int64_t seg_rows = 0, int64_t seg_stride = 0, uint32_t* mm = nullptr) {
   if (bits == 8) {
-    return zf32 ? launch_tile_bits<8, false, true>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride)
-                : launch_tile_bits<8, false, false>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride);
+    return zf32 ? launch_tile_bits<8, false, true>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride)
+                : launch_tile_bits<8, false, false>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride);
   }
   if (pack)
-    return zf32 ? launch_tile_bits<4, true, true>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride)
-                : launch_tile_bits<4, true, false>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride);
-  return zf32 ? launch_tile_bits<4, false, true>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride)
-              : launch_tile_bits<4, false, false>(x, rows, row_len, codes, scale, zero, flag, st, seg_rows, seg_stride);
+    return zf32 ? launch_tile_bits<4, true, true>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride)
+                : launch_tile_bits<4, true, false>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride);
+  return zf32 ? launch_tile_bits<4, false, true>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride)
+              : launch_tile_bits<4, false, false>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride);
 }
 
 static bool tile_ok(int dtype, int64_t row_len, int64_t row_stride, const void* src,
@@ -218,7 +219,7 @@ static int rows_generic(const T* x, int64_t rows, int64_t row_len, int64_t row_s
   CKL();
   k_params<false><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
       KIND_ROWS, rows, nch, pmn, pmx, nullptr, nullptr, 0, 1, bits, InTraits<T>::wide, scale,
-      zero, fastp);
+      zero, fastp, nullptr);
   CKL();
   (void)zf32;
   const int64_t n = rows * row_len;
@@ -347,10 +348,13 @@ extern "C" int alise_dequantize_rows(const uint8_t* codes, const double* scale, 
 // ------------------------------------------------------------------ KV job layout
 struct KvGeom {
   int64_t planes, plane_elems, rows_pp, code_bytes_pp, ppc, n_chunks, rec_bytes, slab_bytes;
+  // chunk record: [codes][fp16 (min, -max) per group]; (scale, zero) are recomputed
+  // from (min, max) on upload (k_expand_params), 4 bytes per group instead of 12
   int64_t codes_sec(int64_t np) const { return align256(np * code_bytes_pp); }
-  int64_t scale_sec(int64_t np) const { return align256(np * rows_pp * 8); }
-  int64_t zero_sec(int64_t np) const { return align256(np * rows_pp * 4); }
-  int64_t rec(int64_t np) const { return codes_sec(np) + scale_sec(np) + zero_sec(np); }
+  int64_t mm_sec(int64_t np) const { return align256(np * rows_pp * 4); }
+  int64_t rec(int64_t np) const { return codes_sec(np) + mm_sec(np); }
+  // device scratch for a chunk's expanded (scale f64, zero f32)
+  int64_t pws_bytes() const { return align256(ppc * rows_pp * 8) + align256(ppc * rows_pp * 4); }
   int64_t np_of(int64_t c) const { return std::min(ppc, planes - c * ppc); }
 };
 
@@ -413,24 +417,24 @@ static int64_t cols_workspace(const alise_kv_desc* d, const KvGeom& g, int* nch_
   nch = (d->tokens + tchunk - 1) / tchunk;
   *nch_out = (int)nch;
   *tchunk_out = tchunk;
-  return 2 * align256(g.ppc * nch * d->hidden * 4) + align256(g.ppc * g.rows_pp * 16);
+  return 2 * align256(g.ppc * nch * d->hidden * 4) + align256(g.ppc * g.rows_pp * 16) + g.pws_bytes();
 }
 
-// Quantize np planes starting at kv into one chunk record at rec.
+// Quantize np planes starting at kv into one chunk record at rec ([codes][min/max]).
 static int quant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, const uint16_t* kv,
                        uint8_t* rec, int* flag, void* ws, cudaStream_t st) {
   uint8_t* codes = rec;
-  double* scale = reinterpret_cast<double*>(rec + g.codes_sec(np));
-  float* zero = reinterpret_cast<float*>(rec + g.codes_sec(np) + g.scale_sec(np));
+  uint32_t* mm = reinterpret_cast<uint32_t*>(rec + g.codes_sec(np));
   const int64_t rows = np * g.rows_pp;
   if (d->kind == ALISE_KIND_ROWS)
-    return launch_tile(d->bits, d->packed != 0, true, kv, rows, d->group, codes, scale, zero, flag, st);
+    return launch_tile(d->bits, d->packed != 0, true, kv, rows, d->group, codes, nullptr, nullptr, flag, st,
+                       0, 0, mm);
   const int cpr = d->kind == ALISE_KIND_CHANNEL ? 1 : (int)d->head_dim;
   if (d->hidden % 128 == 0 && cpr <= 128 && 128 % cpr == 0) {
     dim3 grid((unsigned)(d->hidden / 128), (unsigned)np);
-    if (d->bits == 8) k_quant_cols<8, false><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, scale, zero, flag);
-    else if (d->packed) k_quant_cols<4, true><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, scale, zero, flag);
-    else k_quant_cols<4, false><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, scale, zero, flag);
+    if (d->bits == 8) k_quant_cols<8, false><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, mm, flag);
+    else if (d->packed) k_quant_cols<4, true><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, mm, flag);
+    else k_quant_cols<4, false><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, mm, flag);
     CKL();
     return ALISE_OK;
   }
@@ -441,12 +445,15 @@ static int quant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, cons
   float* pmn = reinterpret_cast<float*>(w);
   float* pmx = reinterpret_cast<float*>(w + align256(g.ppc * nch * d->hidden * 4));
   float4* fastp = reinterpret_cast<float4*>(w + 2 * align256(g.ppc * nch * d->hidden * 4));
+  char* pw = w + 2 * align256(g.ppc * nch * d->hidden * 4) + align256(g.ppc * g.rows_pp * 16);
+  double* scale = reinterpret_cast<double*>(pw);
+  float* zero = reinterpret_cast<float*>(pw + align256(g.ppc * g.rows_pp * 8));
   dim3 grid((unsigned)((d->hidden / 8 + 127) / 128), (unsigned)nch, (unsigned)np);
   k_minmax_cols<<<grid, 128, 0, st>>>(kv, d->tokens, d->hidden, tchunk, pmn, pmx, flag);
   CKL();
   k_params<true><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
       d->kind, rows, nch, nullptr, nullptr, pmn, pmx, d->hidden, d->head_dim > 0 ? d->head_dim : 1,
-      d->bits, false, scale, zero, fastp);
+      d->bits, false, scale, zero, fastp, mm);
   CKL();
   const int64_t nvec = np * g.plane_elems / 8;
   const int gr = grid_for(nvec, 256, 16);
@@ -461,11 +468,23 @@ static int quant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, cons
   return ALISE_OK;
 }
 
-static int dequant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, const uint8_t* rec,
-                         uint16_t* kv, cudaStream_t st) {
-  const uint8_t* codes = rec;
-  const double* scale = reinterpret_cast<const double*>(rec + g.codes_sec(np));
-  const float* zero = reinterpret_cast<const float*>(rec + g.codes_sec(np) + g.scale_sec(np));
+// (min, max) of `groups` groups -> (scale, zero) into the scratch pws
+static int expand_params(int bits, const uint32_t* mm, int64_t groups, void* pws, int64_t cap_groups,
+                         double** scale, float** zero, cudaStream_t st) {
+  char* w = reinterpret_cast<char*>(pws);
+  *scale = reinterpret_cast<double*>(w);
+  *zero = reinterpret_cast<float*>(w + align256(cap_groups * 8));
+  if (groups <= 0) return ALISE_OK;
+  const unsigned grid = (unsigned)((groups + 255) / 256);
+  if (bits == 8) k_expand_params<8><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero);
+  else k_expand_params<4><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero);
+  CKL();
+  return ALISE_OK;
+}
+
+// Dequantize np planes from codes with expanded (scale, zero).
+static int dequant_chunk_sz(const alise_kv_desc* d, const KvGeom& g, int64_t np, const uint8_t* codes,
+                            const double* scale, const float* zero, uint16_t* kv, cudaStream_t st) {
   const int64_t D = d->head_dim > 0 ? d->head_dim : 1;
   const int cpr = d->kind == ALISE_KIND_CHANNEL ? 1 : (int)D;
   if (d->kind != ALISE_KIND_ROWS && d->hidden % 128 == 0 && cpr <= 128 && 128 % cpr == 0) {
@@ -479,6 +498,17 @@ static int dequant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, co
   return dequant_launch<uint16_t>(d->kind, codes, scale, zero, true, np * g.plane_elems,
                                   d->kind == ALISE_KIND_ROWS ? d->group : 1, d->tokens, d->hidden,
                                   D, d->bits, d->packed != 0, kv, st);
+}
+
+// Expand a chunk record's (min, max) into pws, then dequantize it.
+static int dequant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, const uint8_t* rec,
+                         uint16_t* kv, void* pws, cudaStream_t st) {
+  double* scale;
+  float* zero;
+  int s = expand_params(d->bits, reinterpret_cast<const uint32_t*>(rec + g.codes_sec(np)), np * g.rows_pp, pws,
+                        g.ppc * g.rows_pp, &scale, &zero, st);
+  if (s) return s;
+  return dequant_chunk_sz(d, g, np, rec, scale, zero, kv, st);
 }
 
 extern "C" int alise_kv_quantize(const alise_kv_desc* d, const uint16_t* kv, uint8_t* slab,
@@ -505,11 +535,13 @@ extern "C" int alise_kv_dequantize(const alise_kv_desc* d, const uint8_t* slab, 
   KvGeom g;
   int s = geom(d, &g);
   if (s) return s;
-  for (int64_t c = 0; c < g.n_chunks; ++c) {
-    s = dequant_chunk(d, g, g.np_of(c), slab + c * g.rec_bytes, kv + c * g.ppc * g.plane_elems, S(stream));
-    if (s) return s;
-  }
-  return ALISE_OK;
+  cudaStream_t st = S(stream);
+  void* pws = nullptr;
+  CK(cudaMallocAsync(&pws, g.pws_bytes(), st));
+  for (int64_t c = 0; c < g.n_chunks && !s; ++c)
+    s = dequant_chunk(d, g, g.np_of(c), slab + c * g.rec_bytes, kv + c * g.ppc * g.plane_elems, pws, st);
+  CK(cudaFreeAsync(pws, st));
+  return s;
 }
 
 // ------------------------------------------------------------------ swapper
@@ -525,6 +557,8 @@ struct alise_swapper {
   int next_out = 0, next_in = 0;
   void* ws = nullptr;
   int64_t ws_bytes = 0;
+  uint8_t* pws[kSlots] = {};  // per upload slot: the chunk's expanded (scale, zero)
+  int64_t pws_bytes = 0;
   // optional per-chunk kernel timing (bench roofline): event pairs around each
   // quantize / dequantize chunk on the compute stream
   bool timing = false;
@@ -573,6 +607,17 @@ static int sw_ensure(alise_swapper* sw, int64_t slot_bytes, int64_t ws_bytes) {
   return ALISE_OK;
 }
 
+static int sw_ensure_pws(alise_swapper* sw, int64_t bytes) {
+  if (bytes <= sw->pws_bytes) return ALISE_OK;
+  CK(cudaDeviceSynchronize());
+  for (int i = 0; i < kSlots; ++i) {
+    if (sw->pws[i]) CK(cudaFree(sw->pws[i]));
+    CK(cudaMalloc(&sw->pws[i], bytes));
+  }
+  sw->pws_bytes = bytes;
+  return ALISE_OK;
+}
+
 extern "C" int alise_swapper_create(int device, int mode, int64_t ring_bytes, alise_swapper** out) {
   if (mode != ALISE_SWAP_STAGED && mode != ALISE_SWAP_ZEROCOPY) return fail(ALISE_EINVAL, "bad swap mode");
   CK(cudaSetDevice(device));
@@ -600,6 +645,8 @@ extern "C" int alise_swapper_destroy(alise_swapper* sw) {
   CK(cudaDeviceSynchronize());
   sw_release_rings(sw);
   if (sw->ws) cudaFree(sw->ws);
+  for (int i = 0; i < kSlots; ++i)
+    if (sw->pws[i]) cudaFree(sw->pws[i]);
   for (int i = 0; i < kSlots; ++i) {
     cudaEventDestroy(sw->out_ready[i]);
     cudaEventDestroy(sw->out_free[i]);
@@ -722,16 +769,26 @@ extern "C" int alise_kv_upload(alise_swapper* sw, const alise_kv_desc* d, const 
     void* dptr;
     s = host_dev_ptr(host_slab, &dptr);
     if (s) return s;
-    for (int64_t c = 0; c < g.n_chunks; ++c) {
+    void* pws = nullptr;  // stream-ordered scratch: concurrent zero-copy uploads never share it
+    CK(cudaMallocAsync(&pws, g.pws_bytes(), st));
+    for (int64_t c = 0; c < g.n_chunks && !s; ++c) {
+      const uint8_t* rec = reinterpret_cast<const uint8_t*>(dptr) + c * g.rec_bytes;
+      double* scale;
+      float* zero;
+      s = expand_params(d->bits, reinterpret_cast<const uint32_t*>(rec + g.codes_sec(g.np_of(c))),
+                        g.np_of(c) * g.rows_pp, pws, g.ppc * g.rows_pp, &scale, &zero, st);
+      if (s) break;
       TSTART(t_d);
-      s = dequant_chunk(d, g, g.np_of(c), reinterpret_cast<const uint8_t*>(dptr) + c * g.rec_bytes,
-                        kv + c * g.ppc * g.plane_elems, st);
+      s = dequant_chunk_sz(d, g, g.np_of(c), rec, scale, zero, kv + c * g.ppc * g.plane_elems, st);
       TSTOP(t_d);
-      if (s) return s;
     }
+    CK(cudaFreeAsync(pws, st));
+    if (s) return s;
     if (done_event) CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(done_event), st));
     return ALISE_OK;
   }
+  s = sw_ensure_pws(sw, g.pws_bytes());
+  if (s) return s;
   for (int64_t c = 0; c < g.n_chunks; ++c) {
     const int slot = sw->next_in;
     sw->next_in = (slot + 1) % kSlots;
@@ -741,8 +798,13 @@ extern "C" int alise_kv_upload(alise_swapper* sw, const alise_kv_desc* d, const 
                        cudaMemcpyHostToDevice, sw->s_in));
     CK(cudaEventRecord(sw->in_ready[slot], sw->s_in));
     CK(cudaStreamWaitEvent(st, sw->in_ready[slot], 0));
+    double* scale;
+    float* zero;
+    s = expand_params(d->bits, reinterpret_cast<const uint32_t*>(sw->ring_in[slot] + g.codes_sec(np)),
+                      np * g.rows_pp, sw->pws[slot], g.ppc * g.rows_pp, &scale, &zero, st);
+    if (s) return s;
     TSTART(t_d);
-    s = dequant_chunk(d, g, np, sw->ring_in[slot], kv + c * g.ppc * g.plane_elems, st);
+    s = dequant_chunk_sz(d, g, np, sw->ring_in[slot], scale, zero, kv + c * g.ppc * g.plane_elems, st);
     TSTOP(t_d);
     if (s) return s;
     CK(cudaEventRecord(sw->in_free[slot], st));
@@ -762,9 +824,8 @@ struct RangeGeom {
   int64_t R;          // quantization rows per plane in the range
   int64_t run_vals;   // values per plane in the range
   int64_t run_codes;  // code bytes per plane in the range
-  int64_t c_off, s_off, z_off;  // slab offsets of the range inside a plane's sections
-  int64_t ring_s(int64_t np) const { return align256(np * run_codes); }
-  int64_t ring_z(int64_t np) const { return ring_s(np) + align256(np * R * 8); }
+  int64_t c_off, m_off;  // slab offsets of the range inside a plane's codes / (min, max)
+  int64_t ring_m(int64_t np) const { return align256(np * run_codes); }
 };
 
 static int range_geom(const alise_kv_desc* d, const KvGeom& g, int64_t t0, int64_t t1, RangeGeom* r) {
@@ -777,8 +838,7 @@ static int range_geom(const alise_kv_desc* d, const KvGeom& g, int64_t t0, int64
   r->run_vals = (t1 - t0) * d->hidden;
   r->run_codes = r->run_vals / pk;
   r->c_off = t0 * d->hidden / pk;
-  r->s_off = t0 * rpt * 8;
-  r->z_off = t0 * rpt * 4;
+  r->m_off = t0 * rpt * 4;
   (void)g;
   return ALISE_OK;
 }
@@ -806,8 +866,8 @@ extern "C" int alise_kv_offload_range(alise_swapper* sw, const alise_kv_desc* d,
     CK(cudaStreamWaitEvent(st, sw->out_free[slot], 0));
     TSTART(t_q);
     s = launch_tile(d->bits, d->packed != 0, true, kv + c * g.ppc * g.plane_elems + t0 * d->hidden, np * rg.R,
-                    d->group, ring, reinterpret_cast<double*>(ring + rg.ring_s(np)), ring + rg.ring_z(np), flag,
-                    st, rg.R, g.plane_elems);
+                    d->group, ring, nullptr, nullptr, flag, st, rg.R, g.plane_elems,
+                    reinterpret_cast<uint32_t*>(ring + rg.ring_m(np)));
     TSTOP(t_q);
     if (s) return s;
     CK(cudaEventRecord(sw->out_ready[slot], st));
@@ -815,10 +875,8 @@ extern "C" int alise_kv_offload_range(alise_swapper* sw, const alise_kv_desc* d,
     uint8_t* rec = host + c * g.rec_bytes;
     CK(cudaMemcpy2DAsync(rec + rg.c_off, g.code_bytes_pp, ring, rg.run_codes, rg.run_codes, np,
                          cudaMemcpyDeviceToHost, sw->s_out));
-    CK(cudaMemcpy2DAsync(rec + g.codes_sec(np) + rg.s_off, g.rows_pp * 8, ring + rg.ring_s(np), rg.R * 8,
-                         rg.R * 8, np, cudaMemcpyDeviceToHost, sw->s_out));
-    CK(cudaMemcpy2DAsync(rec + g.codes_sec(np) + g.scale_sec(np) + rg.z_off, g.rows_pp * 4,
-                         ring + rg.ring_z(np), rg.R * 4, rg.R * 4, np, cudaMemcpyDeviceToHost, sw->s_out));
+    CK(cudaMemcpy2DAsync(rec + g.codes_sec(np) + rg.m_off, g.rows_pp * 4, ring + rg.ring_m(np), rg.R * 4,
+                         rg.R * 4, np, cudaMemcpyDeviceToHost, sw->s_out));
     CK(cudaEventRecord(sw->out_free[slot], sw->s_out));
   }
   if (done_event) CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(done_event), sw->s_out));
@@ -837,6 +895,8 @@ extern "C" int alise_kv_upload_range(alise_swapper* sw, const alise_kv_desc* d, 
   if (s) return s;
   s = sw_ensure(sw, g.rec_bytes, 0);
   if (s) return s;
+  s = sw_ensure_pws(sw, g.pws_bytes());
+  if (s) return s;
   cudaStream_t st = S(stream);
   const uint8_t* host = reinterpret_cast<const uint8_t*>(host_slab);
   for (int64_t c = 0; c < g.n_chunks; ++c) {
@@ -848,16 +908,17 @@ extern "C" int alise_kv_upload_range(alise_swapper* sw, const alise_kv_desc* d, 
     CK(cudaStreamWaitEvent(sw->s_in, sw->in_free[slot], 0));
     CK(cudaMemcpy2DAsync(ring, rg.run_codes, rec + rg.c_off, g.code_bytes_pp, rg.run_codes, np,
                          cudaMemcpyHostToDevice, sw->s_in));
-    CK(cudaMemcpy2DAsync(ring + rg.ring_s(np), rg.R * 8, rec + g.codes_sec(np) + rg.s_off, g.rows_pp * 8,
-                         rg.R * 8, np, cudaMemcpyHostToDevice, sw->s_in));
-    CK(cudaMemcpy2DAsync(ring + rg.ring_z(np), rg.R * 4, rec + g.codes_sec(np) + g.scale_sec(np) + rg.z_off,
-                         g.rows_pp * 4, rg.R * 4, np, cudaMemcpyHostToDevice, sw->s_in));
+    CK(cudaMemcpy2DAsync(ring + rg.ring_m(np), rg.R * 4, rec + g.codes_sec(np) + rg.m_off, g.rows_pp * 4,
+                         rg.R * 4, np, cudaMemcpyHostToDevice, sw->s_in));
     CK(cudaEventRecord(sw->in_ready[slot], sw->s_in));
     CK(cudaStreamWaitEvent(st, sw->in_ready[slot], 0));
+    double* rs;
+    float* rz;
+    s = expand_params(d->bits, reinterpret_cast<const uint32_t*>(ring + rg.ring_m(np)), np * rg.R, sw->pws[slot],
+                      g.ppc * g.rows_pp, &rs, &rz, st);
+    if (s) return s;
     TSTART(t_d);
     uint16_t* dst = kv + c * g.ppc * g.plane_elems + t0 * d->hidden;
-    const double* rs = reinterpret_cast<const double*>(ring + rg.ring_s(np));
-    const float* rz = reinterpret_cast<const float*>(ring + rg.ring_z(np));
     if (rg.run_vals % (d->packed ? 32 : 16) == 0 && rg.run_codes % 16 == 0) {
       s = dequant_launch<uint16_t>(KIND_ROWS, ring, rs, rz, true, np * rg.run_vals, d->group, d->tokens,
                                    d->hidden, 1, d->bits, d->packed != 0, dst, st, rg.run_vals, g.plane_elems);

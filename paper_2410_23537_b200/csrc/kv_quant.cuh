@@ -15,7 +15,8 @@
 // (k_quant_tile) — cp.async double-buffered warp tiles in shared memory,
 // half2 min/max + warp shuffles, lane-per-row float64 parameter solve, fp32x2
 // codes with a proven exactness window, 64/32-bit coalesced stores.  HBM traffic =
-// 2 B read + b/8 B written per element + 12-16 B per row.
+// 2 B read + b/8 B written per element + 4 B per row (transfer slabs: fp16 min/max) or
+// 12-16 B per row (drop-in API: float64 scale + zero).
 // Other shapes use a three-phase path: partial min/max -> per-row params -> codes.
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -76,7 +77,7 @@ __device__ __forceinline__ int64_t seg_of(int64_t n, const Segs& s) {
 //      constants (qmath.cuh TileParams);
 //   C: reload (L1/L2 hit), codes via one fp32x2 FMA + integer decision per value,
 //      warp-uniform float64 re-run of the rare values near a rounding boundary.
-// HBM traffic: 2 B read + b/8 B written per value + 12-16 B per row.
+// HBM traffic: 2 B read + b/8 B written per value + 4 B (slab) / 12-16 B (API) per row.
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t f2bits(float f) { return __float_as_uint(f); }
 
@@ -108,7 +109,7 @@ template <int BITS, bool PACK, int VPL, bool ZF32, int TP, int WPB, int MINB, in
 __global__ void __launch_bounds__(32 * WPB, MINB)
 k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
                 uint8_t* __restrict__ codes, double* __restrict__ scale, void* __restrict__ zero,
-                int* __restrict__ flag, const Segs seg) {
+                uint32_t* __restrict__ mmx, int* __restrict__ flag, const Segs seg) {
   // TP = passes of 8 rows per warp tile (TILE = 8 * TP rows; 32 keeps every lane busy
   // in the parameter solve).  A lane stages TP x VPL 16-byte vectors per tile.
   constexpr int PASSES = TP;
@@ -235,9 +236,13 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
     double s_row, z_row;
     const TileParams tp = tile_params_f16(fmn, fmx, dq, s_row, z_row);
     if (own) {
-      scale[my_row] = s_row;
-      if (ZF32) reinterpret_cast<float*>(zero)[my_row] = (float)z_row;
-      else reinterpret_cast<double*>(zero)[my_row] = z_row;
+      if (mmx) {  // transfer slabs carry the row's fp16 (min, -max): (scale, zero) follow exactly
+        mmx[my_row] = mine;
+      } else {
+        scale[my_row] = s_row;
+        if (ZF32) reinterpret_cast<float*>(zero)[my_row] = (float)z_row;
+        else reinterpret_cast<double*>(zero)[my_row] = z_row;
+      }
     }
     // ---------------- C: codes from shared memory
     // full tiles (every row live, every lane's vectors in range) take an unpredicated
@@ -485,11 +490,11 @@ k_dequant_wide(const uint4* __restrict__ codes, const double* __restrict__ scale
 template <int BITS, bool PACK>
 __global__ void __launch_bounds__(256, 3)
 k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int64_t rows_per_plane,
-             uint8_t* __restrict__ codes, double* __restrict__ scale, float* __restrict__ zero,
-             int* __restrict__ flag) {
+             uint8_t* __restrict__ codes, uint32_t* __restrict__ mm, int* __restrict__ flag) {
   constexpr float QMAXF = (float)((1 << BITS) - 1);
   __shared__ __half2 s_mm[16][128];      // (min, -max) per token lane and column
-  __shared__ float s_inv[128], s_zc[128], s_thr[128];
+  __shared__ float s_inv[128], s_zc[128], s_thr[128], s_zd[128];
+  __shared__ double s_sd[128];
   const int tid = threadIdx.x;
   const int cv = tid & 15, tl = tid >> 4;
   const int64_t plane = blockIdx.y;
@@ -542,12 +547,13 @@ k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int
     double sd, zd;
     const TileParams tp = tile_params_f16(fmn, fmx, qdiv_make((double)((1 << BITS) - 1)), sd, zd);
     const int64_t r = plane * rows_per_plane + (col0 / cpr) + tid;
-    scale[r] = sd;
-    zero[r] = (float)zd;
+    mm[r] = *reinterpret_cast<const uint32_t*>(&m);  // the group's fp16 (min, -max)
     for (int u = 0; u < cpr; ++u) {
       s_inv[tid * cpr + u] = tp.inv_s;
       s_zc[tid * cpr + u] = tp.zc;
       s_thr[tid * cpr + u] = tp.thr;
+      s_sd[tid * cpr + u] = sd;
+      s_zd[tid * cpr + u] = (float)zd;
     }
   }
   __syncthreads();
@@ -581,8 +587,7 @@ k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int
         const float f = __half2float(reinterpret_cast<const __half*>(&d)[j]);
         const float y = fmaf(f, inv[j], zc[j]);
         if (!(fabsf(fmaf(f, inv[j], -__fadd_rn(y, -zc[j]))) < thr[j])) {
-          const int64_t r = plane * rows_per_plane + (col0 + cv * 8 + j) / cpr;
-          const double sd = scale[r], zd = (double)zero[r];
+          const double sd = s_sd[cv * 8 + j], zd = (double)s_zd[cv * 8 + j];
           float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, sd), zd));
           c[j] = (uint32_t)fminf(fmaxf(rr, 0.f), QMAXF);
         }
@@ -605,6 +610,25 @@ k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int
     for (int u = 0; u < 4; ++u) code_vec(d[u], t + 16 * u);
   }
   for (; t < T; t += 16) code_vec(__ldg(reinterpret_cast<const uint4*>(base + t * Hd)), t);
+}
+
+// Transfer-slab parameters -> (scale, zero): a group's fp16 (min, -max) determines its
+// float64 scale and zero through exactly the quantizer's solve (kvmanager.py:130-146),
+// so the slab carries 4 bytes per group instead of 12.  One thread per group.
+template <int BITS>
+__global__ void __launch_bounds__(256)
+k_expand_params(const uint32_t* __restrict__ mm, int64_t groups, double* __restrict__ scale,
+                float* __restrict__ zero) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= groups) return;
+  const uint32_t w = mm[r];
+  const __half2 h = *reinterpret_cast<const __half2*>(&w);
+  float fmn = __low2float(h), fmx = -__high2float(h);
+  if (!(isfinite(fmn) && isfinite(fmx))) { fmn = 0.f; fmx = 0.f; }  // flagged at quantize time
+  double s, z;
+  tile_params_f16(fmn, fmx, qdiv_make((double)((1 << BITS) - 1)), s, z);
+  scale[r] = s;
+  zero[r] = (float)z;
 }
 
 // Column dequantize for CHANNEL / HEAD kinds: each thread owns 8 columns of a strip
@@ -770,7 +794,7 @@ __global__ void k_params(int kind, int64_t rows, int nch, const double* __restri
                          const double* __restrict__ pmx_rows, const float* __restrict__ pmn_cols,
                          const float* __restrict__ pmx_cols, int64_t Hd, int64_t D, int bits,
                          bool wide, double* __restrict__ scale, void* __restrict__ zero,
-                         float4* __restrict__ fastp) {
+                         float4* __restrict__ fastp, uint32_t* __restrict__ mm) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
@@ -792,6 +816,10 @@ __global__ void k_params(int kind, int64_t rows, int nch, const double* __restri
         mx = fmax(mx, (double)m1[j]);
       }
     }
+  }
+  if (mm) {  // fp16 inputs: mn / mx are fp16 values, exact as halves
+    const __half2 h = __halves2half2(__double2half(mn), __double2half(-mx));
+    mm[r] = *reinterpret_cast<const uint32_t*>(&h);
   }
   const QParams q = make_params(mn, mx, bits, wide, qdiv_make((double)((1 << bits) - 1)));
   scale[r] = q.s;

@@ -726,7 +726,7 @@ class DeviceMemoryState(MemoryState):
     def _range_bytes(self, layout: KVLayout, t0: int, t1: int) -> int:
         pk = 2 if layout.packed else 1
         rpt = layout.hidden // layout.group if layout.kind == "rows" else 0
-        return 2 * layout.layers * (t1 - t0) * (layout.hidden // pk + rpt * 12)
+        return 2 * layout.layers * (t1 - t0) * (layout.hidden // pk + rpt * 4)  # codes + fp16 (min, max)
 
     def _alloc_slab(self, nbytes: int) -> int:
         while True:

@@ -26,7 +26,9 @@ def _layout(km, kv, kind, group, bits, packed=False, ppc=0):
 
 
 def _slab_to_rows(km, layout, slab, shape, kind, group, head_dim):
-    """Decode a host/device slab into (codes in reference row order, scale, zero)."""
+    """Decode a host/device slab into (codes in reference row order, scale, zero).  A chunk
+    record is [codes, native order][fp16 (min, -max) per group]; (scale, zero) follow from
+    (min, max) by the reference solve (oracle params_from_minmax)."""
     import math
     g = layout.geometry()
     L, two, T, Hd = shape
@@ -35,22 +37,22 @@ def _slab_to_rows(km, layout, slab, shape, kind, group, head_dim):
     rows_pp = g["rows"] // planes
     per_plane_codes = T * Hd // (2 if layout.packed else 1)
     a256 = lambda x: (x + 255) // 256 * 256
-    codes, scales, zeros = [], [], []
+    codes, mms = [], []
     for c in range(g["n_chunks"]):
         np_ = min(ppc, planes - c * ppc)
         base = c * g["chunk_bytes"]
         cs = a256(np_ * per_plane_codes)
-        ss = a256(np_ * rows_pp * 8)
         codes.append(slab[base: base + np_ * per_plane_codes])
-        scales.append(slab[base + cs: base + cs + np_ * rows_pp * 8].view(np.float64))
-        zeros.append(slab[base + cs + ss: base + cs + ss + np_ * rows_pp * 4].view(np.float32))
+        mms.append(slab[base + cs: base + cs + np_ * rows_pp * 4].view(np.float16).reshape(-1, 2))
     native = np.concatenate(codes)
     if layout.packed:
         lo, hi = native & 15, native >> 4
         native = np.stack([lo, hi], axis=1).reshape(-1)
     native = native.reshape(shape)
     rows = ko.view_rows(native, kind, group=group, head_dim=head_dim)
-    return rows, np.concatenate(scales)[:, None], np.concatenate(zeros).astype(np.float64)[:, None]
+    mm = np.concatenate(mms).astype(np.float64)
+    scale, zero = ko.params_from_minmax(mm[:, 0], -mm[:, 1], layout.bits)
+    return rows, scale[:, None], zero.astype(np.float32).astype(np.float64)[:, None]
 
 
 # ----------------------------------------------------------------- drop-in API
