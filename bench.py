@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--packed", action="store_true")
     ap.add_argument("--mode", default="staged", choices=["staged", "zerocopy"])
     ap.add_argument("--host-slabs", type=int, default=4)
+    ap.add_argument("--lag", type=int, default=1, help="upload job j-lag while offloading job j")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -286,9 +287,11 @@ def _kv_bench(args, world, rank, local, layouts=None, e2e=True):
     up_pending = [False] * len(kvs)
     stream = torch.cuda.current_stream()
 
+    lag = max(1, min(getattr(args, "lag", 1), H - 1))  # upload job j - lag while offloading job j
+
     def step():
         n = len(kvs)
-        for j in range(n + 1):
+        for j in range(n + lag):
             if j < n:
                 s = j % H
                 if used_up[s]:
@@ -296,12 +299,13 @@ def _kv_bench(args, world, rank, local, layouts=None, e2e=True):
                 if up_pending[j]:               # previous step's upload wrote kvs[j]
                     km._lib.call("alise_stream_wait", km._lib.stream_ptr(), ev_job[j].h)
                 eng.offload(my_layouts[j], kvs[j], slabs[s], flag=flag, event=ev_off[s].h)
-            if j > 0:
-                s = (j - 1) % H
+            u = j - lag
+            if 0 <= u < n:
+                s = u % H
                 eng.depend(ev_off[s].h)         # upload reads what the offload wrote
-                eng.upload(my_layouts[j - 1], slabs[s], kvs[j - 1], event=ev_up[s].h)
-                km._lib.call("alise_event_record", ev_job[j - 1].h, km._lib.stream_ptr(eng.up_stream))
-                up_pending[j - 1] = True
+                eng.upload(my_layouts[u], slabs[s], kvs[u], event=ev_up[s].h)
+                km._lib.call("alise_event_record", ev_job[u].h, km._lib.stream_ptr(eng.up_stream))
+                up_pending[u] = True
                 used_up[s] = True
         # the step ends when both directions are done
         if n:

@@ -1,0 +1,22 @@
+"""C3 swap pipeline (256 ShareGPT-mix jobs, INT4 g=64 packed) with different
+offload/upload lags: fp16 GB/s and link utilisation."""
+import json
+import sys
+
+sys.path.insert(0, ".")
+sys.argv = ["bench.py"]
+import bench  # noqa: E402
+from paper_2410_23537_b200 import kvmanager as km  # noqa: E402
+from paper_2410_23537_b200 import synthetic  # noqa: E402
+
+args = bench.parse()
+args.steps, args.warmup = 2, 1
+links = bench.link_peaks(0)
+ctx = synthetic.sharegpt_job_tokens(256, seed=0)
+lays = [km.KVLayout(args.layers, int(t), args.hidden, args.head_dim, kind="rows", group=64, bits=4, packed=True)
+        for t in ctx]
+for lag in (1, 2, 3):
+    args.lag = lag
+    r = bench.kv_bench(args, 1, 0, 0, layouts=lays, e2e=False)
+    print(json.dumps({"lag": lag, "GBs": round(r["value"], 1), "link": round(r["link_GBs_total"], 1),
+                      "link_frac": round(r["link_GBs_total"] / links["duplex_total_GBs"], 3)}), flush=True)
