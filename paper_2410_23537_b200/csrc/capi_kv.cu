@@ -475,9 +475,21 @@ static int expand_params(int bits, const uint32_t* mm, int64_t groups, void* pws
   *scale = reinterpret_cast<double*>(w);
   *zero = reinterpret_cast<float*>(w + align256(cap_groups * 8));
   if (groups <= 0) return ALISE_OK;
-  const unsigned grid = (unsigned)((groups + 255) / 256);
-  if (bits == 8) k_expand_params<8><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero);
-  else k_expand_params<4><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero);
+  static int ng = -1;  // groups per thread (interleaved float64 chains); ALISE_EXPAND_NG (tuning)
+  if (ng < 0) {
+    const char* e = getenv("ALISE_EXPAND_NG");
+    ng = e ? atoi(e) : 1;
+  }
+#define EXP(NG)                                                                                  \
+  do {                                                                                           \
+    const unsigned grid = (unsigned)((groups + 256 * NG - 1) / (256 * NG));                      \
+    if (bits == 8) k_expand_params<8, NG><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero);     \
+    else k_expand_params<4, NG><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero);               \
+  } while (0)
+  if (ng == 2) EXP(2);
+  else if (ng == 4) EXP(4);
+  else EXP(1);
+#undef EXP
   CKL();
   return ALISE_OK;
 }

@@ -614,21 +614,52 @@ k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int
 
 // Transfer-slab parameters -> (scale, zero): a group's fp16 (min, -max) determines its
 // float64 scale and zero through exactly the quantizer's solve (kvmanager.py:130-146),
-// so the slab carries 4 bytes per group instead of 12.  One thread per group.
-template <int BITS>
+// so the slab carries 4 bytes per group instead of 12.  The solve is a chain of
+// dependent float64 operations; each thread runs NG groups' chains interleaved (the
+// snap loop iterates until every one of its groups is at a fixed point, a group that
+// converged keeps its value), which hides the float64 latency.
+template <int BITS, int NG>
 __global__ void __launch_bounds__(256)
 k_expand_params(const uint32_t* __restrict__ mm, int64_t groups, double* __restrict__ scale,
                 float* __restrict__ zero) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= groups) return;
-  const uint32_t w = mm[r];
-  const __half2 h = *reinterpret_cast<const __half2*>(&w);
-  float fmn = __low2float(h), fmx = -__high2float(h);
-  if (!(isfinite(fmn) && isfinite(fmx))) { fmn = 0.f; fmx = 0.f; }  // flagged at quantize time
-  double s, z;
-  tile_params_f16(fmn, fmx, qdiv_make((double)((1 << BITS) - 1)), s, z);
-  scale[r] = s;
-  zero[r] = (float)z;
+  const QDiv dq = qdiv_make((double)((1 << BITS) - 1));
+  const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * NG;
+  if (r0 >= groups) return;
+  double mn[NG], mx[NG], s[NG], z[NG], hz[NG], lz[NG];
+  bool live[NG];
+#pragma unroll
+  for (int u = 0; u < NG; ++u) {
+    const int64_t r = r0 + u;
+    uint32_t w = r < groups ? mm[r] : 0u;
+    const __half2 h = *reinterpret_cast<const __half2*>(&w);
+    float fmn = __low2float(h), fmx = -__high2float(h);
+    if (!(isfinite(fmn) && isfinite(fmx))) { fmn = 0.f; fmx = 0.f; }  // flagged at quantize time
+    mn[u] = (double)fmn;
+    mx[u] = (double)fmx;
+    live[u] = mx[u] != mn[u];
+    s[u] = live[u] ? qdiv(__dsub_rn(mx[u], mn[u]), dq) : 1.0;       // constant group: (1, -min)
+    z[u] = live[u] ? rint(__ddiv_rn(-mn[u], s[u])) : -mn[u];
+    hz[u] = __dsub_rn(dq.b, z[u]);
+    lz[u] = __dsub_rn(0.0, z[u]);
+  }
+#pragma unroll 1
+  for (int it = 0; it < 32; ++it) {
+    bool any = false;
+#pragma unroll
+    for (int u = 0; u < NG; ++u) {
+      const double nxt = qdiv(__dsub_rn(__dmul_rn(s[u], hz[u]), __dmul_rn(s[u], lz[u])), dq);
+      if (live[u] && nxt != s[u]) s[u] = nxt; else live[u] = false;
+      any |= live[u];
+    }
+    if (!any) break;
+  }
+#pragma unroll
+  for (int u = 0; u < NG; ++u) {
+    if (r0 + u < groups) {
+      scale[r0 + u] = s[u];
+      zero[r0 + u] = (float)z[u];
+    }
+  }
 }
 
 // Column dequantize for CHANNEL / HEAD kinds: each thread owns 8 columns of a strip
