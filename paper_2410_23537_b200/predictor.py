@@ -438,6 +438,48 @@ def train_fallback(corpus, config: PredictorConfig, seed: int = 0, embedder=None
 
 
 # ----------------------------------------------------------------- length predictor
+class _GraphedRequest:
+    """One-query predict path captured as a CUDA graph (pinned host in/out buffers)."""
+
+    def __init__(self, predictor):
+        import torch
+        self.p = predictor
+        d = predictor.config.dimension
+        self.h_in = torch.zeros(1, d, dtype=torch.float32).pin_memory()
+        self.h_out = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.h_ret = torch.zeros(1, dtype=torch.uint8).pin_memory()
+        self.d_in = torch.zeros(1, d, dtype=torch.float32, device="cuda")
+        self.key = None
+        self.graph = None
+
+    def _key(self):
+        w = self.p.regressor.device_weights()
+        return (self.p.store.size, tuple(int(t.data_ptr()) for t in w), float(self.p.regressor.b2))
+
+    def _capture(self):
+        import torch
+        # warm-up outside the capture: allocates the store's scratch and sets kernel attributes
+        self.p.predict_batch(self.d_in)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.d_in.copy_(self.h_in, non_blocking=True)
+            out, ret = self.p.predict_batch(self.d_in)
+            self.h_out.copy_(out, non_blocking=True)
+            self.h_ret.copy_(ret, non_blocking=True)
+        self.graph = g
+        self.key = self._key()
+
+    def __call__(self, vector):
+        import torch
+        if self.graph is None or self._key() != self.key:
+            self._capture()
+        self.h_in.numpy()[0] = np.asarray(vector, dtype=np.float64)
+        self.graph.replay()
+        torch.cuda.current_stream().synchronize()
+        return int(self.h_out[0]), int(self.h_ret[0])
+
+
 class LengthPredictor:
     """Retrieval-first length predictor with regressor fallback (predictor.py:286-352)."""
 
@@ -492,8 +534,19 @@ class LengthPredictor:
                   math.log(cfg.max_len) + 1.0, _lib.ptr(out), _lib.ptr(ret), _lib.stream_ptr(stream))
         return out, ret
 
+    def enable_graphs(self, on: bool = True):
+        """Serve predict_vector (one request) by replaying a CUDA graph of the whole
+        per-request path: query upload, prep, tcgen05 scan, rescoring, finish and the
+        result download become one graph launch (re-captured when the DB size or the
+        fallback weights change)."""
+        self._graph = _GraphedRequest(self) if on else None
+
     def predict_vector(self, vector) -> tuple:
         """Predict from an already-embedded prompt; returns (length, provenance)."""
+        g = getattr(self, "_graph", None)
+        if g is not None and self.store.size > 0:
+            length, ret = g(vector)
+            return length, (RETRIEVED if ret else FALLBACK)
         out, ret = self.predict_batch(np.asarray(vector, dtype=np.float64)[None, :])
         return int(out[0].item()), (RETRIEVED if int(ret[0].item()) else FALLBACK)
 

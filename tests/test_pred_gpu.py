@@ -295,3 +295,25 @@ def test_shared_thresholds_with_ties_across_tile_groups(pr, B):
     Q[B // 2:] = g.standard_normal((B - B // 2, d)).astype(np.float32)
     Q /= np.linalg.norm(Q, axis=1, keepdims=True)
     check_batch(pr, db, lens, Q.astype(np.float32), 8)
+
+
+def test_graphed_single_request_matches_eager(pr):
+    """predict_vector through the captured CUDA graph == the eager path, including after
+    the DB grows (re-capture) and for fallback (MLP) queries."""
+    from paper_2410_23537_b200 import synthetic
+    db, lens = synthetic.predictor_db(30_000, 256, seed=3, dup_groups=30)
+    reg = pr.FallbackRegressor(256, 32, seed=0)
+    reg.b2 = 5.0
+    store = pr.VectorStore(256, 40_000)
+    store.add_batch(db[:20_000], lens[:20_000])
+    p = pr.LengthPredictor(pr.PredictorConfig(dimension=256, db_capacity=40_000), regressor=reg, store=store)
+    Q = synthetic.predictor_queries(db, 24, seed=4).astype(np.float64)
+    eager = [p.predict_vector(q) for q in Q]
+    p.enable_graphs()
+    assert [p.predict_vector(q) for q in Q] == eager
+    store.add_batch(db[20_000:], lens[20_000:])    # size change -> re-capture
+    p.enable_graphs(False)
+    eager2 = [p.predict_vector(q) for q in Q]
+    p.enable_graphs()
+    assert [p.predict_vector(q) for q in Q] == eager2
+    assert any(r == pr.FALLBACK for _, r in eager2) and any(r == pr.RETRIEVED for _, r in eager2)

@@ -31,3 +31,14 @@ for i in range(64):
 ts.sort()
 print(json.dumps({"api": "LengthPredictor.predict_vector", "N": N, "p50_ms": ts[32] * 1e3, "p90_ms": ts[57] * 1e3,
                   "min_ms": ts[0] * 1e3}))
+p.enable_graphs()
+ref = [p.predict_vector(Q[i]) for i in range(64)]
+ts = []
+for i in range(64):
+    t0 = time.perf_counter()
+    r = p.predict_vector(Q[i])
+    ts.append(time.perf_counter() - t0)
+    assert r == ref[i]
+ts.sort()
+print(json.dumps({"api": "LengthPredictor.predict_vector (CUDA graph)", "N": N, "p50_ms": ts[32] * 1e3,
+                  "p90_ms": ts[57] * 1e3, "min_ms": ts[0] * 1e3}))
