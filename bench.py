@@ -166,6 +166,16 @@ def load_peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+def load_sustained_bf16():
+    """Sustained (back-to-back, power-capped clocks) bf16 peak, if the driver measured it."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            v = json.load(fh).get("bf16_tflops_sustained")
+        return float(v) if v else None
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------------- CPU baseline (oracle port)
 def _cpu_worker(payload):
     import numpy as np
@@ -744,7 +754,12 @@ def main():
                              "flops_per_launch": pred["scan_flops_per_launch"],
                              "avg_launch_ms": pred["scan_ms_avg"],
                              "traffic": traffic.get("k_scan", {}).get("dram_bytes_per_launch"),
-                             "traffic_source": traffic.get("k_scan", {}).get("source")},
+                             "traffic_source": traffic.get("k_scan", {}).get("source"),
+                             # the scan runs back to back at power-capped clocks (ncu: ~1.45-1.5 GHz
+                             # SM clock under it); frac above is against the burst peak
+                             "peak_sustained": load_sustained_bf16(),
+                             "frac_sustained": (round(ach / load_sustained_bf16(), 4)
+                                                if ach and load_sustained_bf16() else None)},
                 "e2e": pred["e2e"], "inexact_candidates": pred["inexact"],
                 "retrieved_frac": round(pred["retrieved_frac"], 4),
                 "gpu_launches_per_step": 5 + (2 if world > 1 else 0),
