@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--bits", type=int, default=8)
     ap.add_argument("--packed", action="store_true")
     ap.add_argument("--mode", default="staged", choices=["staged", "zerocopy"])
-    ap.add_argument("--host-slabs", type=int, default=4)
+    ap.add_argument("--host-slabs", type=int, default=8)
     ap.add_argument("--lag", type=int, default=1, help="upload job j-lag while offloading job j")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
