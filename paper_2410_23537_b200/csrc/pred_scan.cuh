@@ -747,16 +747,6 @@ __device__ double super_round(uint64_t (&acc)[SUPER_L]) {
   return neg ? -v : v;
 }
 
-// Single thread (reference implementation of the superaccumulator path).
-__device__ __noinline__ double exact_dot_super(const float* __restrict__ a, const float* __restrict__ b,
-                                               int64_t dim) {
-  uint64_t acc[SUPER_L];
-#pragma unroll
-  for (int i = 0; i < SUPER_L; ++i) acc[i] = 0;
-  for (int64_t d = 0; d < dim; ++d) super_add(acc, __ldg(a + d), __ldg(b + d));
-  return super_round(acc);
-}
-
 // Warp-cooperative: each lane accumulates dim/32 products, the 640-bit partial sums are
 // added across lanes (mod 2^640, carries propagated limb by limb), every lane rounds.
 // Called by all 32 lanes (warp-uniform branch).
