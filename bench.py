@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--mode", default="staged", choices=["staged", "zerocopy"])
     ap.add_argument("--host-slabs", type=int, default=8)
     ap.add_argument("--lag", type=int, default=1, help="upload job j-lag while offloading job j")
+    ap.add_argument("--planes-per-chunk", type=int, default=0, help="transfer chunk (0: 128 MiB of codes)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -275,7 +276,8 @@ def _kv_bench(args, world, rank, local, layouts=None, e2e=True):
     torch.cuda.set_device(dev)
     if layouts is None:
         layouts = [km.KVLayout(args.layers, args.tokens, args.hidden, args.head_dim, kind=args.kind,
-                               group=args.group, bits=args.bits, packed=args.packed)] * args.jobs
+                               group=args.group, bits=args.bits, packed=args.packed,
+                               planes_per_chunk=args.planes_per_chunk)] * args.jobs
     sizes = [lay.elements * 2 for lay in layouts]
     mine = synthetic.lpt_assign(sizes, world)[rank]
     my_layouts = [layouts[j] for j in mine]
