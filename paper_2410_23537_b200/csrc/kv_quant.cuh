@@ -248,7 +248,7 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
     // full tiles (every row live, every lane's vectors in range) take an unpredicated
     // path with compile-time offsets; the code is the low byte / nibble of
     // y = fma(x, inv_s, z + 1.5*2^23), e = fma(x, inv_s, K - y) proves it (qmath.cuh)
-    uint32_t pmask = 0;  // flagged vectors of this lane: bit p * VPL + i
+    uint32_t pmask = 0;  // flagged passes of this lane: bit p
 #pragma unroll
     for (int p = 0; p < PASSES; ++p) {
       const int rl = p * 8 + sub;
@@ -261,14 +261,13 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
       const float2 nzc2 = make_float2(-zc, -zc);
       const uint8_t* srow = b + rl * ROWB + q4 * 16;
       uint8_t* crow = codes + ((uint64_t)(r * (full ? (int64_t)RL : (int64_t)row_len) + q4 * 8) >> (PACK ? 1 : 0));
-      uint32_t umask = 0;  // vectors holding a value near a rounding boundary
+      float dmax = 0.f;  // largest |e| of this lane's values in the pass
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
         if (!full && !(live_row && q4 + 4 * i < nvec)) continue;
         const uint4 d = *reinterpret_cast<const uint4*>(srow + i * 64);
         const __half2* h = reinterpret_cast<const __half2*>(&d);
         uint32_t c[8];
-        float dmax = 0.f;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float2 f = __half22float2(h[k]);
@@ -279,7 +278,6 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
           c[2 * k] = f2bits(y.x);
           c[2 * k + 1] = f2bits(y.y);
         }
-        umask |= (dmax >= thr ? 1u : 0u) << i;
         if (PACK) {
           __stcs(reinterpret_cast<uint32_t*>(crow + i * 16), pack_int4x8(c));
         } else {
@@ -287,11 +285,12 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
                  make_uint2(gather4(c[0], c[1], c[2], c[3]), gather4(c[4], c[5], c[6], c[7])));
         }
       }
-      pmask |= umask << (p * VPL);
+      pmask |= (dmax >= thr ? 1u : 0u) << p;  // a value of the pass is near a rounding boundary
     }
-    // ---------------- D: rare fix-up of flagged vectors (a value near a rounding boundary),
-    // all lanes together: lane j recomputes the byte holding value j (INT8) or values
-    // 2j, 2j+1 (packed INT4) with the reference float64 ops where the check fails
+    // ---------------- D: rare fix-up of flagged (lane, pass) pairs (a value near a
+    // rounding boundary), all lanes together: the pair's 8*VPL values are spread one code
+    // byte per lane (INT8: one value; packed INT4: values 2j, 2j+1); each lane re-checks
+    // its value(s) and runs the reference float64 ops where the check fails
     __syncwarp();  // the vector stores above are visible to the whole warp
     uint32_t pending = __ballot_sync(0xffffffffu, pmask != 0);
 #pragma unroll 1
@@ -301,20 +300,25 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
       uint32_t m = __shfl_sync(0xffffffffu, pmask, src);
 #pragma unroll 1
       while (m) {
-        const int bit = __ffs(m) - 1;
+        const int p = __ffs(m) - 1;
         m &= m - 1;
-        const int rl = (bit / VPL) * 8 + (src >> 2);
-        const int vv = (src & 3) + 4 * (bit % VPL);
+        const int rl = p * 8 + (src >> 2);
         const float inv_s = __shfl_sync(0xffffffffu, tp.inv_s, rl);
         const float zc = __shfl_sync(0xffffffffu, tp.zc, rl);
         const float thr = __shfl_sync(0xffffffffu, tp.thr, rl);
         const double sd = __shfl_sync(0xffffffffu, s_row, rl);
         const double zd = __shfl_sync(0xffffffffu, z_row, rl);
-        constexpr int PER = PACK ? 2 : 1;  // values per code byte
-        if (lane < 8 / PER) {
-          const int64_t r = row0 + rl;
-          const uint16_t* hv = reinterpret_cast<const uint16_t*>(b + rl * ROWB + vv * 16) + lane * PER;
+        constexpr int PER = PACK ? 2 : 1;        // values per code byte
+        constexpr int NB = 8 * VPL / PER;        // code bytes of the pair
+        const int64_t r = row0 + rl;
+#pragma unroll 1
+        for (int bi = lane; bi < NB; bi += 32) {
+          const int i = (bi * PER) >> 3, j0 = (bi * PER) & 7;
+          const int vv = (src & 3) + 4 * i;
+          if (r >= rows || vv >= nvec) continue;
+          const uint16_t* hv = reinterpret_cast<const uint16_t*>(b + rl * ROWB + vv * 16) + j0;
           uint32_t byte = 0;
+          bool fix = false;
 #pragma unroll
           for (int u = 0; u < PER; ++u) {
             const float xf = h2f(hv[u]);
@@ -323,10 +327,11 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
             if (!(fabsf(fmaf(xf, inv_s, -__fadd_rn(y, -zc))) < thr)) {
               const float rc = (float)rint(__dadd_rn(__ddiv_rn((double)xf, sd), zd));
               cc = (uint32_t)fminf(fmaxf(rc, 0.f), QMAXF);
+              fix = true;
             }
             byte |= cc << (4 * u);
           }
-          codes[(r * row_len + vv * 8) / PER + lane] = (uint8_t)byte;
+          if (fix) codes[(r * row_len + vv * 8 + j0) / PER] = (uint8_t)byte;
         }
       }
     }
