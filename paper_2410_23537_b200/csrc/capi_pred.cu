@@ -89,7 +89,7 @@ struct alise_db {
   int32_t* cand_n = nullptr;
   float* topc = nullptr;
   int32_t* need = nullptr;
-  uint32_t* gkth = nullptr;  // shared running k-th per query (scan threshold sharing)
+  uint32_t* gkth = nullptr;  // shared lower bound of the k-th per query, then [bp][KMAX] rank slots
   CUtensorMap tmQ;
   // optional kernel timing (bench roofline): event pairs around each scan launch
   bool timing = false;
@@ -223,7 +223,7 @@ static int ensure_scratch(alise_db* db, int64_t Bp, int splits, cudaStream_t st)
   CK(cudaMalloc(&db->cand_n, sizeof(int32_t) * sp * bp));
   CK(cudaMalloc(&db->topc, sizeof(float) * sp * bp * KMAX));
   CK(cudaMalloc(&db->need, sizeof(int32_t) * bp));
-  CK(cudaMalloc(&db->gkth, sizeof(uint32_t) * bp));
+  CK(cudaMalloc(&db->gkth, sizeof(uint32_t) * bp * (1 + KMAX)));
   db->bp_cap = bp;
   db->splits_cap = sp;
   return make_map(&db->tmQ, db->q16, bp, db->dp, BM);
@@ -285,7 +285,16 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   a.cand_n = db->cand_n;
   a.topc = db->topc;
   a.gkth = db->gkth;
-  CK(cudaMemsetAsync(db->gkth, 0, sizeof(uint32_t) * Bp, st));
+  static int warm = -1;
+  if (warm < 0) {
+    const char* e = getenv("ALISE_SCAN_WARM");
+    warm = e ? atoi(e) : 1;
+  }
+  a.warm = warm;
+  // [Bp] shared k-th, then [Bp][KMAX] rank slots (16-byte aligned: Bp % 128 == 0): one memset
+  a.gslot = db->gkth + Bp;
+  a.slot_m = (k + base_g - 1) / base_g;
+  CK(cudaMemsetAsync(db->gkth, 0, sizeof(uint32_t) * Bp * (1 + KMAX), st));
   static bool attr_set[4] = {false, false, false, false};
   const int kt = (k <= 8 ? 0 : 1) + (two_sm ? 2 : 0);
   if (!attr_set[kt]) {
@@ -317,6 +326,24 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
     CK(cudaEventRecord(e1, st));
     db->ev.push_back(e0);
     db->ev.push_back(e1);
+  }
+  static int stats = -1;
+  if (stats < 0) {
+    const char* e = getenv("ALISE_SCAN_STATS");
+    stats = e ? atoi(e) : 0;
+  }
+  if (stats) {  // diagnostics: candidate counts after the scan
+    CK(cudaStreamSynchronize(st));
+    std::vector<int32_t> cn((size_t)splits * Bp);
+    CK(cudaMemcpy(cn.data(), db->cand_n, cn.size() * 4, cudaMemcpyDeviceToHost));
+    double tot = 0;
+    int ovf = 0;
+    for (int sp = 0; sp < splits; ++sp)
+      for (int64_t q = 0; q < B; ++q) {
+        const int c = cn[(size_t)sp * Bp + q];
+        if (c < 0) ++ovf; else tot += c;
+      }
+    fprintf(stderr, "[scan stats] B=%lld splits=%d cand/query=%.1f ovf=%d\n", (long long)B, splits, tot / B, ovf);
   }
   CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
   k_rescore<<<(unsigned)B, 256, 0, st>>>(qblk, base_g, extra_g, (int)Bp, B, k, db->size, db->dim, queries, db->v32, db->lens,

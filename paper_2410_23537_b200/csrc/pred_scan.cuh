@@ -34,7 +34,7 @@ constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int KMAX = 16;       // largest supported k
 constexpr int CAP = 128;       // candidate slots per (split, query)
-constexpr int SCAN_SMEM = STAGES * STAGE_BYTES + 1024 + 256 + BM * 33 * 4;
+constexpr int SCAN_SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int MAXC = 512;      // candidates rescored per query
 
 // ------------------------------------------------------------------ DB maintenance
@@ -114,7 +114,17 @@ struct ScanArgs {
   int32_t* cand_n;   // [n_splits][Bp]   (-1 = overflow)
   float* topc;       // [n_splits][Bp][KMAX]
   uint32_t* gkth;    // [Bp] shared running k-th per query (ord_key; 0 = none yet)
+  int warm;          // warm-start bound from each group's first tile (QueryScan)
+  uint32_t* gslot;   // [Bp][KMAX] rank slots per query (ord_key; 0 = empty)
+  int slot_m;        // ranks each group publishes into the slots
 };
+
+__device__ __forceinline__ uint4 ld_relaxed_v4(const uint32_t* p) {
+  uint4 r;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
 
 // Order-preserving float <-> uint32 (atomicMax on the key = max on the float).
 __device__ __forceinline__ uint32_t ord_key(float f) {
@@ -125,46 +135,37 @@ __device__ __forceinline__ float ord_val(uint32_t k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
-// Threshold sharing across the tile groups of a query: every group's running k-th
-// coarse score is a lower bound of the final k-th over all rows, so the largest
-// published one minus 2*delta is a valid candidate threshold for every group
-// (the candidate set stays a superset of the exact top-k).  Called once per tile.
-__device__ __forceinline__ void share_threshold(uint32_t* __restrict__ gk, float kth, float td, float& thr,
-                                                uint32_t& pub, float& kfloor) {
-  if (kth > -__int_as_float(0x7f800000)) {
-    const uint32_t key = ord_key(kth);
-    if (key > pub) {
-      atomicMax(gk, key);
-      pub = key;
-    }
-  }
-  const float g = ord_val(*reinterpret_cast<volatile uint32_t*>(gk));
-  if (g - td > thr) thr = g - td;
-  // a group's top list only has to hold values above the shared k-th: the group that
-  // published it holds k values >= it, so the union of the lists keeps its k-th
-  if (g > kfloor) kfloor = g;
+// Running top-k of one query in registers, right-aligned: slots [0, KT-k) hold +inf
+// (never displaced), the k live values are top[KT-k..KT-1] sorted descending, so the
+// k-th is always top[KT-1] (a static register: a runtime index would move the list to
+// local memory).  p[i] = s > top[i] is monotone in i, so every slot is computed in
+// parallel from the old list (depth 3 instead of a KT-long chain).
+template <int KT>
+__device__ __forceinline__ void topk_init(float (&top)[KT], int k) {
+#pragma unroll
+  for (int x = 0; x < KT; ++x) top[x] = x < KT - k ? __int_as_float(0x7f800000) : -__int_as_float(0x7f800000);
 }
 
 template <int KT>
-__device__ __forceinline__ float topk_insert(float (&top)[KT], float s, int k) {
-  // top[] sorted descending over its first k slots; returns the new k-th value
+__device__ __forceinline__ float topk_insert(float (&top)[KT], float s) {
+  bool p[KT];
 #pragma unroll
-  for (int i = 0; i < KT; ++i) {
-    if (i < k && s > top[i]) {
-      const float t = top[i];
-      top[i] = s;
-      s = t;
-    }
-  }
-  float kth = top[0];
+  for (int i = 0; i < KT; ++i) p[i] = s > top[i];
 #pragma unroll
-  for (int i = 0; i < KT; ++i)
-    if (i == k - 1) kth = top[i];
-  return kth;
+  for (int i = KT - 1; i > 0; --i) top[i] = p[i] ? (p[i - 1] ? top[i - 1] : s) : top[i];
+  top[0] = p[0] ? s : top[0];
+  return top[KT - 1];
+}
+
+template <int KT>
+__device__ __forceinline__ void topk_store(const float (&top)[KT], int k, float* __restrict__ out) {
+#pragma unroll
+  for (int x = 0; x < KT; ++x)
+    if (x >= KT - k) out[x - (KT - k)] = top[x];
 }
 
 // Compaction of a full candidate buffer against the risen threshold (rare).
-__device__ __noinline__ int compact_candidates(float* __restrict__ cs, int32_t* __restrict__ cr, float thr) {
+__device__ __forceinline__ int compact_candidates(float* __restrict__ cs, int32_t* __restrict__ cr, float thr) {
   int w = 0;
   for (int u = 0; u < CAP; ++u) {
     const float sv = cs[u];
@@ -175,6 +176,209 @@ __device__ __noinline__ int compact_candidates(float* __restrict__ cs, int32_t* 
     }
   }
   return w;
+}
+
+// Per-(query, tile group) state of the scan epilogue (one thread): running top-k of the
+// coarse scores, candidate threshold thr = (lower bound g of the final k-th) - 2*delta,
+// and the candidate buffer.  Any g <= the final k-th keeps the candidate set a superset
+// (rows below g - 2*delta cannot be in the exact top-k).  Each group sees only 1/G of
+// the DB, so g is raised faster than by the group's own k-th:
+//  * warm start: on its first full tile a group takes the k-th largest of the tile's
+//    eight 32-row chunk maxima (k distinct rows reach it; k <= 8);
+//  * gkth: the largest bound any group of the query has published, exchanged once per
+//    64 scores (loads issued one block ahead of their use);
+//  * rank slots: group g publishes its m best values (m = ceil(k / G)) into slots
+//    (g*m + i) % k with atomic max.  A slot's value is at most the current i-th best of
+//    the group that wrote it and distinct slots come from distinct (group, rank) pairs,
+//    i.e. distinct rows, so once all k slots are filled their minimum is a bound of the
+//    k-th over the union of the groups (much tighter than the best group's own k-th).
+// Values <= kfloor (the best shared bound) are not inserted into top[]: the union of
+// the groups' lists already holds k values >= it (correctness does not depend on it:
+// the rescoring k-th is taken from the union of the lists, a subset of all rows).
+template <int KT>
+struct QueryScan {
+  float top[KT];
+  float thr, kth, kfloor, td;
+  uint32_t pub, gk;
+  uint32_t* gkp;  // this query's shared bound (nullptr for padding queries)
+  int cnt;
+  bool ovf;
+  float* cs;
+  int32_t* cr;
+  uint32_t* sl;  // this query's rank slots
+  int m, sbase;
+  bool dirty;    // top[] changed since the last slot publish
+  uint4 sv[KT / 4];
+
+  __device__ __forceinline__ void init(const ScanArgs& a, int q, size_t base, int k, int g) {
+    topk_init<KT>(top, k);
+    td = a.two_delta[q];
+    // padding queries (q >= B) never pass
+    thr = q < a.B ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
+    kth = -__int_as_float(0x7f800000);
+    kfloor = -__int_as_float(0x7f800000);
+    pub = 0;
+    gk = 0;
+    gkp = q < a.B ? a.gkth + q : nullptr;
+    cnt = 0;
+    ovf = false;
+    cs = a.cand_s + base * CAP;
+    cr = a.cand_r + base * CAP;
+    sl = a.gslot + (size_t)q * KMAX;
+    m = a.slot_m;
+    sbase = g * m;
+    dirty = false;
+    pref();
+  }
+
+  __device__ __forceinline__ void raise(float g) {
+    const float t = __fsub_rn(g, td);
+    if (t > thr) thr = t;
+    if (g > kfloor) kfloor = g;
+  }
+
+  __device__ __forceinline__ void publish(float g) {
+    const uint32_t key = ord_key(g);
+    if (key > pub) {
+      atomicMax(gkp, key);
+      pub = key;
+    }
+  }
+
+  // warm start from the chunk maxima of the group's first full tile
+  __device__ __forceinline__ void warm(const float (&cm)[8], int k) {
+    if (!gkp || k > 8) return;
+    float tk[KT];
+    topk_init<KT>(tk, k);
+#pragma unroll
+    for (int x = 0; x < 8; ++x) topk_insert<KT>(tk, cm[x]);
+    const float g = tk[KT - 1];
+    raise(g);
+    publish(g);
+  }
+
+  // issue the shared-bound loads for the next block (consumed by the next sync, a whole
+  // block of scores later, so the L2 latency is hidden)
+  __device__ __forceinline__ void pref() {
+    if (!gkp) return;
+    gk = *reinterpret_cast<volatile uint32_t*>(gkp);
+#pragma unroll
+    for (int x = 0; x < KT / 4; ++x) sv[x] = ld_relaxed_v4(sl + 4 * x);
+  }
+
+  // after the block: publish the own k-th and best values, take the loaded bounds
+  __device__ __forceinline__ void sync(int k) {
+    if (!gkp) return;
+    if (kth > -__int_as_float(0x7f800000)) publish(kth);
+    if (gk) raise(ord_val(gk));
+    if (dirty) {
+      dirty = false;
+#pragma unroll
+      for (int x = 0; x < KT; ++x) {
+        const int r = x - (KT - k);  // rank of slot x in the right-aligned list
+        if (r >= 0 && r < m && top[x] > -__int_as_float(0x7f800000))
+          atomicMax(sl + (sbase + r) % k, ord_key(top[x]));
+      }
+    }
+    uint32_t mn = 0xffffffffu;
+#pragma unroll
+    for (int x = 0; x < KT / 4; ++x) {
+      if (4 * x + 0 < k) mn = min(mn, sv[x].x);
+      if (4 * x + 1 < k) mn = min(mn, sv[x].y);
+      if (4 * x + 2 < k) mn = min(mn, sv[x].z);
+      if (4 * x + 3 < k) mn = min(mn, sv[x].w);
+    }
+    if (mn) raise(ord_val(mn));
+    pref();
+  }
+
+  // one coarse score sc of DB row `row` (a real row)
+  __device__ __forceinline__ void hit(float sc, int row) {
+    if (!(sc >= thr)) return;
+    if (sc > kth && sc > kfloor) {
+      kth = topk_insert<KT>(top, sc);
+      thr = fmaxf(thr, __fsub_rn(kth, td));
+      dirty = true;
+    }
+    if (ovf) return;
+    if (cnt == CAP) {
+      cnt = compact_candidates(cs, cr, thr);
+      if (cnt == CAP) {
+        ovf = true;
+        return;
+      }
+    }
+    cs[cnt] = sc;
+    cr[cnt] = row;
+    ++cnt;
+  }
+
+  __device__ __forceinline__ void finish(const ScanArgs& a, size_t base, int k) {
+    a.cand_n[base] = ovf ? -1 : cnt;
+    topk_store<KT>(top, k, a.topc + base * KMAX);
+  }
+};
+
+// max of 32 scores and of their eight 4-value groups
+__device__ __forceinline__ float chunk_max(const float (&v)[32], float (&m8)[8]) {
+#pragma unroll
+  for (int x = 0; x < 8; ++x) m8[x] = fmaxf(fmaxf(v[4 * x], v[4 * x + 1]), fmaxf(v[4 * x + 2], v[4 * x + 3]));
+  return fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+}
+
+// First full tile of a group: the eight chunk maxima of this thread's query (TMEM
+// columns [col, col + 256) of the thread's lane) give the warm-start bound.
+template <int KT>
+__device__ __forceinline__ void warm_from_tile(QueryScan<KT>& qs, uint32_t taddr, int k) {
+  float cm[8];
+#pragma unroll 1
+  for (int c2 = 0; c2 < BN / 64; ++c2) {
+    uint32_t r0[32], r1[32];
+    sm100::tmem_ld32_async(taddr + c2 * 64, r0);
+    sm100::tmem_ld32_async(taddr + c2 * 64 + 32, r1);
+    sm100::tmem_wait_ld();
+    float v0[32], v1[32], m8[8];
+#pragma unroll
+    for (int x = 0; x < 32; ++x) {
+      v0[x] = __uint_as_float(r0[x]);
+      v1[x] = __uint_as_float(r1[x]);
+    }
+    const float a0 = chunk_max(v0, m8), a1 = chunk_max(v1, m8);
+#pragma unroll
+    for (int c = 0; c < BN / 64; ++c)
+      if (c == c2) { cm[2 * c] = a0; cm[2 * c + 1] = a1; }
+  }
+  qs.warm(cm, k);
+}
+
+// Scores of one 32-row chunk (v[x] = row rbase + x): one max-reduction and one
+// compare per 32 scores on the hot path; the warp then walks the union of the 4-value
+// groups its lanes hit, the group's values picked by a warp-uniform switch so each
+// lane tests them by static register.
+template <int KT>
+__device__ __forceinline__ void scan_chunk(QueryScan<KT>& qs, const float (&v)[32], int rbase, int64_t n_rows) {
+  float m8[8];
+  const float mx = chunk_max(v, m8);
+  if (!__any_sync(0xffffffffu, mx >= qs.thr)) return;
+  uint32_t gm = 0;
+#pragma unroll
+  for (int x = 0; x < 8; ++x) gm |= (m8[x] >= qs.thr ? 1u : 0u) << x;
+  uint32_t gu = __reduce_or_sync(0xffffffffu, gm);
+  const int64_t rlim = n_rows - rbase;  // value x is a real row iff x < rlim
+  while (gu) {
+    const int g8 = __ffs(gu) - 1;
+    gu &= gu - 1;
+    float w[4];
+    switch (g8) {
+#define ALISE_PICK(G) case G: w[0] = v[4 * G]; w[1] = v[4 * G + 1]; w[2] = v[4 * G + 2]; w[3] = v[4 * G + 3]; break;
+      ALISE_PICK(0) ALISE_PICK(1) ALISE_PICK(2) ALISE_PICK(3)
+      ALISE_PICK(4) ALISE_PICK(5) ALISE_PICK(6) default: ALISE_PICK(7)
+#undef ALISE_PICK
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      if (4 * g8 + x < rlim) qs.hit(w[x], rbase + 4 * g8 + x);
+  }
 }
 
 // Persistent CTAs.  Work item w = (query block qb, tile group g): the CTA keeps one
@@ -191,7 +395,6 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* stage32 = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);  // [128][33]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // work item w -> (qb = w % n_qb, g = w / n_qb); n_work = sum over qb of G(qb)
@@ -270,106 +473,44 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
   } else {  // ---------------- epilogue: warps 2..5, thread = query
     const int quarter = warp & 3;
     const int tq = quarter * 32 + lane;
-    float* my_stage = stage32 + tq * 33;
     const int k = a.k;
     int i = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
       const int qb = w % a.n_qb, g = w / a.n_qb;
       const int G = a.base_g + (qb < a.extra_g ? 1 : 0);
       const int q = qb * BM + tq;
-      float top[KT];
-#pragma unroll
-      for (int x = 0; x < KT; ++x) top[x] = -__int_as_float(0x7f800000);
-      const float td = a.two_delta[q];
-      // padding queries (q >= B) never pass
-      float thr = q < a.B ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
-      float kth = -__int_as_float(0x7f800000);
-      uint32_t pub = 0;
-      float kfloor = -__int_as_float(0x7f800000);  // shared k-th: lower values never enter top[]
-      int cnt = 0;
-      bool ovf = false;
       const size_t base = ((size_t)g * a.Bp + q);
-      float* cs = a.cand_s + base * CAP;
-      int32_t* cr = a.cand_r + base * CAP;
+      QueryScan<KT> qs;
+      qs.init(a, q, base, k, g);
       for (int t = g; t < a.n_tiles; t += G, ++i) {
         const int acc = i & 1;
         const uint32_t aph = (i >> 1) & 1;
         sm100::mbar_wait(&tfull[acc], aph);
         sm100::tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+        if (a.warm && t == g && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT>(qs, taddr, k);
 #pragma unroll 1
         for (int c2 = 0; c2 < BN / 64; ++c2) {
           // two TMEM loads in flight per wait
           uint32_t r0[32], r1[32];
-          const uint32_t ta = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c2 * 64;
+          const uint32_t ta = taddr + c2 * 64;
           sm100::tmem_ld32_async(ta, r0);
           sm100::tmem_ld32_async(ta + 32, r1);
           sm100::tmem_wait_ld();
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-          const int c = 2 * c2 + h;
-          float v[32];
+            float v[32];
 #pragma unroll
-          for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(h ? r1[x] : r0[x]);
-          // hot path: one max-reduction and one compare per 32 scores
-          float m8[8];
-#pragma unroll
-          for (int x = 0; x < 8; ++x) m8[x] = fmaxf(fmaxf(v[4 * x], v[4 * x + 1]), fmaxf(v[4 * x + 2], v[4 * x + 3]));
-          const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-          const bool hit = mx >= thr;
-          if (__any_sync(0xffffffffu, hit)) {
-            // only the 4-value groups some lane hits are staged and tested (the warp
-            // executes the union of the lanes' groups, usually one or two of eight)
-            uint32_t gm = 0;
-#pragma unroll
-            for (int x = 0; x < 8; ++x) gm |= (m8[x] >= thr ? 1u : 0u) << x;
-            const uint32_t gu = __reduce_or_sync(0xffffffffu, gm);
-            uint32_t mask = 0;
-#pragma unroll
-            for (int g8 = 0; g8 < 8; ++g8) {
-              if (gu & (1u << g8)) {
-#pragma unroll
-                for (int x = 4 * g8; x < 4 * g8 + 4; ++x) {
-                  my_stage[x] = v[x];
-                  mask |= (v[x] >= thr ? 1u : 0u) << x;
-                }
-              }
-            }
-            const int rbase = t * BN + c * 32;
-            if (rbase + 32 > a.n_rows) mask &= (a.n_rows > rbase) ? (0xffffffffu >> (32 - (a.n_rows - rbase))) : 0u;
-            while (mask) {
-              const int j = __ffs(mask) - 1;
-              mask &= mask - 1;
-              const float sc = my_stage[j];
-              if (!(sc >= thr)) continue;
-              if (sc > kth && sc > kfloor) {  // beats the running k-th: insert
-                kth = topk_insert<KT>(top, sc, k);
-                thr = fmaxf(thr, kth - td);
-              }
-              if (ovf) continue;
-              if (cnt == CAP) {
-                cnt = compact_candidates(cs, cr, thr);
-                if (cnt == CAP) {
-                  ovf = true;
-                  continue;
-                }
-              }
-              cs[cnt] = sc;
-              cr[cnt] = rbase + j;
-              ++cnt;
-            }
+            for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(h ? r1[x] : r0[x]);
+            scan_chunk<KT>(qs, v, t * BN + (2 * c2 + h) * 32, a.n_rows);
           }
-          }
+          qs.sync(k);
         }
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
-        if (q < a.B) share_threshold(a.gkth + q, kth, td, thr, pub, kfloor);
       }
-      a.cand_n[base] = ovf ? -1 : cnt;
-#pragma unroll
-      for (int x = 0; x < KT; ++x)
-        if (x < k) a.topc[base * KMAX + x] = top[x];
+      qs.finish(a, base, k);
     }
   }
   sm100::tc_fence_before();
@@ -493,99 +634,38 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
       const int qp = w % a.n_qb, g = w / a.n_qb;
       const int G = a.base_g + (qp < a.extra_g ? 1 : 0);
       const int q = qp * 2 * BM + (int)rank * BM + tq;
-      float top[KT];
-#pragma unroll
-      for (int x = 0; x < KT; ++x) top[x] = -__int_as_float(0x7f800000);
-      const float td = a.two_delta[q];
-      float thr = q < a.B ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
-      float kth = -__int_as_float(0x7f800000);
-      uint32_t pub = 0;
-      float kfloor = -__int_as_float(0x7f800000);  // shared k-th: lower values never enter top[]
-      int cnt = 0;
-      bool ovf = false;
       const size_t base = ((size_t)g * a.Bp + q);
-      float* cs = a.cand_s + base * CAP;
-      int32_t* cr = a.cand_r + base * CAP;
+      QueryScan<KT> qs;
+      qs.init(a, q, base, k, g);
       for (int t = g; t < a.n_tiles; t += G, ++i) {
         const int acc = i & 1;
         const uint32_t aph = (i >> 1) & 1;
         sm100::mbar_wait(&tfull[acc], aph);
         sm100::tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+        if (a.warm && t == g && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT>(qs, taddr, k);
 #pragma unroll 1
         for (int c2 = 0; c2 < BN / 64; ++c2) {
           // two TMEM loads in flight per wait
           uint32_t r0[32], r1[32];
-          const uint32_t ta = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c2 * 64;
+          const uint32_t ta = taddr + c2 * 64;
           sm100::tmem_ld32_async(ta, r0);
           sm100::tmem_ld32_async(ta + 32, r1);
           sm100::tmem_wait_ld();
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-          const int c = 2 * c2 + h;
-          float v[32];
+            float v[32];
 #pragma unroll
-          for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(h ? r1[x] : r0[x]);
-          float m8[8];
-#pragma unroll
-          for (int x = 0; x < 8; ++x) m8[x] = fmaxf(fmaxf(v[4 * x], v[4 * x + 1]), fmaxf(v[4 * x + 2], v[4 * x + 3]));
-          const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-          const bool hit = mx >= thr;
-          if (__any_sync(0xffffffffu, hit)) {
-            // only the 4-value groups some lane hits are staged and tested (the warp
-            // executes the union of the lanes' groups, usually one or two of eight)
-            uint32_t gm = 0;
-#pragma unroll
-            for (int x = 0; x < 8; ++x) gm |= (m8[x] >= thr ? 1u : 0u) << x;
-            const uint32_t gu = __reduce_or_sync(0xffffffffu, gm);
-            uint32_t mask = 0;
-#pragma unroll
-            for (int g8 = 0; g8 < 8; ++g8) {
-              if (gu & (1u << g8)) {
-#pragma unroll
-                for (int x = 4 * g8; x < 4 * g8 + 4; ++x) {
-                  mask |= (v[x] >= thr ? 1u : 0u) << x;
-                }
-              }
-            }
-            const int rbase = t * BN + c * 32;
-            if (rbase + 32 > a.n_rows) mask &= (a.n_rows > rbase) ? (0xffffffffu >> (32 - (a.n_rows - rbase))) : 0u;
-            while (mask) {
-              const int j = __ffs(mask) - 1;
-              mask &= mask - 1;
-              float sc = v[0];  // v[j] (rare path: a select chain instead of a smem stage)
-#pragma unroll
-              for (int x = 1; x < 32; ++x)
-                if (x == j) sc = v[x];
-              if (!(sc >= thr)) continue;
-              if (sc > kth && sc > kfloor) {
-                kth = topk_insert<KT>(top, sc, k);
-                thr = fmaxf(thr, kth - td);
-              }
-              if (ovf) continue;
-              if (cnt == CAP) {
-                cnt = compact_candidates(cs, cr, thr);
-                if (cnt == CAP) {
-                  ovf = true;
-                  continue;
-                }
-              }
-              cs[cnt] = sc;
-              cr[cnt] = rbase + j;
-              ++cnt;
-            }
+            for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(h ? r1[x] : r0[x]);
+            scan_chunk<KT>(qs, v, t * BN + (2 * c2 + h) * 32, a.n_rows);
           }
-          }
+          qs.sync(k);
         }
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-        if (q < a.B) share_threshold(a.gkth + q, kth, td, thr, pub, kfloor);
       }
-      a.cand_n[base] = ovf ? -1 : cnt;
-#pragma unroll
-      for (int x = 0; x < KT; ++x)
-        if (x < k) a.topc[base * KMAX + x] = top[x];
+      qs.finish(a, base, k);
     }
   }
   sm100::tc_fence_before();
