@@ -29,8 +29,11 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Build the library (in-tree by default).  `out`/`defines` build a variant (e.g.
+    -DALISE_DOT_U=8) at another path for A/B runs through ALISE_LIB."""
+    lib = out or LIB
+    if out is None and not force and not _stale():
         return LIB
     objs = []
     for src in SOURCES:
@@ -38,7 +41,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if not os.path.exists(path):
             continue
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", path, "-o", obj]
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", path, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.run(cmd, check=True)
@@ -49,16 +52,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.run([CXX, "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-I", os.path.join(ROOT, "include"),
                         "-c", path, "-o", obj], check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     # static cudart: the library loads (and its symbols can be checked) on hosts
     # without a CUDA driver; libcuda is resolved lazily at the first CUDA call
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
                     *objs, "-cudart", "static"], check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=out, defines=defs))

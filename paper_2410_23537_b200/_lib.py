@@ -11,7 +11,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libalise_b200.so")
+# ALISE_LIB: an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("ALISE_LIB") or os.path.join(_HERE, "libalise_b200.so")
 
 OK, EINVAL, ENONFINITE, ECAPACITY, ECUDA = 0, 1, 2, 3, 4
 DT_F16, DT_F32, DT_F64 = 0, 1, 2

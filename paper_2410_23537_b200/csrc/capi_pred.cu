@@ -346,9 +346,12 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
     fprintf(stderr, "[scan stats] B=%lld splits=%d cand/query=%.1f ovf=%d\n", (long long)B, splits, tot / B, ovf);
   }
   CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
-  k_rescore<<<(unsigned)B, 256, 0, st>>>(qblk, base_g, extra_g, (int)Bp, B, k, db->size, db->dim, queries, db->v32, db->lens,
-                                         db->seqs, db->two_delta, db->cand_s, db->cand_r, db->cand_n, db->topc,
-                                         out_sim, out_seq, out_len, out_count, db->need, db->inexact);
+  // small batches are latency bound (one DRAM round trip per candidate row), large ones
+  // throughput bound (registers / occupancy)
+  auto rescore = B <= 512 ? k_rescore<24> : k_rescore<8>;
+  rescore<<<(unsigned)B, 256, 0, st>>>(qblk, base_g, extra_g, (int)Bp, B, k, db->size, db->dim, queries, db->v32,
+                                       db->lens, db->seqs, db->two_delta, db->cand_s, db->cand_r, db->cand_n,
+                                       db->topc, out_sim, out_seq, out_len, out_count, db->need, db->inexact);
   CKL();
   k_exhaustive<<<(unsigned)B, 256, 0, st>>>(B, k, db->size, db->dim, queries, db->v32, db->lens, db->seqs, db->need,
                                             out_sim, out_seq, out_len, out_count, db->inexact);

@@ -688,25 +688,29 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
   e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
 }
 
+
 // Warp-cooperative exact dot of two fp32 vectors.  Returns the float64 value and sets
 // `ok` when it is provably the correctly rounded exact sum (fp32*fp32 products are
 // exact in float64; the double-double accumulation error is < (dim+64)*2^-104*sum|p|).
+// U elements per lane in flight per step: 24 = one DRAM round trip per 768 dims (latency
+// bound small batches), 8 = fewer registers (throughput bound large batches).
+template <int U>
 __device__ double warp_exact_dot(const float* __restrict__ a, const float* __restrict__ b, int64_t dim,
                                  bool& ok) {
   const int lane = threadIdx.x & 31;
   double hi = 0.0, lo = 0.0, ab = 0.0;
-  // 8 elements per lane in flight per step (rows are random DB rows: DRAM latency);
-  // out-of-range elements are 0, which leaves hi, lo and ab unchanged
-  for (int64_t d0 = lane; d0 < dim; d0 += 256) {
-    float av[8], bv[8];
+  // rows are random DB rows (DRAM latency); out-of-range elements are 0, which leaves
+  // hi, lo and ab unchanged
+  for (int64_t d0 = lane; d0 < dim; d0 += 32 * U) {
+    float av[U], bv[U];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t d = d0 + 32 * u;
       av[u] = d < dim ? __ldg(a + d) : 0.f;
       bv[u] = d < dim ? __ldg(b + d) : 0.f;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < U; ++u) {
       const double p = __dmul_rn((double)av[u], (double)bv[u]);
       double s, e;
       two_sum(hi, p, s, e);
@@ -863,8 +867,11 @@ __device__ __noinline__ double warp_exact_dot_super(const float* __restrict__ a,
   return super_round(acc);
 }
 
+__device__ __forceinline__ int nw_last(unsigned bd) { return (int)(bd >> 5) - 1; }
+
 // Per query: global coarse k-th from the splits' top lists, candidate compaction,
 // exact rescoring, (-sim, seq) order.  Block = 256 threads.
+template <int U>
 __global__ void __launch_bounds__(256)
 k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
           const float* __restrict__ v32, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
@@ -874,68 +881,64 @@ k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n
           int32_t* __restrict__ need_exhaustive, unsigned int* __restrict__ inexact_count) {
   const int64_t q = blockIdx.x;
   if (q >= B) return;
-  __shared__ float s_top[8192];
+  __shared__ float s_top[8192];  // the splits' top lists (host: n_splits * k <= 8192)
+  __shared__ int s_off[513];     // n_splits <= 512 (host)
   __shared__ int s_rows[MAXC];
   __shared__ double s_sim[MAXC];
   __shared__ int64_t s_seq[MAXC];
-  __shared__ float s_rv[8];
-  __shared__ int s_ri[8];
+  __shared__ float s_wk[8 * KMAX];
+  __shared__ float s_kth;
   __shared__ int s_n;
   __shared__ int s_flag;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) { s_n = 0; s_flag = 0; }
-  // 1) kk-th largest coarse score across the splits' top lists (real rows' scores):
-  //    kk rounds of block-wide argmax with removal
   const int n_splits = base_g + ((q / qblk) < extra_g ? 1 : 0);
-  const int m = n_splits * k;  // host guarantees m <= 8192
   const int64_t kk = k < n_rows ? k : n_rows;
   const float NEG = -__int_as_float(0x7f800000);
+#ifdef ALISE_RESCORE_TIMING
+  const long long T0 = clock64();
+#endif
+  // 1) stage the splits' top lists and candidate counts (all loads in flight at once)
+  const int m = n_splits * k;
+  if (tid == 0) { s_n = 0; s_flag = 0; }
   for (int i = tid; i < m; i += blockDim.x) {
-    const int sp = i / k, j = i % k;
-    s_top[i] = topc[((size_t)sp * Bp + q) * KMAX + j];
+    const int sp = i / k, j = i - sp * k;
+    s_top[i] = __ldg(topc + ((size_t)sp * Bp + q) * KMAX + j);
   }
-  __syncthreads();
-  float kth = NEG;
-  for (int64_t round = 0; round < kk; ++round) {
-    float bv = NEG;
-    int bi = 0x7fffffff;
-    for (int i = tid; i < m; i += blockDim.x) {
-      const float v = s_top[i];
-      if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
-    }
-    for (int o = 16; o; o >>= 1) {
-      const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; }
-    }
-    if (lane == 0) { s_rv[warp] = bv; s_ri[warp] = bi; }
-    __syncthreads();
-    if (tid == 0) {
-      float v = s_rv[0];
-      int ix = s_ri[0];
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-        if (s_rv[w] > v || (s_rv[w] == v && s_ri[w] < ix)) { v = s_rv[w]; ix = s_ri[w]; }
-      s_rv[0] = v;
-      if (ix >= 0 && ix < m) s_top[ix] = NEG;
-    }
-    __syncthreads();
-    kth = s_rv[0];
-    __syncthreads();
-  }
-  const float thr = kth - two_delta[q];
-  // 2) gather candidates above the final threshold: every split's count loaded in
-  //    parallel, then a warp per split (candidate order is irrelevant: step 4 ranks)
-  //    and the (split, slot) entries flattened over the whole block through a prefix
-  //    sum of the counts, so every candidate load is in flight at once
-  int* s_off = reinterpret_cast<int*>(s_top);  // the top lists are consumed: [n_splits + 1]
   for (int sp = tid; sp < n_splits; sp += blockDim.x) {
     const int cnt = cand_n[(size_t)sp * Bp + q];
     s_off[sp + 1] = cnt < 0 ? 0 : cnt;
     if (cnt < 0) s_flag = 1;
   }
   __syncthreads();
-  if (warp == 0) {  // inclusive scan of s_off[1..n_splits] (n_splits <= 512)
+  // 2) kk-th largest coarse score over the lists: each warp takes the kk largest of its
+  //    slice (kk rounds of warp argmax, the winner's slot cleared), warp 0 repeats that
+  //    over the warps' results; warp 7 meanwhile scans the counts into offsets
+  {
+    const int nw = blockDim.x >> 5;
+    const int per = (m + nw - 1) / nw;
+    const int lo = warp * per, hi = min(m, lo + per);
+    for (int64_t round = 0; round < kk; ++round) {
+      float bv = NEG;
+      int bi = -1;
+      for (int i = lo + lane; i < hi; i += 32) {
+        const float v = s_top[i];
+        if (v > bv) { bv = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (v2 > bv || (v2 == bv && i2 > bi)) { bv = v2; bi = i2; }
+      }
+      if (lane == 0) {
+        s_wk[warp * KMAX + round] = bv;
+        if (bi >= 0) s_top[bi] = NEG;
+      }
+      __syncwarp();
+    }
+  }
+  if (warp == nw_last(blockDim.x)) {
     int carry = 0;
     for (int base = 1; base <= n_splits; base += 32) {
       const int i = base + lane;
@@ -951,6 +954,36 @@ k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n
     if (lane == 0) s_off[0] = 0;
   }
   __syncthreads();
+  if (warp == 0) {
+    const int mw = (int)(blockDim.x >> 5) * (int)kk;
+    float kth = NEG;
+    for (int64_t round = 0; round < kk; ++round) {
+      float bv = NEG;
+      int bi = -1;
+      for (int i = lane; i < mw; i += 32) {
+        const float v = s_wk[(i / kk) * KMAX + i % kk];
+        if (v > bv) { bv = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (v2 > bv || (v2 == bv && i2 > bi)) { bv = v2; bi = i2; }
+      }
+      if (lane == 0 && bi >= 0) s_wk[(bi / kk) * KMAX + bi % kk] = NEG;
+      __syncwarp();
+      kth = bv;
+    }
+    if (lane == 0) s_kth = kth;
+  }
+  __syncthreads();
+#ifdef ALISE_RESCORE_TIMING
+  const long long T1 = clock64();
+#endif
+  const float thr = s_kth - two_delta[q];
+  // 3) gather candidates above the final threshold: the (split, slot) entries are
+  //    flattened over the whole block through the prefix sum of the counts, so every
+  //    candidate load is in flight at once (candidate order is irrelevant: step 5 ranks)
   const int total = s_off[n_splits];
   for (int i0 = tid; i0 < total; i0 += 8 * blockDim.x) {
     size_t ev[8];
@@ -979,16 +1012,19 @@ k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n
     }
   }
   __syncthreads();
+#ifdef ALISE_RESCORE_TIMING
+  const long long T2 = clock64();
+#endif
   const int n = s_n;
   if (n > MAXC || s_flag) {
     if (tid == 0) need_exhaustive[q] = 1;
     return;
   }
-  // 3) exact float64 scores, one warp per candidate
+  // 4) exact float64 scores, one warp per candidate
   for (int c = warp; c < n; c += blockDim.x >> 5) {
     const int row = s_rows[c];
     bool ok;
-    double sim = warp_exact_dot(v32 + (size_t)row * dim, q32 + q * dim, dim, ok);
+    double sim = warp_exact_dot<U>(v32 + (size_t)row * dim, q32 + q * dim, dim, ok);
     if (!ok) {  // warp-uniform: the certificate is computed from butterfly-reduced sums
       sim = warp_exact_dot_super(v32 + (size_t)row * dim, q32 + q * dim, dim);
       if (lane == 0) atomicAdd(inexact_count, 1u);
@@ -999,7 +1035,10 @@ k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n
     }
   }
   __syncthreads();
-  // 4) rank by (-sim, seq); seqs are unique
+#ifdef ALISE_RESCORE_TIMING
+  const long long T3 = clock64();
+#endif
+  // 5) rank by (-sim, seq); seqs are unique
   for (int c = tid; c < n; c += blockDim.x) {
     const double sv = s_sim[c];
     const int64_t qv = s_seq[c];
@@ -1012,6 +1051,11 @@ k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n
     }
   }
   if (tid == 0) out_count[q] = (int32_t)(n < kk ? n : kk);
+#ifdef ALISE_RESCORE_TIMING
+  if (tid == 0 && q < 4)
+    printf("[rescore q=%lld] splits=%d total=%d n=%d cycles: select+counts %lld gather %lld dots %lld rank %lld\n",
+           (long long)q, n_splits, total, n, T1 - T0, T2 - T1, T3 - T2, clock64() - T3);
+#endif
 }
 
 // Exhaustive exact top-k for queries flagged by k_rescore (candidate overflow from
@@ -1034,7 +1078,7 @@ k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restr
   for (int i = 0; i < KMAX; ++i) { tsim[i] = -__longlong_as_double(0x7ff0000000000000ll); tseq[i] = INT64_MAX; trow[i] = -1; }
   for (int64_t row = warp; row < n_rows; row += blockDim.x >> 5) {
     bool ok;
-    double sim = warp_exact_dot(v32 + row * dim, q32 + q * dim, dim, ok);
+    double sim = warp_exact_dot<8>(v32 + row * dim, q32 + q * dim, dim, ok);
     if (!ok) {
       sim = warp_exact_dot_super(v32 + row * dim, q32 + q * dim, dim);
       if (lane == 0) atomicAdd(inexact_count, 1u);
@@ -1145,11 +1189,36 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
     }
     if (__syncthreads_or(mlp)) {
       const int64_t nw = dim * hidden;
-      for (int64_t i = threadIdx.x; i < nw; i += blockDim.x) smem_fin[i] = W1[i];
-      float* xs = reinterpret_cast<float*>(smem_fin + nw) + (threadIdx.x >> 5) * dim;
-      if (q < B)
-        for (int64_t i = lane; i < dim; i += 32) xs[i] = x[q * dim + i];
-      __syncthreads();
+      float* xs0 = reinterpret_cast<float*>(smem_fin + nw);
+      const int64_t q0 = (int64_t)blockIdx.x * (blockDim.x >> 5);
+      const int64_t nq = B - q0 < (int64_t)(blockDim.x >> 5) ? B - q0 : (int64_t)(blockDim.x >> 5);
+      // one bulk (TMA) copy of W1 and of the block's query rows when the addresses allow
+      // it; a plain load/store loop has one L2 round trip in flight per thread
+      const bool bulk = ((reinterpret_cast<uintptr_t>(W1) | reinterpret_cast<uintptr_t>(x + q0 * dim)) & 15) == 0 &&
+                        (dim & 3) == 0 && (nw & 1) == 0;
+      if (bulk) {
+        __shared__ uint64_t fin_bar;
+        if (threadIdx.x == 0) {
+          sm100::mbar_init(&fin_bar, 1);
+          sm100::fence_barrier_init();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const uint32_t wb = (uint32_t)(nw * 8), xb = (uint32_t)(nq * dim * 4);
+          sm100::mbar_arrive_expect_tx(&fin_bar, wb + xb);
+          for (uint32_t o = 0; o < wb; o += 32768)
+            sm100::bulk_g2s(reinterpret_cast<uint8_t*>(smem_fin) + o, reinterpret_cast<const uint8_t*>(W1) + o,
+                            wb - o < 32768 ? wb - o : 32768, &fin_bar);
+          sm100::bulk_g2s(xs0, x + q0 * dim, xb, &fin_bar);
+        }
+        sm100::mbar_wait(&fin_bar, 0);
+      } else {
+        for (int64_t i = threadIdx.x; i < nw; i += blockDim.x) smem_fin[i] = W1[i];
+        float* xs = xs0 + (threadIdx.x >> 5) * dim;
+        if (q < B)
+          for (int64_t i = lane; i < dim; i += 32) xs[i] = x[q * dim + i];
+        __syncthreads();
+      }
       smem_w1 = smem_fin;
     }
   }

@@ -1,0 +1,4 @@
+set -x
+timeout 900 python -m pytest tests/test_pred_gpu.py -q -x 2>&1 | tail -3
+timeout 600 python tools/pred_kernels.py 1000000 4096,256,1 2>&1 | grep '^{' | cut -c1-250
+ALISE_LIB=variants/lib_rtime.so timeout 600 python tools/pred_bench.py 1000000 1 2>&1 | grep "rescore q=" | tail -3
