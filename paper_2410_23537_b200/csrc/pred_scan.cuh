@@ -1176,6 +1176,10 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
                          uint8_t* __restrict__ out_ret, bool stage) {
   const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+#ifdef ALISE_FINISH_TIMING
+  const long long F0 = clock64();
+  long long F1 = 0, F2 = 0;
+#endif
   // stage W1 (and each warp's query) in shared memory when some query of the block
   // takes the MLP branch and the launch provided the space
   extern __shared__ double smem_fin[];
@@ -1223,6 +1227,9 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
     }
   }
   if (q >= B) return;
+#ifdef ALISE_FINISH_TIMING
+  F1 = clock64();
+#endif
   const int c = counts[q];
   int nq = 0;
   double w[KMAX], prod[KMAX], vals[KMAX];
@@ -1265,13 +1272,25 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
     const int64_t j = lane + 32 * t;
     double acc = 0.0;
     if (j < hidden) {
-#pragma unroll 8
-      for (int64_t d = 0; d < dim; ++d) acc = __dadd_rn(acc, __dmul_rn((double)xq[d], Wm[d * hidden + j]));
+      // products of 32 terms first (independent: loads, converts and multiplies
+      // pipeline), then their index-order adds: the chain runs at the add latency
+      int64_t d0 = 0;
+      for (; d0 + 32 <= dim; d0 += 32) {
+        double pr[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) pr[u] = __dmul_rn((double)xq[d0 + u], Wm[(d0 + u) * hidden + j]);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, pr[u]);
+      }
+      for (int64_t d = d0; d < dim; ++d) acc = __dadd_rn(acc, __dmul_rn((double)xq[d], Wm[d * hidden + j]));
       hv[t] = tanh(__dadd_rn(acc, b1[j]));
     } else {
       hv[t] = 0.0;
     }
   }
+#ifdef ALISE_FINISH_TIMING
+  F2 = clock64();
+#endif
   // sequential sum over hidden units in index order (lane 0 gathers)
   for (int64_t j = 0; j < hidden; ++j) {
     const int t = (int)(j / 32), src = (int)(j % 32);
@@ -1289,6 +1308,9 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
     r = fmin(fmax(r, 1.0), (double)max_len);
     out_len[q] = (int32_t)r;
     out_ret[q] = 0;
+#ifdef ALISE_FINISH_TIMING
+    if (q < 2) printf("[finish q=%lld] stage %lld hidden %lld out %lld\n", (long long)q, F1 - F0, F2 - F1, clock64() - F2);
+#endif
   }
 }
 
