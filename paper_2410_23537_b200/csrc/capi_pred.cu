@@ -294,6 +294,8 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   // [Bp] shared k-th, then [Bp][KMAX] rank slots (16-byte aligned: Bp % 128 == 0): one memset
   a.gslot = db->gkth + Bp;
   a.slot_m = (k + base_g - 1) / base_g;
+  // long groups warm up early in their run: one exchange per tile is enough
+  a.sync_tile = n_tiles / std::max(1, base_g) >= 256 ? 1 : 0;
   CK(cudaMemsetAsync(db->gkth, 0, sizeof(uint32_t) * Bp * (1 + KMAX), st));
   static bool attr_set[4] = {false, false, false, false};
   const int kt = (k <= 8 ? 0 : 1) + (two_sm ? 2 : 0);

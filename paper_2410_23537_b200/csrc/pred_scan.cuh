@@ -117,6 +117,7 @@ struct ScanArgs {
   int warm;          // warm-start bound from each group's first tile (QueryScan)
   uint32_t* gslot;   // [Bp][KMAX] rank slots per query (ord_key; 0 = empty)
   int slot_m;        // ranks each group publishes into the slots
+  int sync_tile;     // exchange the shared bounds once per tile instead of per 64 scores
 };
 
 __device__ __forceinline__ uint4 ld_relaxed_v4(const uint32_t* p) {
@@ -186,7 +187,7 @@ __device__ __forceinline__ int compact_candidates(float* __restrict__ cs, int32_
 //  * warm start: on its first full tile a group takes the k-th largest of the tile's
 //    eight 32-row chunk maxima (k distinct rows reach it; k <= 8);
 //  * gkth: the largest bound any group of the query has published, exchanged once per
-//    64 scores (loads issued one block ahead of their use);
+//    64 scores, or per tile when groups are long (loads issued one exchange ahead);
 //  * rank slots: group g publishes its m best values (m = ceil(k / G)) into slots
 //    (g*m + i) % k with atomic max.  A slot's value is at most the current i-th best of
 //    the group that wrote it and distinct slots come from distinct (group, rank) pairs,
@@ -319,11 +320,15 @@ struct QueryScan {
   }
 };
 
-// max of 32 scores and of their eight 4-value groups
-__device__ __forceinline__ float chunk_max(const float (&v)[32], float (&m8)[8]) {
+// max of 32 scores as a tree of 3-input maxes (FMNMX3: 16 instructions)
+__device__ __forceinline__ float max32(const float (&v)[32]) {
+  float t[11];
 #pragma unroll
-  for (int x = 0; x < 8; ++x) m8[x] = fmaxf(fmaxf(v[4 * x], v[4 * x + 1]), fmaxf(v[4 * x + 2], v[4 * x + 3]));
-  return fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+  for (int x = 0; x < 10; ++x) t[x] = fmaxf(fmaxf(v[3 * x], v[3 * x + 1]), v[3 * x + 2]);
+  t[10] = fmaxf(v[30], v[31]);
+  const float u0 = fmaxf(fmaxf(t[0], t[1]), t[2]), u1 = fmaxf(fmaxf(t[3], t[4]), t[5]);
+  const float u2 = fmaxf(fmaxf(t[6], t[7]), t[8]), u3 = fmaxf(t[9], t[10]);
+  return fmaxf(fmaxf(u0, u1), fmaxf(u2, u3));
 }
 
 // First full tile of a group: the eight chunk maxima of this thread's query (TMEM
@@ -337,13 +342,13 @@ __device__ __forceinline__ void warm_from_tile(QueryScan<KT>& qs, uint32_t taddr
     sm100::tmem_ld32_async(taddr + c2 * 64, r0);
     sm100::tmem_ld32_async(taddr + c2 * 64 + 32, r1);
     sm100::tmem_wait_ld();
-    float v0[32], v1[32], m8[8];
+    float v0[32], v1[32];
 #pragma unroll
     for (int x = 0; x < 32; ++x) {
       v0[x] = __uint_as_float(r0[x]);
       v1[x] = __uint_as_float(r1[x]);
     }
-    const float a0 = chunk_max(v0, m8), a1 = chunk_max(v1, m8);
+    const float a0 = max32(v0), a1 = max32(v1);
 #pragma unroll
     for (int c = 0; c < BN / 64; ++c)
       if (c == c2) { cm[2 * c] = a0; cm[2 * c + 1] = a1; }
@@ -357,9 +362,11 @@ __device__ __forceinline__ void warm_from_tile(QueryScan<KT>& qs, uint32_t taddr
 // lane tests them by static register.
 template <int KT>
 __device__ __forceinline__ void scan_chunk(QueryScan<KT>& qs, const float (&v)[32], int rbase, int64_t n_rows) {
+  if (!__any_sync(0xffffffffu, max32(v) >= qs.thr)) return;
+  // rare path: which 4-value groups hit
   float m8[8];
-  const float mx = chunk_max(v, m8);
-  if (!__any_sync(0xffffffffu, mx >= qs.thr)) return;
+#pragma unroll
+  for (int x = 0; x < 8; ++x) m8[x] = fmaxf(fmaxf(v[4 * x], v[4 * x + 1]), fmaxf(v[4 * x + 2], v[4 * x + 3]));
   uint32_t gm = 0;
 #pragma unroll
   for (int x = 0; x < 8; ++x) gm |= (m8[x] >= qs.thr ? 1u : 0u) << x;
@@ -504,7 +511,7 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
             for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(h ? r1[x] : r0[x]);
             scan_chunk<KT>(qs, v, t * BN + (2 * c2 + h) * 32, a.n_rows);
           }
-          qs.sync(k);
+          if (!a.sync_tile || c2 == BN / 64 - 1) qs.sync(k);
         }
         sm100::tc_fence_before();
         __syncwarp();
@@ -659,7 +666,7 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
             for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(h ? r1[x] : r0[x]);
             scan_chunk<KT>(qs, v, t * BN + (2 * c2 + h) * 32, a.n_rows);
           }
-          qs.sync(k);
+          if (!a.sync_tile || c2 == BN / 64 - 1) qs.sync(k);
         }
         sm100::tc_fence_before();
         __syncwarp();
