@@ -317,3 +317,26 @@ def test_graphed_single_request_matches_eager(pr):
     p.enable_graphs()
     assert [p.predict_vector(q) for q in Q] == eager2
     assert any(r == pr.FALLBACK for _, r in eager2) and any(r == pr.RETRIEVED for _, r in eager2)
+
+
+@pytest.mark.parametrize("B,k,negative", [(1, 3, False), (1, 16, False), (300, 16, False), (1, 8, True),
+                                          (300, 5, True)])
+def test_scan_bounds_many_groups(pr, B, k, negative):
+    """Warm-start bound, shared k-th and rank slots across many tile groups (B = 1 runs
+    148 groups of the 1-SM scan, B = 300 two CTA-pair blocks of 2-SM groups), for k
+    not dividing the slot count and for all-negative similarities (order-preserving keys
+    of negative scores, warm start from negative chunk maxima)."""
+    g = np.random.default_rng(1000 * B + k)
+    n, d = 150_000, 64
+    db = g.standard_normal((n, d)).astype(np.float32)
+    if negative:  # every row in the positive orthant, every query in the negative one
+        db = np.abs(db)
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = g.standard_normal((B, d)).astype(np.float32)
+    if negative:
+        Q = -np.abs(Q)
+    else:
+        Q[: B // 2] = db[g.integers(0, n, size=B // 2)] + 0.05 * g.standard_normal((B // 2, d)).astype(np.float32)
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    check_batch(pr, db, lens, Q.astype(np.float32), k)
