@@ -243,7 +243,18 @@ def link_peaks(dev_index: int):
             h.copy_(d, non_blocking=True)
         with torch.cuda.stream(s2):
             d2.copy_(h2, non_blocking=True)
-    duplex = max(2 * n / timed(both) / 1e9 for _ in range(3))
+
+    def both_chunked(parts=8):
+        # the swap path's shape: many 128 MiB chunks in flight per direction
+        c = n // parts
+        for i in range(parts):
+            with torch.cuda.stream(s1):
+                h[i * c:(i + 1) * c].copy_(d[i * c:(i + 1) * c], non_blocking=True)
+            with torch.cuda.stream(s2):
+                d2[i * c:(i + 1) * c].copy_(h2[i * c:(i + 1) * c], non_blocking=True)
+    # best of several trials of both shapes (a peak probe should not under-read)
+    duplex = max([2 * n / timed(both) / 1e9 for _ in range(4)] +
+                 [2 * n / timed(both_chunked) / 1e9 for _ in range(4)])
     del d, d2, h, h2
     return {"d2h_GBs": d2h, "h2d_GBs": h2d, "duplex_total_GBs": duplex}
 

@@ -263,7 +263,15 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   const int n_tiles = (int)((db->size + BN - 1) / BN);
   const int units = two_sm ? sm_count_pred() / 2 : sm_count_pred();
   int base_g, extra_g;
-  const int splits = choose_groups(n_qb, n_tiles, units, &base_g, &extra_g);
+  const int groups = choose_groups(n_qb, n_tiles, units, &base_g, &extra_g);
+  // 2-SM scan with k <= 8: two epilogue warps per TMEM lane quarter, each its own split
+  static int halves = -1;
+  if (halves < 0) {
+    const char* e = getenv("ALISE_SCAN2_HALVES");
+    halves = e ? std::max(1, std::min(2, atoi(e))) : 2;
+  }
+  const int nh = (two_sm && k <= 8) ? halves : 1;
+  const int splits = groups * nh;
   int s = ensure_scratch(db, Bp, splits, st);
   if (s) return s;
   k_query_prep<<<(unsigned)Bp, 128, 0, st>>>(queries, B, db->dim, db->dp, db->vmax, db->q16, db->two_delta);
@@ -293,18 +301,19 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   a.warm = warm;
   // [Bp] shared k-th, then [Bp][KMAX] rank slots (16-byte aligned: Bp % 128 == 0): one memset
   a.gslot = db->gkth + Bp;
-  a.slot_m = (k + base_g - 1) / base_g;
+  a.slot_m = (k + base_g * nh - 1) / (base_g * nh);
   // long groups warm up early in their run: one exchange per tile is enough
   a.sync_tile = n_tiles / std::max(1, base_g) >= 256 ? 1 : 0;
   CK(cudaMemsetAsync(db->gkth, 0, sizeof(uint32_t) * Bp * (1 + KMAX), st));
-  static bool attr_set[4] = {false, false, false, false};
-  const int kt = (k <= 8 ? 0 : 1) + (two_sm ? 2 : 0);
+  static bool attr_set[5] = {false, false, false, false, false};
+  const int kt = two_sm ? (k <= 8 ? (nh == 2 ? 4 : 2) : 3) : (k <= 8 ? 0 : 1);
   if (!attr_set[kt]) {
     switch (kt) {
       case 0: CK(cudaFuncSetAttribute(k_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM)); break;
       case 1: CK(cudaFuncSetAttribute(k_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_SMEM)); break;
-      case 2: CK(cudaFuncSetAttribute(k_scan2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN2_SMEM)); break;
-      default: CK(cudaFuncSetAttribute(k_scan2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN2_SMEM)); break;
+      case 2: CK(cudaFuncSetAttribute(k_scan2<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN2_SMEM)); break;
+      case 3: CK(cudaFuncSetAttribute(k_scan2<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN2_SMEM)); break;
+      default: CK(cudaFuncSetAttribute(k_scan2<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN2_SMEM)); break;
     }
     attr_set[kt] = true;
   }
@@ -320,8 +329,9 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   switch (kt) {
     case 0: k_scan<8><<<grid, 192, SCAN_SMEM, st>>>(db->tmQ, db->tmD, a); break;
     case 1: k_scan<16><<<grid, 192, SCAN_SMEM, st>>>(db->tmQ, db->tmD, a); break;
-    case 2: k_scan2<8><<<grid, 192, SCAN2_SMEM, st>>>(db->tmQ, db->tmD2, a); break;
-    default: k_scan2<16><<<grid, 192, SCAN2_SMEM, st>>>(db->tmQ, db->tmD2, a); break;
+    case 2: k_scan2<8, 1><<<grid, 192, SCAN2_SMEM, st>>>(db->tmQ, db->tmD2, a); break;
+    case 3: k_scan2<16, 1><<<grid, 192, SCAN2_SMEM, st>>>(db->tmQ, db->tmD2, a); break;
+    default: k_scan2<8, 2><<<grid, 320, SCAN2_SMEM, st>>>(db->tmQ, db->tmD2, a); break;
   }
   CKL();
   if (db->timing) {
@@ -351,7 +361,7 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   // small batches are latency bound (one DRAM round trip per candidate row), large ones
   // throughput bound (registers / occupancy)
   auto rescore = B <= 512 ? k_rescore<24> : k_rescore<8>;
-  rescore<<<(unsigned)B, 256, 0, st>>>(qblk, base_g, extra_g, (int)Bp, B, k, db->size, db->dim, queries, db->v32,
+  rescore<<<(unsigned)B, 256, 0, st>>>(qblk, nh, base_g, extra_g, (int)Bp, B, k, db->size, db->dim, queries, db->v32,
                                        db->lens, db->seqs, db->two_delta, db->cand_s, db->cand_r, db->cand_n,
                                        db->topc, out_sim, out_seq, out_len, out_count, db->need, db->inexact);
   CKL();

@@ -331,13 +331,14 @@ __device__ __forceinline__ float max32(const float (&v)[32]) {
   return fmaxf(fmaxf(u0, u1), fmaxf(u2, u3));
 }
 
-// First full tile of a group: the eight chunk maxima of this thread's query (TMEM
-// columns [col, col + 256) of the thread's lane) give the warm-start bound.
-template <int KT>
+// First full tile of a group: eight maxima over this thread's columns of the tile (TMEM
+// columns [taddr, taddr + 64*NC2) of its lane: 32-value chunks for NC2 = 4, 16-value
+// halves for NC2 = 2) give the warm-start bound.
+template <int KT, int NC2>
 __device__ __forceinline__ void warm_from_tile(QueryScan<KT>& qs, uint32_t taddr, int k) {
   float cm[8];
 #pragma unroll 1
-  for (int c2 = 0; c2 < BN / 64; ++c2) {
+  for (int c2 = 0; c2 < NC2; ++c2) {
     uint32_t r0[32], r1[32];
     sm100::tmem_ld32_async(taddr + c2 * 64, r0);
     sm100::tmem_ld32_async(taddr + c2 * 64 + 32, r1);
@@ -348,10 +349,27 @@ __device__ __forceinline__ void warm_from_tile(QueryScan<KT>& qs, uint32_t taddr
       v0[x] = __uint_as_float(r0[x]);
       v1[x] = __uint_as_float(r1[x]);
     }
-    const float a0 = max32(v0), a1 = max32(v1);
+    float mm[4];
+    if (NC2 == 4) {
+      mm[0] = max32(v0);
+      mm[1] = max32(v1);
+    } else {
+      mm[0] = mm[1] = mm[2] = mm[3] = -__int_as_float(0x7f800000);
 #pragma unroll
-    for (int c = 0; c < BN / 64; ++c)
-      if (c == c2) { cm[2 * c] = a0; cm[2 * c + 1] = a1; }
+      for (int x = 0; x < 16; ++x) {
+        mm[0] = fmaxf(mm[0], v0[x]);
+        mm[1] = fmaxf(mm[1], v0[16 + x]);
+        mm[2] = fmaxf(mm[2], v1[x]);
+        mm[3] = fmaxf(mm[3], v1[16 + x]);
+      }
+    }
+    constexpr int PER = 8 / NC2;
+#pragma unroll
+    for (int c = 0; c < NC2; ++c)
+      if (c == c2) {
+#pragma unroll
+        for (int x = 0; x < PER; ++x) cm[PER * c + x] = mm[x];
+      }
   }
   qs.warm(cm, k);
 }
@@ -495,7 +513,7 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
         sm100::mbar_wait(&tfull[acc], aph);
         sm100::tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-        if (a.warm && t == g && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT>(qs, taddr, k);
+        if (a.warm && t == g && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT, 4>(qs, taddr, k);
 #pragma unroll 1
         for (int c2 = 0; c2 < BN / 64; ++c2) {
           // two TMEM loads in flight per wait
@@ -542,8 +560,8 @@ constexpr int B2_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's 128 DB rows
 constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
 constexpr int SCAN2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 256;
 
-template <int KT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+template <int KT, int NH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * NH, 1)
 k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmD, const ScanArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -568,7 +586,7 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
     }
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&tfull[s], 1);
-      sm100::mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy used)
+      sm100::mbar_init(&tempty[s], 8 * NH);  // 4*NH epilogue warps x 2 CTAs (leader's copy used)
     }
     sm100::fence_barrier_init();
   }
@@ -630,10 +648,14 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
         }
       }
     }
-  } else {  // ---------------- epilogue: warps 2..5 of both CTAs, thread = query
+  } else {  // ---------------- epilogue: warps 2..(1 + 4*NH) of both CTAs, thread = query
+    // NH = 2: two warps per TMEM lane quarter, each owning 128 of the tile's 256
+    // columns as its own split (g*NH + half): half the epilogue work per warp and tile
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int tq = quarter * 32 + lane;
     const int k = a.k;
+    constexpr int NC2 = BN / 64 / NH;
     const uint32_t tempty_leader0 = sm100::mapa(sm100::smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = sm100::mapa(sm100::smem_u32(&tempty[1]), 0);
     int i = 0;
@@ -641,18 +663,20 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
       const int qp = w % a.n_qb, g = w / a.n_qb;
       const int G = a.base_g + (qp < a.extra_g ? 1 : 0);
       const int q = qp * 2 * BM + (int)rank * BM + tq;
-      const size_t base = ((size_t)g * a.Bp + q);
+      const int gs = g * NH + half;
+      const size_t base = ((size_t)gs * a.Bp + q);
       QueryScan<KT> qs;
-      qs.init(a, q, base, k, g);
+      qs.init(a, q, base, k, gs);
       for (int t = g; t < a.n_tiles; t += G, ++i) {
         const int acc = i & 1;
         const uint32_t aph = (i >> 1) & 1;
         sm100::mbar_wait(&tfull[acc], aph);
         sm100::tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-        if (a.warm && t == g && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT>(qs, taddr, k);
+        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * (BN / NH);
+        const int cbase = t * BN + half * (BN / NH);
+        if (a.warm && t == g && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT, NC2>(qs, taddr, k);
 #pragma unroll 1
-        for (int c2 = 0; c2 < BN / 64; ++c2) {
+        for (int c2 = 0; c2 < NC2; ++c2) {
           // two TMEM loads in flight per wait
           uint32_t r0[32], r1[32];
           const uint32_t ta = taddr + c2 * 64;
@@ -664,9 +688,9 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
             float v[32];
 #pragma unroll
             for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(h ? r1[x] : r0[x]);
-            scan_chunk<KT>(qs, v, t * BN + (2 * c2 + h) * 32, a.n_rows);
+            scan_chunk<KT>(qs, v, cbase + (2 * c2 + h) * 32, a.n_rows);
           }
-          if (!a.sync_tile || c2 == BN / 64 - 1) qs.sync(k);
+          if (!a.sync_tile || c2 == NC2 - 1) qs.sync(k);
         }
         sm100::tc_fence_before();
         __syncwarp();
@@ -880,7 +904,7 @@ __device__ __forceinline__ int nw_last(unsigned bd) { return (int)(bd >> 5) - 1;
 // exact rescoring, (-sim, seq) order.  Block = 256 threads.
 template <int U>
 __global__ void __launch_bounds__(256)
-k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
+k_rescore(int qblk, int smul, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
           const float* __restrict__ v32, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
           const float* __restrict__ two_delta, const float* __restrict__ cand_s, const int32_t* __restrict__ cand_r,
           const int32_t* __restrict__ cand_n, const float* __restrict__ topc, double* __restrict__ out_sim,
@@ -899,7 +923,7 @@ k_rescore(int qblk, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n
   __shared__ int s_flag;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int n_splits = base_g + ((q / qblk) < extra_g ? 1 : 0);
+  const int n_splits = smul * (base_g + ((q / qblk) < extra_g ? 1 : 0));
   const int64_t kk = k < n_rows ? k : n_rows;
   const float NEG = -__int_as_float(0x7f800000);
 #ifdef ALISE_RESCORE_TIMING
