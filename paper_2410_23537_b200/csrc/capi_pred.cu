@@ -194,21 +194,6 @@ extern "C" int alise_db_inexact(alise_db* db, unsigned int* count) {
   return ALISE_OK;
 }
 
-// Tile groups: one persistent CTA per (query block, group).  Every SM gets a CTA:
-// query block qb owns base + (qb < extra) groups.  Returns the max groups per block.
-static int choose_groups(int n_qb, int n_tiles, int sms, int* base, int* extra) {
-  if (n_qb >= sms) {
-    *base = 1;
-    *extra = 0;
-    return 1;
-  }
-  int b = sms / n_qb, e = sms % n_qb;
-  const int cap = std::max(1, std::min(n_tiles, 8192 / KMAX));
-  if (b >= cap) { b = cap; e = 0; }
-  *base = b;
-  *extra = e;
-  return b + (e ? 1 : 0);
-}
 
 static int ensure_scratch(alise_db* db, int64_t Bp, int splits, cudaStream_t st) {
   if (Bp <= db->bp_cap && splits <= db->splits_cap) return ALISE_OK;
@@ -262,8 +247,15 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   const int n_qb = (int)(Bp / qblk);
   const int n_tiles = (int)((db->size + BN - 1) / BN);
   const int units = two_sm ? sm_count_pred() / 2 : sm_count_pred();
-  int base_g, extra_g;
-  const int groups = choose_groups(n_qb, n_tiles, units, &base_g, &extra_g);
+  // work split (pred_scan.cuh next_seg): G groups per query block, E excess groups cut
+  // into nc chunks of C tiles so every unit scans about the same number of tiles
+  const int G = std::max(1, std::min(n_tiles, (units + n_qb - 1) / n_qb));
+  const int E = std::max(0, n_qb * G - units);
+  const int n_units = std::min(units, n_qb * G);
+  const int glen = n_tiles / G;  // length of group G-1 (the excess groups)
+  const int nc = E ? std::max(1, n_units / E) : 0;
+  const int C = E ? (glen + nc - 1) / nc : 0;
+  const int groups = E ? std::max(G, G - 1 + (glen + C - 1) / C) : G;
   // 2-SM scan with k <= 8: two epilogue warps per TMEM lane quarter, each its own split
   static int halves = -1;
   if (halves < 0) {
@@ -282,8 +274,11 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   a.n_tiles = n_tiles;
   a.n_qb = n_qb;
   a.n_splits = splits;
-  a.base_g = base_g;
-  a.extra_g = extra_g;
+  a.G = G;
+  a.units = n_units;
+  a.E = E;
+  a.nc = nc;
+  a.C = C;
   a.B = (int)B;
   a.Bp = (int)Bp;
   a.k = k;
@@ -301,9 +296,9 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   a.warm = warm;
   // [Bp] shared k-th, then [Bp][KMAX] rank slots (16-byte aligned: Bp % 128 == 0): one memset
   a.gslot = db->gkth + Bp;
-  a.slot_m = (k + base_g * nh - 1) / (base_g * nh);
+  a.slot_m = (k + G * nh - 1) / (G * nh);
   // long groups warm up early in their run: one exchange per tile is enough
-  a.sync_tile = n_tiles / std::max(1, base_g) >= 256 ? 1 : 0;
+  a.sync_tile = n_tiles / G >= 256 ? 1 : 0;
   CK(cudaMemsetAsync(db->gkth, 0, sizeof(uint32_t) * Bp * (1 + KMAX), st));
   static bool attr_set[5] = {false, false, false, false, false};
   const int kt = two_sm ? (k <= 8 ? (nh == 2 ? 4 : 2) : 3) : (k <= 8 ? 0 : 1);
@@ -317,8 +312,7 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
     }
     attr_set[kt] = true;
   }
-  const int work = n_qb * base_g + extra_g;
-  const unsigned grid = two_sm ? (unsigned)(2 * std::min(work, units)) : (unsigned)std::min(work, units);
+  const unsigned grid = two_sm ? (unsigned)(2 * n_units) : (unsigned)n_units;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (db->timing) {
     CK(cudaEventCreate(&e0));
@@ -361,7 +355,7 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   // small batches are latency bound (one DRAM round trip per candidate row), large ones
   // throughput bound (registers / occupancy)
   auto rescore = B <= 512 ? k_rescore<24> : k_rescore<8>;
-  rescore<<<(unsigned)B, 256, 0, st>>>(qblk, nh, base_g, extra_g, (int)Bp, B, k, db->size, db->dim, queries, db->v32,
+  rescore<<<(unsigned)B, 256, 0, st>>>(qblk, nh, a, (int)Bp, B, k, db->size, db->dim, queries, db->v32,
                                        db->lens, db->seqs, db->two_delta, db->cand_s, db->cand_r, db->cand_n,
                                        db->topc, out_sim, out_seq, out_len, out_count, db->need, db->inexact);
   CKL();

@@ -102,9 +102,12 @@ struct ScanArgs {
   int64_t n_rows;    // valid DB rows (slots [0, n_rows))
   int n_tiles;       // ceil(n_rows / BN)
   int n_qb;          // query blocks of 128
-  int n_splits;      // max tile groups per query block (candidate-list slots)
-  int base_g;        // query block qb owns G(qb) = base_g + (qb < extra_g) tile groups;
-  int extra_g;       //   group g of qb scans tiles g, g + G(qb), ...
+  int n_splits;      // max splits per query block (candidate-list slots, see next_seg)
+  int G;             // tile groups per query block: group g scans tiles g, g + G, ...
+  int units;         // persistent CTAs (1-SM) or CTA pairs (2-SM)
+  int E;             // excess groups (see next_seg)
+  int nc;            // chunks per excess group
+  int C;             // tiles per chunk
   int B;             // real query count
   int Bp;            // padded query count
   int k;
@@ -179,6 +182,63 @@ __device__ __forceinline__ int compact_candidates(float* __restrict__ cs, int32_
   return w;
 }
 
+// ---------------------------------------------------------------- work split
+// Every query block has G tile groups (group g = tiles g, g+G, ...), G = ceil(units /
+// n_qb), so n_qb*G - E = units for E < n_qb excess groups: group G-1 of the last E
+// query blocks.  Unit p first scans one whole non-excess group (all units sweep the DB
+// in near lock step: L2 reuse across query blocks), then chunks of the excess groups
+// (nc chunks of C tiles per excess group; chunk c of every excess group covers the same
+// tile positions, so those run in lock step too).  Every unit does about the same number
+// of tiles: with whole groups only, the units of the blocks that get one group fewer
+// would run 1/G longer than the rest.  Each group or chunk is a split (its own candidate
+// list): splits 0..G-1 are the groups, chunk c of a block's excess group is split G-1+c.
+struct WorkSeg {
+  int qb, split, g, pos, count;  // tiles g + (pos + i) * G, i < count
+};
+
+__device__ __forceinline__ int grp_len(int n_tiles, int G, int g) { return n_tiles / G + (g < n_tiles % G ? 1 : 0); }
+
+__device__ __forceinline__ int splits_of_block(const ScanArgs& a, int qb) {
+  if (qb < a.n_qb - a.E) return a.G;
+  const int len = grp_len(a.n_tiles, a.G, a.G - 1);
+  return a.G - 1 + (len + a.C - 1) / a.C;
+}
+
+// next segment of unit p (state starts at 0)
+__device__ __forceinline__ bool next_seg(const ScanArgs& a, int p, int& state, WorkSeg& s) {
+  if (state == 0) {
+    state = 1;
+    const int full = (a.n_qb - a.E) * a.G;
+    if (p < full) {
+      s.qb = p / a.G;
+      s.g = p % a.G;
+    } else {
+      const int p2 = p - full;
+      s.qb = a.n_qb - a.E + p2 / (a.G - 1);
+      s.g = p2 % (a.G - 1);
+    }
+    s.split = s.g;
+    s.pos = 0;
+    s.count = grp_len(a.n_tiles, a.G, s.g);
+    return true;
+  }
+  const int len = grp_len(a.n_tiles, a.G, a.G - 1);
+  for (;;) {
+    const int cid = p + a.units * (state - 1);
+    if (cid >= a.E * a.nc) return false;
+    ++state;
+    const int e = cid / a.nc, c = cid % a.nc;
+    const int pos0 = c * a.C;
+    if (pos0 >= len) continue;
+    s.qb = a.n_qb - a.E + e;
+    s.g = a.G - 1;
+    s.split = a.G - 1 + c;
+    s.pos = pos0;
+    s.count = min(a.C, len - pos0);
+    return true;
+  }
+}
+
 // Per-(query, tile group) state of the scan epilogue (one thread): running top-k of the
 // coarse scores, candidate threshold thr = (lower bound g of the final k-th) - 2*delta,
 // and the candidate buffer.  Any g <= the final k-th keeps the candidate set a superset
@@ -230,6 +290,19 @@ struct QueryScan {
     sbase = g * m;
     dirty = false;
     pref();
+    // a split that starts mid-run (an excess chunk) takes the query's shared bounds now
+    if (gkp) {
+      if (gk) raise(ord_val(gk));
+      uint32_t mn = 0xffffffffu;
+#pragma unroll
+      for (int x = 0; x < KT / 4; ++x) {
+        if (4 * x + 0 < k) mn = min(mn, sv[x].x);
+        if (4 * x + 1 < k) mn = min(mn, sv[x].y);
+        if (4 * x + 2 < k) mn = min(mn, sv[x].z);
+        if (4 * x + 3 < k) mn = min(mn, sv[x].w);
+      }
+      if (mn) raise(ord_val(mn));
+    }
   }
 
   __device__ __forceinline__ void raise(float g) {
@@ -422,8 +495,6 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // work item w -> (qb = w % n_qb, g = w / n_qb); n_work = sum over qb of G(qb)
-  const int n_work = a.n_qb * a.base_g + a.extra_g;
 
   if (warp == 0 && lane == 0) {
     sm100::prefetch_tmap(&tmQ);
@@ -448,10 +519,12 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        const int qb = w % a.n_qb, g = w / a.n_qb;
-        const int G = a.base_g + (qb < a.extra_g ? 1 : 0);
-        for (int t = g; t < a.n_tiles; t += G) {
+      int st = 0;
+      WorkSeg sg;
+      while (next_seg(a, blockIdx.x, st, sg)) {
+        const int qb = sg.qb;
+        for (int u = 0; u < sg.count; ++u) {
+          const int t = sg.g + (sg.pos + u) * a.G;
           for (int kb = 0; kb < a.n_kb; ++kb) {
             sm100::mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -469,10 +542,10 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        const int qb = w % a.n_qb, g = w / a.n_qb;
-        const int G = a.base_g + (qb < a.extra_g ? 1 : 0);
-        for (int t = g; t < a.n_tiles; t += G, ++i) {
+      int st = 0;
+      WorkSeg sg;
+      while (next_seg(a, blockIdx.x, st, sg)) {
+        for (int u = 0; u < sg.count; ++u, ++i) {
           const int acc = i & 1;
           const uint32_t aph = (i >> 1) & 1;
           sm100::mbar_wait(&tempty[acc], aph ^ 1);
@@ -500,20 +573,21 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
     const int tq = quarter * 32 + lane;
     const int k = a.k;
     int i = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-      const int qb = w % a.n_qb, g = w / a.n_qb;
-      const int G = a.base_g + (qb < a.extra_g ? 1 : 0);
-      const int q = qb * BM + tq;
-      const size_t base = ((size_t)g * a.Bp + q);
+    int st = 0;
+    WorkSeg sg;
+    while (next_seg(a, blockIdx.x, st, sg)) {
+      const int q = sg.qb * BM + tq;
+      const size_t base = ((size_t)sg.split * a.Bp + q);
       QueryScan<KT> qs;
-      qs.init(a, q, base, k, g);
-      for (int t = g; t < a.n_tiles; t += G, ++i) {
+      qs.init(a, q, base, k, sg.split);
+      for (int u = 0; u < sg.count; ++u, ++i) {
+        const int t = sg.g + (sg.pos + u) * a.G;
         const int acc = i & 1;
         const uint32_t aph = (i >> 1) & 1;
         sm100::mbar_wait(&tfull[acc], aph);
         sm100::tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-        if (a.warm && t == g && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT, 4>(qs, taddr, k);
+        if (a.warm && u == 0 && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT, 4>(qs, taddr, k);
 #pragma unroll 1
         for (int c2 = 0; c2 < BN / 64; ++c2) {
           // two TMEM loads in flight per wait
@@ -574,8 +648,7 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_ctarank();
-  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-  const int n_work = a.n_qb * a.base_g + a.extra_g;  // n_qb counts query pairs (256 queries)
+  const int pair = blockIdx.x >> 1;
 
   if (warp == 0 && lane == 0) {
     sm100::prefetch_tmap(&tmQ);
@@ -600,10 +673,12 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = pair; w < n_work; w += n_pairs) {
-        const int qp = w % a.n_qb, g = w / a.n_qb;
-        const int G = a.base_g + (qp < a.extra_g ? 1 : 0);
-        for (int t = g; t < a.n_tiles; t += G) {
+      int st = 0;
+      WorkSeg sg;
+      while (next_seg(a, pair, st, sg)) {
+        const int qp = sg.qb;
+        for (int u = 0; u < sg.count; ++u) {
+          const int t = sg.g + (sg.pos + u) * a.G;
           for (int kb = 0; kb < a.n_kb; ++kb) {
             sm100::mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * STAGE2_BYTES;
@@ -622,10 +697,10 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
-      for (int w = pair; w < n_work; w += n_pairs) {
-        const int qp = w % a.n_qb, g = w / a.n_qb;
-        const int G = a.base_g + (qp < a.extra_g ? 1 : 0);
-        for (int t = g; t < a.n_tiles; t += G, ++i) {
+      int st = 0;
+      WorkSeg sg;
+      while (next_seg(a, pair, st, sg)) {
+        for (int u = 0; u < sg.count; ++u, ++i) {
           const int acc = i & 1;
           const uint32_t aph = (i >> 1) & 1;
           sm100::mbar_wait(&tempty[acc], aph ^ 1);
@@ -659,22 +734,23 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
     const uint32_t tempty_leader0 = sm100::mapa(sm100::smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = sm100::mapa(sm100::smem_u32(&tempty[1]), 0);
     int i = 0;
-    for (int w = pair; w < n_work; w += n_pairs) {
-      const int qp = w % a.n_qb, g = w / a.n_qb;
-      const int G = a.base_g + (qp < a.extra_g ? 1 : 0);
-      const int q = qp * 2 * BM + (int)rank * BM + tq;
-      const int gs = g * NH + half;
+    int st = 0;
+    WorkSeg sg;
+    while (next_seg(a, pair, st, sg)) {
+      const int q = sg.qb * 2 * BM + (int)rank * BM + tq;
+      const int gs = sg.split * NH + half;
       const size_t base = ((size_t)gs * a.Bp + q);
       QueryScan<KT> qs;
       qs.init(a, q, base, k, gs);
-      for (int t = g; t < a.n_tiles; t += G, ++i) {
+      for (int u = 0; u < sg.count; ++u, ++i) {
+        const int t = sg.g + (sg.pos + u) * a.G;
         const int acc = i & 1;
         const uint32_t aph = (i >> 1) & 1;
         sm100::mbar_wait(&tfull[acc], aph);
         sm100::tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * (BN / NH);
         const int cbase = t * BN + half * (BN / NH);
-        if (a.warm && t == g && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT, NC2>(qs, taddr, k);
+        if (a.warm && u == 0 && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT, NC2>(qs, taddr, k);
 #pragma unroll 1
         for (int c2 = 0; c2 < NC2; ++c2) {
           // two TMEM loads in flight per wait
@@ -904,7 +980,7 @@ __device__ __forceinline__ int nw_last(unsigned bd) { return (int)(bd >> 5) - 1;
 // exact rescoring, (-sim, seq) order.  Block = 256 threads.
 template <int U>
 __global__ void __launch_bounds__(256)
-k_rescore(int qblk, int smul, int base_g, int extra_g, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
+k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
           const float* __restrict__ v32, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
           const float* __restrict__ two_delta, const float* __restrict__ cand_s, const int32_t* __restrict__ cand_r,
           const int32_t* __restrict__ cand_n, const float* __restrict__ topc, double* __restrict__ out_sim,
@@ -923,7 +999,7 @@ k_rescore(int qblk, int smul, int base_g, int extra_g, int Bp, int64_t B, int k,
   __shared__ int s_flag;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int n_splits = smul * (base_g + ((q / qblk) < extra_g ? 1 : 0));
+  const int n_splits = smul * splits_of_block(wa, (int)(q / qblk));
   const int64_t kk = k < n_rows ? k : n_rows;
   const float NEG = -__int_as_float(0x7f800000);
 #ifdef ALISE_RESCORE_TIMING

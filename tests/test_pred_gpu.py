@@ -276,7 +276,7 @@ def test_binary_snapshot_round_trip(pr, tmp_path):
     assert torch.equal(a[1] - 200, b[1])  # re-added from seq 0 in the same order
 
 
-@pytest.mark.parametrize("B", [1, 256, 700])
+@pytest.mark.parametrize("B", [1, 256, 700, 1100, 2000])
 def test_shared_thresholds_with_ties_across_tile_groups(pr, B):
     """The scan's tile groups share their running k-th (atomic max per query) and keep
     only values above it in their top lists; exact ties of the k-th spread over many
