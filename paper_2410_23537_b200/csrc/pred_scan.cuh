@@ -244,8 +244,8 @@ __device__ __forceinline__ bool next_seg(const ScanArgs& a, int p, int& state, W
 // and the candidate buffer.  Any g <= the final k-th keeps the candidate set a superset
 // (rows below g - 2*delta cannot be in the exact top-k).  Each group sees only 1/G of
 // the DB, so g is raised faster than by the group's own k-th:
-//  * warm start: on its first full tile a group takes the k-th largest of the tile's
-//    eight 32-row chunk maxima (k distinct rows reach it; k <= 8);
+//  * warm start: on its first full tile a split takes the k-th largest of the tile's
+//    32 maxima of 8 consecutive rows (k distinct rows reach it; k <= 32);
 //  * gkth: the largest bound any group of the query has published, exchanged once per
 //    64 scores, or per tile when groups are long (loads issued one exchange ahead);
 //  * rank slots: group g publishes its m best values (m = ceil(k / G)) into slots
@@ -319,14 +319,9 @@ struct QueryScan {
     }
   }
 
-  // warm start from the chunk maxima of the group's first full tile
-  __device__ __forceinline__ void warm(const float (&cm)[8], int k) {
-    if (!gkp || k > 8) return;
-    float tk[KT];
-    topk_init<KT>(tk, k);
-#pragma unroll
-    for (int x = 0; x < 8; ++x) topk_insert<KT>(tk, cm[x]);
-    const float g = tk[KT - 1];
+  // warm start: a bound from the split's first full tile (warm_from_tile)
+  __device__ __forceinline__ void warm(float g) {
+    if (!gkp || !(g > -__int_as_float(0x7f800000))) return;
     raise(g);
     publish(g);
   }
@@ -404,47 +399,31 @@ __device__ __forceinline__ float max32(const float (&v)[32]) {
   return fmaxf(fmaxf(u0, u1), fmaxf(u2, u3));
 }
 
-// First full tile of a group: eight maxima over this thread's columns of the tile (TMEM
-// columns [taddr, taddr + 64*NC2) of its lane: 32-value chunks for NC2 = 4, 16-value
-// halves for NC2 = 2) give the warm-start bound.
-template <int KT, int NC2>
-__device__ __forceinline__ void warm_from_tile(QueryScan<KT>& qs, uint32_t taddr, int k) {
-  float cm[8];
+// First full tile of a split: the k-th largest of the 32 maxima of 8 consecutive
+// columns over the whole 256-column tile of this thread's query (TMEM lane; both
+// epilogue halves of a lane quarter may read all columns) is the warm-start bound:
+// k distinct rows reach it (k <= 32).
+template <int KT>
+__device__ __forceinline__ void warm_from_tile(QueryScan<KT>& qs, uint32_t tile_addr, int k) {
+  float tk[KT];
+  topk_init<KT>(tk, k);
 #pragma unroll 1
-  for (int c2 = 0; c2 < NC2; ++c2) {
+  for (int c2 = 0; c2 < BN / 64; ++c2) {
     uint32_t r0[32], r1[32];
-    sm100::tmem_ld32_async(taddr + c2 * 64, r0);
-    sm100::tmem_ld32_async(taddr + c2 * 64 + 32, r1);
+    sm100::tmem_ld32_async(tile_addr + c2 * 64, r0);
+    sm100::tmem_ld32_async(tile_addr + c2 * 64 + 32, r1);
     sm100::tmem_wait_ld();
-    float v0[32], v1[32];
 #pragma unroll
-    for (int x = 0; x < 32; ++x) {
-      v0[x] = __uint_as_float(r0[x]);
-      v1[x] = __uint_as_float(r1[x]);
+    for (int x = 0; x < 8; ++x) {
+      const uint32_t* r = x < 4 ? r0 : r1;
+      const int o = (x & 3) * 8;
+      float m = __uint_as_float(r[o]);
+#pragma unroll
+      for (int y = 1; y < 8; ++y) m = fmaxf(m, __uint_as_float(r[o + y]));
+      if (m > tk[KT - 1]) topk_insert<KT>(tk, m);
     }
-    float mm[4];
-    if (NC2 == 4) {
-      mm[0] = max32(v0);
-      mm[1] = max32(v1);
-    } else {
-      mm[0] = mm[1] = mm[2] = mm[3] = -__int_as_float(0x7f800000);
-#pragma unroll
-      for (int x = 0; x < 16; ++x) {
-        mm[0] = fmaxf(mm[0], v0[x]);
-        mm[1] = fmaxf(mm[1], v0[16 + x]);
-        mm[2] = fmaxf(mm[2], v1[x]);
-        mm[3] = fmaxf(mm[3], v1[16 + x]);
-      }
-    }
-    constexpr int PER = 8 / NC2;
-#pragma unroll
-    for (int c = 0; c < NC2; ++c)
-      if (c == c2) {
-#pragma unroll
-        for (int x = 0; x < PER; ++x) cm[PER * c + x] = mm[x];
-      }
   }
-  qs.warm(cm, k);
+  qs.warm(tk[KT - 1]);
 }
 
 // Scores of one 32-row chunk (v[x] = row rbase + x): one max-reduction and one
@@ -587,7 +566,7 @@ k_scan(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
         sm100::mbar_wait(&tfull[acc], aph);
         sm100::tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-        if (a.warm && u == 0 && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT, 4>(qs, taddr, k);
+        if (a.warm && u == 0 && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT>(qs, taddr, k);
 #pragma unroll 1
         for (int c2 = 0; c2 < BN / 64; ++c2) {
           // two TMEM loads in flight per wait
@@ -750,7 +729,8 @@ k_scan2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtenso
         sm100::tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * (BN / NH);
         const int cbase = t * BN + half * (BN / NH);
-        if (a.warm && u == 0 && (int64_t)(t + 1) * BN <= a.n_rows) warm_from_tile<KT, NC2>(qs, taddr, k);
+        if (a.warm && u == 0 && (int64_t)(t + 1) * BN <= a.n_rows)
+          warm_from_tile<KT>(qs, taddr - half * (BN / NH), k);
 #pragma unroll 1
         for (int c2 = 0; c2 < NC2; ++c2) {
           // two TMEM loads in flight per wait
