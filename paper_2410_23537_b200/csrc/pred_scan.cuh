@@ -988,9 +988,17 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   // 1) stage the splits' top lists and candidate counts (all loads in flight at once)
   const int m = n_splits * k;
   if (tid == 0) { s_n = 0; s_flag = 0; }
-  for (int i = tid; i < m; i += blockDim.x) {
-    const int sp = i / k, j = i - sp * k;
-    s_top[i] = __ldg(topc + ((size_t)sp * Bp + q) * KMAX + j);
+  for (int i0 = tid; i0 < m; i0 += 8 * blockDim.x) {
+    float tv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {  // 8 loads in flight per thread
+      const int i = i0 + u * (int)blockDim.x;
+      const int sp = i / k, j = i - sp * k;
+      tv[u] = i < m ? __ldg(topc + ((size_t)sp * Bp + q) * KMAX + j) : NEG;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + u * (int)blockDim.x < m) s_top[i0 + u * blockDim.x] = tv[u];
   }
   for (int sp = tid; sp < n_splits; sp += blockDim.x) {
     const int cnt = cand_n[(size_t)sp * Bp + q];
@@ -1005,7 +1013,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
     const int nw = blockDim.x >> 5;
     const int per = (m + nw - 1) / nw;
     const int lo = warp * per, hi = min(m, lo + per);
-    for (int64_t round = 0; round < kk; ++round) {
+    for (int round = 0; round < (int)kk; ++round) {
       float bv = NEG;
       int bi = -1;
       for (int i = lo + lane; i < hi; i += 32) {
@@ -1019,7 +1027,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
         if (v2 > bv || (v2 == bv && i2 > bi)) { bv = v2; bi = i2; }
       }
       if (lane == 0) {
-        s_wk[warp * KMAX + round] = bv;
+        s_wk[warp * (int)kk + round] = bv;
         if (bi >= 0) s_top[bi] = NEG;
       }
       __syncwarp();
@@ -1044,11 +1052,11 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   if (warp == 0) {
     const int mw = (int)(blockDim.x >> 5) * (int)kk;
     float kth = NEG;
-    for (int64_t round = 0; round < kk; ++round) {
+    for (int round = 0; round < (int)kk; ++round) {
       float bv = NEG;
       int bi = -1;
       for (int i = lane; i < mw; i += 32) {
-        const float v = s_wk[(i / kk) * KMAX + i % kk];
+        const float v = s_wk[i];
         if (v > bv) { bv = v; bi = i; }
       }
 #pragma unroll
@@ -1057,7 +1065,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
         const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
         if (v2 > bv || (v2 == bv && i2 > bi)) { bv = v2; bi = i2; }
       }
-      if (lane == 0 && bi >= 0) s_wk[(bi / kk) * KMAX + bi % kk] = NEG;
+      if (lane == 0 && bi >= 0) s_wk[bi] = NEG;
       __syncwarp();
       kth = bv;
     }
