@@ -977,6 +977,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   __shared__ float s_kth;
   __shared__ int s_n;
   __shared__ int s_flag;
+  __shared__ int s_nt;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int n_splits = smul * splits_of_block(wa, (int)(q / qblk));
@@ -985,9 +986,21 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
 #ifdef ALISE_RESCORE_TIMING
   const long long T0 = clock64();
 #endif
-  // 1) stage the splits' top lists and candidate counts (all loads in flight at once)
+  // 1) stage the splits' top lists and candidate counts (all loads in flight at once).
+  //    The scan leaves a lower bound L of the final coarse k-th (shared k-th, rank
+  //    slots) such that the union of the lists holds k values >= L, so only list values
+  //    >= L can decide the k-th: they are compacted (usually about k of the n_splits*k)
   const int m = n_splits * k;
-  if (tid == 0) { s_n = 0; s_flag = 0; }
+  float L = NEG;
+  {
+    const uint32_t g0 = wa.gkth[q];
+    if (g0) L = ord_val(g0);
+    uint32_t mn = 0xffffffffu;
+    for (int x = 0; x < k; ++x) mn = min(mn, wa.gslot[(size_t)q * KMAX + x]);
+    if (mn) L = fmaxf(L, ord_val(mn));
+  }
+  if (tid == 0) { s_n = 0; s_flag = 0; s_nt = 0; }
+  __syncthreads();
   for (int i0 = tid; i0 < m; i0 += 8 * blockDim.x) {
     float tv[8];
 #pragma unroll
@@ -998,7 +1011,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (i0 + u * (int)blockDim.x < m) s_top[i0 + u * blockDim.x] = tv[u];
+      if (i0 + u * (int)blockDim.x < m && tv[u] >= L) s_top[atomicAdd(&s_nt, 1)] = tv[u];
   }
   for (int sp = tid; sp < n_splits; sp += blockDim.x) {
     const int cnt = cand_n[(size_t)sp * Bp + q];
@@ -1009,10 +1022,12 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   // 2) kk-th largest coarse score over the lists: each warp takes the kk largest of its
   //    slice (kk rounds of warp argmax, the winner's slot cleared), warp 0 repeats that
   //    over the warps' results; warp 7 meanwhile scans the counts into offsets
-  {
+  const int mt = s_nt;             // compacted list values
+  const bool one_warp = mt <= 256;  // few values: warp 0 selects directly
+  if (!one_warp) {
     const int nw = blockDim.x >> 5;
-    const int per = (m + nw - 1) / nw;
-    const int lo = warp * per, hi = min(m, lo + per);
+    const int per = (mt + nw - 1) / nw;
+    const int lo = warp * per, hi = min(mt, lo + per);
     for (int round = 0; round < (int)kk; ++round) {
       float bv = NEG;
       int bi = -1;
@@ -1050,13 +1065,14 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   }
   __syncthreads();
   if (warp == 0) {
-    const int mw = (int)(blockDim.x >> 5) * (int)kk;
+    float* src = one_warp ? s_top : s_wk;
+    const int mw = one_warp ? mt : (int)(blockDim.x >> 5) * (int)kk;
     float kth = NEG;
     for (int round = 0; round < (int)kk; ++round) {
       float bv = NEG;
       int bi = -1;
       for (int i = lane; i < mw; i += 32) {
-        const float v = s_wk[i];
+        const float v = src[i];
         if (v > bv) { bv = v; bi = i; }
       }
 #pragma unroll
@@ -1065,7 +1081,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
         const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
         if (v2 > bv || (v2 == bv && i2 > bi)) { bv = v2; bi = i2; }
       }
-      if (lane == 0 && bi >= 0) s_wk[bi] = NEG;
+      if (lane == 0 && bi >= 0) src[bi] = NEG;
       __syncwarp();
       kth = bv;
     }

@@ -1,0 +1,3 @@
+ALISE_LIB=variants/lib_rtime.so timeout 600 python tools/pred_bench.py 1000000 256 2>&1 | grep "rescore q=" | tail -2
+timeout 900 python -m pytest tests/test_pred_gpu.py tests/test_sharding.py -q -x 2>&1 | tail -2
+timeout 600 python tools/pred_kernels.py 1000000 4096,1024,256,1 2>&1 | grep '^{' | cut -c1-200
