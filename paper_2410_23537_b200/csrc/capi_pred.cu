@@ -355,7 +355,13 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   // small batches are latency bound (one DRAM round trip per candidate row), large ones
   // throughput bound (registers / occupancy)
   auto rescore = B <= 512 ? k_rescore<24> : k_rescore<8>;
-  rescore<<<(unsigned)B, 256, 0, st>>>(qblk, nh, a, (int)Bp, B, k, db->size, db->dim, queries, db->v32,
+  static int rthreads = -1;
+  if (rthreads < 0) {
+    const char* e = getenv("ALISE_RESCORE_THREADS");
+    rthreads = e ? atoi(e) : 128;
+  }
+  // large batches: smaller blocks keep more queries in flight per SM
+  rescore<<<(unsigned)B, B <= 512 ? 256 : rthreads, 0, st>>>(qblk, nh, a, (int)Bp, B, k, db->size, db->dim, queries, db->v32,
                                        db->lens, db->seqs, db->two_delta, db->cand_s, db->cand_r, db->cand_n,
                                        db->topc, out_sim, out_seq, out_len, out_count, db->need, db->inexact);
   CKL();

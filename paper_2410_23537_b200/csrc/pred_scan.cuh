@@ -968,7 +968,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
           int32_t* __restrict__ need_exhaustive, unsigned int* __restrict__ inexact_count) {
   const int64_t q = blockIdx.x;
   if (q >= B) return;
-  __shared__ float s_top[8192];  // the splits' top lists (host: n_splits * k <= 8192)
+  __shared__ float s_top[4096];  // list values >= the bound (more: exhaustive path)
   __shared__ int s_off[513];     // n_splits <= 512 (host)
   __shared__ int s_rows[MAXC];
   __shared__ double s_sim[MAXC];
@@ -1011,7 +1011,10 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (i0 + u * (int)blockDim.x < m && tv[u] >= L) s_top[atomicAdd(&s_nt, 1)] = tv[u];
+      if (i0 + u * (int)blockDim.x < m && tv[u] >= L) {
+        const int at = atomicAdd(&s_nt, 1);
+        if (at < 4096) s_top[at] = tv[u];
+      }
   }
   for (int sp = tid; sp < n_splits; sp += blockDim.x) {
     const int cnt = cand_n[(size_t)sp * Bp + q];
@@ -1019,6 +1022,10 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
     if (cnt < 0) s_flag = 1;
   }
   __syncthreads();
+  if (s_nt > 4096) {  // thousands of list values tie at the bound: exhaustive path
+    if (tid == 0) need_exhaustive[q] = 1;
+    return;
+  }
   // 2) kk-th largest coarse score over the lists: each warp takes the kk largest of its
   //    slice (kk rounds of warp argmax, the winner's slot cleared), warp 0 repeats that
   //    over the warps' results; warp 7 meanwhile scans the counts into offsets
