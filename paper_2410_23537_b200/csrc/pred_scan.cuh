@@ -845,7 +845,41 @@ __device__ double warp_exact_dot(const float* __restrict__ a, const float* __res
 constexpr int SUPER_L = 10;
 constexpr int SUPER_BASE = -320;
 
-// Add the exact product a*b (fp32 x fp32) into a 640-bit two's complement accumulator.
+// Add the exact product a*b (fp32 x fp32) into a 640-bit two's complement accumulator:
+// the product is spread over the ten limbs with static selects and added (or
+// subtracted) with one carry chain, so the accumulator stays in registers.
+__device__ __forceinline__ void add640(uint64_t (&a)[SUPER_L], const uint64_t (&b)[SUPER_L]) {
+  asm("add.cc.u64 %0, %0, %10;\n\t"
+      "addc.cc.u64 %1, %1, %11;\n\t"
+      "addc.cc.u64 %2, %2, %12;\n\t"
+      "addc.cc.u64 %3, %3, %13;\n\t"
+      "addc.cc.u64 %4, %4, %14;\n\t"
+      "addc.cc.u64 %5, %5, %15;\n\t"
+      "addc.cc.u64 %6, %6, %16;\n\t"
+      "addc.cc.u64 %7, %7, %17;\n\t"
+      "addc.cc.u64 %8, %8, %18;\n\t"
+      "addc.u64 %9, %9, %19;"
+      : "+l"(a[0]), "+l"(a[1]), "+l"(a[2]), "+l"(a[3]), "+l"(a[4]), "+l"(a[5]), "+l"(a[6]), "+l"(a[7]),
+        "+l"(a[8]), "+l"(a[9])
+      : "l"(b[0]), "l"(b[1]), "l"(b[2]), "l"(b[3]), "l"(b[4]), "l"(b[5]), "l"(b[6]), "l"(b[7]), "l"(b[8]),
+        "l"(b[9]));
+}
+__device__ __forceinline__ void sub640(uint64_t (&a)[SUPER_L], const uint64_t (&b)[SUPER_L]) {
+  asm("sub.cc.u64 %0, %0, %10;\n\t"
+      "subc.cc.u64 %1, %1, %11;\n\t"
+      "subc.cc.u64 %2, %2, %12;\n\t"
+      "subc.cc.u64 %3, %3, %13;\n\t"
+      "subc.cc.u64 %4, %4, %14;\n\t"
+      "subc.cc.u64 %5, %5, %15;\n\t"
+      "subc.cc.u64 %6, %6, %16;\n\t"
+      "subc.cc.u64 %7, %7, %17;\n\t"
+      "subc.cc.u64 %8, %8, %18;\n\t"
+      "subc.u64 %9, %9, %19;"
+      : "+l"(a[0]), "+l"(a[1]), "+l"(a[2]), "+l"(a[3]), "+l"(a[4]), "+l"(a[5]), "+l"(a[6]), "+l"(a[7]),
+        "+l"(a[8]), "+l"(a[9])
+      : "l"(b[0]), "l"(b[1]), "l"(b[2]), "l"(b[3]), "l"(b[4]), "l"(b[5]), "l"(b[6]), "l"(b[7]), "l"(b[8]),
+        "l"(b[9]));
+}
 __device__ __forceinline__ void super_add(uint64_t (&acc)[SUPER_L], float fa, float fb) {
   const uint32_t bx = __float_as_uint(fa), by = __float_as_uint(fb);
   uint32_t mx = bx & 0x7fffffu, my = by & 0x7fffffu;
@@ -854,32 +888,15 @@ __device__ __forceinline__ void super_add(uint64_t (&acc)[SUPER_L], float fa, fl
   if (ex) mx |= 0x800000u; else ex = 1;
   if (ey) my |= 0x800000u; else ey = 1;
   const uint64_t m = (uint64_t)mx * my;                // < 2^48
-  const int e = (ex - 150) + (ey - 150) - SUPER_BASE;  // >= 22
+  const int e = (ex - 150) + (ey - 150) - SUPER_BASE;  // >= 22, li <= 8 for finite inputs
   const int li = e >> 6, sh = e & 63;
   const uint64_t lo = m << sh;
   const uint64_t hi = sh ? (m >> (64 - sh)) : 0;
-  if (((bx ^ by) >> 31) == 0) {
-    uint64_t s0 = acc[li] + lo;
-    uint64_t carry = s0 < lo;
-    acc[li] = s0;
-    uint64_t s1 = acc[li + 1] + hi;
-    uint64_t c2 = s1 < hi;
-    s1 += carry;
-    c2 |= (s1 < carry);
-    acc[li + 1] = s1;
-    for (int j = li + 2; j < SUPER_L && c2; ++j) { acc[j] += 1; c2 = acc[j] == 0; }
-  } else {
-    const uint64_t d0 = acc[li] - lo;
-    uint64_t borrow = acc[li] < lo;
-    acc[li] = d0;
-    const uint64_t t1 = acc[li + 1];
-    uint64_t d1 = t1 - hi;
-    uint64_t b2 = t1 < hi;
-    b2 |= (d1 < borrow);
-    d1 -= borrow;
-    acc[li + 1] = d1;
-    for (int j = li + 2; j < SUPER_L && b2; ++j) { b2 = acc[j] == 0; acc[j] -= 1; }
-  }
+  uint64_t b[SUPER_L];
+#pragma unroll
+  for (int j = 0; j < SUPER_L; ++j) b[j] = j == li ? lo : (j == li + 1 ? hi : 0ull);
+  if (((bx ^ by) >> 31) == 0) add640(acc, b);
+  else sub640(acc, b);
 }
 
 // Round a 640-bit two's complement fixed-point value (LSB 2^-320) to float64 (RN-even).
@@ -898,8 +915,17 @@ __device__ double super_round(uint64_t (&acc)[SUPER_L]) {
   if (top < 0) return 0.0;
   const int msb = top * 64 + (63 - __clzll(acc[top]));
   auto bit = [&](int p) -> uint64_t { return p < 0 ? 0ull : (acc[p >> 6] >> (p & 63)) & 1ull; };
-  uint64_t mant = 0;
-  for (int p = msb; p > msb - 53; --p) mant = (mant << 1) | bit(p);
+  // the 53 bits [msb-52, msb] span at most two limbs
+  uint64_t mant;
+  const int w = msb - 52;
+  if (w < 0) {
+    mant = acc[0] << (-w);
+  } else {
+    const int li = w >> 6, sh = w & 63;
+    mant = acc[li] >> sh;
+    if (sh && li + 1 < L) mant |= acc[li + 1] << (64 - sh);
+  }
+  mant &= (1ull << 53) - 1;
   const uint64_t guard = bit(msb - 53);
   bool sticky = false;
   const int sp = msb - 54;  // bits [0, sp] are sticky
@@ -940,16 +966,10 @@ __device__ __noinline__ double warp_exact_dot_super(const float* __restrict__ a,
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    uint64_t c = 0;
+    uint64_t other[SUPER_L];
 #pragma unroll
-    for (int i = 0; i < SUPER_L; ++i) {
-      const uint64_t other = __shfl_xor_sync(0xffffffffu, acc[i], o);
-      const uint64_t s1 = acc[i] + other;
-      const uint64_t c1 = s1 < other;
-      const uint64_t s2 = s1 + c;
-      c = c1 | (s2 < c);
-      acc[i] = s2;
-    }
+    for (int i = 0; i < SUPER_L; ++i) other[i] = __shfl_xor_sync(0xffffffffu, acc[i], o);
+    add640(acc, other);
   }
   return super_round(acc);
 }
@@ -1170,7 +1190,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   }
   if (tid == 0) out_count[q] = (int32_t)(n < kk ? n : kk);
 #ifdef ALISE_RESCORE_TIMING
-  if (tid == 0 && q < 4)
+  if (tid == 0 && (q < 4 || T3 - T2 > 40000))
     printf("[rescore q=%lld] splits=%d total=%d n=%d cycles: select+counts %lld gather %lld dots %lld rank %lld\n",
            (long long)q, n_splits, total, n, T1 - T0, T2 - T1, T3 - T2, clock64() - T3);
 #endif

@@ -340,3 +340,25 @@ def test_scan_bounds_many_groups(pr, B, k, negative):
         Q[: B // 2] = db[g.integers(0, n, size=B // 2)] + 0.05 * g.standard_normal((B // 2, d)).astype(np.float32)
     Q /= np.linalg.norm(Q, axis=1, keepdims=True)
     check_batch(pr, db, lens, Q.astype(np.float32), k)
+
+
+def test_midpoint_ties_take_the_superaccumulator(pr):
+    """Exact dot products at a float64 rounding midpoint (1 + 2^-53: the double-double
+    certificate cannot decide) are resolved by the 640-bit superaccumulator and must
+    round to even exactly like the oracle's fsum."""
+    g = np.random.default_rng(77)
+    n, d = 3000, 64
+    db = (g.standard_normal((n, d)) / 16).astype(np.float32)
+    crafted = np.arange(100, 3000, 300)
+    for j, r in enumerate(crafted):
+        db[r] = 0.0
+        db[r, 0] = 1.0
+        db[r, 1] = 1.0 + j  # dot = 1 + (1 + j) * 2^-53: midpoints for even (1 + j)
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = np.zeros((3, d), np.float32)
+    Q[:, 0] = 1.0
+    Q[:, 1] = np.float32(2.0 ** -53)
+    Q[1, 2] = np.float32(2.0 ** -30)
+    Q[2] = -Q[2]
+    store = check_batch(pr, db, lens, Q, 8)
+    assert store.inexact_count() > 0
