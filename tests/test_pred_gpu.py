@@ -362,3 +362,17 @@ def test_midpoint_ties_take_the_superaccumulator(pr):
     Q[2] = -Q[2]
     store = check_batch(pr, db, lens, Q, 8)
     assert store.inexact_count() > 0
+
+
+def test_more_query_blocks_than_units(pr):
+    """B = 19200 on the 2-SM scan: 75 query blocks of 256 for 74 CTA pairs, so every
+    block has one tile group and the last one is scanned in chunks by all units."""
+    g = np.random.default_rng(5)
+    n, d, B = 3000, 32, 19200
+    db = g.standard_normal((n, d)).astype(np.float32)
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = g.standard_normal((B, d)).astype(np.float32)
+    Q[::3] = db[g.integers(0, n, size=Q[::3].shape[0])] + 0.05 * g.standard_normal((Q[::3].shape[0], d)).astype(np.float32)
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    check_batch(pr, db, lens, Q.astype(np.float32), 8)
