@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--mode", default="staged", choices=["staged", "zerocopy"])
     ap.add_argument("--host-slabs", type=int, default=8)
     ap.add_argument("--lag", type=int, default=1, help="upload job j-lag while offloading job j")
-    ap.add_argument("--planes-per-chunk", type=int, default=0, help="transfer chunk (0: 128 MiB of codes)")
+    ap.add_argument("--planes-per-chunk", type=int, default=0, help="transfer chunk (0: 512 MiB of codes)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

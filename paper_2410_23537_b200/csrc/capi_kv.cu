@@ -387,7 +387,16 @@ static int geom(const alise_kv_desc* d, KvGeom* g) {
   int64_t ppc = d->planes_per_chunk;
   // default transfer chunk: 128 MiB of codes (4 quantize launches per 1 GiB fp16 job at INT8:
   // long enough that a launch's tail is small, short enough that the first copy starts early)
-  if (ppc <= 0) ppc = std::max<int64_t>(1, (int64_t(128) << 20) / g->code_bytes_pp);
+  // default transfer chunk: 512 MiB of codes (a whole 1 GiB fp16 C2 job at INT8).  The
+  // host link gates every chunk launch, and a larger launch amortises its ramp on an
+  // idle GPU (C2 in-step quantize: 3.2 / 4.2 / 4.8 TB/s at 128 / 256 / 512 MiB); the
+  // staging ring holds kSlots chunks per direction
+  static int64_t chunk_mib = -1;
+  if (chunk_mib < 0) {
+    const char* e = getenv("ALISE_CHUNK_MIB");
+    chunk_mib = e ? std::max(1, atoi(e)) : 512;
+  }
+  if (ppc <= 0) ppc = std::max<int64_t>(1, (chunk_mib << 20) / g->code_bytes_pp);
   g->ppc = std::min(ppc, g->planes);
   g->n_chunks = (g->planes + g->ppc - 1) / g->ppc;
   g->rec_bytes = g->rec(g->ppc);

@@ -12,7 +12,8 @@ from paper_2410_23537_b200 import kvmanager as km  # noqa: E402
 from paper_2410_23537_b200 import synthetic  # noqa: E402
 
 J, H = 8, 8
-lay = km.KVLayout(32, 2048, 4096, 128, kind="rows", group=128, bits=8)
+PPC = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # planes per transfer chunk (0: default)
+lay = km.KVLayout(32, 2048, 4096, 128, kind="rows", group=128, bits=8, planes_per_chunk=PPC)
 geo = lay.geometry()
 pool = km.HostSlabPool(H * ((geo["slab_bytes"] + 255) // 256 * 256))
 slabs = [pool.alloc(geo["slab_bytes"]) for _ in range(H)]
@@ -41,7 +42,7 @@ for mode in ("offload_only", "offload_with_upload", "offload_only_keepalive"):
             torch.cuda.synchronize()
     eng.set_timing(False)
     qms, qn, dms, dn = eng.kernel_stats()
-    chunk_bytes = 406847488.0
+    chunk_bytes = 406847488.0 * (PPC / 16 if PPC else 1)
     out[mode] = {"quant_launch_ms": qms / max(qn, 1), "quant_GBs": chunk_bytes / (qms / max(qn, 1)) / 1e6,
                  "launches": qn, "dequant_launch_ms": dms / max(dn, 1) if dn else None}
 print(json.dumps(out))
