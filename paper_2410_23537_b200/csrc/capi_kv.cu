@@ -606,8 +606,17 @@ static int sw_release_rings(alise_swapper* sw) {
   return ALISE_OK;
 }
 
+// Staging buffers grow geometrically (at least doubling, 2 MiB granularity): a growth
+// synchronises the device, so a stream of jobs of increasing size (C5 replay) must not
+// trigger one per job.
+static int64_t grow_to(int64_t need, int64_t have) {
+  const int64_t g = std::max(need, 2 * have);
+  return (g + (2 << 20) - 1) / (2 << 20) * (2 << 20);
+}
+
 static int sw_ensure(alise_swapper* sw, int64_t slot_bytes, int64_t ws_bytes) {
   if (sw->mode == ALISE_SWAP_STAGED && slot_bytes > sw->slot_bytes) {
+    slot_bytes = grow_to(slot_bytes, sw->slot_bytes);
     CK(cudaStreamSynchronize(sw->s_out));
     CK(cudaStreamSynchronize(sw->s_in));
     CK(cudaDeviceSynchronize());
@@ -620,6 +629,7 @@ static int sw_ensure(alise_swapper* sw, int64_t slot_bytes, int64_t ws_bytes) {
     sw->slot_bytes = slot_bytes;
   }
   if (ws_bytes > sw->ws_bytes) {
+    ws_bytes = grow_to(ws_bytes, sw->ws_bytes);
     CK(cudaDeviceSynchronize());
     if (sw->ws) CK(cudaFree(sw->ws));
     CK(cudaMalloc(&sw->ws, ws_bytes));
@@ -630,6 +640,7 @@ static int sw_ensure(alise_swapper* sw, int64_t slot_bytes, int64_t ws_bytes) {
 
 static int sw_ensure_pws(alise_swapper* sw, int64_t bytes) {
   if (bytes <= sw->pws_bytes) return ALISE_OK;
+  bytes = grow_to(bytes, sw->pws_bytes);
   CK(cudaDeviceSynchronize());
   for (int i = 0; i < kSlots; ++i) {
     if (sw->pws[i]) CK(cudaFree(sw->pws[i]));
