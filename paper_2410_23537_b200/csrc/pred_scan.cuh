@@ -1158,7 +1158,14 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
     if (tid == 0) need_exhaustive[q] = 1;
     return;
   }
-  // 4) exact float64 scores, one warp per candidate
+  // 4) exact float64 scores, one warp per candidate.  The warp first prefetches all of
+  //    its candidate rows into L2 (random DB rows: one DRAM round trip for all of them
+  //    instead of one per candidate)
+  for (int c = warp; c < n; c += blockDim.x >> 5) {
+    const char* rp = reinterpret_cast<const char*>(v32 + (size_t)s_rows[c] * dim);
+    for (int64_t off = (int64_t)lane * 128; off < dim * 4; off += 32 * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + off));
+  }
   for (int c = warp; c < n; c += blockDim.x >> 5) {
     const int row = s_rows[c];
     bool ok;
