@@ -406,7 +406,7 @@ static int geom(const alise_kv_desc* d, KvGeom* g) {
 
 extern "C" int alise_kv_layout(const alise_kv_desc* d, int64_t* slab_bytes, int64_t* rows,
                                int64_t* chunk_bytes, int64_t* n_chunks) {
-  KvGeom g;
+  KvGeom g{};
   int st = geom(d, &g);
   if (st) return st;
   if (slab_bytes) *slab_bytes = g.slab_bytes;
@@ -534,7 +534,7 @@ static int dequant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, co
 
 extern "C" int alise_kv_quantize(const alise_kv_desc* d, const uint16_t* kv, uint8_t* slab,
                                  int* flag, void* stream) {
-  KvGeom g;
+  KvGeom g{};
   int s = geom(d, &g);
   if (s) return s;
   cudaStream_t st = S(stream);
@@ -553,7 +553,7 @@ extern "C" int alise_kv_quantize(const alise_kv_desc* d, const uint16_t* kv, uin
 
 extern "C" int alise_kv_dequantize(const alise_kv_desc* d, const uint8_t* slab, uint16_t* kv,
                                    void* stream) {
-  KvGeom g;
+  KvGeom g{};
   int s = geom(d, &g);
   if (s) return s;
   cudaStream_t st = S(stream);
@@ -744,7 +744,7 @@ static int host_dev_ptr(const void* host, void** dev) {
 extern "C" int alise_kv_offload(alise_swapper* sw, const alise_kv_desc* d, const uint16_t* kv,
                                 void* host_slab, int* flag, void* stream, void* done_event) {
   if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
-  KvGeom g;
+  KvGeom g{};
   int s = geom(d, &g);
   if (s) return s;
   int nch;
@@ -790,7 +790,7 @@ extern "C" int alise_kv_offload(alise_swapper* sw, const alise_kv_desc* d, const
 extern "C" int alise_kv_upload(alise_swapper* sw, const alise_kv_desc* d, const void* host_slab,
                                uint16_t* kv, void* stream, void* done_event) {
   if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
-  KvGeom g;
+  KvGeom g{};
   int s = geom(d, &g);
   if (s) return s;
   s = sw_ensure(sw, g.rec_bytes, 0);
@@ -880,10 +880,10 @@ extern "C" int alise_kv_offload_range(alise_swapper* sw, const alise_kv_desc* d,
                                       void* done_event) {
   if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
   if (sw->mode != ALISE_SWAP_STAGED) return fail(ALISE_EINVAL, "token-range transfers use the staged mode");
-  KvGeom g;
+  KvGeom g{};
   int s = geom(d, &g);
   if (s) return s;
-  RangeGeom rg;
+  RangeGeom rg{};
   s = range_geom(d, g, t0, t1, &rg);
   if (s) return s;
   s = sw_ensure(sw, g.rec_bytes, 0);
@@ -919,10 +919,10 @@ extern "C" int alise_kv_upload_range(alise_swapper* sw, const alise_kv_desc* d, 
                                      uint16_t* kv, int64_t t0, int64_t t1, void* stream, void* done_event) {
   if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
   if (sw->mode != ALISE_SWAP_STAGED) return fail(ALISE_EINVAL, "token-range transfers use the staged mode");
-  KvGeom g;
+  KvGeom g{};
   int s = geom(d, &g);
   if (s) return s;
-  RangeGeom rg;
+  RangeGeom rg{};
   s = range_geom(d, g, t0, t1, &rg);
   if (s) return s;
   s = sw_ensure(sw, g.rec_bytes, 0);
