@@ -202,6 +202,16 @@ int alise_db_inexact(alise_db *db, unsigned int *count);
  * first).  Outputs [B][k]; count[b] = min(k, size). */
 int alise_db_topk(alise_db *db, const float *queries, int64_t B, int k, double *out_sim,
                   int64_t *out_seq, int32_t *out_len, int32_t *out_count, void *stream);
+/* alise_db_topk in two steps for a sharded DB: the scan leaves per-query lower bounds
+ * of the shard's coarse k-th in out_bound (float [B], -inf if none); after an all-reduce
+ * (max) of the bounds over the shards, alise_db_topk_rescore returns the exact shard
+ * top-k restricted to rows that can still enter the global top-k (counts may be < k).
+ * ext_bound may be NULL (= alise_db_topk).  The two calls must use the same queries. */
+int alise_db_topk_scan(alise_db *db, const float *queries, int64_t B, int k, float *out_bound,
+                       void *stream);
+int alise_db_topk_rescore(alise_db *db, const float *queries, int64_t B, int k,
+                          const float *ext_bound, double *out_sim, int64_t *out_seq,
+                          int32_t *out_len, int32_t *out_count, void *stream);
 /* Bench instrumentation: CUDA events around every coarse-scan launch; kernel_stats
  * returns the summed scan time, launch count and algorithmic flops (2*B*size*dim). */
 int alise_db_timing(alise_db *db, int enable);

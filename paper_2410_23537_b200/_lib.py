@@ -70,6 +70,8 @@ _SIGS = {
     "alise_db_kernel_stats": [vp, vp, vp, vp],
     "alise_db_export": [vp, vp, vp, vp, i64, vp],
     "alise_db_topk": [vp, vp, i64, i32, vp, vp, vp, vp, vp],
+    "alise_db_topk_scan": [vp, vp, i64, i32, vp, vp],
+    "alise_db_topk_rescore": [vp, vp, i64, i32, vp, vp, vp, vp, vp, vp],
     "alise_embed_batch": [vp, vp, i64, i64, vp, vp, vp],
     "alise_topk_merge": [i32, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp],
     "alise_predict_finish": [i64, i32, vp, vp, vp, dp, vp, i64, vp, vp, vp, dp, i64, i64, dp,

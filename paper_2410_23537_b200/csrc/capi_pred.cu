@@ -89,6 +89,11 @@ struct alise_db {
   int32_t* cand_n = nullptr;
   float* topc = nullptr;
   int32_t* need = nullptr;
+  // state of the last scan (alise_db_topk_scan -> alise_db_topk_rescore)
+  ScanArgs last{};
+  int64_t last_B = -1;
+  int last_k = 0, last_qblk = 0, last_nh = 1;
+  const float* last_q = nullptr;
   uint32_t* gkth = nullptr;  // shared lower bound of the k-th per query, then [bp][KMAX] rank slots
   CUtensorMap tmQ;
   // optional kernel timing (bench roofline): event pairs around each scan launch
@@ -225,16 +230,9 @@ static int sm_count_pred() {
   return n;
 }
 
-extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int k, double* out_sim,
-                             int64_t* out_seq, int32_t* out_len, int32_t* out_count, void* stream) {
-  if (!db || B < 0) return fail(ALISE_EINVAL, "bad topk call");
-  if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
-  cudaStream_t st = S(stream);
-  if (B == 0) return ALISE_OK;
-  if (db->size == 0) {
-    CK(cudaMemsetAsync(out_count, 0, sizeof(int32_t) * B, st));
-    return ALISE_OK;
-  }
+// Coarse scan of a search (db->size > 0, B > 0): query prep, the tcgen05 scan with the
+// fused candidate filter; leaves the candidates and bounds in the DB scratch.
+static int topk_scan(alise_db* db, const float* queries, int64_t B, int k, cudaStream_t st) {
   // 2-SM (cta_group::2) scan for batches above one query block; 1-SM otherwise
   static int force = -2;
   if (force == -2) {
@@ -351,6 +349,23 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
       }
     fprintf(stderr, "[scan stats] B=%lld splits=%d cand/query=%.1f ovf=%d\n", (long long)B, splits, tot / B, ovf);
   }
+  db->last = a;
+  db->last_B = B;
+  db->last_k = k;
+  db->last_qblk = qblk;
+  db->last_nh = nh;
+  db->last_q = queries;
+  return ALISE_OK;
+}
+
+// Exact rescoring of the last scan.  ext (may be NULL): per-query lower bounds of the
+// final coarse k-th from other shards (all-reduced max of alise_db_topk_scan's bounds):
+// candidates below ext - 2*delta cannot enter the global top-k and are not rescored.
+static int topk_rescore(alise_db* db, const float* queries, int64_t B, int k, const float* ext, double* out_sim,
+                        int64_t* out_seq, int32_t* out_len, int32_t* out_count, cudaStream_t st) {
+  const ScanArgs& a = db->last;
+  const int qblk = db->last_qblk, nh = db->last_nh;
+  const int64_t Bp = a.Bp;
   CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
   // small batches are latency bound (one DRAM round trip per candidate row), large ones
   // throughput bound (registers / occupancy)
@@ -363,12 +378,64 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   // large batches: smaller blocks keep more queries in flight per SM
   rescore<<<(unsigned)B, B <= 512 ? 256 : rthreads, 0, st>>>(qblk, nh, a, (int)Bp, B, k, db->size, db->dim, queries, db->v32,
                                        db->lens, db->seqs, db->two_delta, db->cand_s, db->cand_r, db->cand_n,
-                                       db->topc, out_sim, out_seq, out_len, out_count, db->need, db->inexact);
+                                       db->topc, ext, out_sim, out_seq, out_len, out_count, db->need, db->inexact);
   CKL();
   k_exhaustive<<<(unsigned)B, 256, 0, st>>>(B, k, db->size, db->dim, queries, db->v32, db->lens, db->seqs, db->need,
                                             out_sim, out_seq, out_len, out_count, db->inexact);
   CKL();
   return ALISE_OK;
+}
+
+
+extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int k, double* out_sim,
+                             int64_t* out_seq, int32_t* out_len, int32_t* out_count, void* stream) {
+  if (!db || B < 0) return fail(ALISE_EINVAL, "bad topk call");
+  if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
+  cudaStream_t st = S(stream);
+  if (B == 0) return ALISE_OK;
+  if (db->size == 0) {
+    CK(cudaMemsetAsync(out_count, 0, sizeof(int32_t) * B, st));
+    return ALISE_OK;
+  }
+  int s = topk_scan(db, queries, B, k, st);
+  if (s) return s;
+  return topk_rescore(db, queries, B, k, nullptr, out_sim, out_seq, out_len, out_count, st);
+}
+
+extern "C" int alise_db_topk_scan(alise_db* db, const float* queries, int64_t B, int k, float* out_bound,
+                                  void* stream) {
+  if (!db || B < 0 || !out_bound) return fail(ALISE_EINVAL, "bad topk scan call");
+  if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
+  cudaStream_t st = S(stream);
+  if (B == 0) return ALISE_OK;
+  if (db->size == 0) {
+    db->last_B = B;
+    db->last_k = k;
+    db->last_q = queries;
+    k_bounds<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(B, k, nullptr, nullptr, out_bound);
+    CKL();
+    return ALISE_OK;
+  }
+  int s = topk_scan(db, queries, B, k, st);
+  if (s) return s;
+  k_bounds<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(B, k, db->last.gkth, db->last.gslot, out_bound);
+  CKL();
+  return ALISE_OK;
+}
+
+extern "C" int alise_db_topk_rescore(alise_db* db, const float* queries, int64_t B, int k, const float* ext_bound,
+                                     double* out_sim, int64_t* out_seq, int32_t* out_len, int32_t* out_count,
+                                     void* stream) {
+  if (!db || B < 0) return fail(ALISE_EINVAL, "bad topk rescore call");
+  if (B != db->last_B || k != db->last_k || queries != db->last_q)
+    return fail(ALISE_EINVAL, "alise_db_topk_rescore must follow alise_db_topk_scan of the same queries");
+  cudaStream_t st = S(stream);
+  if (B == 0) return ALISE_OK;
+  if (db->size == 0) {
+    CK(cudaMemsetAsync(out_count, 0, sizeof(int32_t) * B, st));
+    return ALISE_OK;
+  }
+  return topk_rescore(db, queries, B, k, ext_bound, out_sim, out_seq, out_len, out_count, st);
 }
 
 extern "C" int alise_db_timing(alise_db* db, int enable) {

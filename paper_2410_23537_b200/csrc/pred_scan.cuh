@@ -974,6 +974,24 @@ __device__ __noinline__ double warp_exact_dot_super(const float* __restrict__ a,
   return super_round(acc);
 }
 
+// Per-query lower bound of the final coarse k-th left by a scan (shared k-th, rank
+// slots); -inf when none (or for an empty shard: gkth == nullptr).  Every shard's bound
+// is below the global k-th, so their max is a global bound (sharded search).
+__global__ void k_bounds(int64_t B, int k, const uint32_t* __restrict__ gkth, const uint32_t* __restrict__ gslot,
+                         float* __restrict__ out) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= B) return;
+  float L = -__int_as_float(0x7f800000);
+  if (gkth) {
+    const uint32_t g0 = gkth[q];
+    if (g0) L = ord_val(g0);
+    uint32_t mn = 0xffffffffu;
+    for (int x = 0; x < k; ++x) mn = min(mn, gslot[(size_t)q * KMAX + x]);
+    if (mn) L = fmaxf(L, ord_val(mn));
+  }
+  out[q] = L;
+}
+
 __device__ __forceinline__ int nw_last(unsigned bd) { return (int)(bd >> 5) - 1; }
 
 // Per query: global coarse k-th from the splits' top lists, candidate compaction,
@@ -983,9 +1001,10 @@ __global__ void __launch_bounds__(256)
 k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
           const float* __restrict__ v32, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
           const float* __restrict__ two_delta, const float* __restrict__ cand_s, const int32_t* __restrict__ cand_r,
-          const int32_t* __restrict__ cand_n, const float* __restrict__ topc, double* __restrict__ out_sim,
-          int64_t* __restrict__ out_seq, int32_t* __restrict__ out_len, int32_t* __restrict__ out_count,
-          int32_t* __restrict__ need_exhaustive, unsigned int* __restrict__ inexact_count) {
+          const int32_t* __restrict__ cand_n, const float* __restrict__ topc, const float* __restrict__ ext,
+          double* __restrict__ out_sim, int64_t* __restrict__ out_seq, int32_t* __restrict__ out_len,
+          int32_t* __restrict__ out_count, int32_t* __restrict__ need_exhaustive,
+          unsigned int* __restrict__ inexact_count) {
   const int64_t q = blockIdx.x;
   if (q >= B) return;
   __shared__ float s_top[4096];  // list values >= the bound (more: exhaustive path)
@@ -1118,7 +1137,9 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
 #ifdef ALISE_RESCORE_TIMING
   const long long T1 = clock64();
 #endif
-  const float thr = s_kth - two_delta[q];
+  // (a bound from other shards can only raise the threshold: rows below it minus
+  // 2*delta cannot enter the global top-k)
+  const float thr = fmaxf(s_kth, ext ? ext[q] : -__int_as_float(0x7f800000)) - two_delta[q];
   // 3) gather candidates above the final threshold: the (split, slot) entries are
   //    flattened over the whole block through the prefix sum of the counts, so every
   //    candidate load is in flight at once (candidate order is irrelevant: step 5 ranks)

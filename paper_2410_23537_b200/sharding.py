@@ -73,6 +73,18 @@ def all_gather_records(local, group=None):
     return out
 
 
+def all_reduce_max(t, group=None):
+    """In-place max all-reduce of a CUDA tensor (NCCL; gloo stages through the host)."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    else:
+        tc = t.cpu()
+        dist.all_reduce(tc, op=dist.ReduceOp.MAX, group=group)
+        t.copy_(tc)
+    return t
+
+
 class ShardedVectorStore:
     """A VectorStore sharded over the ranks of a process group (one GPU each).
 
@@ -139,13 +151,18 @@ class ShardedVectorStore:
         q = torch.as_tensor(queries if isinstance(queries, torch.Tensor) else np.asarray(queries))
         q = q.to(dev, torch.float32).reshape(-1, self.dimension).contiguous()
         B = q.shape[0]
-        if self.local.size:
-            sims, seqs, lens, cnt, q = self.local.search_batch(q, k)
-        else:
-            sims = torch.zeros((B, k), dtype=torch.float64, device=dev)
-            seqs = torch.zeros((B, k), dtype=torch.int64, device=dev)
-            lens = torch.zeros((B, k), dtype=torch.int32, device=dev)
-            cnt = torch.zeros(B, dtype=torch.int32, device=dev)
+        # scan, all-reduce (max) of the per-query coarse k-th lower bounds, then exact
+        # rescoring of only the rows that can still enter the global top-k
+        sims = torch.zeros((B, k), dtype=torch.float64, device=dev)
+        seqs = torch.zeros((B, k), dtype=torch.int64, device=dev)
+        lens = torch.zeros((B, k), dtype=torch.int32, device=dev)
+        cnt = torch.zeros(B, dtype=torch.int32, device=dev)
+        bound = torch.empty(B, dtype=torch.float32, device=dev)
+        h = self.local._h
+        _lib.call("alise_db_topk_scan", h, _lib.ptr(q), B, k, _lib.ptr(bound), _lib.stream_ptr())
+        all_reduce_max(bound, self.group)
+        _lib.call("alise_db_topk_rescore", h, _lib.ptr(q), B, k, _lib.ptr(bound), _lib.ptr(sims), _lib.ptr(seqs),
+                  _lib.ptr(lens), _lib.ptr(cnt), _lib.stream_ptr())
         g_sims, g_seqs, g_lens, g_cnt = all_gather_records((sims, seqs, lens, cnt), self.group)
         o_sim = torch.empty((B, k), dtype=torch.float64, device=dev)
         o_seq = torch.empty((B, k), dtype=torch.int64, device=dev)
