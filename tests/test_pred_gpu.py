@@ -376,3 +376,54 @@ def test_more_query_blocks_than_units(pr):
     Q[::3] = db[g.integers(0, n, size=Q[::3].shape[0])] + 0.05 * g.standard_normal((Q[::3].shape[0], d)).astype(np.float32)
     Q /= np.linalg.norm(Q, axis=1, keepdims=True)
     check_batch(pr, db, lens, Q.astype(np.float32), 8)
+
+
+def test_split_search_api(pr):
+    """alise_db_topk_scan + alise_db_topk_rescore (the sharded path's two steps): with its
+    own bound the result equals alise_db_topk; with a higher external bound it is a
+    prefix of it (only rows that can still enter the global top-k); an empty shard gives
+    -inf bounds and no records."""
+    import torch
+
+    from paper_2410_23537_b200 import _lib
+    g = np.random.default_rng(12)
+    n, d, B, k = 20000, 96, 300, 8
+    db = g.standard_normal((n, d)).astype(np.float32)
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = g.standard_normal((B, d)).astype(np.float32)
+    Q[: B // 2] = db[g.integers(0, n, size=B // 2)] + 0.05 * g.standard_normal((B // 2, d)).astype(np.float32)
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    store = pr.VectorStore(d, n)
+    store.add_batch(db, lens)
+    q = torch.from_numpy(Q).cuda()
+    ref = store.search_batch(q, k)
+
+    def split(st, ext_fn):
+        outs = [torch.empty((B, k), dtype=torch.float64, device="cuda"),
+                torch.empty((B, k), dtype=torch.int64, device="cuda"),
+                torch.empty((B, k), dtype=torch.int32, device="cuda"), torch.empty(B, dtype=torch.int32, device="cuda")]
+        bound = torch.empty(B, dtype=torch.float32, device="cuda")
+        _lib.call("alise_db_topk_scan", st._h, _lib.ptr(q), B, k, _lib.ptr(bound), _lib.stream_ptr())
+        ext = ext_fn(bound)
+        _lib.call("alise_db_topk_rescore", st._h, _lib.ptr(q), B, k, _lib.ptr(ext), *[_lib.ptr(t) for t in outs],
+                  _lib.stream_ptr())
+        torch.cuda.synchronize()
+        return bound, outs
+
+    bound, outs = split(store, lambda b: b)
+    assert torch.equal(outs[3], ref[3])
+    for a, r in zip(outs[:3], ref[:3]):
+        assert torch.equal(a, r)
+    assert torch.isfinite(bound).all()
+    # a higher external bound keeps a prefix of the exact top-k
+    _, outs2 = split(store, lambda b: b + 0.02)
+    c2, c1 = outs2[3].cpu().numpy(), ref[3].cpu().numpy()
+    assert (c2 <= c1).all() and (c2 < c1).any()
+    for i in range(B):
+        assert torch.equal(outs2[1][i, :c2[i]], ref[1][i, :c2[i]])
+    # empty shard
+    empty = pr.VectorStore(d, 64)
+    b0, outs0 = split(empty, lambda b: b)
+    assert torch.isinf(b0).all() and (b0 < 0).all()
+    assert (outs0[3] == 0).all()
