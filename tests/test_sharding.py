@@ -68,6 +68,17 @@ def _worker(rank, world, port, result_dir):
         sq[i, :c] = torch.from_numpy(q_)
         ln[i, :c] = torch.from_numpy(l_.astype(np.int32))
         cnt[i] = c
+    # the sharded search's bound exchange: each shard's local k-th is a lower bound of
+    # the global k-th; after the max all-reduce only records at or above it are kept
+    # (exact sims here, so no coarse-error margin), and the merge is still exact
+    bound = torch.full((B,), -np.inf, dtype=torch.float32)
+    for i in range(B):
+        if cnt[i] == k:
+            bound[i] = float(np.nextafter(np.float32(sims[i, k - 1].item()), np.float32(-np.inf)))
+    sharding.all_reduce_max(bound)
+    for i in range(B):
+        keep = int((sims[i, :cnt[i]] >= bound[i].double()).sum())
+        cnt[i] = keep
     gs, gq, gl, gc = sharding.all_gather_records((sims, sq, ln, cnt))
     o_sim, o_seq, o_len, o_cnt = sharding.merge_topk_host(gs.numpy(), gq.numpy(), gl.numpy(), gc.numpy(), k)
     ref = po.search_exact_batch(db, lens, seqs, Q, k)
