@@ -182,7 +182,7 @@ def _cpu_worker(payload):
     import numpy as np
 
     from oracle import kv_oracle
-    from paper_2410_23537_b200 import synthetic
+    from harness import synthetic
     (plane_idx, tokens, hidden, group, bits) = payload
     x = synthetic.kv_job(1, tokens, hidden, seed=0, job=1000 + plane_idx, group=group)[0, 0]
     rows = x.reshape(-1, group)
@@ -281,7 +281,7 @@ def _kv_bench(args, world, rank, local, layouts=None, e2e=True):
     import torch
 
     from paper_2410_23537_b200 import kvmanager as km
-    from paper_2410_23537_b200 import synthetic
+    from harness import synthetic
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -445,7 +445,8 @@ def pred_bench(args, world, rank, local):
 
     from paper_2410_23537_b200 import _lib
     from paper_2410_23537_b200 import predictor as pr
-    from paper_2410_23537_b200 import sharding, synthetic
+    from paper_2410_23537_b200 import sharding
+    from harness import synthetic
 
     dev = torch.device("cuda", local)
     N, D, B, K = args.pred_n, args.pred_dim, args.pred_b, 8
@@ -636,7 +637,7 @@ def main():
     kv3 = None
     if not args.no_c3:
         from paper_2410_23537_b200 import kvmanager as km
-        from paper_2410_23537_b200 import synthetic
+        from harness import synthetic
         ctx = synthetic.sharegpt_job_tokens(256, seed=0)
         lays = [km.KVLayout(args.layers, int(t), args.hidden, args.head_dim, kind="rows", group=64, bits=4,
                             packed=True) for t in ctx]
@@ -651,7 +652,7 @@ def main():
         kvch = kv_bench(args, world, rank, local, layouts=lays, e2e=False)
     c5 = None
     if not args.no_c5:
-        from paper_2410_23537_b200 import replay
+        from harness import replay
         rec = replay.load(os.path.join(ROOT, "tests", "golden", "c5_swaps.json.gz"))
         mine = list(range(rank, len(rec["replicas"]), world)) if world > 1 else [0]
         outs = [replay.replay(rec, replica=r, check_data=False) for r in mine]

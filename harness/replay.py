@@ -17,7 +17,7 @@ import gzip
 import json
 import time
 
-from . import kvmanager as km
+from paper_2410_23537_b200 import kvmanager as km
 
 
 def load(path):
@@ -58,7 +58,7 @@ def replay(rec: dict, replica: int = 0, group: int = 128, check_data: bool = Tru
     since a job's host copy was written (same ledger, fewer bytes on the link)."""
     import torch
 
-    from . import synthetic
+    from harness import synthetic
 
     layers, hidden, heads = rec["model"]
     bits = rec["bits"]

@@ -358,6 +358,18 @@ struct KvGeom {
   int64_t np_of(int64_t c) const { return std::min(ppc, planes - c * ppc); }
 };
 
+
+// Default transfer chunk in MiB of codes (ALISE_CHUNK_MIB, default 512: a whole 1 GiB
+// fp16 C2 job at INT8).
+static int64_t chunk_mib() {
+  static int64_t mib = -1;
+  if (mib < 0) {
+    const char* e = getenv("ALISE_CHUNK_MIB");
+    mib = e ? std::max(1, atoi(e)) : 512;
+  }
+  return mib;
+}
+
 static int geom(const alise_kv_desc* d, KvGeom* g) {
   if (!d || d->layers <= 0 || d->tokens <= 0 || d->hidden <= 0)
     return fail(ALISE_EINVAL, "kv desc: layers/tokens/hidden must be positive");
@@ -385,18 +397,11 @@ static int geom(const alise_kv_desc* d, KvGeom* g) {
   }
   g->code_bytes_pp = d->packed ? g->plane_elems / 2 : g->plane_elems;
   int64_t ppc = d->planes_per_chunk;
-  // default transfer chunk: 128 MiB of codes (4 quantize launches per 1 GiB fp16 job at INT8:
-  // long enough that a launch's tail is small, short enough that the first copy starts early)
   // default transfer chunk: 512 MiB of codes (a whole 1 GiB fp16 C2 job at INT8).  The
   // host link gates every chunk launch, and a larger launch amortises its ramp on an
   // idle GPU (C2 in-step quantize: 3.2 / 4.2 / 4.8 TB/s at 128 / 256 / 512 MiB); the
   // staging ring holds kSlots chunks per direction
-  static int64_t chunk_mib = -1;
-  if (chunk_mib < 0) {
-    const char* e = getenv("ALISE_CHUNK_MIB");
-    chunk_mib = e ? std::max(1, atoi(e)) : 512;
-  }
-  if (ppc <= 0) ppc = std::max<int64_t>(1, (chunk_mib << 20) / g->code_bytes_pp);
+  if (ppc <= 0) ppc = std::max<int64_t>(1, (chunk_mib() << 20) / g->code_bytes_pp);
   g->ppc = std::min(ppc, g->planes);
   g->n_chunks = (g->planes + g->ppc - 1) / g->ppc;
   g->rec_bytes = g->rec(g->ppc);
@@ -608,9 +613,13 @@ static int sw_release_rings(alise_swapper* sw) {
 
 // Staging buffers grow geometrically (at least doubling, 2 MiB granularity): a growth
 // synchronises the device, so a stream of jobs of increasing size (C5 replay) must not
-// trigger one per job.
+// trigger one per job.  The doubling stops at 1.5x the default chunk's codes (a chunk
+// record is its codes plus at most half as many parameter bytes), so the staged rings
+// (2 directions x kSlots) stay within 2 x 3 x 768 MiB of HBM at the 512 MiB default
+// unless a single (layer, k|v) plane needs more.
 static int64_t grow_to(int64_t need, int64_t have) {
-  const int64_t g = std::max(need, 2 * have);
+  const int64_t cap = (chunk_mib() << 20) * 3 / 2;
+  const int64_t g = std::max(need, std::min(2 * have, cap));
   return (g + (2 << 20) - 1) / (2 << 20) * (2 << 20);
 }
 

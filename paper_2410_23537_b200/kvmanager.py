@@ -11,9 +11,10 @@ argument meanings and errors; what changes is that
   stream it to pinned host memory over the host link (and back, dequantized),
   while the byte ledger and transfer-time model stay identical.
 
-The byte accounting, EWT (Eq. 6-7) and the swap planner (Alg. 2) are the host
-control plane; they are kept in Python with the reference semantics because
-the simulator engine (``simcore._Run``) drives them per iteration.
+The byte ledger (``MemoryState``) stays in Python with the reference semantics; EWT
+(Eq. 6-7, ``ewt_ms``), the swap planner (Alg. 2, ``plan_swaps``) and the engine's
+rank -> EWT -> plan step (``rank_and_plan`` / ``JobTable``) call the C++ control plane
+in csrc/control.cpp, bit-identical to the reference functions.
 """
 from __future__ import annotations
 

@@ -583,33 +583,3 @@ def eval_accuracy(pairs, bin_width: int, latencies_ms=None) -> dict:
     return {"count": len(pairs), "accuracy": hits / len(pairs), "pred_error": rel,
             "mean_latency_ms": float(np.mean(latencies_ms)) if latencies_ms else 0.0}
 
-
-def smoke_check():
-    """Tiny exact top-k + predict check used by __graft_entry__.smoke()."""
-    import torch
-
-    from oracle import pred_oracle
-    g = np.random.default_rng(3)
-    n, d = 700, 64
-    db = g.standard_normal((n, d)).astype(np.float32)
-    db /= np.linalg.norm(db, axis=1, keepdims=True)
-    db[100:111] = db[5]  # tie group
-    lens = g.integers(1, 2048, size=n).astype(np.int32)
-    Q = np.concatenate([db[[5, 17, 300]] + 0.01 * g.standard_normal((3, d)).astype(np.float32),
-                        g.standard_normal((5, d)).astype(np.float32)])
-    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
-    Q = Q.astype(np.float32)
-    store = VectorStore(d, 1024)
-    store.add_batch(db, lens)
-    sims, seqs, slens, cnt, _ = store.search_batch(Q, 8)
-    torch.cuda.synchronize()
-    for i in range(len(Q)):
-        es, el, eq = pred_oracle.search_exact(db, lens, np.arange(n), Q[i], 8)
-        assert np.array_equal(seqs[i].cpu().numpy(), eq), (i, seqs[i], eq)
-        assert np.array_equal(sims[i].cpu().numpy(), es)
-    reg = FallbackRegressor(d, 32, seed=0)
-    reg.b2 = 5.0
-    pred = LengthPredictor(PredictorConfig(dimension=d, db_capacity=1024), regressor=reg, store=store)
-    out, ret = pred.predict_batch(Q)
-    ref_len, ref_ret = pred_oracle.predict_batch(db, lens, np.arange(n), Q, reg.w1, reg.b1, reg.w2, reg.b2)
-    assert np.array_equal(out.cpu().numpy(), ref_len) and np.array_equal(ret.cpu().numpy().astype(bool), ref_ret)

@@ -5,10 +5,11 @@
   path.
 * Predictor: the query DB is row-sharded by insert sequence, ``seq % G == rank``.
   With a global capacity ``G * local_capacity`` each shard's FIFO ring evicts exactly
-  the rows the single global ring (predictor.py:138) would.  A batched search runs the
-  exact per-shard top-k on every rank, all-gathers the per-shard (sim, seq, len,
-  count) records over NCCL (NVLink) and merges them by (-sim, seq) — the only
-  exchange step of the path.
+  the rows the single global ring (predictor.py:138) would.  A batched search has two
+  exchange steps over NCCL (NVLink): after the per-shard coarse scan, a max
+  all-reduce of the per-query exact-score lower bounds (B floats) lets every shard
+  rescore only rows that can still enter the global top-k; then the per-shard (sim,
+  seq, len, count) records are all-gathered and merged by (-sim, seq).
 """
 from __future__ import annotations
 

@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 from servesim import kvmanager as rk  # noqa: E402
 from servesim import predictor as rp  # noqa: E402
 
-from paper_2410_23537_b200 import synthetic  # noqa: E402
+from harness import synthetic  # noqa: E402
 from oracle import kv_oracle  # noqa: E402
 
 

@@ -260,7 +260,7 @@ def test_llama7b_job_round_trip_properties(km):
     """Full C2-size job (1 GiB fp16): bit-exact against the C oracle on sampled rows,
     and the reference's error bound |x - deq| <= scale/2 on every element."""
     import torch
-    from paper_2410_23537_b200 import synthetic
+    from harness import synthetic
     layout = km.KVLayout(32, 2048, 4096, 128, kind="rows", group=128, bits=8)
     kv = synthetic.kv_job_torch(32, 2048, 4096, seed=0, job=3, group=128)
     g = layout.geometry()
@@ -287,7 +287,7 @@ def test_c5_replay_matches_reference_ledger():
     round trip equals the device-to-device quantize/dequantize of its original."""
     import os
 
-    from paper_2410_23537_b200 import replay
+    from harness import replay
     from tests.conftest import GOLDEN
     rec = replay.load(os.path.join(GOLDEN, "c5_swaps.json.gz"))
     out = replay.replay(rec, replica=3, max_events=1200)
@@ -329,7 +329,7 @@ def test_delta_offload_equals_full_offload(km, group, bits, packed, ppc):
     offload; uploading in ranges restores exactly the full upload (kvmanager.py:108-154
     applied per (token, group) row)."""
     import torch
-    from paper_2410_23537_b200 import synthetic
+    from harness import synthetic
     L, T, H = 3, 96, 4096
     kv = synthetic.kv_job_torch(L, T, H, seed=0, job=5, group=group, device="cuda")
     lay = km.KVLayout(L, T, H, 128, kind="rows", group=group, bits=bits, packed=packed, planes_per_chunk=ppc)
@@ -390,7 +390,7 @@ def test_c5_replay_delta_offload_same_ledger():
     dequantized values)."""
     import os
 
-    from paper_2410_23537_b200 import replay
+    from harness import replay
     from tests.conftest import GOLDEN
     rec = replay.load(os.path.join(GOLDEN, "c5_swaps.json.gz"))
     full = replay.replay(rec, replica=3, max_events=900, check_data=False)

@@ -188,7 +188,7 @@ def test_reference_prediction_known_answers(pr):
 @pytest.mark.slow
 def test_c4_scale_200k_x_768(pr):
     """C4 shape at 1/5 scale (200k x 768 DB, 512 queries, planted duplicates)."""
-    from paper_2410_23537_b200 import synthetic
+    from harness import synthetic
     db, lens = synthetic.predictor_db(200_000, 768, seed=0, dup_groups=200)
     Q = synthetic.predictor_queries(db, 512, seed=0)
     check_batch(pr, db, lens, Q, 8)
@@ -300,7 +300,7 @@ def test_shared_thresholds_with_ties_across_tile_groups(pr, B):
 def test_graphed_single_request_matches_eager(pr):
     """predict_vector through the captured CUDA graph == the eager path, including after
     the DB grows (re-capture) and for fallback (MLP) queries."""
-    from paper_2410_23537_b200 import synthetic
+    from harness import synthetic
     db, lens = synthetic.predictor_db(30_000, 256, seed=3, dup_groups=30)
     reg = pr.FallbackRegressor(256, 32, seed=0)
     reg.b2 = 5.0

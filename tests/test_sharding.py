@@ -9,7 +9,8 @@ import pytest
 import torch.multiprocessing as mp
 
 from oracle import pred_oracle as po
-from paper_2410_23537_b200 import sharding, synthetic
+from paper_2410_23537_b200 import sharding
+from harness import synthetic
 
 
 def test_lpt_balances_c3_jobs():

@@ -9,7 +9,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2410_23537_b200 import kvmanager as km  # noqa: E402
-from paper_2410_23537_b200 import synthetic  # noqa: E402
+from harness import synthetic  # noqa: E402
 
 J, H = 8, 8
 PPC = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # planes per transfer chunk (0: default)

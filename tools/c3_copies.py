@@ -8,7 +8,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2410_23537_b200 import kvmanager as km  # noqa: E402
-from paper_2410_23537_b200 import synthetic  # noqa: E402
+from harness import synthetic  # noqa: E402
 
 ctx = synthetic.sharegpt_job_tokens(256, seed=0)
 sizes = [km.KVLayout(32, int(t), 4096, 128, kind="rows", group=64, bits=4, packed=True).geometry()["slab_bytes"]

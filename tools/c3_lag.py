@@ -7,7 +7,7 @@ sys.path.insert(0, ".")
 sys.argv = ["bench.py"]
 import bench  # noqa: E402
 from paper_2410_23537_b200 import kvmanager as km  # noqa: E402
-from paper_2410_23537_b200 import synthetic  # noqa: E402
+from harness import synthetic  # noqa: E402
 
 args = bench.parse()
 args.steps, args.warmup = 2, 1

@@ -4,7 +4,7 @@ import os
 import sys
 
 sys.path.insert(0, ".")
-from paper_2410_23537_b200 import replay  # noqa: E402
+from harness import replay  # noqa: E402
 
 rec = replay.load(os.path.join("tests", "golden", "c5_swaps.json.gz"))
 for delta in (False, True, False, True):

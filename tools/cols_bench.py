@@ -10,7 +10,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2410_23537_b200 import kvmanager as km  # noqa: E402
-from paper_2410_23537_b200 import synthetic  # noqa: E402
+from harness import synthetic  # noqa: E402
 
 res = []
 for kind, bits, packed in [("channel", 8, False), ("head", 8, False), ("channel", 4, True)]:

@@ -7,7 +7,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2410_23537_b200 import kvmanager as km  # noqa: E402
-from paper_2410_23537_b200 import synthetic  # noqa: E402
+from harness import synthetic  # noqa: E402
 
 CASES = [("rows", 128, 8, False), ("rows", 64, 4, True), ("rows", 64, 8, False),
          ("channel", 0, 8, False), ("head", 0, 8, False)]

@@ -10,7 +10,7 @@ from torch.profiler import ProfilerActivity, profile
 
 sys.path.insert(0, ".")
 from paper_2410_23537_b200 import predictor as pr  # noqa: E402
-from paper_2410_23537_b200 import synthetic  # noqa: E402
+from harness import synthetic  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 BS = [int(b) for b in sys.argv[2].split(",")] if len(sys.argv) > 2 else [256, 64, 1]

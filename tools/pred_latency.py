@@ -9,7 +9,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2410_23537_b200 import predictor as pr  # noqa: E402
-from paper_2410_23537_b200 import synthetic  # noqa: E402
+from harness import synthetic  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 D = 768

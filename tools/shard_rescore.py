@@ -9,7 +9,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2410_23537_b200 import _lib  # noqa: E402
 from paper_2410_23537_b200 import predictor as pr  # noqa: E402
-from paper_2410_23537_b200 import synthetic  # noqa: E402
+from harness import synthetic  # noqa: E402
 
 N, D, B, K, G = 1_000_000, 768, 4096, 8, 8
 db, lens = synthetic.predictor_db(N, D, seed=0, dup_groups=1000)

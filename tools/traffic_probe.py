@@ -9,7 +9,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2410_23537_b200 import kvmanager as km  # noqa: E402
 from paper_2410_23537_b200 import predictor as pr  # noqa: E402
-from paper_2410_23537_b200 import synthetic  # noqa: E402
+from harness import synthetic  # noqa: E402
 
 lay = km.KVLayout(32, 2048, 4096, 128, kind="rows", group=128, bits=8)
 kv = synthetic.kv_job_torch(32, 2048, 4096, seed=0, job=1, group=128)
