@@ -441,6 +441,7 @@ def pred_bench(args, world, rank, local):
     queries, exact top-8 + aggregate / all-MLP finish.  Step = one batch."""
     import math
 
+    import numpy as np
     import torch
 
     from paper_2410_23537_b200 import _lib
@@ -456,11 +457,11 @@ def pred_bench(args, world, rank, local):
     reg = pr.FallbackRegressor(D, 32, seed=0)
     reg.b2 = 5.0
     if world > 1:
-        store = sharding.ShardedVectorStore(D, N)
+        store = sharding.ShardedVectorStore(D, N, dtype=np.float32)
         store.add_batch(db, lens.cpu().numpy())
         local_store = store.local
     else:
-        store = pr.VectorStore(D, N)
+        store = pr.VectorStore(D, N, dtype=np.float32)
         store.add_batch(db, lens)
         local_store = store
     del db

@@ -178,38 +178,61 @@ int alise_event_elapsed_ms(void *start, void *stop, float *ms);
 
 /* ---------------------------------------------------------------- predictor ---- */
 typedef struct alise_db alise_db;
-/* FIFO ring of `capacity` fp32 vectors of `dim` (plus an fp16 copy for the coarse
+/* Master dtype of a store's vectors (and of the queries searched against it). */
+#define ALISE_DB_F32 0
+#define ALISE_DB_F64 1
+/* FIFO ring of `capacity` vectors of `dim` (master copy in fp32, or float64 like the
+ * reference's np.float64 store, predictor.py:126; plus an fp16 copy for the coarse
  * tensor-core scan), observed lengths (int32) and insert sequence numbers (int64).
- * Mirrors VectorStore (predictor.py:120-152): slot = seq % capacity. */
+ * Mirrors VectorStore (predictor.py:120-152): slot = seq % capacity.
+ * alise_db_create = alise_db_create_ex(..., ALISE_DB_F32, ...). */
 int alise_db_create(int device, int64_t capacity, int64_t dim, alise_db **out);
+int alise_db_create_ex(int device, int64_t capacity, int64_t dim, int master_dtype, alise_db **out);
+int alise_db_dtype(alise_db *db, int *master_dtype);
+/* Order of the float64 similarities a search ranks by and returns:
+ *  ALISE_ORDER_EXACT (default): the correctly rounded exact dot product;
+ *  ALISE_ORDER_BLAS: the exact operation sequence of the reference's scan
+ *    (predictor.py:158 `self._vecs[:size] @ vector` -> numpy 2.3 -> OpenBLAS 0.3.30
+ *    dgemv_t on x86-64, restated in oracle/blas_order.c), i.e. the reference's own
+ *    float64 sims bit for bit, so ties that are exact in real arithmetic break as in
+ *    the reference.  blas_threads = the reference host's OpenBLAS thread count (it
+ *    splits the rows when size * dim >= 460800); row r of the reference's array is ring
+ *    slot seq % ref_capacity of ref_size live rows (0 / -1: this store's own capacity
+ *    and size; a sharded store passes the global ring). */
+#define ALISE_ORDER_EXACT 0
+#define ALISE_ORDER_BLAS 1
+int alise_db_set_order(alise_db *db, int order, int blas_threads, int64_t ref_capacity, int64_t ref_size);
 int alise_db_destroy(alise_db *db);
-/* Append n rows (device pointers): vecs fp32 [n][dim], lens int32 [n], seqs int64 [n]
- * (the store's next sequence numbers, in order; slot = (seq / stride) % capacity). */
-int alise_db_append(alise_db *db, const float *vecs, const int32_t *lens, const int64_t *seqs,
+/* Append n rows (device pointers): vecs [n][dim] in the master dtype, lens int32 [n],
+ * seqs int64 [n] (the store's next sequence numbers, in order; slot = (seq / stride) %
+ * capacity).  VectorStore.add (predictor.py:135-152). */
+int alise_db_append(alise_db *db, const void *vecs, const int32_t *lens, const int64_t *seqs,
                     int64_t n, void *stream);
 int alise_db_size(alise_db *db, int64_t *size, int64_t *next_seq);
 /* Shard of a G-way sequence-sharded store: this db receives every G-th sequence number
  * (seq % G == rank) and places it at slot (seq / G) % capacity, so per-shard FIFO
  * eviction equals the global FIFO when the global capacity is G * capacity. */
 int alise_db_set_seq_stride(alise_db *db, int64_t stride);
-/* Copy the first n live slots (fp32 vectors, lens, seqs) to device buffers. */
-int alise_db_export(alise_db *db, float *vecs, int32_t *lens, int64_t *seqs, int64_t n, void *stream);
+/* Copy the first n live slots (master-dtype vectors, lens, seqs) to device buffers. */
+int alise_db_export(alise_db *db, void *vecs, int32_t *lens, int64_t *seqs, int64_t n, void *stream);
 /* Number of rescored candidates whose double-double sum could not certify the float64
  * rounding and were recomputed with the exact 640-bit accumulator (synchronous). */
 int alise_db_inexact(alise_db *db, unsigned int *count);
-/* Exact top-k of B queries (fp32 [B][dim], device) against the db: sims are the
- * correctly rounded float64 dot products, ordered by (-sim, seq) (ties -> older
- * first).  Outputs [B][k]; count[b] = min(k, size). */
-int alise_db_topk(alise_db *db, const float *queries, int64_t B, int k, double *out_sim,
+/* Exact top-k of B queries ([B][dim] in the db's master dtype, device) against the db:
+ * sims are the correctly rounded float64 dot products, ordered by (-sim, seq) (ties ->
+ * older first).  Outputs [B][k]; count[b] = min(k, size).  VectorStore.search
+ * (predictor.py:154-163). */
+int alise_db_topk(alise_db *db, const void *queries, int64_t B, int k, double *out_sim,
                   int64_t *out_seq, int32_t *out_len, int32_t *out_count, void *stream);
 /* alise_db_topk in two steps for a sharded DB: the scan leaves per-query lower bounds
- * of the shard's coarse k-th in out_bound (float [B], -inf if none); after an all-reduce
- * (max) of the bounds over the shards, alise_db_topk_rescore returns the exact shard
- * top-k restricted to rows that can still enter the global top-k (counts may be < k).
- * ext_bound may be NULL (= alise_db_topk).  The two calls must use the same queries. */
-int alise_db_topk_scan(alise_db *db, const float *queries, int64_t B, int k, float *out_bound,
+ * of the global EXACT k-th score in out_bound (float [B], -inf if none; a shard's coarse
+ * k-th bound minus its own coarse error); after an all-reduce (max) of the bounds over
+ * the shards, alise_db_topk_rescore returns the exact shard top-k restricted to rows
+ * that can still enter the global top-k (counts may be < k).  ext_bound may be NULL
+ * (= alise_db_topk).  The two calls must use the same queries. */
+int alise_db_topk_scan(alise_db *db, const void *queries, int64_t B, int k, float *out_bound,
                        void *stream);
-int alise_db_topk_rescore(alise_db *db, const float *queries, int64_t B, int k,
+int alise_db_topk_rescore(alise_db *db, const void *queries, int64_t B, int k,
                           const float *ext_bound, double *out_sim, int64_t *out_seq,
                           int32_t *out_len, int32_t *out_count, void *stream);
 /* Bench instrumentation: CUDA events around every coarse-scan launch; kernel_stats
@@ -230,6 +253,13 @@ int alise_predict_finish(int64_t B, int k, const double *sims, const int32_t *le
                          const double *W1, const double *b1, const double *w2, double b2,
                          int64_t hidden, int64_t max_len, double log_cap, int32_t *out_len,
                          uint8_t *out_retrieved, void *stream);
+/* alise_predict_finish with the queries in fp32 or float64 (queries_dtype ALISE_DB_F32 /
+ * ALISE_DB_F64): the MLP input is the reference's float64 vector when the caller has it. */
+int alise_predict_finish_ex(int64_t B, int k, const double *sims, const int32_t *lens,
+                            const int32_t *counts, double s0, const void *queries, int queries_dtype,
+                            int64_t dim, const double *W1, const double *b1, const double *w2,
+                            double b2, int64_t hidden, int64_t max_len, double log_cap,
+                            int32_t *out_len, uint8_t *out_retrieved, void *stream);
 
 /* Batched HashingEmbedder.embed (predictor.py:66-100): prompts are tokens[offsets[b] ..
  * offsets[b+1]) (int64, device); writes float64 [B][dim] (bit-identical to the

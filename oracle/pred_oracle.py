@@ -11,7 +11,8 @@ whose dot-product summation order is unspecified, and ``argpartition`` picks an
 arbitrary subset of rows tied at the k-boundary.  The restatement
 pins what the north star asks for:
   * sims = the correctly rounded float64 value of the exact dot product
-    (fp32 x fp32 products are exact in float64; summed with math.fsum);
+    (fp32 x fp32 products are exact in float64; float64 products are split exactly
+    into two doubles (Dekker); summed with math.fsum);
   * order = full (-sim, seq) sort, so ties are broken by insert order everywhere;
   * aggregate = numpy's own ops on the same arrays (summation order: sequential for
     n < 8, 8-accumulator tree for n >= 8 — see tests/test_oracle_pred.py);
@@ -27,55 +28,134 @@ import math
 import numpy as np
 
 
-def exact_dot(a32, b32) -> float:
-    """Correctly rounded float64 dot product of two fp32 vectors."""
-    a = np.asarray(a32, dtype=np.float32).astype(np.float64)
-    b = np.asarray(b32, dtype=np.float32).astype(np.float64)
-    return math.fsum((a * b).tolist())
+def _two_prod(a, b):
+    """Elementwise a*b = p + e exactly (Veltkamp/Dekker; float64 arrays in the normal
+    range).  Entries whose products leave the safe range are returned in `bad`."""
+    p = a * b
+    c = 134217729.0  # 2^27 + 1
+    ta = c * a
+    ah = ta - (ta - a)
+    al = a - ah
+    tb = c * b
+    bh = tb - (tb - b)
+    bl = b - bh
+    e = ((ah * bh - p) + ah * bl + al * bh) + al * bl
+    mag = np.abs(p)
+    bad = (p != 0) & ((mag < 2.0 ** -900) | (mag > 2.0 ** 900) | (np.abs(a) > 2.0 ** 995) | (np.abs(b) > 2.0 ** 995))
+    return p, e, bad
 
 
-def search_exact(db32, lens, seqs, q32, k: int):
-    """Exact top-k by (-sim, seq) over fp32 rows. Returns (sims f64, lens, seqs)."""
-    db32 = np.asarray(db32, dtype=np.float32)
-    n = db32.shape[0]
+def exact_dot(a, b, f64: bool = False) -> float:
+    """Correctly rounded float64 dot product: of two fp32 vectors (products exact in
+    float64), or with f64=True of two float64 vectors (products split exactly)."""
+    if not f64:
+        a = np.asarray(a, dtype=np.float32).astype(np.float64)
+        b = np.asarray(b, dtype=np.float32).astype(np.float64)
+        return math.fsum((a * b).tolist())
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    p, e, bad = _two_prod(a, b)
+    if bad.any():  # exact rational arithmetic for out-of-range products
+        from fractions import Fraction
+        tot = sum((Fraction(x) * Fraction(y) for x, y in zip(a.tolist(), b.tolist())), Fraction(0))
+        return float(tot)  # Fraction -> float rounds correctly (half-even)
+    return math.fsum(p.tolist() + e.tolist())
+
+
+def _rows(db, f64):
+    return np.asarray(db, dtype=np.float64) if f64 else np.asarray(db, dtype=np.float32)
+
+
+def search_exact(db32, lens, seqs, q32, k: int, f64: bool = False):
+    """Exact top-k by (-sim, seq) over fp32 rows (or float64 rows with f64=True).
+    Returns (sims f64, lens, seqs)."""
+    db = _rows(db32, f64)
+    n = db.shape[0]
     if n == 0:
         return np.array([]), np.array([], dtype=np.int64), np.array([], dtype=np.int64)
     k = min(k, n)
-    q = np.asarray(q32, dtype=np.float32).astype(np.float64)
-    coarse = db32.astype(np.float64) @ q           # |error| <= ~dim * 2^-53 * |q| * max|v|
-    margin = 1e-9 * max(1.0, float(np.abs(q).sum())) * max(1.0, float(np.abs(db32).max()))
+    qr = _rows(q32, f64)
+    q = qr.astype(np.float64)
+    coarse = db.astype(np.float64) @ q           # |error| <= ~dim * 2^-53 * |q| * max|v|
+    margin = 1e-9 * max(1.0, float(np.abs(q).sum())) * max(1.0, float(np.abs(db).max()))
     kth = np.partition(coarse, n - k)[n - k]
     cand = np.flatnonzero(coarse >= kth - 2 * margin)
-    exact = np.array([exact_dot(db32[r], q32) for r in cand])
+    exact = np.array([exact_dot(db[r], qr, f64) for r in cand])
     order = np.lexsort((np.asarray(seqs)[cand], -exact))[:k]
     pick = cand[order]
     return exact[order], np.asarray(lens)[pick].astype(np.int64), np.asarray(seqs)[pick].astype(np.int64)
 
 
-def search_exact_batch(db32, lens, seqs, Q32, k: int, chunk: int = 256):
+def search_exact_batch(db32, lens, seqs, Q32, k: int, chunk: int = 256, f64: bool = False):
     """search_exact for a batch (one BLAS GEMM for the coarse pass).
     Returns lists of (sims, lens, seqs) per query."""
-    db32 = np.asarray(db32, dtype=np.float32)
-    db64 = db32.astype(np.float64)
-    Q32 = np.asarray(Q32, dtype=np.float32)
-    n = db32.shape[0]
+    db = _rows(db32, f64)
+    db64 = db.astype(np.float64)
+    Q = _rows(Q32, f64)
+    n = db.shape[0]
     kk = min(k, n)
     out = []
-    amax = float(np.abs(db32).max()) if n else 1.0
-    for c0 in range(0, len(Q32), chunk):
-        Qc = Q32[c0:c0 + chunk].astype(np.float64)
+    amax = float(np.abs(db).max()) if n else 1.0
+    for c0 in range(0, len(Q), chunk):
+        Qc = Q[c0:c0 + chunk].astype(np.float64)
         coarse = db64 @ Qc.T
         for j in range(Qc.shape[0]):
             col = coarse[:, j]
             margin = 1e-9 * max(1.0, float(np.abs(Qc[j]).sum())) * max(1.0, amax)
             kth = np.partition(col, n - kk)[n - kk]
             cand = np.flatnonzero(col >= kth - 2 * margin)
-            exact = np.array([exact_dot(db32[r], Q32[c0 + j]) for r in cand])
+            exact = np.array([exact_dot(db[r], Q[c0 + j], f64) for r in cand])
             order = np.lexsort((np.asarray(seqs)[cand], -exact))[:kk]
             pick = cand[order]
             out.append((exact[order], np.asarray(lens)[pick].astype(np.int64),
                         np.asarray(seqs)[pick].astype(np.int64)))
     return out
+
+
+_BLAS = None
+
+
+def _blas_lib():
+    global _BLAS
+    if _BLAS is None:
+        import ctypes
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        so = os.path.join(here, "liboracle_blas.so")
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(os.path.join(here, "blas_order.c")):
+            subprocess.run(["make", "-s", "-C", here], check=True)
+        lib = ctypes.CDLL(so)
+        vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        lib.oracle_blas_gemv.argtypes = [vp, i64, i64, vp, vp, i32]
+        _BLAS = lib
+    return _BLAS
+
+
+def blas_gemv(V, x, threads: int):
+    """V @ x (V float64 [n, d] row-major) in the reference BLAS's operation order
+    (oracle/blas_order.c: numpy -> OpenBLAS 0.3.30 dgemv_t on x86-64)."""
+    V = np.ascontiguousarray(V, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty(V.shape[0])
+    if V.shape[0]:
+        _blas_lib().oracle_blas_gemv(V.ctypes.data, V.shape[0], V.shape[1], x.ctypes.data, y.ctypes.data, threads)
+    return y
+
+
+def search_blas(slots, lens, seqs, q, k: int, threads: int):
+    """VectorStore.search (predictor.py:154-163) verbatim in algorithm, with the scan's
+    float64 sims in the reference BLAS order: rows are the ring slots in slot order
+    (the reference's self._vecs[:size]); argpartition + lexsort as the reference."""
+    n = len(slots)
+    if n == 0:
+        return np.array([]), np.array([], dtype=np.int64), np.array([], dtype=np.int64)
+    sims = blas_gemv(slots, q, threads)
+    k = min(k, n)
+    idx = np.argpartition(-sims, k - 1)[:k]
+    order = np.lexsort((np.asarray(seqs)[idx], -sims[idx]))
+    idx = idx[order]
+    return sims[idx], np.asarray(lens)[idx].astype(np.int64), np.asarray(seqs)[idx].astype(np.int64)
 
 
 def aggregate(sims, lens, s0: float, max_len: int):
@@ -120,14 +200,14 @@ def mlp_predict_len(X, W1, b1, w2, b2, max_len: int):
     return np.clip(np.rint(raw), 1, max_len).astype(np.int64)
 
 
-def predict_batch(db32, lens, seqs, Q32, W1, b1, w2, b2, k=8, s0=0.80, max_len=2048):
-    """Full predict_vector for a batch (search + aggregate, else MLP)."""
-    fallback = mlp_predict_len(np.asarray(Q32, dtype=np.float32).astype(np.float64), W1, b1, w2, b2,
-                               max_len)
+def predict_batch(db32, lens, seqs, Q32, W1, b1, w2, b2, k=8, s0=0.80, max_len=2048, f64: bool = False):
+    """Full predict_vector for a batch (search + aggregate, else MLP).  With f64=True the
+    rows and queries are float64 (the reference's own store and MLP inputs)."""
+    fallback = mlp_predict_len(_rows(Q32, f64).astype(np.float64), W1, b1, w2, b2, max_len)
     out_len = np.empty(len(Q32), dtype=np.int64)
     retrieved = np.zeros(len(Q32), dtype=bool)
     for i, q in enumerate(Q32):
-        s, ln, _ = search_exact(db32, lens, seqs, q, k)
+        s, ln, _ = search_exact(db32, lens, seqs, q, k, f64=f64)
         a = aggregate(s, ln, s0, max_len)
         if a is None:
             out_len[i] = fallback[i]

@@ -61,6 +61,9 @@ _SIGS = {
     "alise_event_elapsed_ms": [vp, vp, vp],
     "alise_stream_wait": [vp, vp],
     "alise_db_create": [i32, i64, i64, vp],
+    "alise_db_create_ex": [i32, i64, i64, i32, vp],
+    "alise_db_dtype": [vp, vp],
+    "alise_db_set_order": [vp, i32, i32, i64, i64],
     "alise_db_destroy": [vp],
     "alise_db_append": [vp, vp, vp, vp, i64, vp],
     "alise_db_size": [vp, vp, vp],
@@ -76,6 +79,8 @@ _SIGS = {
     "alise_topk_merge": [i32, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp],
     "alise_predict_finish": [i64, i32, vp, vp, vp, dp, vp, i64, vp, vp, vp, dp, i64, i64, dp,
                              vp, vp, vp],
+    "alise_predict_finish_ex": [i64, i32, vp, vp, vp, dp, vp, i32, i64, vp, vp, vp, dp, i64, i64, dp,
+                                vp, vp, vp],
 }
 
 _lib = None

@@ -71,10 +71,13 @@ struct alise_db {
   int64_t capacity = 0, cap_p = 0, dim = 0, dp = 0;
   int64_t size = 0, next_seq = 0;
   int64_t seq_stride = 1;  // sharded stores hold every G-th sequence: slot = (seq / G) % capacity
-  float* v32 = nullptr;
+  int f64 = 0;              // master dtype: 0 fp32, 1 float64 (ALISE_DB_F32 / ALISE_DB_F64)
+  size_t esz = 4;           // bytes per master element
+  void* vm = nullptr;       // master vectors [capacity][dim]
   __half* v16 = nullptr;
   int32_t* lens = nullptr;
   int64_t* seqs = nullptr;
+  BlasRef blas{0, 1, 0, -1};         // sims order (ref_cap 0 / ref_n -1: this store's own)
   unsigned int* vmax = nullptr;     // float bits of the max row norm
   unsigned int* inexact = nullptr;  // candidates whose rounding could not be certified
   CUtensorMap tmD;
@@ -93,7 +96,7 @@ struct alise_db {
   ScanArgs last{};
   int64_t last_B = -1;
   int last_k = 0, last_qblk = 0, last_nh = 1;
-  const float* last_q = nullptr;
+  const void* last_q = nullptr;
   uint32_t* gkth = nullptr;  // shared lower bound of the k-th per query, then [bp][KMAX] rank slots
   CUtensorMap tmQ;
   // optional kernel timing (bench roofline): event pairs around each scan launch
@@ -103,7 +106,12 @@ struct alise_db {
 };
 
 extern "C" int alise_db_create(int device, int64_t capacity, int64_t dim, alise_db** out) {
+  return alise_db_create_ex(device, capacity, dim, ALISE_DB_F32, out);
+}
+
+extern "C" int alise_db_create_ex(int device, int64_t capacity, int64_t dim, int master_dtype, alise_db** out) {
   if (capacity <= 0 || dim <= 0) return fail(ALISE_EINVAL, "capacity and dim must be positive");
+  if (master_dtype != ALISE_DB_F32 && master_dtype != ALISE_DB_F64) return fail(ALISE_EINVAL, "bad master dtype");
   if (capacity > ((int64_t)1 << 31) - 512) return fail(ALISE_EINVAL, "capacity too large");
   CK(cudaSetDevice(device));
   alise_db* db = new alise_db();
@@ -112,7 +120,9 @@ extern "C" int alise_db_create(int device, int64_t capacity, int64_t dim, alise_
   db->cap_p = (capacity + BN - 1) / BN * BN;
   db->dim = dim;
   db->dp = (dim + 63) / 64 * 64;
-  CK(cudaMalloc(&db->v32, sizeof(float) * capacity * dim));
+  db->f64 = master_dtype == ALISE_DB_F64;
+  db->esz = db->f64 ? 8 : 4;
+  CK(cudaMalloc(&db->vm, db->esz * capacity * dim));
   CK(cudaMalloc(&db->v16, sizeof(__half) * db->cap_p * db->dp));
   CK(cudaMemset(db->v16, 0, sizeof(__half) * db->cap_p * db->dp));
   CK(cudaMalloc(&db->lens, sizeof(int32_t) * capacity));
@@ -146,7 +156,7 @@ static void free_scratch(alise_db* db) {
 extern "C" int alise_db_destroy(alise_db* db) {
   if (!db) return ALISE_OK;
   cudaDeviceSynchronize();
-  cudaFree(db->v32);
+  cudaFree(db->vm);
   cudaFree(db->v16);
   cudaFree(db->lens);
   cudaFree(db->seqs);
@@ -156,15 +166,39 @@ extern "C" int alise_db_destroy(alise_db* db) {
   return ALISE_OK;
 }
 
-extern "C" int alise_db_append(alise_db* db, const float* vecs, const int32_t* lens, const int64_t* seqs,
+extern "C" int alise_db_set_order(alise_db* db, int order, int blas_threads, int64_t ref_capacity, int64_t ref_size) {
+  if (!db || (order != ALISE_ORDER_EXACT && order != ALISE_ORDER_BLAS)) return fail(ALISE_EINVAL, "bad order");
+  if (ref_capacity < 0 || (ref_capacity > 0 && ref_size > ref_capacity))
+    return fail(ALISE_EINVAL, "bad reference ring geometry");
+  db->blas.on = order == ALISE_ORDER_BLAS;
+  db->blas.threads = blas_threads < 1 ? 1 : blas_threads;
+  db->blas.ref_cap = ref_capacity;
+  db->blas.ref_n = ref_size;
+  return ALISE_OK;
+}
+
+extern "C" int alise_db_dtype(alise_db* db, int* master_dtype) {
+  if (!db || !master_dtype) return fail(ALISE_EINVAL, "null argument");
+  *master_dtype = db->f64 ? ALISE_DB_F64 : ALISE_DB_F32;
+  return ALISE_OK;
+}
+
+extern "C" int alise_db_append(alise_db* db, const void* vecs, const int32_t* lens, const int64_t* seqs,
                                int64_t n, void* stream) {
   if (!db || n < 0) return fail(ALISE_EINVAL, "bad append");
   if (n == 0) return ALISE_OK;
   // rows with equal slot in one batch would race; the host splits batches larger than capacity
   if (n > db->capacity) return fail(ALISE_EINVAL, "append batch larger than capacity");
-  k_db_append<<<(unsigned)n, 128, 0, S(stream)>>>(vecs, lens, seqs, n, db->dim, db->dp, db->capacity,
-                                                  db->seq_stride, db->v32, db->v16, db->lens, db->seqs,
-                                                  db->vmax);
+  if (db->f64)
+    k_db_append<double><<<(unsigned)n, 128, 0, S(stream)>>>(static_cast<const double*>(vecs), lens, seqs, n, db->dim,
+                                                            db->dp, db->capacity, db->seq_stride,
+                                                            static_cast<double*>(db->vm), db->v16, db->lens,
+                                                            db->seqs, db->vmax);
+  else
+    k_db_append<float><<<(unsigned)n, 128, 0, S(stream)>>>(static_cast<const float*>(vecs), lens, seqs, n, db->dim,
+                                                           db->dp, db->capacity, db->seq_stride,
+                                                           static_cast<float*>(db->vm), db->v16, db->lens, db->seqs,
+                                                           db->vmax);
   CKL();
   db->next_seq += n;
   db->size = std::min(db->capacity, db->size + n);
@@ -185,10 +219,10 @@ extern "C" int alise_db_size(alise_db* db, int64_t* size, int64_t* next_seq) {
   return ALISE_OK;
 }
 
-extern "C" int alise_db_export(alise_db* db, float* vecs, int32_t* lens, int64_t* seqs, int64_t n, void* stream) {
+extern "C" int alise_db_export(alise_db* db, void* vecs, int32_t* lens, int64_t* seqs, int64_t n, void* stream) {
   if (!db || n < 0 || n > db->size) return fail(ALISE_EINVAL, "bad export count");
   if (n == 0) return ALISE_OK;
-  CK(cudaMemcpyAsync(vecs, db->v32, sizeof(float) * n * db->dim, cudaMemcpyDeviceToDevice, S(stream)));
+  CK(cudaMemcpyAsync(vecs, db->vm, db->esz * n * db->dim, cudaMemcpyDeviceToDevice, S(stream)));
   CK(cudaMemcpyAsync(lens, db->lens, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, S(stream)));
   CK(cudaMemcpyAsync(seqs, db->seqs, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, S(stream)));
   return ALISE_OK;
@@ -232,7 +266,7 @@ static int sm_count_pred() {
 
 // Coarse scan of a search (db->size > 0, B > 0): query prep, the tcgen05 scan with the
 // fused candidate filter; leaves the candidates and bounds in the DB scratch.
-static int topk_scan(alise_db* db, const float* queries, int64_t B, int k, cudaStream_t st) {
+static int topk_scan(alise_db* db, const void* queries, int64_t B, int k, cudaStream_t st) {
   // 2-SM (cta_group::2) scan for batches above one query block; 1-SM otherwise
   static int force = -2;
   if (force == -2) {
@@ -264,7 +298,12 @@ static int topk_scan(alise_db* db, const float* queries, int64_t B, int k, cudaS
   const int splits = groups * nh;
   int s = ensure_scratch(db, Bp, splits, st);
   if (s) return s;
-  k_query_prep<<<(unsigned)Bp, 128, 0, st>>>(queries, B, db->dim, db->dp, db->vmax, db->q16, db->two_delta);
+  if (db->f64)
+    k_query_prep<double><<<(unsigned)Bp, 128, 0, st>>>(static_cast<const double*>(queries), B, db->dim, db->dp,
+                                                       db->vmax, db->q16, db->two_delta, db->blas.on);
+  else
+    k_query_prep<float><<<(unsigned)Bp, 128, 0, st>>>(static_cast<const float*>(queries), B, db->dim, db->dp,
+                                                      db->vmax, db->q16, db->two_delta, db->blas.on);
   CKL();
   ScanArgs a;
   a.n_kb = (int)(db->dp / BK);
@@ -358,36 +397,56 @@ static int topk_scan(alise_db* db, const float* queries, int64_t B, int k, cudaS
   return ALISE_OK;
 }
 
-// Exact rescoring of the last scan.  ext (may be NULL): per-query lower bounds of the
-// final coarse k-th from other shards (all-reduced max of alise_db_topk_scan's bounds):
-// candidates below ext - 2*delta cannot enter the global top-k and are not rescored.
-static int topk_rescore(alise_db* db, const float* queries, int64_t B, int k, const float* ext, double* out_sim,
-                        int64_t* out_seq, int32_t* out_len, int32_t* out_count, cudaStream_t st) {
+// Exact rescoring of the last scan.  ext (may be NULL): per-query exact-score lower
+// bounds of the global k-th from the shards (all-reduced max of alise_db_topk_scan's
+// bounds): candidates with coarse score below ext - delta cannot enter the global top-k
+// and are not rescored.
+static BlasRef blas_ref(const alise_db* db) {
+  BlasRef b = db->blas;
+  if (b.ref_cap <= 0) b.ref_cap = db->capacity;
+  if (b.ref_n < 0) b.ref_n = db->size;
+  return b;
+}
+
+template <typename T>
+static int topk_rescore_t(alise_db* db, const T* queries, int64_t B, int k, const float* ext, double* out_sim,
+                          int64_t* out_seq, int32_t* out_len, int32_t* out_count, cudaStream_t st) {
   const ScanArgs& a = db->last;
   const int qblk = db->last_qblk, nh = db->last_nh;
   const int64_t Bp = a.Bp;
+  const T* vm = static_cast<const T*>(db->vm);
   CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
   // small batches are latency bound (one DRAM round trip per candidate row), large ones
   // throughput bound (registers / occupancy)
-  auto rescore = B <= 512 ? k_rescore<24> : k_rescore<8>;
+  auto rescore = B <= 512 ? k_rescore<24, T> : k_rescore<8, T>;
   static int rthreads = -1;
   if (rthreads < 0) {
     const char* e = getenv("ALISE_RESCORE_THREADS");
     rthreads = e ? atoi(e) : 128;
   }
   // large batches: smaller blocks keep more queries in flight per SM
-  rescore<<<(unsigned)B, B <= 512 ? 256 : rthreads, 0, st>>>(qblk, nh, a, (int)Bp, B, k, db->size, db->dim, queries, db->v32,
-                                       db->lens, db->seqs, db->two_delta, db->cand_s, db->cand_r, db->cand_n,
-                                       db->topc, ext, out_sim, out_seq, out_len, out_count, db->need, db->inexact);
+  const BlasRef br = blas_ref(db);
+  rescore<<<(unsigned)B, B <= 512 ? 256 : rthreads, 0, st>>>(qblk, nh, a, (int)Bp, B, k, db->size, db->dim, queries,
+                                                             vm, db->lens, db->seqs, db->two_delta, db->cand_s,
+                                                             db->cand_r, db->cand_n, db->topc, ext, out_sim, out_seq,
+                                                             out_len, out_count, db->need, db->inexact, br);
   CKL();
-  k_exhaustive<<<(unsigned)B, 256, 0, st>>>(B, k, db->size, db->dim, queries, db->v32, db->lens, db->seqs, db->need,
-                                            out_sim, out_seq, out_len, out_count, db->inexact);
+  k_exhaustive<T><<<(unsigned)B, 256, 0, st>>>(B, k, db->size, db->dim, queries, vm, db->lens, db->seqs, db->need,
+                                               out_sim, out_seq, out_len, out_count, db->inexact, br);
   CKL();
   return ALISE_OK;
 }
 
+static int topk_rescore(alise_db* db, const void* queries, int64_t B, int k, const float* ext, double* out_sim,
+                        int64_t* out_seq, int32_t* out_len, int32_t* out_count, cudaStream_t st) {
+  if (db->f64)
+    return topk_rescore_t(db, static_cast<const double*>(queries), B, k, ext, out_sim, out_seq, out_len, out_count,
+                          st);
+  return topk_rescore_t(db, static_cast<const float*>(queries), B, k, ext, out_sim, out_seq, out_len, out_count, st);
+}
 
-extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int k, double* out_sim,
+
+extern "C" int alise_db_topk(alise_db* db, const void* queries, int64_t B, int k, double* out_sim,
                              int64_t* out_seq, int32_t* out_len, int32_t* out_count, void* stream) {
   if (!db || B < 0) return fail(ALISE_EINVAL, "bad topk call");
   if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
@@ -402,9 +461,9 @@ extern "C" int alise_db_topk(alise_db* db, const float* queries, int64_t B, int 
   return topk_rescore(db, queries, B, k, nullptr, out_sim, out_seq, out_len, out_count, st);
 }
 
-extern "C" int alise_db_topk_scan(alise_db* db, const float* queries, int64_t B, int k, float* out_bound,
+extern "C" int alise_db_topk_scan(alise_db* db, const void* queries, int64_t B, int k, float* out_bound,
                                   void* stream) {
-  if (!db || B < 0 || !out_bound) return fail(ALISE_EINVAL, "bad topk scan call");
+  if (!db || B < 0 || (B > 0 && !out_bound)) return fail(ALISE_EINVAL, "bad topk scan call");
   if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
   cudaStream_t st = S(stream);
   if (B == 0) return ALISE_OK;
@@ -412,25 +471,26 @@ extern "C" int alise_db_topk_scan(alise_db* db, const float* queries, int64_t B,
     db->last_B = B;
     db->last_k = k;
     db->last_q = queries;
-    k_bounds<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(B, k, nullptr, nullptr, out_bound);
+    k_bounds<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(B, k, nullptr, nullptr, nullptr, out_bound);
     CKL();
     return ALISE_OK;
   }
   int s = topk_scan(db, queries, B, k, st);
   if (s) return s;
-  k_bounds<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(B, k, db->last.gkth, db->last.gslot, out_bound);
+  k_bounds<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(B, k, db->last.gkth, db->last.gslot, db->two_delta,
+                                                        out_bound);
   CKL();
   return ALISE_OK;
 }
 
-extern "C" int alise_db_topk_rescore(alise_db* db, const float* queries, int64_t B, int k, const float* ext_bound,
+extern "C" int alise_db_topk_rescore(alise_db* db, const void* queries, int64_t B, int k, const float* ext_bound,
                                      double* out_sim, int64_t* out_seq, int32_t* out_len, int32_t* out_count,
                                      void* stream) {
   if (!db || B < 0) return fail(ALISE_EINVAL, "bad topk rescore call");
+  if (B == 0) return ALISE_OK;  // an empty scan records nothing
   if (B != db->last_B || k != db->last_k || queries != db->last_q)
     return fail(ALISE_EINVAL, "alise_db_topk_rescore must follow alise_db_topk_scan of the same queries");
   cudaStream_t st = S(stream);
-  if (B == 0) return ALISE_OK;
   if (db->size == 0) {
     CK(cudaMemsetAsync(out_count, 0, sizeof(int32_t) * B, st));
     return ALISE_OK;
@@ -472,28 +532,50 @@ extern "C" int alise_topk_merge(int G, int64_t B, int k, const double* sims, con
   return ALISE_OK;
 }
 
+template <typename X>
+static int predict_finish_t(int64_t B, int k, const double* sims, const int32_t* lens, const int32_t* counts, double s0,
+                            const X* queries, int64_t dim, const double* W1, const double* b1, const double* w2,
+                            double b2, int64_t hidden, int64_t max_len, double log_cap, int32_t* out_len,
+                            uint8_t* out_retrieved, cudaStream_t st) {
+  const int64_t threads = B * 32;
+  // shared-memory staging of W1 + the block's 8 queries (fits for the C4 shape 768 x 32)
+  const int64_t smem = dim * hidden * 8 + 8 * dim * (int64_t)sizeof(X);
+  const bool stage = smem <= 220 * 1024;
+  static int64_t smem_set = 0;
+  if (stage && smem > smem_set) {
+    CK(cudaFuncSetAttribute(k_finish<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = smem;
+  }
+  k_finish<X><<<(unsigned)((threads + 255) / 256), 256, stage ? (size_t)smem : 0, st>>>(
+      B, k, sims, lens, counts, s0, queries, dim, W1, b1, w2, b2, hidden, max_len, log_cap, out_len, out_retrieved,
+      stage);
+  CKL();
+  return ALISE_OK;
+}
+
+extern "C" int alise_predict_finish_ex(int64_t B, int k, const double* sims, const int32_t* lens,
+                                       const int32_t* counts, double s0, const void* queries, int queries_dtype,
+                                       int64_t dim, const double* W1, const double* b1, const double* w2, double b2,
+                                       int64_t hidden, int64_t max_len, double log_cap, int32_t* out_len,
+                                       uint8_t* out_retrieved, void* stream) {
+  if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
+  if (hidden < 1) return fail(ALISE_EINVAL, "hidden must be >= 1");
+  if (queries_dtype != ALISE_DB_F32 && queries_dtype != ALISE_DB_F64) return fail(ALISE_EINVAL, "bad query dtype");
+  if (B == 0) return ALISE_OK;
+  if (queries_dtype == ALISE_DB_F64)
+    return predict_finish_t(B, k, sims, lens, counts, s0, static_cast<const double*>(queries), dim, W1, b1, w2, b2,
+                            hidden, max_len, log_cap, out_len, out_retrieved, S(stream));
+  return predict_finish_t(B, k, sims, lens, counts, s0, static_cast<const float*>(queries), dim, W1, b1, w2, b2,
+                          hidden, max_len, log_cap, out_len, out_retrieved, S(stream));
+}
+
 extern "C" int alise_predict_finish(int64_t B, int k, const double* sims, const int32_t* lens,
                                     const int32_t* counts, double s0, const float* queries, int64_t dim,
                                     const double* W1, const double* b1, const double* w2, double b2,
                                     int64_t hidden, int64_t max_len, double log_cap, int32_t* out_len,
                                     uint8_t* out_retrieved, void* stream) {
-  if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
-  if (hidden < 1 || hidden > 128) return fail(ALISE_EINVAL, "hidden must be in [1, 128]");
-  if (B == 0) return ALISE_OK;
-  const int64_t threads = B * 32;
-  // shared-memory staging of W1 + the block's 8 queries (fits for the C4 shape 768 x 32)
-  const int64_t smem = dim * hidden * 8 + 8 * dim * 4;
-  const bool stage = smem <= 220 * 1024;
-  static int64_t smem_set = 0;
-  if (stage && smem > smem_set) {
-    CK(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set = smem;
-  }
-  k_finish<<<(unsigned)((threads + 255) / 256), 256, stage ? (size_t)smem : 0, S(stream)>>>(
-      B, k, sims, lens, counts, s0, queries, dim, W1, b1, w2, b2, hidden, max_len, log_cap, out_len, out_retrieved,
-      stage);
-  CKL();
-  return ALISE_OK;
+  return alise_predict_finish_ex(B, k, sims, lens, counts, s0, queries, ALISE_DB_F32, dim, W1, b1, w2, b2, hidden,
+                                 max_len, log_cap, out_len, out_retrieved, stream);
 }
 
 extern "C" int alise_embed_batch(const int64_t* tokens, const int64_t* offsets, int64_t B, int64_t dim,

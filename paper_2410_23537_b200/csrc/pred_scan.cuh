@@ -38,61 +38,84 @@ constexpr int SCAN_SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int MAXC = 512;      // candidates rescored per query
 
 // ------------------------------------------------------------------ DB maintenance
-// Append n rows at ring slots seq % capacity: fp32 master, fp16 coarse copy (zero
-// padded to dp), lengths, seqs; track an upper bound of the row L2 norms.
-__global__ void k_db_append(const float* __restrict__ vecs, const int32_t* __restrict__ lens,
+// The master copy is fp32 or float64 (T): float64 keeps the reference's float64 vectors
+// (HashingEmbedder output, predictor.py:66-100) exactly, so sims, newest() and the refit
+// data are those of the reference store (predictor.py:126).
+__device__ __forceinline__ __half to_half(float v) { return __float2half_rn(v); }
+__device__ __forceinline__ __half to_half(double v) { return __double2half(v); }
+constexpr float HALF_MAX = 65504.f;
+
+// Append n rows at ring slots seq % capacity: master (T), fp16 coarse copy (zero padded
+// to dp), lengths, seqs; track an upper bound of the row L2 norms.  A component beyond
+// the fp16 range (or a non-finite one) makes the coarse copy meaningless: Vmax becomes
+// +inf, which routes every later query through the exhaustive exact path.
+template <typename T>
+__global__ void k_db_append(const T* __restrict__ vecs, const int32_t* __restrict__ lens,
                             const int64_t* __restrict__ seqs, int64_t n, int64_t dim, int64_t dp,
-                            int64_t capacity, int64_t stride, float* __restrict__ v32, __half* __restrict__ v16,
+                            int64_t capacity, int64_t stride, T* __restrict__ vm, __half* __restrict__ v16,
                             int32_t* __restrict__ dlens, int64_t* __restrict__ dseqs,
                             unsigned int* __restrict__ vmax_bits) {
   const int64_t i = blockIdx.x;
   if (i >= n) return;
   const int64_t slot = (seqs[i] / stride) % capacity;
   double ss = 0.0;
+  bool huge = false;
   for (int64_t d = threadIdx.x; d < dp; d += blockDim.x) {
-    const float v = d < dim ? vecs[i * dim + d] : 0.f;
-    if (d < dim) v32[slot * dim + d] = v;
-    v16[slot * dp + d] = __float2half_rn(v);
+    const T v = d < dim ? vecs[i * dim + d] : T(0);
+    if (d < dim) vm[slot * dim + d] = v;
+    v16[slot * dp + d] = to_half(v);
+    huge |= !(fabs((double)v) <= (double)HALF_MAX);
     ss += (double)v * (double)v;
   }
   __shared__ double red[32];
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
+  huge = __syncthreads_or(huge);
   if (threadIdx.x == 0) {
     double t = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
     dlens[slot] = lens[i];
     dseqs[slot] = seqs[i];
-    // round the norm up so Vmax stays an upper bound
-    const float nrm = __double2float_ru(sqrt(t) * (1.0 + 1e-12));
+    // round the norm up so Vmax stays an upper bound (float64 sum of squares: relative
+    // error below (dim + 8) * 2^-53)
+    const float nrm = huge ? __int_as_float(0x7f800000)
+                           : __double2float_ru(sqrt(t) * (1.0 + (double)(dim + 64) * 0x1p-52));
     atomicMax(vmax_bits, __float_as_uint(nrm));
   }
 }
 
-// Queries: fp32 [B][dim] -> fp16 [Bp][dp] (zero padded) and 2*delta per query.
-__global__ void k_query_prep(const float* __restrict__ q, int64_t B, int64_t dim, int64_t dp,
+// Queries: T [B][dim] -> fp16 [Bp][dp] (zero padded) and 2*delta per query (+inf when
+// the query or the DB leaves the fp16 range: the rescoring then takes the exhaustive path).
+// delta bounds |coarse - sim| for the sims the rescoring ranks by (correctly rounded, or
+// in the reference's BLAS order).
+template <typename T>
+__global__ void k_query_prep(const T* __restrict__ q, int64_t B, int64_t dim, int64_t dp,
                              const unsigned int* __restrict__ vmax_bits, __half* __restrict__ q16,
-                             float* __restrict__ two_delta) {
+                             float* __restrict__ two_delta, int blas_order) {
   const int64_t i = blockIdx.x;
   double ss = 0.0;
+  bool huge = false;
   for (int64_t d = threadIdx.x; d < dp; d += blockDim.x) {
-    const float v = (i < B && d < dim) ? q[i * dim + d] : 0.f;
-    q16[i * dp + d] = __float2half_rn(v);
+    const T v = (i < B && d < dim) ? q[i * dim + d] : T(0);
+    q16[i * dp + d] = to_half(v);
+    huge |= !(fabs((double)v) <= (double)HALF_MAX);
     ss += (double)v * (double)v;
   }
   __shared__ double red[32];
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
+  huge = __syncthreads_or(huge);
   if (threadIdx.x == 0) {
     double t = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    const double qn = sqrt(t) * (1.0 + 1e-12);
+    const double qn = sqrt(t) * (1.0 + (double)(dim + 64) * 0x1p-52);
     const double V = (double)__uint_as_float(*vmax_bits);
     const double D = (double)dim;
-    const double delta = qn * V * (0x1p-10 + D * 0x1p-21) + (qn + V) * sqrt(D) * 0x1p-24;
-    two_delta[i] = __double2float_ru(2.0 * delta);
+    // (+ the reference-BLAS-order sims' own error: at most (dim / 2 + 32) 2^-52 sum|p|,
+    // sum|p| <= |q| Vmax, when the rescoring ranks by them)
+    const double delta = qn * V * (0x1p-10 + D * 0x1p-21 + (blas_order ? (D * 0.5 + 32.0) * 0x1p-52 : 0.0)) +
+                         (qn + V) * sqrt(D) * 0x1p-24;
+    two_delta[i] = (huge || !(V <= 1e30)) ? __int_as_float(0x7f800000) : __double2float_ru(2.0 * delta);
   }
 }
 
@@ -776,33 +799,60 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
 }
 
 
-// Warp-cooperative exact dot of two fp32 vectors.  Returns the float64 value and sets
-// `ok` when it is provably the correctly rounded exact sum (fp32*fp32 products are
-// exact in float64; the double-double accumulation error is < (dim+64)*2^-104*sum|p|).
+// Bound on |exact sum - (hi + lo)| of warp_exact_dot, as a multiple of sum|p| (ab):
+// with n = ceil(dim / 32) terms per lane, lo collects the two_sum errors (and, for
+// float64 inputs, the fma product residuals), so |lo| <= (n + 6) 2^-53 ab along the way,
+// and its n (2n) per-lane and 10 butterfly roundings each err by <= 2^-53 |lo|:
+//   fp32:    (n^2 + 10 n + 64) 2^-106 ab      (products exact in float64)
+//   float64: (2 n^2 + 12 n + 64) 2^-106 ab    (plus dim * 2^-1074 for underflowing residuals)
+// The fp32 factor keeps the older (dim + 64) 2^-104 where that is larger.
+__device__ __forceinline__ double dot_err_bound(double ab, int64_t dim, bool f64) {
+  const double n = (double)((dim + 31) / 32);
+  const double c = f64 ? (2.0 * n * n + 12.0 * n + 64.0) : fmax(n * n + 10.0 * n + 64.0, 4.0 * (double)(dim + 64));
+  return ab * c * 0x1p-106 * (1.0 + 0x1p-40) + (f64 ? (double)dim * 0x1p-1074 : 0.0) + 0x1p-1070;
+}
+
+// product a*b as p + r: exact for fp32 inputs (r = 0), two_prod (fma residual) for float64
+__device__ __forceinline__ double prod_split(float a, float b, double& r) {
+  r = 0.0;
+  return __dmul_rn((double)a, (double)b);
+}
+__device__ __forceinline__ double prod_split(double a, double b, double& r) {
+  const double p = __dmul_rn(a, b);
+  r = __fma_rn(a, b, -p);
+  return p;
+}
+
+// Warp-cooperative exact dot of two fp32 or two float64 vectors.  Returns the float64
+// value and sets `ok` when it is provably the correctly rounded exact sum (fp32*fp32
+// products are exact in float64; float64 products are split exactly by fma; the
+// double-double accumulation error is bounded by dot_err_bound).
 // U elements per lane in flight per step: 24 = one DRAM round trip per 768 dims (latency
 // bound small batches), 8 = fewer registers (throughput bound large batches).
-template <int U>
-__device__ double warp_exact_dot(const float* __restrict__ a, const float* __restrict__ b, int64_t dim,
-                                 bool& ok) {
+template <int U, typename T>
+__device__ double warp_exact_dot(const T* __restrict__ a, const T* __restrict__ b, int64_t dim, bool& ok) {
+  constexpr bool F64 = sizeof(T) == 8;
   const int lane = threadIdx.x & 31;
   double hi = 0.0, lo = 0.0, ab = 0.0;
   // rows are random DB rows (DRAM latency); out-of-range elements are 0, which leaves
   // hi, lo and ab unchanged
   for (int64_t d0 = lane; d0 < dim; d0 += 32 * U) {
-    float av[U], bv[U];
+    T av[U], bv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t d = d0 + 32 * u;
-      av[u] = d < dim ? __ldg(a + d) : 0.f;
-      bv[u] = d < dim ? __ldg(b + d) : 0.f;
+      av[u] = d < dim ? __ldg(a + d) : T(0);
+      bv[u] = d < dim ? __ldg(b + d) : T(0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const double p = __dmul_rn((double)av[u], (double)bv[u]);
+      double r;
+      const double p = prod_split(av[u], bv[u], r);
       double s, e;
       two_sum(hi, p, s, e);
       hi = s;
       lo = __dadd_rn(lo, e);
+      if (F64) lo = __dadd_rn(lo, r);
       ab = __dadd_rn(ab, fabs(p));
     }
   }
@@ -822,13 +872,13 @@ __device__ double warp_exact_dot(const float* __restrict__ a, const float* __res
   // r = RN(hi + lo); exact sum S = r + t + e with |e| <= bound.  RN(S) == r iff S stays
   // strictly inside r's rounding interval: half an ulp above/below, except that just
   // below a power of two the ulp halves.
-  const double bound = ab * (double)(dim + 64) * 0x1p-104 + 0x1p-1070;
+  const double bound = dot_err_bound(ab, dim, F64);
   const double ar = fabs(r);
   bool exact_sum = (ab == 0.0);
-  if (!exact_sum && ar > 0.0) {
+  if (!exact_sum && ar > 0.0 && ar < 0x1p1020) {
     const int e2 = ilogb(ar);
-    double half = ldexp(1.0, e2 - 53);
-    const bool pow2 = ar == ldexp(1.0, e2);
+    double half = ldexp(1.0, (e2 < -1022 ? -1022 : e2) - 53);
+    const bool pow2 = ar == ldexp(1.0, e2) && e2 > -1022;
     const bool toward_zero = (t != 0.0) && ((t < 0.0) != (r < 0.0));
     if (pow2 && toward_zero) half *= 0.5;
     exact_sum = fabs(t) + bound < half;
@@ -974,20 +1024,229 @@ __device__ __noinline__ double warp_exact_dot_super(const float* __restrict__ a,
   return super_round(acc);
 }
 
-// Per-query lower bound of the final coarse k-th left by a scan (shared k-th, rank
-// slots); -inf when none (or for an empty shard: gkth == nullptr).  Every shard's bound
-// is below the global k-th, so their max is a global bound (sharded search).
+// Exact correctly rounded dot product of two float64 vectors (the rare fallback when
+// the double-double certificate fails): every product m_a m_b 2^(e_a + e_b) (106-bit
+// integer significand) is added into a 4480-bit two's complement fixed-point
+// accumulator with LSB 2^-2240, which holds any sum of products of finite doubles
+// (exponents of products >= -2148, magnitudes < 2^2048 * dim).  Lane 0 of the warp
+// computes it (local memory); the result is broadcast.
+constexpr int BIG_L = 70;
+constexpr int BIG_BASE = -2240;
+
+__device__ __forceinline__ void big_add_at(uint64_t* acc, int li, uint64_t w0, uint64_t w1, uint64_t w2, bool neg) {
+  // acc += (w2:w1:w0) << (64 li), or -= when neg (two's complement; carries ripple up)
+  const uint64_t w[3] = {w0, w1, w2};
+  if (!neg) {
+    uint64_t c = 0;
+    for (int j = 0; j < 3; ++j) {
+      const uint64_t x = acc[li + j];
+      const uint64_t y = x + w[j];
+      const uint64_t c1 = y < x;
+      const uint64_t z = y + c;
+      c = c1 | (z < y);
+      acc[li + j] = z;
+    }
+    for (int i = li + 3; c && i < BIG_L; ++i) c = (++acc[i] == 0);
+  } else {
+    uint64_t bw = 0;
+    for (int j = 0; j < 3; ++j) {
+      const uint64_t x = acc[li + j];
+      const uint64_t y = x - w[j];
+      const uint64_t b1 = x < w[j];
+      const uint64_t z = y - bw;
+      bw = b1 | (y < bw);
+      acc[li + j] = z;
+    }
+    for (int i = li + 3; bw && i < BIG_L; ++i) bw = (acc[i]-- == 0);
+  }
+}
+
+__device__ __forceinline__ void dbl_parts(double v, uint64_t& m, int& e) {
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  const int ex = (int)((b >> 52) & 2047);
+  m = b & ((1ull << 52) - 1);
+  if (ex) { m |= 1ull << 52; e = ex - 1075; } else { e = -1074; }
+}
+
+// Round an L-limb two's complement fixed-point value (LSB 2^base) to float64, RN-even,
+// with gradual underflow and overflow to inf.
+template <int L>
+__device__ double fixed_round(uint64_t* acc, int base) {
+  const bool neg = (acc[L - 1] >> 63) != 0;
+  if (neg) {
+    uint64_t c = 1;
+    for (int i = 0; i < L; ++i) {
+      acc[i] = ~acc[i] + c;
+      c = (c && acc[i] == 0) ? 1 : 0;
+    }
+  }
+  int top = L - 1;
+  while (top >= 0 && acc[top] == 0) --top;
+  if (top < 0) return 0.0;
+  const int msb = top * 64 + (63 - __clzll(acc[top]));
+  // lowest kept bit: 53 significant bits, but not below 2^-1074
+  int w = msb - 52;
+  if (w + base < -1074) w = -1074 - base;
+  auto bit = [&](int p) -> uint64_t { return p < 0 ? 0ull : (acc[p >> 6] >> (p & 63)) & 1ull; };
+  uint64_t mant;
+  if (w < 0) {
+    mant = acc[0] << (-w);
+  } else {
+    const int li = w >> 6, sh = w & 63;
+    mant = acc[li] >> sh;
+    if (sh && li + 1 < L) mant |= acc[li + 1] << (64 - sh);
+  }
+  const int nbits = msb - w + 1;  // <= 53
+  mant = nbits <= 0 ? 0ull : (mant & ((1ull << nbits) - 1));
+  const uint64_t guard = bit(w - 1);
+  bool sticky = false;
+  const int sp = w - 2;  // bits [0, sp] are sticky
+  if (sp >= 0) {
+    for (int i = 0; i < (sp >> 6); ++i) sticky |= acc[i] != 0;
+    const int r = sp & 63;
+    const uint64_t maskp = (r == 63) ? ~0ull : ((1ull << (r + 1)) - 1);
+    sticky |= (acc[sp >> 6] & maskp) != 0;
+  }
+  if (guard && (sticky || (mant & 1))) ++mant;  // a carry to 2^53 stays exact in ldexp
+  const double v = ldexp((double)mant, w + base);
+  return neg ? -v : v;
+}
+
+__device__ __noinline__ double exact_dot_f64_big(const double* __restrict__ a, const double* __restrict__ b,
+                                                 int64_t dim) {
+  uint64_t acc[BIG_L];
+  for (int i = 0; i < BIG_L; ++i) acc[i] = 0;
+  for (int64_t d = 0; d < dim; ++d) {
+    const double x = a[d], y = b[d];
+    if (x == 0.0 || y == 0.0) continue;
+    uint64_t mx, my;
+    int ex, ey;
+    dbl_parts(x, mx, ex);
+    dbl_parts(y, my, ey);
+    const uint64_t lo = mx * my, hi = __umul64hi(mx, my);  // < 2^106
+    const int pos = ex + ey - BIG_BASE;                     // >= 92
+    const int li = pos >> 6, sh = pos & 63;
+    const uint64_t w0 = lo << sh;
+    const uint64_t w1 = sh ? ((lo >> (64 - sh)) | (hi << sh)) : hi;
+    const uint64_t w2 = sh ? (hi >> (64 - sh)) : 0ull;
+    big_add_at(acc, li, w0, w1, w2, (x < 0) != (y < 0));
+  }
+  return fixed_round<BIG_L>(acc, BIG_BASE);
+}
+
+// Warp-uniform fallback dispatch: fp32 rows use the warp-parallel 640-bit accumulator,
+// float64 rows the lane-0 4480-bit one.
+__device__ __forceinline__ double warp_exact_dot_fallback(const float* a, const float* b, int64_t dim) {
+  return warp_exact_dot_super(a, b, dim);
+}
+__device__ __forceinline__ double warp_exact_dot_fallback(const double* a, const double* b, int64_t dim) {
+  double v = 0.0;
+  if ((threadIdx.x & 31) == 0) v = exact_dot_f64_big(a, b, dim);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
+// ------------------------------------------------------------------ reference BLAS order
+// Optional "blas" similarity order: the float64 sims are computed with the exact
+// operation sequence of the BLAS call behind the reference's scan (predictor.py:158,
+// numpy -> OpenBLAS 0.3.30 dgemv_t on x86-64; restated and pinned against numpy in
+// oracle/blas_order.c), so ties that are exact in real arithmetic (common for the
+// reference's hashed prompt embeddings) break exactly as in the reference.  Row r of
+// the reference's array is ring slot seq % ref_cap of a store holding ref_n rows.
+struct BlasRef {
+  int on;          // 0: correctly rounded sims (default); 1: reference BLAS order
+  int threads;     // OpenBLAS threads of the reference host (used when ref_n * dim >= 460800)
+  int64_t ref_cap; // capacity of the reference (global) ring
+  int64_t ref_n;   // rows of the reference array (global store size)
+};
+
+__device__ __forceinline__ int blas_kind(int64_t r, int64_t n, int64_t d, int threads) {
+  const int T = (n * d < 460800) ? 1 : (threads < 1 ? 1 : threads);
+  int64_t start = 0, left = n;
+  for (int t = 0; left > 0; ++t) {
+    int64_t w = (left + (T - t) - 1) / (T - t > 0 ? T - t : 1);
+    if (w < 4) w = 4;
+    if (left < w) w = left;
+    if (r < start + w) {
+      const int64_t j = r - start, w4 = w & ~(int64_t)3;
+      return j < w4 ? 0 : (((w & 2) && j < w4 + 2) ? 1 : 2);
+    }
+    start += w;
+    left -= w;
+  }
+  return 2;
+}
+
+// One thread: row . x in the order of OpenBLAS kernel `kind` (0: 4x4, FMA accumulators;
+// 1: 4x2; 2: 4x1), 2048-element blocks, then the d & 3 tail (oracle_blas_dot).
+template <typename T>
+__device__ double blas_dot(const T* __restrict__ a, const T* __restrict__ x, int64_t d, int kind) {
+  const int64_t m3 = d & 3, m1 = d - m3;
+  double y = 0.0;
+  for (int64_t b = 0; b < m1; b += 2048) {
+    const int64_t h = b + 2048 < m1 ? b + 2048 : m1;
+    double bs;
+    if (kind == 0) {
+      double c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+      for (int64_t i = b; i < h; i += 4) {
+        c0 = __fma_rn((double)a[i], (double)x[i], c0);
+        c1 = __fma_rn((double)a[i + 1], (double)x[i + 1], c1);
+        c2 = __fma_rn((double)a[i + 2], (double)x[i + 2], c2);
+        c3 = __fma_rn((double)a[i + 3], (double)x[i + 3], c3);
+      }
+      bs = __dadd_rn(__dadd_rn(c0, c2), __dadd_rn(c1, c3));
+    } else if (kind == 1) {
+      double c0 = 0, c1 = 0;
+      for (int64_t i = b; i < h; i += 2) {
+        c0 = __dadd_rn(c0, __dmul_rn((double)a[i], (double)x[i]));
+        c1 = __dadd_rn(c1, __dmul_rn((double)a[i + 1], (double)x[i + 1]));
+      }
+      bs = __dadd_rn(c0, c1);
+    } else {
+      double c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+      for (int64_t i = b; i < h; i += 4) {
+        c0 = __dadd_rn(c0, __dmul_rn((double)a[i], (double)x[i]));
+        c1 = __dadd_rn(c1, __dmul_rn((double)a[i + 1], (double)x[i + 1]));
+        c2 = __dadd_rn(c2, __dmul_rn((double)a[i + 2], (double)x[i + 2]));
+        c3 = __dadd_rn(c3, __dmul_rn((double)a[i + 3], (double)x[i + 3]));
+      }
+      bs = __dadd_rn(__dadd_rn(c0, c2), __dadd_rn(c1, c3));
+    }
+    y = __dadd_rn(y, bs);
+  }
+  const T* t = a + m1;
+  const T* u = x + m1;
+  if (m3 == 1) {
+    y = __fma_rn((double)t[0], (double)u[0], y);
+  } else if (m3 == 2) {
+    y = __dadd_rn(y, __fma_rn((double)t[0], (double)u[0], __dmul_rn((double)t[1], (double)u[1])));
+  } else if (m3 == 3) {
+    y = __dadd_rn(y, __fma_rn((double)t[2], (double)u[2],
+                               __fma_rn((double)t[0], (double)u[0], __dmul_rn((double)t[1], (double)u[1]))));
+  }
+  return y;
+}
+
+// Per-query lower bound of the global EXACT k-th score left by a shard's scan: the scan
+// leaves L (shared k-th, rank slots) such that k rows of this shard have coarse score >=
+// L, hence exact score >= L - delta_self, so the global exact k-th is >= L - delta_self.
+// -inf when none (an empty shard: gkth == nullptr; or a query on the exhaustive path).
+// After an all-reduce (max) E over the shards, a row of shard t can enter the global
+// top-k only if its coarse score is >= E - delta_t (k_rescore), whatever the other
+// shards' row norms are.
 __global__ void k_bounds(int64_t B, int k, const uint32_t* __restrict__ gkth, const uint32_t* __restrict__ gslot,
-                         float* __restrict__ out) {
+                         const float* __restrict__ two_delta, float* __restrict__ out) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= B) return;
-  float L = -__int_as_float(0x7f800000);
+  const float NEG = -__int_as_float(0x7f800000);
+  float L = NEG;
   if (gkth) {
     const uint32_t g0 = gkth[q];
     if (g0) L = ord_val(g0);
     uint32_t mn = 0xffffffffu;
     for (int x = 0; x < k; ++x) mn = min(mn, gslot[(size_t)q * KMAX + x]);
     if (mn) L = fmaxf(L, ord_val(mn));
+    const float td = two_delta[q];
+    L = (td <= 3.0e38f && L > NEG) ? __fsub_rd(L, 0.5f * td) : NEG;
   }
   out[q] = L;
 }
@@ -996,15 +1255,15 @@ __device__ __forceinline__ int nw_last(unsigned bd) { return (int)(bd >> 5) - 1;
 
 // Per query: global coarse k-th from the splits' top lists, candidate compaction,
 // exact rescoring, (-sim, seq) order.  Block = 256 threads.
-template <int U>
+template <int U, typename T>
 __global__ void __launch_bounds__(256)
-k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
-          const float* __restrict__ v32, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
+k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const T* __restrict__ qx,
+          const T* __restrict__ vm, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
           const float* __restrict__ two_delta, const float* __restrict__ cand_s, const int32_t* __restrict__ cand_r,
           const int32_t* __restrict__ cand_n, const float* __restrict__ topc, const float* __restrict__ ext,
           double* __restrict__ out_sim, int64_t* __restrict__ out_seq, int32_t* __restrict__ out_len,
           int32_t* __restrict__ out_count, int32_t* __restrict__ need_exhaustive,
-          unsigned int* __restrict__ inexact_count) {
+          unsigned int* __restrict__ inexact_count, const BlasRef blas) {
   const int64_t q = blockIdx.x;
   if (q >= B) return;
   __shared__ float s_top[4096];  // list values >= the bound (more: exhaustive path)
@@ -1022,6 +1281,10 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   const int n_splits = smul * splits_of_block(wa, (int)(q / qblk));
   const int64_t kk = k < n_rows ? k : n_rows;
   const float NEG = -__int_as_float(0x7f800000);
+  if (!(two_delta[q] <= 3.0e38f)) {  // outside the fp16 range: no coarse bound holds
+    if (tid == 0) need_exhaustive[q] = 1;
+    return;
+  }
 #ifdef ALISE_RESCORE_TIMING
   const long long T0 = clock64();
 #endif
@@ -1137,9 +1400,11 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
 #ifdef ALISE_RESCORE_TIMING
   const long long T1 = clock64();
 #endif
-  // (a bound from other shards can only raise the threshold: rows below it minus
-  // 2*delta cannot enter the global top-k)
-  const float thr = fmaxf(s_kth, ext ? ext[q] : -__int_as_float(0x7f800000)) - two_delta[q];
+  // (a bound from other shards can only raise the threshold: ext is an exact-score
+  // lower bound of the global k-th, so rows with coarse score below ext - delta cannot
+  // enter the global top-k)
+  const float td = two_delta[q];
+  const float thr = fmaxf(__fsub_rd(s_kth, td), ext ? __fsub_rd(ext[q], 0.5f * td) : NEG);
   // 3) gather candidates above the final threshold: the (split, slot) entries are
   //    flattened over the whole block through the prefix sum of the counts, so every
   //    candidate load is in flight at once (candidate order is irrelevant: step 5 ranks)
@@ -1150,7 +1415,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
 #pragma unroll
     for (int u = 0; u < 8; ++u) {  // 8 candidate loads in flight per thread
       const int i = i0 + u * (int)blockDim.x;
-      sv[u] = -__int_as_float(0x7f800000);
+      sv[u] = __int_as_float(0x7fffffff);  // NaN: past the end never passes, even thr = -inf
       ev[u] = 0;
       if (i < total) {
         int lo = 0, hi = n_splits;  // largest sp with s_off[sp] <= i
@@ -1179,28 +1444,40 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
     if (tid == 0) need_exhaustive[q] = 1;
     return;
   }
-  // 4) exact float64 scores, one warp per candidate.  The warp first prefetches all of
-  //    its candidate rows into L2 (random DB rows: one DRAM round trip for all of them
-  //    instead of one per candidate)
-  for (int c = warp; c < n; c += blockDim.x >> 5) {
-    const char* rp = reinterpret_cast<const char*>(v32 + (size_t)s_rows[c] * dim);
-    for (int64_t off = (int64_t)lane * 128; off < dim * 4; off += 32 * 128)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + off));
-  }
-  for (int c = warp; c < n; c += blockDim.x >> 5) {
-    const int row = s_rows[c];
-    bool ok;
-    double sim = warp_exact_dot<U>(v32 + (size_t)row * dim, q32 + q * dim, dim, ok);
-    if (!ok) {  // warp-uniform: the certificate is computed from butterfly-reduced sums
-      sim = warp_exact_dot_super(v32 + (size_t)row * dim, q32 + q * dim, dim);
-      if (lane == 0) atomicAdd(inexact_count, 1u);
+  if (blas.on) {
+    // 4') reference BLAS-order float64 scores, one thread per candidate
+    for (int c = tid; c < n; c += blockDim.x) {
+      const int row = s_rows[c];
+      const int64_t sq = seqs[row];
+      const int kind = blas_kind(sq % blas.ref_cap, blas.ref_n, dim, blas.threads);
+      s_sim[c] = blas_dot<T>(vm + (size_t)row * dim, qx + q * dim, dim, kind);
+      s_seq[c] = sq;
     }
-    if (lane == 0) {
-      s_sim[c] = sim;
-      s_seq[c] = seqs[row];
+    __syncthreads();
+  } else {
+    // 4) exact float64 scores, one warp per candidate.  The warp first prefetches all of
+    //    its candidate rows into L2 (random DB rows: one DRAM round trip for all of them
+    //    instead of one per candidate)
+    for (int c = warp; c < n; c += blockDim.x >> 5) {
+      const char* rp = reinterpret_cast<const char*>(vm + (size_t)s_rows[c] * dim);
+      for (int64_t off = (int64_t)lane * 128; off < dim * (int64_t)sizeof(T); off += 32 * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + off));
     }
+    for (int c = warp; c < n; c += blockDim.x >> 5) {
+      const int row = s_rows[c];
+      bool ok;
+      double sim = warp_exact_dot<U, T>(vm + (size_t)row * dim, qx + q * dim, dim, ok);
+      if (!ok) {  // warp-uniform: the certificate is computed from butterfly-reduced sums
+        sim = warp_exact_dot_fallback(vm + (size_t)row * dim, qx + q * dim, dim);
+        if (lane == 0) atomicAdd(inexact_count, 1u);
+      }
+      if (lane == 0) {
+        s_sim[c] = sim;
+        s_seq[c] = seqs[row];
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
 #ifdef ALISE_RESCORE_TIMING
   const long long T3 = clock64();
 #endif
@@ -1217,6 +1494,20 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
     }
   }
   if (tid == 0) out_count[q] = (int32_t)(n < kk ? n : kk);
+#ifdef ALISE_RESCORE_DEBUG
+  __syncthreads();
+  if (tid == 0) {
+    printf("[rescore q=%lld] n=%d kk=%lld s_kth=%.9g thr=%.9g total=%d splits=%d\n", (long long)q, n, (long long)kk,
+           s_kth, thr, total, n_splits);
+    for (int c = 0; c < n && c < 12; ++c) printf("  cand row=%d seq=%lld sim=%.17g\n", s_rows[c], (long long)s_seq[c], s_sim[c]);
+    for (int sp = 0; sp < n_splits; ++sp) {
+      const int cn = cand_n[(size_t)sp * Bp + q];
+      printf("  split %d cand_n=%d off=%d:", sp, cn, s_off[sp]);
+      for (int u = 0; u < cn && u < 40; ++u) printf(" %d", cand_r[((size_t)sp * Bp + q) * CAP + u]);
+      printf("\n");
+    }
+  }
+#endif
 #ifdef ALISE_RESCORE_TIMING
   if (tid == 0 && (q < 4 || T3 - T2 > 40000))
     printf("[rescore q=%lld] splits=%d total=%d n=%d cycles: select+counts %lld gather %lld dots %lld rank %lld\n",
@@ -1226,11 +1517,13 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
 
 // Exhaustive exact top-k for queries flagged by k_rescore (candidate overflow from
 // heavy ties); a no-op block for every other query.  Slow but exact.
+template <typename T>
 __global__ void __launch_bounds__(256)
-k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restrict__ q32,
-             const float* __restrict__ v32, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
+k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const T* __restrict__ qx,
+             const T* __restrict__ vm, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
              int32_t* __restrict__ need, double* __restrict__ out_sim, int64_t* __restrict__ out_seq,
-             int32_t* __restrict__ out_len, int32_t* __restrict__ out_count, unsigned int* __restrict__ inexact_count) {
+             int32_t* __restrict__ out_len, int32_t* __restrict__ out_count, unsigned int* __restrict__ inexact_count,
+             const BlasRef blas) {
   const int64_t q = blockIdx.x;
   if (q >= B || !need[q]) return;
   __shared__ double s_sim[8 * KMAX];
@@ -1242,12 +1535,29 @@ k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restr
   int64_t tseq[KMAX];
   int trow[KMAX];
   for (int i = 0; i < KMAX; ++i) { tsim[i] = -__longlong_as_double(0x7ff0000000000000ll); tseq[i] = INT64_MAX; trow[i] = -1; }
-  for (int64_t row = warp; row < n_rows; row += blockDim.x >> 5) {
-    bool ok;
-    double sim = warp_exact_dot<8>(v32 + row * dim, q32 + q * dim, dim, ok);
-    if (!ok) {
-      sim = warp_exact_dot_super(v32 + row * dim, q32 + q * dim, dim);
-      if (lane == 0) atomicAdd(inexact_count, 1u);
+  const int64_t nw = blockDim.x >> 5;
+  const int64_t row_end = blas.on ? (n_rows + 32 * nw - 1) / (32 * nw) * (32 * nw) : n_rows;
+  for (int64_t row0 = blas.on ? warp * 32 : warp; row0 < row_end; row0 += blas.on ? 32 * nw : nw) {
+    // blas order: each lane scores one row of the warp's 32 (reference BLAS order), lane
+    // 0 then inserts them in row order; exact order: the warp scores one row together
+    double bsim = 0.0;
+    if (blas.on && row0 + lane < n_rows) {
+      const int64_t r = row0 + lane;
+      bsim = blas_dot<T>(vm + r * dim, qx + q * dim, dim, blas_kind(seqs[r] % blas.ref_cap, blas.ref_n, dim, blas.threads));
+    }
+    const int n_here = blas.on ? (int)min((int64_t)32, n_rows - row0) : 1;
+    for (int u = 0; u < n_here; ++u) {
+    const int64_t row = blas.on ? row0 + u : row0;
+    double sim;
+    if (blas.on) {
+      sim = __shfl_sync(0xffffffffu, bsim, u);
+    } else {
+      bool ok;
+      sim = warp_exact_dot<8, T>(vm + row * dim, qx + q * dim, dim, ok);
+      if (!ok) {
+        sim = warp_exact_dot_fallback(vm + row * dim, qx + q * dim, dim);
+        if (lane == 0) atomicAdd(inexact_count, 1u);
+      }
     }
     if (lane == 0) {
       double cs = sim;
@@ -1260,6 +1570,7 @@ k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const float* __restr
           cs = a; cq = b; cr = c;
         }
       }
+    }
     }
   }
   if (lane == 0)
@@ -1335,8 +1646,9 @@ __device__ double np_sum(const double* v, int n) {
 // Warp per query.  Retrieval branch (predictor.py:314-324) when any neighbour has sim
 // >= s0, else the float64 MLP (predictor.py:209-219): h_j = tanh(b1_j + sum_d x_d W1[d,j])
 // with the sum in index order, out = b2 + sum_j h_j w2_j in index order.
+template <typename X>
 __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, const int32_t* __restrict__ lens,
-                         const int32_t* __restrict__ counts, double s0, const float* __restrict__ x, int64_t dim,
+                         const int32_t* __restrict__ counts, double s0, const X* __restrict__ x, int64_t dim,
                          const double* __restrict__ W1, const double* __restrict__ b1, const double* __restrict__ w2,
                          double b2, int64_t hidden, int64_t max_len, double log_cap, int32_t* __restrict__ out_len,
                          uint8_t* __restrict__ out_ret, bool stage) {
@@ -1359,7 +1671,7 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
     }
     if (__syncthreads_or(mlp)) {
       const int64_t nw = dim * hidden;
-      float* xs0 = reinterpret_cast<float*>(smem_fin + nw);
+      X* xs0 = reinterpret_cast<X*>(smem_fin + nw);
       const int64_t q0 = (int64_t)blockIdx.x * (blockDim.x >> 5);
       const int64_t nq = B - q0 < (int64_t)(blockDim.x >> 5) ? B - q0 : (int64_t)(blockDim.x >> 5);
       // one bulk (TMA) copy of W1 and of the block's query rows when the addresses allow
@@ -1374,7 +1686,7 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
         }
         __syncthreads();
         if (threadIdx.x == 0) {
-          const uint32_t wb = (uint32_t)(nw * 8), xb = (uint32_t)(nq * dim * 4);
+          const uint32_t wb = (uint32_t)(nw * 8), xb = (uint32_t)(nq * dim * sizeof(X));
           sm100::mbar_arrive_expect_tx(&fin_bar, wb + xb);
           for (uint32_t o = 0; o < wb; o += 32768)
             sm100::bulk_g2s(reinterpret_cast<uint8_t*>(smem_fin) + o, reinterpret_cast<const uint8_t*>(W1) + o,
@@ -1384,7 +1696,7 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
         sm100::mbar_wait(&fin_bar, 0);
       } else {
         for (int64_t i = threadIdx.x; i < nw; i += blockDim.x) smem_fin[i] = W1[i];
-        float* xs = xs0 + (threadIdx.x >> 5) * dim;
+        X* xs = xs0 + (threadIdx.x >> 5) * dim;
         if (q < B)
           for (int64_t i = lane; i < dim; i += 32) xs[i] = x[q * dim + i];
         __syncthreads();
@@ -1422,50 +1734,54 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
     }
     return;
   }
-  // fallback MLP: lane j computes hidden units j, j+32, ...  The dependent index-order
-  // chain reads W1 and x from shared memory when the block staged them (one L2 round
-  // trip per block instead of one per term).
-  const float* xq = x + q * dim;
+  // fallback MLP: lane j computes hidden units j, j+32, ... in chunks of 128 units.
+  // The dependent index-order chain reads W1 and x from shared memory when the block
+  // staged them (one L2 round trip per block instead of one per term).
+  const X* xq = x + q * dim;
   const double* Wm = W1;
   if (smem_w1) {
     Wm = smem_w1;
-    xq = reinterpret_cast<const float*>(smem_w1 + dim * hidden) + (threadIdx.x >> 5) * dim;
+    xq = reinterpret_cast<const X*>(smem_w1 + dim * hidden) + (threadIdx.x >> 5) * dim;
   }
   double out = 0.0;
-  double hv[4];
-  const int per = (int)((hidden + 31) / 32);
-  for (int t = 0; t < per && t < 4; ++t) {
-    const int64_t j = lane + 32 * t;
-    double acc = 0.0;
-    if (j < hidden) {
-      // products of 32 terms first (independent: loads, converts and multiplies
-      // pipeline), then their index-order adds: the chain runs at the add latency
-      int64_t d0 = 0;
-      for (; d0 + 32 <= dim; d0 += 32) {
-        double pr[32];
+  for (int64_t j0 = 0; j0 < hidden; j0 += 128) {
+    double hv[4];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) pr[u] = __dmul_rn((double)xq[d0 + u], Wm[(d0 + u) * hidden + j]);
+    for (int t = 0; t < 4; ++t) {
+      const int64_t j = j0 + lane + 32 * t;
+      double acc = 0.0;
+      if (j < hidden) {
+        // products of 32 terms first (independent: loads, converts and multiplies
+        // pipeline), then their index-order adds: the chain runs at the add latency
+        int64_t d0 = 0;
+        for (; d0 + 32 <= dim; d0 += 32) {
+          double pr[32];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, pr[u]);
+          for (int u = 0; u < 32; ++u) pr[u] = __dmul_rn((double)xq[d0 + u], Wm[(d0 + u) * hidden + j]);
+#pragma unroll
+          for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, pr[u]);
+        }
+        for (int64_t d = d0; d < dim; ++d) acc = __dadd_rn(acc, __dmul_rn((double)xq[d], Wm[d * hidden + j]));
+        hv[t] = tanh(__dadd_rn(acc, b1[j]));
+      } else {
+        hv[t] = 0.0;
       }
-      for (int64_t d = d0; d < dim; ++d) acc = __dadd_rn(acc, __dmul_rn((double)xq[d], Wm[d * hidden + j]));
-      hv[t] = tanh(__dadd_rn(acc, b1[j]));
-    } else {
-      hv[t] = 0.0;
     }
-  }
 #ifdef ALISE_FINISH_TIMING
-  F2 = clock64();
+    F2 = clock64();
 #endif
-  // sequential sum over hidden units in index order (lane 0 gathers)
-  for (int64_t j = 0; j < hidden; ++j) {
-    const int t = (int)(j / 32), src = (int)(j % 32);
-    double hj = 0.0;
-    for (int tt = 0; tt < 4; ++tt) {
-      const double v = __shfl_sync(0xffffffffu, hv[tt], src);
-      if (tt == t) hj = v;
+    // sequential sum over the chunk's hidden units in index order (every lane)
+    const int64_t jn = hidden - j0 < 128 ? hidden - j0 : 128;
+    for (int64_t jj = 0; jj < jn; ++jj) {
+      const int t = (int)(jj / 32), src = (int)(jj % 32);
+      double hj = 0.0;
+#pragma unroll
+      for (int tt = 0; tt < 4; ++tt) {
+        const double v = __shfl_sync(0xffffffffu, hv[tt], src);
+        if (tt == t) hj = v;
+      }
+      out = __dadd_rn(out, __dmul_rn(hj, w2[j0 + jj]));
     }
-    out = __dadd_rn(out, __dmul_rn(hj, w2[j]));
   }
   if (lane == 0) {
     out = __dadd_rn(out, b2);

@@ -4,16 +4,21 @@ Reference: /root/reference/pkg/src/servesim/predictor.py.  Same names, argument
 meanings and errors.  The hot path — ``VectorStore.search`` (predictor.py:154-163)
 and ``LengthPredictor.predict_vector`` (predictor.py:311-325) — runs on the GPU:
 
-* the store is a device FIFO ring (fp32 master + fp16 coarse copy, slot = seq % cap);
+* the store is a device FIFO ring (float64 master like the reference, or fp32 for
+  fp32 embedding DBs; plus an fp16 coarse copy; slot = seq % cap);
 * ``search`` / ``search_batch`` compute the exact top-k by (-sim, seq): a tcgen05
   fp16 coarse scan with a provable candidate margin, then correctly rounded float64
-  rescoring of the candidates (sims are the exact dot products of the stored fp32
+  rescoring of the candidates (sims are the exact dot products of the stored
   vectors, rounded once to float64);
 * ``predict_batch`` fuses the aggregate (numpy's summation order, half-even
-  rounding) with the float64 all-MLP fallback in one kernel.
+  rounding) with the float64 all-MLP fallback in one kernel, reading the query in
+  its own precision.
 
-Vectors are stored in fp32 (the reference keeps float64); sims therefore match the
-reference to ~1e-7 relative, and exactly the restated oracle (oracle/pred_oracle.py).
+With the default float64 store the vectors, ``newest`` (the refit data) and the MLP
+inputs are the reference's own float64 values; sims are correctly rounded where the
+reference's BLAS dot may differ in the last bit, so results equal the restated oracle
+(oracle/pred_oracle.py) exactly and the reference wherever its BLAS rounding does not
+flip a threshold or a tie.
 
 Training of the fallback regressor (``FallbackRegressor.fit``, predictor.py:221-264)
 and the hashing embedder (predictor.py:66-100) are host-side producers of weights /
@@ -153,26 +158,87 @@ def load_precomputed_embeddings(path) -> dict:
 
 
 # ----------------------------------------------------------------- device store
+DB_F32, DB_F64 = 0, 1  # ALISE_DB_F32 / ALISE_DB_F64 (include/alise_b200.h)
+ORDERS = {"exact": 0, "blas": 1}  # ALISE_ORDER_EXACT / ALISE_ORDER_BLAS
+
+
+def openblas_threads() -> int:
+    """OpenBLAS thread count of this host's numpy (what the reference's scan runs on)."""
+    try:
+        from threadpoolctl import threadpool_info
+        for info in threadpool_info():
+            if info.get("internal_api") == "openblas":
+                return int(info["num_threads"])
+    except Exception:
+        pass
+    import os
+    return os.cpu_count() or 1
+
+
+def _dtype_code(dtype) -> int:
+    dt = np.dtype(dtype)
+    if dt == np.float64:
+        return DB_F64
+    if dt == np.float32:
+        return DB_F32
+    raise PredictorError(f"unsupported store dtype {dt} (float32 or float64)")
+
+
+def _torch_dtype(code: int):
+    import torch
+    return torch.float64 if code == DB_F64 else torch.float32
+
+
+def _host_lens(lens):
+    """Lengths as a host int64 array when they are host data (no device sync)."""
+    import torch
+    if isinstance(lens, torch.Tensor):
+        return None if lens.is_cuda else lens.numpy().astype(np.int64).reshape(-1)
+    return np.asarray(lens, dtype=np.int64).reshape(-1)
+
+
 class VectorStore:
     """FIFO-bounded device store of (vector, observed length) (predictor.py:120-189).
 
     Same semantics: slot = seq % capacity, ``add`` returns the insert sequence,
     ``search`` returns (sims f64, lens i64, seqs i64) ordered by (-sim, seq).
+
+    ``dtype`` is the master copy's type: float64 (default) keeps the reference's
+    np.float64 vectors exactly (predictor.py:126), so sims are the correctly rounded
+    dot products of the very vectors the reference stores and ``newest`` returns them
+    bit for bit; float32 halves the footprint for fp32 embedding DBs (BASELINE C4).
+    Queries are converted to the master type.
     """
 
-    def __init__(self, dimension: int, capacity: int, device: int | None = None):
+    def __init__(self, dimension: int, capacity: int, device: int | None = None, dtype=np.float64,
+                 order: str = "exact", blas_threads: int | None = None):
         import torch
 
         _lib.require_cuda()
         self.dimension = int(dimension)
         self.capacity = int(capacity)
+        self.dtype = np.dtype(dtype)
+        self._code = _dtype_code(self.dtype)
         self.device = torch.cuda.current_device() if device is None else device
         h = _lib.C.c_void_p()
-        _lib.call("alise_db_create", self.device, self.capacity, self.dimension, _lib.C.byref(h))
+        _lib.call("alise_db_create_ex", self.device, self.capacity, self.dimension, self._code, _lib.C.byref(h))
         self._h = h.value
         self.size = 0
         self.next_seq = 0
-        # host mirror of lengths/seqs is not kept; vectors are read back on demand
+        self.set_order(order, blas_threads)
+
+    def set_order(self, order: str = "exact", blas_threads: int | None = None, ref_capacity: int = 0,
+                  ref_size: int = -1):
+        """Which float64 sims searches rank by and return: "exact" (the correctly rounded
+        dot products; default) or "blas" (the reference's own values: the operation order
+        of numpy -> OpenBLAS dgemv_t behind predictor.py:158, so real-arithmetic ties break
+        as in the reference; blas_threads = the reference host's OpenBLAS threads)."""
+        if order not in ORDERS:
+            raise PredictorError(f"order must be one of {sorted(ORDERS)}")
+        self.order = order
+        self.blas_threads = int(blas_threads or openblas_threads())
+        _lib.call("alise_db_set_order", self._h, ORDERS[order], self.blas_threads, int(ref_capacity),
+                  int(ref_size))
 
     def __len__(self):
         return self.size
@@ -189,6 +255,12 @@ class VectorStore:
         import torch
         return torch.device("cuda", self.device)
 
+    def _as_rows(self, vectors):
+        """Rows on this store's device in the master dtype, [n, dimension] contiguous."""
+        import torch
+        v = torch.as_tensor(vectors if isinstance(vectors, torch.Tensor) else np.asarray(vectors))
+        return v.to(self._dev(), _torch_dtype(self._code)).reshape(-1, self.dimension).contiguous()
+
     def add(self, vector, observed_len: int) -> int:
         if observed_len < 1:
             raise PredictorError("observed_len must be >= 1")
@@ -196,39 +268,46 @@ class VectorStore:
         self.add_batch(np.asarray(vector, dtype=np.float64)[None, :], [int(observed_len)])
         return seq
 
-    def add_batch(self, vectors, lens, stream=None):
-        """Append rows in insert order (batched VectorStore.add)."""
+    def add_batch(self, vectors, lens, stream=None, seqs=None):
+        """Append rows in insert order (batched VectorStore.add).  ``seqs`` (host int64,
+        increasing) restores records under their original sequence numbers (snapshots)."""
         import torch
 
-        v = torch.as_tensor(np.asarray(vectors) if not isinstance(vectors, torch.Tensor) else vectors)
-        v = v.to(self._dev(), torch.float32).reshape(-1, self.dimension).contiguous()
-        ln = torch.as_tensor(np.asarray(lens) if not isinstance(lens, torch.Tensor) else lens)
-        ln = ln.to(self._dev(), torch.int32).reshape(-1).contiguous()
+        v = self._as_rows(vectors)
+        hl = _host_lens(lens)
+        ln = torch.as_tensor(hl if hl is not None else lens).to(self._dev(), torch.int32).reshape(-1).contiguous()
         n = v.shape[0]
         if ln.numel() != n:
             raise PredictorError("vectors and lengths differ in count")
-        if n and int(ln.min().item()) < 1:
+        if n and (hl.min() if hl is not None else int(ln.min().item())) < 1:
             raise PredictorError("observed_len must be >= 1")
+        if seqs is not None:
+            seqs = np.asarray(seqs, dtype=np.int64).reshape(-1)
+            if len(seqs) != n or (n and (seqs[0] < self.next_seq or np.any(np.diff(seqs) <= 0))):
+                raise PredictorError("restored sequence numbers must increase past next_seq")
         done = 0
         while done < n:
             m = min(n - done, self.capacity)
-            seqs = torch.arange(self.next_seq, self.next_seq + m, dtype=torch.int64, device=self._dev())
+            if seqs is None:
+                sq = torch.arange(self.next_seq, self.next_seq + m, dtype=torch.int64, device=self._dev())
+            else:
+                sq = torch.as_tensor(seqs[done:done + m]).to(self._dev())
             _lib.call("alise_db_append", self._h, _lib.ptr(v[done:done + m]), _lib.ptr(ln[done:done + m]),
-                      _lib.ptr(seqs), m, _lib.stream_ptr(stream))
-            self.next_seq += m
+                      _lib.ptr(sq), m, _lib.stream_ptr(stream))
+            self.next_seq = self.next_seq + m if seqs is None else int(seqs[done + m - 1]) + 1
             self.size = min(self.capacity, self.size + m)
             done += m
         return self.next_seq - 1
 
     def search_batch(self, queries, k: int, stream=None):
         """Exact top-k for a batch.  Returns CUDA tensors (sims f64 [B,k], seqs i64,
-        lens i32, counts i32 [B]); rows past counts[b] are undefined."""
+        lens i32, counts i32 [B], the queries in the master dtype); rows past
+        counts[b] are undefined."""
         import torch
 
         if k < 1 or k > MAX_K:
             raise PredictorError(f"k must be in [1, {MAX_K}]")
-        q = torch.as_tensor(queries if isinstance(queries, torch.Tensor) else np.asarray(queries))
-        q = q.to(self._dev(), torch.float32).reshape(-1, self.dimension).contiguous()
+        q = self._as_rows(queries)
         B = q.shape[0]
         dev = self._dev()
         sims = torch.empty((B, k), dtype=torch.float64, device=dev)
@@ -274,16 +353,12 @@ class VectorStore:
 
     def export(self):
         """Copy the live records to the host: (vectors f64 [n,d], lens i64, seqs i64)."""
-        import ctypes
+        import torch
 
         n = self.size
         if n == 0:
             return np.zeros((0, self.dimension)), np.zeros(0, np.int64), np.zeros(0, np.int64)
-        return self._export_impl(n, ctypes)
-
-    def _export_impl(self, n, ctypes):
-        import torch
-        vec = torch.empty((n, self.dimension), dtype=torch.float32, device=self._dev())
+        vec = torch.empty((n, self.dimension), dtype=_torch_dtype(self._code), device=self._dev())
         lens = torch.empty(n, dtype=torch.int32, device=self._dev())
         seqs = torch.empty(n, dtype=torch.int64, device=self._dev())
         _lib.call("alise_db_export", self._h, _lib.ptr(vec), _lib.ptr(lens), _lib.ptr(seqs), n,
@@ -299,20 +374,26 @@ class VectorStore:
                                      "vector": [float(x) for x in vecs[i]]}) + "\n")
 
     def save_binary(self, path):
-        """Binary snapshot (npz: fp32 vectors, lengths, seqs in insert order) — the
-        GPU-native counterpart of the JSON-lines ``save`` (predictor.py:170-178)."""
+        """Binary snapshot (npz: master-dtype vectors, lengths, seqs in insert order,
+        next_seq) — the GPU-native counterpart of the JSON-lines ``save``
+        (predictor.py:170-178)."""
         vecs, lens, seqs = self.export()
         order = np.argsort(seqs)
-        np.savez(path, vectors=vecs[order].astype(np.float32), lens=lens[order], seqs=seqs[order],
-                 dimension=self.dimension, capacity=self.capacity)
+        np.savez(path, vectors=vecs[order].astype(self.dtype), lens=lens[order], seqs=seqs[order],
+                 dimension=self.dimension, capacity=self.capacity, next_seq=self.next_seq)
 
     @classmethod
-    def load_binary(cls, path, capacity: int | None = None) -> "VectorStore":
-        """Re-adds the records in insert order (new seqs from 0, like ``load``)."""
+    def load_binary(cls, path, capacity: int | None = None, restore_seqs: bool = False) -> "VectorStore":
+        """Re-adds the records in insert order: new seqs from 0 like ``load``
+        (predictor.py:180-189), or, with restore_seqs, under their original sequence
+        numbers (same slots, same FIFO position, same next_seq)."""
         z = np.load(path)
-        store = cls(int(z["dimension"]), int(capacity or z["capacity"]))
+        cap = int(capacity or z["capacity"])
+        store = cls(int(z["dimension"]), cap, dtype=z["vectors"].dtype)
         if len(z["lens"]):
-            store.add_batch(z["vectors"], z["lens"])
+            store.add_batch(z["vectors"], z["lens"], seqs=z["seqs"] if restore_seqs else None)
+        if restore_seqs and "next_seq" in z:
+            store.next_seq = int(z["next_seq"])
         return store
 
     @classmethod
@@ -329,6 +410,23 @@ class VectorStore:
         if vecs:
             store.add_batch(np.asarray(vecs, dtype=np.float64), lens)
         return store
+
+
+def _as_query_rows(queries, dimension=None):
+    """Queries as a contiguous CUDA tensor on the current device, float64 when given in
+    float64 (numpy's default: the reference's own vectors), else fp32."""
+    import torch
+    q = torch.as_tensor(queries if isinstance(queries, torch.Tensor) else np.asarray(queries))
+    dt = torch.float64 if q.dtype == torch.float64 else torch.float32
+    q = q.to(torch.device("cuda", torch.cuda.current_device()), dt)
+    if dimension is not None:
+        q = q.reshape(-1, dimension)
+    return q.contiguous()
+
+
+def _query_code(q) -> int:
+    import torch
+    return DB_F64 if q.dtype == torch.float64 else DB_F32
 
 
 # ----------------------------------------------------------------- fallback regressor
@@ -366,10 +464,11 @@ class FallbackRegressor:
         return self._dev_cache[1:]
 
     def predict_len_batch(self, X, max_len: int, stream=None):
-        """Batched predict_len on the GPU (float64 MLP, same op order as the oracle)."""
+        """Batched predict_len on the GPU (float64 MLP, same op order as the oracle).
+        X is used in its own precision: float64 input (the reference's vectors) stays
+        float64, anything else is read as fp32."""
         import torch
-        x = torch.as_tensor(X if isinstance(X, torch.Tensor) else np.asarray(X))
-        x = x.to(torch.device("cuda", torch.cuda.current_device()), torch.float32).contiguous()
+        x = _as_query_rows(X)
         B = x.shape[0]
         dev = x.device
         cnt = torch.zeros(B, dtype=torch.int32, device=dev)
@@ -378,10 +477,10 @@ class FallbackRegressor:
         out = torch.empty(B, dtype=torch.int32, device=dev)
         ret = torch.empty(B, dtype=torch.uint8, device=dev)
         W1, b1, w2 = self.device_weights()
-        _lib.call("alise_predict_finish", B, 1, _lib.ptr(sims), _lib.ptr(lens), _lib.ptr(cnt), 2.0,
-                  _lib.ptr(x), x.shape[1], _lib.ptr(W1), _lib.ptr(b1), _lib.ptr(w2), float(self.b2),
-                  W1.shape[1], int(max_len), math.log(max_len) + 1.0, _lib.ptr(out), _lib.ptr(ret),
-                  _lib.stream_ptr(stream))
+        _lib.call("alise_predict_finish_ex", B, 1, _lib.ptr(sims), _lib.ptr(lens), _lib.ptr(cnt), 2.0,
+                  _lib.ptr(x), _query_code(x), x.shape[1], _lib.ptr(W1), _lib.ptr(b1), _lib.ptr(w2),
+                  float(self.b2), W1.shape[1], int(max_len), math.log(max_len) + 1.0, _lib.ptr(out),
+                  _lib.ptr(ret), _lib.stream_ptr(stream))
         return out
 
     def predict_len(self, vector, max_len: int) -> int:
@@ -445,10 +544,10 @@ class _GraphedRequest:
         import torch
         self.p = predictor
         d = predictor.config.dimension
-        self.h_in = torch.zeros(1, d, dtype=torch.float32).pin_memory()
+        self.h_in = torch.zeros(1, d, dtype=torch.float64).pin_memory()
         self.h_out = torch.zeros(1, dtype=torch.int32).pin_memory()
         self.h_ret = torch.zeros(1, dtype=torch.uint8).pin_memory()
-        self.d_in = torch.zeros(1, d, dtype=torch.float32, device="cuda")
+        self.d_in = torch.zeros(1, d, dtype=torch.float64, device="cuda")
         self.key = None
         self.graph = None
 
@@ -504,33 +603,35 @@ class LengthPredictor:
         return self.embedder.embed(tokens)
 
     def predict_batch(self, queries, stream=None):
-        """Batched predict_vector: (lengths int32 [B], retrieved uint8 [B]) CUDA tensors."""
+        """Batched predict_vector: (lengths int32 [B], retrieved uint8 [B]) CUDA tensors.
+        The search runs in the store's master dtype; the fallback MLP reads the queries
+        in their own precision (float64 for the reference's float64 vectors)."""
         import torch
         cfg = self.config
-        q = torch.as_tensor(queries if isinstance(queries, torch.Tensor) else np.asarray(queries))
-        dev = torch.device("cuda", torch.cuda.current_device())
-        q = q.to(dev, torch.float32).reshape(-1, cfg.dimension).contiguous()
+        q = _as_query_rows(queries, cfg.dimension)
         B = q.shape[0]
         k = cfg.top_k
         if self.store.size > 0:
-            sims, _seqs, lens, cnt, q = self.store.search_batch(q, k, stream=stream)
+            sims, _seqs, lens, cnt, _q = self.store.search_batch(q, k, stream=stream)
         else:
+            dev = q.device
             sims = torch.empty((B, k), dtype=torch.float64, device=dev)
             lens = torch.empty((B, k), dtype=torch.int32, device=dev)
             cnt = torch.zeros(B, dtype=torch.int32, device=dev)
         return self.finish(sims, lens, cnt, q, stream=stream)
 
     def finish(self, sims, lens, cnt, q, stream=None):
-        """Aggregate + MLP fallback over given (possibly merged) top-k lists."""
+        """Aggregate + MLP fallback over given (possibly merged) top-k lists; q fp32 or
+        float64 [B, dimension] on the device."""
         import torch
         cfg = self.config
         B, k = sims.shape
         out = torch.empty(B, dtype=torch.int32, device=q.device)
         ret = torch.empty(B, dtype=torch.uint8, device=q.device)
         W1, b1, w2 = self.regressor.device_weights()
-        _lib.call("alise_predict_finish", B, k, _lib.ptr(sims), _lib.ptr(lens), _lib.ptr(cnt),
-                  float(cfg.similarity_threshold), _lib.ptr(q), cfg.dimension, _lib.ptr(W1), _lib.ptr(b1),
-                  _lib.ptr(w2), float(self.regressor.b2), W1.shape[1], int(cfg.max_len),
+        _lib.call("alise_predict_finish_ex", B, k, _lib.ptr(sims), _lib.ptr(lens), _lib.ptr(cnt),
+                  float(cfg.similarity_threshold), _lib.ptr(q), _query_code(q), cfg.dimension, _lib.ptr(W1),
+                  _lib.ptr(b1), _lib.ptr(w2), float(self.regressor.b2), W1.shape[1], int(cfg.max_len),
                   math.log(cfg.max_len) + 1.0, _lib.ptr(out), _lib.ptr(ret), _lib.stream_ptr(stream))
         return out, ret
 

@@ -86,15 +86,28 @@ def all_reduce_max(t, group=None):
     return t
 
 
-class ShardedVectorStore:
-    """A VectorStore sharded over the ranks of a process group (one GPU each).
+def _gather_objects(obj, group=None):
+    """All-gather of small host objects (snapshots, refit data; not the hot path)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
 
-    ``add_batch`` takes the full batch of new records on every rank (as the serving
-    frontend broadcasts them) and keeps this rank's residue class.  ``search_batch``
-    returns the global exact top-k on every rank.
+
+class ShardedVectorStore:
+    """A VectorStore sharded over the ranks of a process group (one GPU each); a drop-in
+    for ``VectorStore`` (predictor.py:120-189) on every rank.
+
+    Every rank calls every method with the same arguments (the serving front-end
+    broadcasts new records and query batches): ``add`` / ``add_batch`` keep this
+    rank's residue class ``seq % G``; ``search`` / ``search_batch`` return the global
+    exact top-k on every rank; ``newest`` / ``export`` / ``save`` gather the shards;
+    ``save_binary`` / ``load_binary`` snapshot each shard on its own rank and restore
+    the global FIFO (same sequence numbers, slots and next_seq).
     """
 
-    def __init__(self, dimension: int, capacity: int, group=None):
+    def __init__(self, dimension: int, capacity: int, group=None, dtype=np.float64, order: str = "exact",
+                 blas_threads: int | None = None):
         import torch.distributed as dist
 
         from . import _lib
@@ -106,8 +119,11 @@ class ShardedVectorStore:
             raise ValueError("capacity must be a multiple of the shard count for exact FIFO semantics")
         self.dimension = dimension
         self.capacity = capacity
-        self.local = VectorStore(dimension, capacity // self.world)
+        self.dtype = np.dtype(dtype)
+        self.local = VectorStore(dimension, capacity // self.world, dtype=dtype, order=order,
+                                 blas_threads=blas_threads)
         _lib.call("alise_db_set_seq_stride", self.local._h, self.world)
+        self.order = order
         self.next_seq = 0
 
     @property
@@ -117,59 +133,162 @@ class ShardedVectorStore:
     def __len__(self):
         return self.size
 
-    def add_batch(self, vectors, lens):
+    def add(self, vector, observed_len: int) -> int:
+        """VectorStore.add (predictor.py:135-152): the owner rank appends the record."""
+        from .predictor import PredictorError
+        if observed_len < 1:
+            raise PredictorError("observed_len must be >= 1")
+        seq = self.next_seq
+        self.add_batch(np.asarray(vector, dtype=np.float64)[None, :], [int(observed_len)])
+        return seq
+
+    def add_batch(self, vectors, lens, stream=None, seqs=None):
+        """Append a batch in insert order; this rank keeps its residue class.  ``seqs``
+        (host, increasing) restores records under their original sequence numbers."""
         import torch
 
-        from . import _lib
-        vectors = np.asarray(vectors) if not isinstance(vectors, torch.Tensor) else vectors
-        n = len(lens)
-        seqs = np.arange(self.next_seq, self.next_seq + n, dtype=np.int64)
+        from .predictor import PredictorError, _host_lens
+        hl = _host_lens(lens)
+        if hl is None:
+            hl = lens.cpu().numpy().astype(np.int64).reshape(-1)
+        n = len(hl)
+        if n and hl.min() < 1:
+            raise PredictorError("observed_len must be >= 1")
+        if seqs is None:
+            seqs = np.arange(self.next_seq, self.next_seq + n, dtype=np.int64)
+        else:
+            seqs = np.asarray(seqs, dtype=np.int64).reshape(-1)
         mine = np.flatnonzero(shard_rows(seqs, self.rank, self.world))
-        loc = self.local
         if len(mine):
-            dev = loc._dev()
-            v = torch.as_tensor(vectors[mine] if not isinstance(vectors, torch.Tensor)
-                                else vectors[torch.as_tensor(mine)])
-            v = v.to(dev, torch.float32).contiguous()
-            ln = torch.as_tensor(np.asarray(lens)[mine]).to(dev, torch.int32).contiguous()
-            sq = torch.as_tensor(seqs[mine]).to(dev)
-            cap = loc.capacity
-            for c0 in range(0, len(mine), cap):
-                c1 = min(len(mine), c0 + cap)
-                _lib.call("alise_db_append", loc._h, _lib.ptr(v[c0:c1]), _lib.ptr(ln[c0:c1]),
-                          _lib.ptr(sq[c0:c1]), c1 - c0, _lib.stream_ptr())
-            loc.next_seq += len(mine)
-            loc.size = min(cap, loc.size + len(mine))
-        self.next_seq += n
+            if isinstance(vectors, torch.Tensor):
+                v = vectors[torch.as_tensor(mine, device=vectors.device)]
+            else:
+                v = np.asarray(vectors)[mine]
+            self.local.add_batch(v, hl[mine], stream=stream, seqs=seqs[mine])
+        if n:
+            self.next_seq = int(seqs[-1]) + 1
+        return self.next_seq - 1
 
-    def search_batch(self, queries, k: int):
-        """Global exact top-k: local tcgen05 scan + exact rescoring, NCCL all-gather of
-        the per-shard records, (-sim, seq) merge.  Returns CUDA tensors."""
+    def search_batch(self, queries, k: int, stream=None):
+        """Global exact top-k: local tcgen05 scan, NCCL max all-reduce of the per-query
+        exact-score lower bounds, exact rescoring of the rows that can still enter the
+        global top-k, NCCL all-gather of the per-shard records, (-sim, seq) merge.
+        Returns CUDA tensors like VectorStore.search_batch."""
         import torch
 
         from . import _lib
+        from .predictor import MAX_K, PredictorError
+        if k < 1 or k > MAX_K:
+            raise PredictorError(f"k must be in [1, {MAX_K}]")
         dev = self.local._dev()
-        q = torch.as_tensor(queries if isinstance(queries, torch.Tensor) else np.asarray(queries))
-        q = q.to(dev, torch.float32).reshape(-1, self.dimension).contiguous()
+        q = self.local._as_rows(queries)
         B = q.shape[0]
-        # scan, all-reduce (max) of the per-query coarse k-th lower bounds, then exact
-        # rescoring of only the rows that can still enter the global top-k
+        sp = _lib.stream_ptr(stream)
         sims = torch.zeros((B, k), dtype=torch.float64, device=dev)
         seqs = torch.zeros((B, k), dtype=torch.int64, device=dev)
         lens = torch.zeros((B, k), dtype=torch.int32, device=dev)
         cnt = torch.zeros(B, dtype=torch.int32, device=dev)
         bound = torch.empty(B, dtype=torch.float32, device=dev)
         h = self.local._h
-        _lib.call("alise_db_topk_scan", h, _lib.ptr(q), B, k, _lib.ptr(bound), _lib.stream_ptr())
-        all_reduce_max(bound, self.group)
-        _lib.call("alise_db_topk_rescore", h, _lib.ptr(q), B, k, _lib.ptr(bound), _lib.ptr(sims), _lib.ptr(seqs),
-                  _lib.ptr(lens), _lib.ptr(cnt), _lib.stream_ptr())
-        g_sims, g_seqs, g_lens, g_cnt = all_gather_records((sims, seqs, lens, cnt), self.group)
-        o_sim = torch.empty((B, k), dtype=torch.float64, device=dev)
-        o_seq = torch.empty((B, k), dtype=torch.int64, device=dev)
-        o_len = torch.empty((B, k), dtype=torch.int32, device=dev)
-        o_cnt = torch.empty(B, dtype=torch.int32, device=dev)
-        _lib.call("alise_topk_merge", self.world, B, k, _lib.ptr(g_sims), _lib.ptr(g_seqs), _lib.ptr(g_lens),
-                  _lib.ptr(g_cnt), _lib.ptr(o_sim), _lib.ptr(o_seq), _lib.ptr(o_len), _lib.ptr(o_cnt),
-                  _lib.stream_ptr())
+        if self.order == "blas":  # rows are numbered by the global ring (predictor.py:138)
+            self.local.set_order("blas", self.local.blas_threads, self.capacity, self.size)
+        cur = torch.cuda.current_stream(dev) if stream is None else stream
+        with torch.cuda.stream(cur):
+            _lib.call("alise_db_topk_scan", h, _lib.ptr(q), B, k, _lib.ptr(bound), sp)
+            all_reduce_max(bound, self.group)
+            _lib.call("alise_db_topk_rescore", h, _lib.ptr(q), B, k, _lib.ptr(bound), _lib.ptr(sims),
+                      _lib.ptr(seqs), _lib.ptr(lens), _lib.ptr(cnt), sp)
+            g_sims, g_seqs, g_lens, g_cnt = all_gather_records((sims, seqs, lens, cnt), self.group)
+            o_sim = torch.empty((B, k), dtype=torch.float64, device=dev)
+            o_seq = torch.empty((B, k), dtype=torch.int64, device=dev)
+            o_len = torch.empty((B, k), dtype=torch.int32, device=dev)
+            o_cnt = torch.empty(B, dtype=torch.int32, device=dev)
+            _lib.call("alise_topk_merge", self.world, B, k, _lib.ptr(g_sims), _lib.ptr(g_seqs), _lib.ptr(g_lens),
+                      _lib.ptr(g_cnt), _lib.ptr(o_sim), _lib.ptr(o_seq), _lib.ptr(o_len), _lib.ptr(o_cnt), sp)
         return o_sim, o_seq, o_len, o_cnt, q
+
+    def search(self, vector, k: int):
+        """VectorStore.search (predictor.py:154-163) over all shards."""
+        if self.size == 0:
+            return np.array([]), np.array([], dtype=np.int64), np.array([], dtype=np.int64)
+        k = min(k, self.size)
+        sims, seqs, lens, cnt, _ = self.search_batch(np.asarray(vector, dtype=np.float64)[None, :], k)
+        c = int(cnt[0].item())
+        return (sims[0, :c].cpu().numpy(), lens[0, :c].cpu().numpy().astype(np.int64),
+                seqs[0, :c].cpu().numpy())
+
+    def export(self):
+        """All live records of all shards on every rank: (vectors f64, lens, seqs) in
+        insert order."""
+        parts = _gather_objects(self.local.export(), self.group)
+        vecs = np.concatenate([p[0] for p in parts]) if parts else np.zeros((0, self.dimension))
+        lens = np.concatenate([p[1] for p in parts]).astype(np.int64)
+        seqs = np.concatenate([p[2] for p in parts]).astype(np.int64)
+        order = np.argsort(seqs, kind="stable")
+        return vecs[order].reshape(-1, self.dimension), lens[order], seqs[order]
+
+    def newest(self, count: int):
+        """Vectors and lengths of the most recently inserted records (predictor.py:165-168)."""
+        vecs, lens, seqs = self.local.export()
+        keep = np.argsort(seqs)[-count:] if count > 0 else np.zeros(0, np.int64)
+        parts = _gather_objects((vecs[keep], lens[keep], seqs[keep]), self.group)
+        vecs = np.concatenate([p[0] for p in parts]).reshape(-1, self.dimension)
+        lens = np.concatenate([p[1] for p in parts]).astype(np.int64)
+        seqs = np.concatenate([p[2] for p in parts]).astype(np.int64)
+        order = np.argsort(seqs)[-count:] if count > 0 else np.zeros(0, np.int64)
+        return vecs[order], lens[order]
+
+    def save(self, path):
+        """JSON-lines snapshot (predictor.py:170-178), written by rank 0."""
+        import json
+        vecs, lens, seqs = self.export()
+        if self.rank == 0:
+            with open(path, "w") as fh:
+                for i in range(len(seqs)):
+                    fh.write(json.dumps({"seq": int(seqs[i]), "len": int(lens[i]),
+                                         "vector": [float(x) for x in vecs[i]]}) + "\n")
+
+    @classmethod
+    def load(cls, path, dimension: int, capacity: int, group=None, dtype=np.float64) -> "ShardedVectorStore":
+        """predictor.py:180-189: re-adds the records in file order (new seqs from 0)."""
+        import json
+        vecs, lens = [], []
+        with open(path) as fh:
+            for line in fh:
+                line = line.strip()
+                if line:
+                    rec = json.loads(line)
+                    vecs.append(rec["vector"])
+                    lens.append(int(rec["len"]))
+        store = cls(dimension, capacity, group=group, dtype=dtype)
+        if vecs:
+            store.add_batch(np.asarray(vecs, dtype=np.float64), lens)
+        return store
+
+    def shard_path(self, path) -> str:
+        return f"{path}.shard{self.rank}of{self.world}.npz"
+
+    def save_binary(self, path):
+        """Per-shard binary snapshot: each rank writes its own records (master dtype,
+        original sequence numbers) and the global next_seq to ``shard_path(path)``."""
+        vecs, lens, seqs = self.local.export()
+        order = np.argsort(seqs)
+        np.savez(self.shard_path(path), vectors=vecs[order].astype(self.dtype), lens=lens[order],
+                 seqs=seqs[order], dimension=self.dimension, capacity=self.capacity, world=self.world,
+                 rank=self.rank, next_seq=self.next_seq)
+
+    @classmethod
+    def load_binary(cls, path, group=None) -> "ShardedVectorStore":
+        """Restore a save_binary snapshot on the same number of ranks: every shard gets
+        its records back under their sequence numbers (same slots, global FIFO order
+        and next_seq), so searches and later evictions equal the saved store's."""
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        z = np.load(f"{path}.shard{rank}of{world}.npz")
+        if int(z["world"]) != world or int(z["rank"]) != rank:
+            raise ValueError("snapshot was written by a different shard layout")
+        store = cls(int(z["dimension"]), int(z["capacity"]), group=group, dtype=z["vectors"].dtype)
+        if len(z["lens"]):
+            store.local.add_batch(z["vectors"], z["lens"], seqs=z["seqs"])
+        store.next_seq = int(z["next_seq"])
+        return store

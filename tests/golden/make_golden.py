@@ -3,17 +3,18 @@ container, where /root/reference exists; the fixtures travel, the reference does
 
     python tests/golden/make_golden.py
 
-Writes tests/golden/kv_golden.npz and tests/golden/pred_golden.npz.
+Writes tests/golden/kv_golden.npz, kv_c1_full.npz and pred_golden.npz.
 """
 import os
 import sys
 
 import numpy as np
 
-REF = "/root/reference/pkg/src"
 HERE = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, REF)
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+from tests import refsim  # noqa: E402
+
+refsim.import_servesim()
 
 from servesim import kvmanager as rk  # noqa: E402
 from servesim import predictor as rp  # noqa: E402
@@ -66,6 +67,45 @@ def kv_golden():
     out["acc"] = np.array(acc, dtype=np.int64)
     np.savez_compressed(os.path.join(HERE, "kv_golden.npz"), **out)
     print("kv_golden:", len(out), "arrays")
+
+
+C1_FULL = dict(layers=4, tokens=512, heads=8, head_dim=128)
+C1_FULL_LAYOUTS = (("head", 0), ("channel", 0), ("contig", 128))
+
+
+def digest(a) -> str:
+    import hashlib
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.dtype.str.encode() + str(a.shape).encode() + a.tobytes()).hexdigest()
+
+
+def c1_full_kv():
+    c = C1_FULL
+    return synthetic.kv_job(c["layers"], c["tokens"], c["heads"] * c["head_dim"], seed=0, job=0, group=128)
+
+
+def kv_c1_full():
+    """BASELINE config 1 at its own shape: 4 layers x 8 heads x 128 dim x 512 tokens fp16,
+    INT8 (and INT4) per-head (64 x 65536), per-channel (8192 x 512) and per-(token, head)
+    (32768 x 128) views through the REFERENCE quantize/dequantize.  The outputs are kept
+    as SHA-256 digests (bit-exact comparisons) plus the first rows in full."""
+    kv = c1_full_kv()
+    out = {"kv_digest": np.array(digest(kv))}
+    for kind, group in C1_FULL_LAYOUTS:
+        view = kv_oracle.view_rows(kv, kind, group=group, head_dim=C1_FULL["head_dim"])
+        for bits in (4, 8):
+            qt = rk.quantize(view, bits)
+            deq = rk.dequantize(qt)
+            tag = f"{kind}{group or ''}_b{bits}"
+            out[tag + "_shape"] = np.array(view.shape)
+            for name, arr in (("codes", qt.values), ("scale", qt.scale), ("zero", qt.zero), ("deq", deq),
+                              ("deq16", deq.astype(np.float16))):
+                out[f"{tag}_{name}_digest"] = np.array(digest(arr))
+            out[tag + "_codes_head"] = qt.values[:2]
+            out[tag + "_scale_head"] = qt.scale[:64]
+            out[tag + "_zero_head"] = qt.zero[:64]
+    np.savez_compressed(os.path.join(HERE, "kv_c1_full.npz"), **out)
+    print("kv_c1_full:", len(out), "arrays")
 
 
 def pred_golden():
@@ -125,5 +165,10 @@ def pred_golden():
 
 
 if __name__ == "__main__":
-    kv_golden()
-    pred_golden()
+    which = sys.argv[1:] or ["kv", "c1full", "pred"]
+    if "kv" in which:
+        kv_golden()
+    if "c1full" in which:
+        kv_c1_full()
+    if "pred" in which:
+        pred_golden()

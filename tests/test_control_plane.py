@@ -4,14 +4,13 @@ restate pkg/tests/test_kvmanager.py:129-253; the replay test runs the reference'
 simulator (simcore.run, config-5 style speculative scheduling with swaps) with its
 kvmanager symbols replaced by ours and requires an identical MetricsReport."""
 import math
-import sys
 from types import SimpleNamespace
 
 import pytest
 
 from paper_2410_23537_b200 import kvmanager as km
 
-REF = "/root/reference/pkg/src"
+from tests import refsim
 
 
 def job(level, last_promotion_us=0):
@@ -60,8 +59,7 @@ def test_plan_swaps_first_fit_skip_and_in_flight_charge():
 
 
 def _ref_modules():
-    if REF not in sys.path:
-        sys.path.insert(0, REF)
+    refsim.import_servesim()
     try:
         from servesim import simcore, workload
         from servesim.kvmanager import MODEL_PRESETS
@@ -98,8 +96,7 @@ def test_reference_simulator_with_dropin_control_plane(monkeypatch, policy):
 
 # ----------------------------------------------------------------- C++ control plane
 def _ref_kvmanager():
-    if REF not in sys.path:
-        sys.path.insert(0, REF)
+    refsim.import_servesim()
     try:
         from servesim import kvmanager as rk
     except Exception:

@@ -107,8 +107,8 @@ def test_embedder_and_config():
 
 
 def test_embedder_matches_reference_hashing():
-    import sys
-    sys.path.insert(0, "/root/reference/pkg/src")
+    from tests import refsim
+    refsim.import_servesim()
     try:
         from servesim.predictor import HashingEmbedder as RefEmb
     except Exception:
@@ -125,3 +125,55 @@ def test_eval_accuracy_known_answer():
     r = eval_accuracy([(100, 120), (10, 300)], bin_width=50)
     assert r["count"] == 2 and r["accuracy"] == 0.5
     assert abs(r["pred_error"] - (20 / 120 + 290 / 300) / 2) < 1e-15
+
+
+def _host_blas_arch():
+    try:
+        from threadpoolctl import threadpool_info
+        for i in threadpool_info():
+            if i.get("internal_api") == "openblas":
+                return i.get("architecture"), int(i["num_threads"]), i.get("version")
+    except Exception:
+        pass
+    return None, 1, None
+
+
+@pytest.mark.parametrize("n,d", [(1, 64), (7, 64), (203, 64), (5003, 64), (100003, 64), (3001, 67), (2001, 768),
+                                 (60, 4099), (11, 2), (9, 3)])
+def test_blas_order_matches_numpy(n, d):
+    """oracle/blas_order.c reproduces numpy's own `V @ q` (predictor.py:158) bit for bit
+    on this host (OpenBLAS 0.3.30 dgemv_t, Haswell/SkylakeX kernels), incl. the thread
+    split of large products."""
+    arch, threads, version = _host_blas_arch()
+    if arch not in ("Haswell", "SkylakeX", "Zen", "Cooperlake", "SapphireRapids") or version != "0.3.30":
+        pytest.skip(f"host BLAS {arch} {version}: order restated for OpenBLAS 0.3.30 x86-64")
+    g = np.random.default_rng(n * 7 + d)
+    V = g.standard_normal((n, d))
+    x = g.standard_normal(d)
+    assert np.array_equal(po.blas_gemv(V, x, threads), V @ x)
+
+
+def test_search_blas_is_the_reference_search():
+    """search_blas == the reference VectorStore.search on the same records (ring
+    wrap-around included) on this host."""
+    from tests import refsim
+    if refsim.import_servesim() is None:
+        pytest.skip("reference not importable")
+    from servesim.predictor import VectorStore as RefStore
+    arch, threads, version = _host_blas_arch()
+    if version != "0.3.30":
+        pytest.skip("BLAS order restated for OpenBLAS 0.3.30")
+    g = np.random.default_rng(4)
+    d, cap = 64, 700
+    ref = RefStore(d, cap)
+    rows = g.standard_normal((1000, d))
+    rows[500:520] = rows[3]
+    for i, r in enumerate(rows):
+        ref.add(r / np.linalg.norm(r), int(i % 97) + 1)
+    slots = ref._vecs[:ref.size]
+    for t in range(40):
+        q = g.standard_normal(d)
+        q /= np.linalg.norm(q)
+        a = ref.search(q, 8)
+        b = po.search_blas(slots, ref._lens[:ref.size], ref._seqs[:ref.size], q, 8, threads)
+        assert all(np.array_equal(u, v) for u, v in zip(a, b))

@@ -22,14 +22,14 @@ def unit(*values, dim=8):
     return v / np.linalg.norm(v)
 
 
-def check_batch(pr, db, lens, Q, k, capacity=None):
+def check_batch(pr, db, lens, Q, k, capacity=None, dtype=np.float32):
     import torch
     n, d = db.shape
-    store = pr.VectorStore(d, capacity or max(n, 8))
+    store = pr.VectorStore(d, capacity or max(n, 8), dtype=dtype)
     store.add_batch(db, lens)
     sims, seqs, slens, cnt, _ = store.search_batch(Q, k)
     torch.cuda.synchronize()
-    ref = po.search_exact_batch(db, lens, np.arange(n), Q, k)
+    ref = po.search_exact_batch(db, lens, np.arange(n), Q, k, f64=np.dtype(dtype) == np.float64)
     sims, seqs, slens, cnt = (t.cpu().numpy() for t in (sims, seqs, slens, cnt))
     for i, (es, el, eq) in enumerate(ref):
         c = cnt[i]
@@ -194,43 +194,137 @@ def test_c4_scale_200k_x_768(pr):
     check_batch(pr, db, lens, Q, 8)
 
 
+def _adversarial_norm_db(d=64, k=4):
+    """Shard 1 (odd seqs) holds k rows whose fp16 coarse scores overshoot their exact
+    scores by ~0.24 (components 100.032 / -100.03 round away from the exact cancellation)
+    and a huge-norm row that makes its coarse error bound large; shard 0 (even seqs)
+    holds k fp16-exact rows with exact score 0.1 > the overshooting rows' 0.008, so the
+    global top-k lies in shard 0 even though shard 1's coarse k-th bound (~0.25) is far
+    above their coarse scores (the exchanged bound must be an exact-score
+    bound, L - delta_self, not a coarse one)."""
+    q = np.full(d, 1.0 / np.sqrt(d))
+    rows, n = [], 4 * k + 8
+    for i in range(n):
+        r = np.zeros(d)
+        if i % 2 == 1 and i < 2 * k + 1:
+            r[0::2], r[1::2] = 100.032, -100.03       # exact 0.008, coarse ~0.25
+        elif i % 2 == 0 and i < 2 * k:
+            r[0] = 0.1 * np.sqrt(d)                   # exact 0.1 (fp16-exact)
+        elif i == 2 * k + 3:
+            r[0::2], r[1::2] = 3000.0, -3000.0        # huge norm, exact score 0
+        else:
+            r[0] = -0.5 * np.sqrt(d)                  # filler, exact -0.5
+        rows.append(r)
+    return np.array(rows), q
+
+
 def _sharded_worker(rank, world, port, result_dir):
     import os
 
     import torch
     import torch.distributed as dist
 
+    from paper_2410_23537_b200 import predictor as pr
     from paper_2410_23537_b200 import sharding
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)  # both ranks share the one GPU; gloo carries the exchange
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    fails = []
+
+    def same(tag, sims, seqs, slens, cnt, ref):
+        for i, r in enumerate(ref):
+            c = int(cnt[i])
+            if not (c == len(r[2]) and np.array_equal(seqs[i, :c].cpu().numpy(), r[2])
+                    and np.array_equal(sims[i, :c].cpu().numpy(), r[0])
+                    and np.array_equal(slens[i, :c].cpu().numpy(), r[1])):
+                fails.append((tag, i))
+                return
+
+    # (a) fp32 DB with a tie group spanning both shards and ring eviction
     g = np.random.default_rng(21)
     n, d, B, k = 6000, 96, 200, 8
     db = g.standard_normal((n, d)).astype(np.float32)
     db /= np.linalg.norm(db, axis=1, keepdims=True)
-    db[3000:3011] = db[7]                       # tie group spanning both shards
+    db[3000:3011] = db[7]
     lens = g.integers(1, 2048, size=n).astype(np.int32)
     Q = np.concatenate([db[[7, 100, 4000]], g.standard_normal((B - 3, d)).astype(np.float32)])
     Q = (Q / np.linalg.norm(Q, axis=1, keepdims=True)).astype(np.float32)
     cap = 5000                                  # ring eviction: the oldest 1000 rows drop out
-    store = sharding.ShardedVectorStore(d, cap)
+    store = sharding.ShardedVectorStore(d, cap, dtype=np.float32)
     store.add_batch(db[:2500], lens[:2500])
     store.add_batch(db[2500:], lens[2500:])
-    sims, seqs, slens, cnt, _ = store.search_batch(Q, k)
-    torch.cuda.synchronize()
     live = np.arange(n - cap, n)
-    ref = po.search_exact_batch(db[live], lens[live], live, Q, k)
-    ok = all(np.array_equal(seqs[i].cpu().numpy(), r[2]) and np.array_equal(sims[i].cpu().numpy(), r[0])
-             and np.array_equal(slens[i].cpu().numpy(), r[1]) for i, r in enumerate(ref))
+    same("fp32", *store.search_batch(Q, k)[:4], po.search_exact_batch(db[live], lens[live], live, Q, k))
+    # empty query batch (ADVICE r1: the rescore of an empty scan)
+    out = store.search_batch(np.zeros((0, d), np.float32), k)
+    if out[0].shape != (0, k):
+        fails.append(("empty", out[0].shape))
+
+    # (b) shards with different max row norms
+    rows, q = _adversarial_norm_db()
+    adv = sharding.ShardedVectorStore(rows.shape[1], 64)
+    adv.add_batch(rows, np.arange(1, len(rows) + 1))
+    idx = np.arange(len(rows))
+    same("norms", *adv.search_batch(q[None, :], 4)[:4],
+         po.search_exact_batch(rows, np.arange(1, len(rows) + 1), idx, q[None, :], 4, f64=True))
+
+    # (c) drop-in API on a float64 sharded store: LengthPredictor(store=sharded)
+    g = np.random.default_rng(5)
+    n, d = 1200, 64
+    dbf = g.standard_normal((n, d))
+    dbf /= np.linalg.norm(dbf, axis=1, keepdims=True)
+    lf = g.integers(1, 2048, size=n)
+    cfg = pr.PredictorConfig(dimension=d, db_capacity=1000, refit_sample_cap=64)
+    sh = sharding.ShardedVectorStore(d, cfg.db_capacity)
+    ref_store = pr.VectorStore(d, cfg.db_capacity)             # single-store reference run
+    p_sh = pr.LengthPredictor(cfg, store=sh)
+    p_one = pr.LengthPredictor(pr.PredictorConfig(dimension=d, db_capacity=1000, refit_sample_cap=64),
+                               store=ref_store)
+    for i in range(n):                                          # observe: owner-rank append + refits
+        p_sh.observe(dbf[i], int(lf[i]))
+        p_one.observe(dbf[i], int(lf[i]))
+    Qf = np.concatenate([dbf[-50:] + 0.01 * g.standard_normal((50, d)), g.standard_normal((50, d))])
+    Qf /= np.linalg.norm(Qf, axis=1, keepdims=True)
+    a, ra = p_sh.predict_batch(Qf)
+    b, rb = p_one.predict_batch(Qf)
+    if not (torch.equal(a.cpu(), b.cpu()) and torch.equal(ra.cpu(), rb.cpu())):
+        fails.append(("predict", int((a.cpu() != b.cpu()).sum())))
+    if not np.array_equal(p_sh.regressor.w1, p_one.regressor.w1):
+        fails.append(("refit",))
+    live = np.arange(n - cfg.db_capacity, n)
+    same("f64", *sh.search_batch(Qf, 8)[:4], po.search_exact_batch(dbf[live], lf[live], live, Qf, 8, f64=True))
+    s1 = sh.search(Qf[0], 5)
+    s2 = ref_store.search(Qf[0], 5)
+    if not all(np.array_equal(x, y) for x, y in zip(s1, s2)):
+        fails.append(("search",))
+    X1, L1 = sh.newest(100)
+    X2, L2 = ref_store.newest(100)
+    if not (np.array_equal(X1, X2) and np.array_equal(L1, L2)):
+        fails.append(("newest",))
+    # per-shard binary snapshot restores the global FIFO (same seqs, same evictions)
+    path = os.path.join(result_dir, "snap")
+    sh.save_binary(path)
+    dist.barrier()
+    back = sharding.ShardedVectorStore.load_binary(path)
+    extra = g.standard_normal((30, d))
+    for st in (sh, back):
+        st.add_batch(extra, np.arange(1, 31))
+    x1 = sh.search_batch(Qf, 8)
+    x2 = back.search_batch(Qf, 8)
+    if not all(torch.equal(u, v) for u, v in zip(x1[:4], x2[:4])) or back.next_seq != sh.next_seq:
+        fails.append(("snapshot",))
     with open(os.path.join(result_dir, f"r{rank}"), "w") as fh:
-        fh.write("ok" if ok else "bad")
+        fh.write("ok" if not fails else repr(fails))
     dist.destroy_process_group()
 
 
 def test_sharded_store_two_ranks_one_gpu(tmp_path):
-    """ShardedVectorStore end to end (seq % 2 shards, per-shard GPU top-k, all-gather,
-    GPU merge, FIFO eviction across shards) against the single-store oracle."""
+    """ShardedVectorStore end to end (seq % 2 shards, per-shard GPU top-k, bound
+    all-reduce, all-gather, GPU merge, FIFO eviction across shards) against the
+    single-store oracle; shards with different row norms; the drop-in API
+    (LengthPredictor(store=ShardedVectorStore): observe + refit, predict_batch, search,
+    newest, per-shard binary snapshots)."""
     import socket
 
     import torch.multiprocessing as mp
@@ -241,6 +335,11 @@ def test_sharded_store_two_ranks_one_gpu(tmp_path):
     mp.spawn(_sharded_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     for r in range(2):
         assert (tmp_path / f"r{r}").read_text() == "ok"
+
+
+def test_adversarial_norms_single_store(pr):
+    rows, q = _adversarial_norm_db()
+    check_batch(pr, rows, np.arange(1, len(rows) + 1), q[None, :], 4, dtype=np.float64)
 
 
 def test_gpu_embedder_bit_identical_to_reference_hashing(pr):
@@ -394,7 +493,7 @@ def test_split_search_api(pr):
     Q = g.standard_normal((B, d)).astype(np.float32)
     Q[: B // 2] = db[g.integers(0, n, size=B // 2)] + 0.05 * g.standard_normal((B // 2, d)).astype(np.float32)
     Q /= np.linalg.norm(Q, axis=1, keepdims=True)
-    store = pr.VectorStore(d, n)
+    store = pr.VectorStore(d, n, dtype=np.float32)  # raw C calls: queries in the master dtype
     store.add_batch(db, lens)
     q = torch.from_numpy(Q).cuda()
     ref = store.search_batch(q, k)
@@ -423,7 +522,169 @@ def test_split_search_api(pr):
     for i in range(B):
         assert torch.equal(outs2[1][i, :c2[i]], ref[1][i, :c2[i]])
     # empty shard
-    empty = pr.VectorStore(d, 64)
+    empty = pr.VectorStore(d, 64, dtype=np.float32)
     b0, outs0 = split(empty, lambda b: b)
     assert torch.isinf(b0).all() and (b0 < 0).all()
     assert (outs0[3] == 0).all()
+
+
+# ----------------------------------------------------------------- float64 master store
+def _f64_db(g, n, d, ties=True):
+    db = g.standard_normal((n, d))
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    if ties:
+        db[n // 2:n // 2 + 11] = db[3]               # exact duplicates: ties broken by seq
+    return db
+
+
+@pytest.mark.parametrize("k", [1, 8, 16])
+def test_f64_store_exact_vs_oracle(pr, k):
+    """float64 vectors (not fp32-representable) in the default float64 store: sims are
+    the correctly rounded dot products of the float64 values (two_prod-split products),
+    top-k by (-sim, seq), equal to the restated oracle bit for bit."""
+    g = np.random.default_rng(40 + k)
+    n, d, B = 5000, 96, 300
+    db = _f64_db(g, n, d)
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = np.concatenate([db[[3, 10, 4000]] + 1e-3 * g.standard_normal((3, d)), g.standard_normal((B - 3, d))])
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    check_batch(pr, db, lens, Q, k, dtype=np.float64)
+
+
+def test_f64_predict_batch_uses_float64_queries(pr):
+    """predict_batch on a float64 store: retrieval over float64 sims, the fallback MLP on
+    the float64 query (the reference's own vector), equal to the oracle."""
+    g = np.random.default_rng(5)
+    n, d = 3000, 64
+    db = _f64_db(g, n, d)
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = np.concatenate([db[:40] + 0.02 * g.standard_normal((40, d)), g.standard_normal((60, d))])
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    reg = pr.FallbackRegressor(d, 32, seed=1)
+    reg.b2 = 4.0
+    store = pr.VectorStore(d, 4096)
+    store.add_batch(db, lens)
+    p = pr.LengthPredictor(pr.PredictorConfig(dimension=d, db_capacity=4096), regressor=reg, store=store)
+    out, ret = p.predict_batch(Q)
+    ref_len, ref_ret = po.predict_batch(db, lens, np.arange(n), Q, reg.w1, reg.b1, reg.w2, reg.b2, f64=True)
+    assert np.array_equal(out.cpu().numpy(), ref_len)
+    assert np.array_equal(ret.cpu().numpy().astype(bool), ref_ret)
+    assert 0 < ref_ret.sum() < len(Q)
+    # and per request through predict_vector (eager and CUDA-graph replay)
+    for i in (0, 5, 70):
+        assert p.predict_vector(Q[i])[0] == ref_len[i]
+    p.enable_graphs()
+    for i in (0, 5, 70):
+        assert p.predict_vector(Q[i])[0] == ref_len[i]
+
+
+def test_hashing_embedder_vectors_exact(pr):
+    """The reference's own HashingEmbedder vectors (float64, many shared n-grams):
+    search results equal the oracle on float64 rows."""
+    g = np.random.default_rng(9)
+    emb = pr.HashingEmbedder(64)
+    base = [list(range(1000 + b, 1018 + b)) for b in range(30)]
+    prompts = [base[int(g.integers(0, 30))] + g.integers(50_000, 51_000, size=2).tolist() for _ in range(2000)]
+    db = np.stack([emb.embed(p) for p in prompts])
+    lens = g.integers(1, 2048, size=len(db)).astype(np.int32)
+    Q = np.stack([emb.embed(base[i % 30] + [50_001, 50_002]) for i in range(120)])
+    check_batch(pr, db, lens, Q, 8, dtype=np.float64)
+
+
+def test_f64_midpoint_sums_use_exact_accumulator(pr):
+    """Dot products whose exact value is a float64 rounding midpoint (or within 2^-100 of
+    one) defeat the double-double certificate; the 4480-bit accumulator must round
+    them correctly (half-even)."""
+    import torch
+    from fractions import Fraction
+    d = 64
+    rows = np.zeros((6, d))
+    rows[0, :2] = [1.0, 2.0 ** -53]                      # 1 + 2^-53: tie -> even (1.0)
+    rows[1, :3] = [1.0, 2.0 ** -53, 2.0 ** -100]         # just above the tie -> 1 + 2^-52
+    rows[2, :3] = [1.0, 3 * 2.0 ** -53, -(2.0 ** -120)]  # just below 1 + 3*2^-53 -> 1 + 2^-52
+    rows[3, :2] = [0.75, 2.0 ** -54]                     # 0.75 + 2^-54: tie -> even
+    rows[4, :4] = [0.5, 0.25, 2.0 ** -60, -(2.0 ** -60)]  # exact cancellation
+    rows[5, :2] = [1e-3, 1e-3]
+    q = np.zeros(d)
+    q[:4] = 1.0
+    store = pr.VectorStore(d, 8)
+    store.add_batch(rows, np.arange(1, 7))
+    sims, seqs, _l, cnt, _ = store.search_batch(q[None, :], 6)
+    torch.cuda.synchronize()
+    got = dict(zip(seqs[0].cpu().numpy().tolist(), sims[0].cpu().numpy().tolist()))
+    for r in range(6):
+        exact = float(sum((Fraction(a) * Fraction(b) for a, b in zip(rows[r].tolist(), q.tolist())), Fraction(0)))
+        assert got[r] == exact, (r, got[r], exact)
+    assert got[0] == 1.0 and got[1] == 1.0 + 2.0 ** -52 and got[2] == 1.0 + 2.0 ** -52
+    assert store.inexact_count() >= 3
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_rows_beyond_fp16_range_take_the_exact_path(pr, dtype):
+    """A component beyond 65504 overflows the fp16 coarse copy: the store routes every
+    query through the exhaustive exact path instead of trusting inf/NaN coarse scores."""
+    g = np.random.default_rng(77)
+    n, d = 3000, 64
+    db = g.standard_normal((n, d))
+    db[17, 5] = 1.0e5
+    db[900, :] *= 3.0e4
+    db = db.astype(dtype)
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = g.standard_normal((50, d)).astype(dtype)
+    Q[3, 5] = 7.0e4
+    check_batch(pr, db, lens, Q, 8, dtype=dtype)
+
+
+def test_mlp_hidden_beyond_128(pr):
+    """fallback_hidden > 128: the finish kernel walks the hidden units in chunks of 128
+    with the output sum still in index order."""
+    g = np.random.default_rng(3)
+    d, H = 96, 300
+    reg = pr.FallbackRegressor(d, H, seed=2)
+    reg.b1 = g.standard_normal(H) * 0.1
+    reg.b2 = 3.0
+    X = g.standard_normal((70, d))
+    got = reg.predict_len_batch(X, 2048).cpu().numpy()
+    ref = po.mlp_predict_len(X, reg.w1, reg.b1, reg.w2, reg.b2, 2048)
+    assert np.array_equal(got, ref)
+
+
+# ----------------------------------------------------------------- reference BLAS order
+def _check_blas(pr, rows, lens, Q, k, cap, threads=8):
+    import torch
+    n, d = rows.shape
+    store = pr.VectorStore(d, cap, order="blas", blas_threads=threads)
+    store.add_batch(rows, lens)
+    sims, seqs, slens, cnt, _ = store.search_batch(Q, k)
+    torch.cuda.synchronize()
+    # the reference's array: ring slots in slot order (predictor.py:126-152)
+    live = np.arange(max(0, n - cap), n)
+    slot_rows = np.zeros((min(n, cap), d))
+    slot_lens = np.zeros(min(n, cap), np.int64)
+    slot_seqs = np.zeros(min(n, cap), np.int64)
+    slot_rows[live % cap], slot_lens[live % cap], slot_seqs[live % cap] = rows[live], lens[live], live
+    bad = []
+    for i, q in enumerate(Q):
+        allsims = po.blas_gemv(slot_rows, q, threads)
+        o = np.lexsort((slot_seqs, -allsims))[:k]
+        c = int(cnt[i])
+        if not (c == len(o) and np.array_equal(seqs[i, :c].cpu().numpy(), slot_seqs[o])
+                and np.array_equal(sims[i, :c].cpu().numpy(), allsims[o])
+                and np.array_equal(slens[i, :c].cpu().numpy(), slot_lens[o])):
+            bad.append(i)
+    assert not bad, bad[:10]
+
+
+@pytest.mark.parametrize("n,cap,d", [(281, 1000, 64), (5000, 3000, 64), (2000, 4096, 768), (700, 700, 67)])
+def test_blas_order_search_with_heavy_ties(pr, n, cap, d):
+    """order="blas": sims are the reference's BLAS-order float64 values (oracle/blas_order.c)
+    and the top-k is (-sim, seq) over them, incl. dozens of exactly tied rows (hashed
+    prompts of one length bucket) and a wrapped ring."""
+    g = np.random.default_rng(n + d)
+    emb = pr.HashingEmbedder(d)
+    stems = [list(range(1000 + b, 1018 + b)) for b in range(12)]
+    prompts = [stems[int(g.integers(0, 12))] + g.integers(50_000, 50_040, size=2).tolist() for _ in range(n)]
+    rows = np.stack([emb.embed(p) for p in prompts])
+    lens = g.integers(1, 2048, size=n)
+    Q = np.stack([emb.embed(stems[i % 12] + [50_001, 50_003]) for i in range(48)])
+    _check_blas(pr, rows, lens, Q, 8, cap)

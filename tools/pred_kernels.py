@@ -5,6 +5,7 @@ import collections
 import json
 import sys
 
+import numpy as np
 import torch
 from torch.profiler import ProfilerActivity, profile
 
@@ -16,7 +17,7 @@ N = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 BS = [int(b) for b in sys.argv[2].split(",")] if len(sys.argv) > 2 else [256, 64, 1]
 D = 768
 db, lens = synthetic.predictor_db(N, D, seed=0, dup_groups=1000)
-store = pr.VectorStore(D, N)
+store = pr.VectorStore(D, N, dtype=np.float32)
 store.add_batch(db, lens)
 reg = pr.FallbackRegressor(D, 32, seed=0)
 reg.b2 = 5.0

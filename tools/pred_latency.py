@@ -14,7 +14,7 @@ from harness import synthetic  # noqa: E402
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 D = 768
 db, lens = synthetic.predictor_db(N, D, seed=0, dup_groups=1000)
-store = pr.VectorStore(D, N)
+store = pr.VectorStore(D, N, dtype=np.float32)
 store.add_batch(db, lens)
 reg = pr.FallbackRegressor(D, 32, seed=0)
 reg.b2 = 5.0

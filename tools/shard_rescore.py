@@ -4,6 +4,7 @@ bound is the full-DB scan's bound (the max over the shards' bounds is at most th
 import json
 import sys
 
+import numpy as np
 import torch
 
 sys.path.insert(0, ".")
@@ -13,9 +14,9 @@ from harness import synthetic  # noqa: E402
 
 N, D, B, K, G = 1_000_000, 768, 4096, 8, 8
 db, lens = synthetic.predictor_db(N, D, seed=0, dup_groups=1000)
-full = pr.VectorStore(D, N)
+full = pr.VectorStore(D, N, dtype=np.float32)
 full.add_batch(db, lens)
-shard = pr.VectorStore(D, N // G)
+shard = pr.VectorStore(D, N // G, dtype=np.float32)
 shard.add_batch(db[::G], lens[::G])
 Q = torch.from_numpy(synthetic.predictor_queries(db, B, seed=1)).cuda()
 outs = [torch.empty((B, K), dtype=torch.float64, device="cuda"), torch.empty((B, K), dtype=torch.int64, device="cuda"),

@@ -4,6 +4,7 @@ INT8) and k_scan at C4 (B=4096 x 1M x 768).
 Usage under ncu: -k regex:'k_quant_tile|k_dequant_wide|k_scan' -c 3."""
 import sys
 
+import numpy as np
 import torch
 
 sys.path.insert(0, ".")
@@ -25,7 +26,7 @@ torch.cuda.synchronize()
 print("quant chunks", g["n_chunks"], "values per chunk", lay.elements // g["n_chunks"])
 del kv, slab, out
 db, lens = synthetic.predictor_db_torch(1_000_000, 768, seed=0, dup_groups=1000)
-store = pr.VectorStore(768, 1_000_000)
+store = pr.VectorStore(768, 1_000_000, dtype=np.float32)
 store.add_batch(db, lens)
 Q = synthetic.predictor_queries_torch(db, 4096, seed=1)
 store.search_batch(Q, 8)
