@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--host-slabs", type=int, default=8)
     ap.add_argument("--lag", type=int, default=1, help="upload job j-lag while offloading job j")
     ap.add_argument("--planes-per-chunk", type=int, default=0, help="transfer chunk (0: 512 MiB of codes)")
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-planes", type=int, default=16)
@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--pred-b", type=int, default=4096)
     ap.add_argument("--pred-dim", type=int, default=768)
     ap.add_argument("--pred-cpu-queries", type=int, default=16)
+    ap.add_argument("--pred-parity", type=int, default=128, help="queries checked against the oracle after timing")
+    ap.add_argument("--no-parity", action="store_true")
     return ap.parse_args()
 
 
@@ -177,42 +179,66 @@ def load_sustained_bf16():
         return None
 
 
-# ----------------------------------------------------------------- CPU baseline (oracle port)
-def _cpu_worker(payload):
+# ----------------------------------------------------------------- CPU baseline (reference)
+def _ref_kv_functions():
+    """(quantize, dequantize, kind): the reference's own servesim.kvmanager from the
+    offline install under baseline/_ref when present ("reference"), else the oracle's
+    numpy restatement of the same algorithm ("port")."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "servesim")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        from servesim import kvmanager as rk
+        return rk.quantize, rk.dequantize, "reference"
+    from oracle import kv_oracle
+
+    def q(x, bits):
+        return kv_oracle.quantize_rows(x, bits)
+
+    def dq(t):
+        return kv_oracle.dequantize_rows(*t)
+    return q, dq, "port"
+
+
+def _cpu_proc(planes, tokens, hidden, group, bits, barrier, out):
     import numpy as np
 
-    from oracle import kv_oracle
     from harness import synthetic
-    (plane_idx, tokens, hidden, group, bits) = payload
-    x = synthetic.kv_job(1, tokens, hidden, seed=0, job=1000 + plane_idx, group=group)[0, 0]
-    rows = x.reshape(-1, group)
+    quantize, dequantize, _kind = _ref_kv_functions()
+    xs = [synthetic.kv_job(1, tokens, hidden, seed=0, job=1000 + p, group=group)[0, 0].reshape(-1, group)
+          for p in planes]                      # inputs made before the timed region
+    barrier.wait()
     t0 = time.perf_counter()
-    codes, scale, zero = kv_oracle.quantize_rows(rows, bits)
+    n = 0
+    for x in xs:
+        qt = quantize(x, bits)
+        y = dequantize(qt).astype(np.float16)    # fp16 KV back, like the GPU path
+        n += x.size + 0 * int(y.size)
     t1 = time.perf_counter()
-    y = kv_oracle.dequantize_rows(codes, scale, zero).astype(np.float16)
-    t2 = time.perf_counter()
-    return rows.size, t1 - t0, t2 - t1, int(y.size)
+    out.put((n, t0, t1))
 
 
 def cpu_kv_sample(args, planes: int):
-    """The reference algorithm (oracle numpy port of kvmanager.quantize/dequantize) on
-    `planes` (layer, K|V) planes of one job, one process per host core."""
+    """The reference quantize/dequantize (kvmanager.py:108-154) on `planes` (layer, K|V)
+    planes of one C2 job, one process per host core (the reference is single-threaded
+    numpy per call), wall clock from the common start to the last finish."""
     import multiprocessing as mp
     cores = os.cpu_count() or 1
-    payload = [(i, args.tokens, args.hidden, args.group, args.bits) for i in range(planes)]
+    procs = max(1, min(cores, planes))
     ctx = mp.get_context("fork")
-    with ctx.Pool(min(cores, planes)) as pool:
-        pool.map(_cpu_worker, payload[: min(cores, planes)])  # warm imports
-        t0 = time.perf_counter()
-        res = pool.map(_cpu_worker, payload)
-        wall = time.perf_counter() - t0
+    barrier = ctx.Barrier(procs)
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_cpu_proc, args=(list(range(i, planes, procs)), args.tokens, args.hidden, args.group,
+                                              args.bits, barrier, q)) for i in range(procs)]
+    for p in ps:
+        p.start()
+    res = [q.get() for _ in ps]
+    for p in ps:
+        p.join()
     elems = sum(r[0] for r in res)
-    procs = min(cores, planes)
-    # compute time only (input generation inside the workers is excluded), assuming
-    # perfect scaling over the worker processes: an upper bound for the CPU path
-    busy = sum(r[1] + r[2] for r in res) / procs
-    return {"elements": elems, "wall_s": busy, "cores": procs,
-            "GBps": 2 * 2 * elems / busy / 1e9}
+    wall = max(r[2] for r in res) - min(r[1] for r in res)
+    return {"elements": elems, "wall_s": wall, "cores": procs, "kind": _ref_kv_functions()[2],
+            "GBps": 2 * 2 * elems / wall / 1e9}
 
 
 # ----------------------------------------------------------------- link peaks
@@ -381,7 +407,27 @@ def _kv_bench(args, world, rank, local, layouts=None, e2e=True):
         iso = {"quant_ms_per_job": i0.elapsed_time(i1) / 5, "job_bytes": my_layouts[0].elements * 2,
                "slab_bytes": geos[0]["slab_bytes"], "launches_per_job": geos[0]["n_chunks"]}
         del dslab
-    res = {"ms_per_step": ms_max / args.steps, "value": value, "nonfinite": bad, "isolated": iso,
+    # parity after the timed region: one more offload + upload of two of this rank's jobs
+    # (the values the next step would swap), sampled planes vs the C oracle
+    parity = {"checked_planes": 0, "checked_values": 0, "mismatches": 0}
+    if kvs and not getattr(args, "no_parity", False):
+        from harness import parity as hp
+        for j in sorted({0, len(kvs) - 1}):
+            lay, gj = my_layouts[j], geos[j]
+            src = kvs[j].clone()
+            out = torch.zeros_like(src)
+            eng.offload(lay, src, slabs[0], flag=flag)
+            eng.upload(lay, slabs[0], out)
+            torch.cuda.synchronize()
+            planes = sorted({0, 1, lay.layers, 2 * lay.layers - 1})
+            npl, nval, badp = hp.kv_check_planes(lay, src.cpu().numpy(), pool.view(slabs[0], gj["slab_bytes"]),
+                                                 out.cpu().numpy(), planes=planes)
+            parity["checked_planes"] += npl
+            parity["checked_values"] += nval
+            parity["mismatches"] += len(badp)
+            del src, out
+    parity = {key: int(sum_over_ranks(val, world)) for key, val in parity.items()}
+    res = {"ms_per_step": ms_max / args.steps, "value": value, "nonfinite": bad, "isolated": iso, "parity": parity,
            "link_bytes_per_step": link_total / args.steps,
            "link_GBs_total": link_total / (ms_max / 1e3) / 1e9,
            "quant_ms_total": qms, "quant_launches": qn, "deq_ms_total": dms, "deq_launches": dn,
@@ -542,6 +588,23 @@ def pred_bench(args, world, rank, local):
                   "api": "LengthPredictor.predict_batch(host queries) -> host lengths, query upload of "
                          "step i+1 overlapped with step i (copy stream), results read back every step"}
     res["shard_rows"] = local_store.size
+    # parity after the timed region (N = 1): sampled queries of the batch vs the oracle
+    if world == 1 and not getattr(args, "no_parity", False):
+        from harness import parity as hp
+        sims, seqs, slens, cnt, _ = local_store.search_batch(Q, K)
+        o_len, o_ret = predictor.predict_batch(Q)
+        vec, lens_h, seqs_h = local_store.export()
+        order = np.argsort(seqs_h)
+        db_h = vec[order].astype(np.float32)
+        g = np.random.default_rng(0)
+        idx = np.sort(np.concatenate([g.choice(B // 2, args.pred_parity // 2, replace=False),
+                                      B // 2 + g.choice(B - B // 2, args.pred_parity - args.pred_parity // 2,
+                                                        replace=False)]))
+        badq = hp.pred_check(db_h, lens_h[order], Q.cpu().numpy(), idx, sims.cpu().numpy(), seqs.cpu().numpy(),
+                             slens.cpu().numpy(), cnt.cpu().numpy(), o_len.cpu().numpy(), o_ret.cpu().numpy(),
+                             reg.w1, reg.b1, reg.w2, reg.b2, k=K)
+        res["parity"] = {"checked_queries": int(len(idx)), "mismatches": len(badq)}
+        del db_h, vec
     del store, local_store, predictor
     torch.cuda.empty_cache()
     return res
@@ -743,6 +806,20 @@ def main():
             "clocks": kv["clocks"],
             "nonfinite_flag": kv["nonfinite"],
         }
+        # bit-exact checks against the oracle after the timed regions (harness/parity.py)
+        par = {"kv_c2": kv["parity"]}
+        if kv3 is not None:
+            par["kv_c3"] = kv3["parity"]
+        if kvch is not None:
+            par["kv_c2_channel"] = kvch["parity"]
+        if pred is not None and "parity" in pred:
+            par["predictor"] = pred["parity"]
+        out["parity"] = {"checked": int(sum(v.get("checked_planes", v.get("checked_queries", 0))
+                                            for v in par.values())),
+                         "mismatches": int(sum(v["mismatches"] for v in par.values())),
+                         "units": "KV (layer, K|V) planes (codes, scale/zero, fp16 round trip) + predictor "
+                                  "queries (top-k seqs/lens/sims, length, provenance)",
+                         "detail": par}
         if "e2e" in kv:
             out["e2e"] = kv["e2e"]
         iso = kv.get("isolated") or {}
@@ -817,11 +894,12 @@ def main():
                                               f"{args.pred_dim} float64 DB (BLAS gemv scan, predictor.py:158)"}
         if cpu is not None:
             out["cpu_baseline"] = {"value": round(cpu["GBps"], 4), "unit": "GB/s", "cores": cpu["cores"],
-                                   "kind": "port",
+                                   "kind": cpu["kind"],
                                    "sample": f"{args.cpu_planes} (layer,K|V) planes of one job "
-                                             f"({cpu['elements']} fp16 values): oracle numpy "
-                                             f"quantize+dequantize (kvmanager.py:108-154), "
-                                             f"one process per core, {cpu['wall_s']:.2f}s"}
+                                             f"({cpu['elements']} fp16 values): "
+                                             f"{'servesim.kvmanager' if cpu['kind'] == 'reference' else 'oracle numpy port of'}"
+                                             f" quantize+dequantize (kvmanager.py:108-154), one process per core, "
+                                             f"wall {cpu['wall_s']:.2f}s"}
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist
@@ -829,8 +907,9 @@ def main():
 
 
 def reference_arm(args, world, rank):
-    """The reference's CPU path (oracle numpy port of kvmanager.quantize/dequantize;
-    the reference is pure Python/numpy and has no GPU or link) on the host cores."""
+    """The reference's CPU path (servesim.kvmanager.quantize/dequantize from the
+    offline install in baseline/_ref, else the oracle's numpy port of it; the reference
+    is pure Python/numpy and has no GPU or link) on the host cores, wall clock."""
     if rank != 0:
         return
     samples = []
@@ -842,6 +921,7 @@ def reference_arm(args, world, rank):
     elems = sum(s["elements"] for s in samples)
     v = 2 * 2 * elems / wall / 1e9
     cores = samples[0]["cores"]
+    kind = samples[0]["kind"]
     out = {"metric": METRIC, "impl": "reference", "value": round(v, 4),
            "unit": "GB/s (fp16 KV swapped out+in per s)", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(1e3 * wall / args.steps, 3),
@@ -850,8 +930,10 @@ def reference_arm(args, world, rank):
            "config": {"workload": f"C2 sample: {args.cpu_planes} (layer,K|V) planes of a Llama-2-7B "
                                   f"job, INT{args.bits} g={args.group} quantize+dequantize",
                       "jobs": args.jobs, "tokens": args.tokens, "bits": args.bits},
-           "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-                            "sample": f"{args.cpu_planes} planes per step, {elems // args.steps} values"},
+           "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": kind,
+                            "sample": f"{args.cpu_planes} planes per step, {elems // args.steps} values, "
+                                      f"{'servesim.kvmanager.quantize/dequantize from baseline/_ref' if kind == 'reference' else 'oracle numpy port'}, "
+                                      f"wall clock over {cores} worker processes"},
            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 

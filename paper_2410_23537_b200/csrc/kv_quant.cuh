@@ -87,9 +87,14 @@ __device__ __forceinline__ uint32_t f2bits(float f) { return __float_as_uint(f);
 __device__ __forceinline__ uint32_t gather4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
+// Two codes per byte (low nibble = even element).  The fast path's provisional code
+// byte can be 0xFF (rint(t32) = -1 just below a group's minimum, flagged and rewritten
+// by the fix-up pass), so each code is masked to its nibble: an unmasked 0xFF in an odd
+// element would spill 0xF into the next byte's even element, which the fix-up of the
+// flagged byte does not rewrite.
 __device__ __forceinline__ uint32_t pack_int4x8(const uint32_t (&c)[8]) {
-  const uint32_t even = gather4(c[0], c[2], c[4], c[6]);
-  const uint32_t odd = gather4(c[1], c[3], c[5], c[7]);
+  const uint32_t even = gather4(c[0], c[2], c[4], c[6]) & 0x0F0F0F0Fu;
+  const uint32_t odd = gather4(c[1], c[3], c[5], c[7]) & 0x0F0F0F0Fu;
   return even | (odd << 4);
 }
 

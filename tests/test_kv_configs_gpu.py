@@ -12,13 +12,11 @@
 * C3 (configs[2]): INT4 g=64 packed at the ShareGPT p95 length (1488 tokens).
 Reference: kvmanager.py:108-154 (quantize / dequantize)."""
 import os
-from concurrent.futures import ThreadPoolExecutor
-
 import numpy as np
 import pytest
 
 from oracle import kv_oracle as ko
-from tests.conftest import GOLDEN, c_quantize, have_gpu
+from tests.conftest import GOLDEN, have_gpu
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a CUDA device")]
 
@@ -90,37 +88,20 @@ def test_c1_true_shape_device_slab(km, c1, kind, group, bits, packed):
     assert ko_digest(got) == str(z[tag + "_deq16_digest"])
 
 
-def _plane_records(lay, slab):
-    """Yield (plane index, codes bytes, fp16 (min, -max) pairs) of every (layer, K|V)
-    plane of a slab: chunk records are [codes, native order][(min, -max) per group],
-    sections 256-byte aligned."""
-    g = lay.geometry()
-    planes = lay.layers * 2
-    ppc = -(-planes // g["n_chunks"])
-    per_codes = lay.tokens * lay.hidden // (2 if lay.packed else 1)
-    rows_pp = g["rows"] // planes
-    a256 = lambda x: (x + 255) // 256 * 256
-    for p in range(planes):
-        c, j = divmod(p, ppc)
-        np_ = min(ppc, planes - c * ppc)
-        base = c * g["chunk_bytes"]
-        codes = slab[base + j * per_codes: base + (j + 1) * per_codes]
-        pbase = base + a256(np_ * per_codes) + j * rows_pp * 4
-        yield p, codes, slab[pbase: pbase + rows_pp * 4].view(np.float16).reshape(-1, 2)
-
-
 def _slab_codes(lay, slab, shape):
-    parts = [c for _, c, _ in _plane_records(lay, slab)]
+    from harness import parity
+    parts = [c for _, c, _ in parity.plane_records(lay, slab)]
     native = np.concatenate(parts)
     if lay.packed:
         native = np.stack([native & 15, native >> 4], axis=1).reshape(-1)
     return native.reshape(shape)
 
 
-def _job_parity(km, c_oracle, lay, kind, kv, threads=8):
+def _job_parity(km, lay, kv):
     """Offload a whole job to pinned host memory and upload it back through the swap
-    engine; check every plane against the C oracle.  Returns (planes, mismatching planes)."""
+    engine; check every plane against the C oracle (harness/parity.py)."""
     import torch
+    from harness import parity
     g = lay.geometry()
     pool = km.HostSlabPool(g["slab_bytes"] + 4096)
     eng = km.KVSwapEngine()
@@ -130,67 +111,85 @@ def _job_parity(km, c_oracle, lay, kind, kv, threads=8):
         eng.offload(lay, kv, addr, flag=flag)
         torch.cuda.synchronize()
         assert int(flag.item()) == 0
-        slab = pool.view(addr, g["slab_bytes"])
         out = torch.zeros_like(kv)
         eng.upload(lay, addr, out)
         torch.cuda.synchronize()
-        src_h = kv.cpu().numpy()
-        out_h = out.cpu().numpy()
-        bad = []
-
-        def check(rec):
-            p, codes, mm = rec
-            layer, s = divmod(p, 2)
-            x = src_h[layer, s][None, None]                   # [1, 1, T, hidden]
-            rows = ko.view_rows(x, kind, group=lay.group, head_dim=lay.head_dim)
-            c_ref, s_ref, z_ref = c_quantize(c_oracle, rows, lay.bits)
-            if lay.packed:
-                codes = np.stack([codes & 15, codes >> 4], axis=1).reshape(-1)
-            got = ko.view_rows(np.asarray(codes).reshape(x.shape), kind, group=lay.group, head_dim=lay.head_dim)
-            scale, zero = ko.params_from_minmax(mm[:, 0].astype(np.float64), -mm[:, 1].astype(np.float64), lay.bits)
-            deq = np.empty(rows.shape)
-            c_oracle.oracle_dequantize(c_ref.ctypes.data, s_ref.ctypes.data, z_ref.ctypes.data, rows.shape[0],
-                                       rows.shape[1], deq.ctypes.data)
-            back = ko.view_rows(out_h[layer, s][None, None], kind, group=lay.group, head_dim=lay.head_dim)
-            ok = (np.array_equal(got, c_ref) and np.array_equal(scale, s_ref[:, 0])
-                  and np.array_equal(zero, z_ref[:, 0]) and np.array_equal(back, deq.astype(np.float16)))
-            if not ok:
-                bad.append(p)
-
-        with ThreadPoolExecutor(threads) as ex:   # the C oracle releases the GIL
-            list(ex.map(check, _plane_records(lay, slab)))
-        return lay.layers * 2, bad
+        planes, _values, bad = parity.kv_check_planes(lay, kv.cpu().numpy(), pool.view(addr, g["slab_bytes"]),
+                                                      out.cpu().numpy())
+        return planes, bad
     finally:
         eng.close()
         pool.close()
 
 
 @pytest.mark.slow
-def test_c2_whole_job_offload_upload_bit_exact(km, c_oracle):
+def test_c2_whole_job_offload_upload_bit_exact(km):
     """C2: one whole 1 GiB Llama-2-7B job, INT8 g=128, every plane bit-exact."""
     from harness import synthetic
     lay = km.KVLayout(32, 2048, 4096, 128, kind="rows", group=128, bits=8)
     kv = synthetic.kv_job_torch(32, 2048, 4096, seed=0, job=3, group=128)
-    planes, bad = _job_parity(km, c_oracle, lay, "contig", kv)
+    planes, bad = _job_parity(km, lay, kv)
     assert planes == 64 and not bad, bad
 
 
 @pytest.mark.slow
-def test_c2_reference_channel_layout_t2048(km, c_oracle):
+def test_c2_reference_channel_layout_t2048(km):
     """The reference's accounting layout (kvmanager.py:72-75: one (scale, zero) per
     (layer, K|V, hidden channel) over the tokens) at T = 2048, 4 layers."""
     from harness import synthetic
     lay = km.KVLayout(4, 2048, 4096, 128, kind="channel", bits=8)
     kv = synthetic.kv_job_torch(4, 2048, 4096, seed=0, job=5, group=128)
-    planes, bad = _job_parity(km, c_oracle, lay, "channel", kv)
+    planes, bad = _job_parity(km, lay, kv)
     assert planes == 8 and not bad, bad
 
 
 @pytest.mark.slow
-def test_c3_int4_g64_packed_p95_job(km, c_oracle):
+def test_c3_int4_g64_packed_p95_job(km):
     """C3: INT4 g=64 packed two per byte, a ShareGPT p95-length job (1488 tokens)."""
     from harness import synthetic
     lay = km.KVLayout(8, 1488, 4096, 128, kind="rows", group=64, bits=4, packed=True)
     kv = synthetic.kv_job_torch(8, 1488, 4096, seed=0, job=11, group=64)
-    planes, bad = _job_parity(km, c_oracle, lay, "contig", kv)
+    planes, bad = _job_parity(km, lay, kv)
     assert planes == 16 and not bad, bad
+
+
+# ----------------------------------------------------------------- C4 at its own shape
+@pytest.mark.slow
+def test_c4_full_db_1m_x_768_batch_4096():
+    """C4 (configs[3]): 1M x 768 fp32 DB with 1000 planted duplicate groups, one batch of
+    4096 queries through LengthPredictor.predict_batch; 256 sampled queries plus one
+    query aimed at each of 100 planted duplicate groups (11-way exact ties) checked
+    against the oracle: top-8 seqs/lens/sims bit-exact, predicted lengths exact."""
+    import torch
+
+    from harness import parity, synthetic
+    from paper_2410_23537_b200 import predictor as pr
+    N, D, B = 1_000_000, 768, 4096
+    db, lens = synthetic.predictor_db_torch(N, D, seed=0, dup_groups=1000, device="cuda")
+    Q = synthetic.predictor_queries_torch(db, B, seed=1)
+    # queries aimed at planted groups: rows that occur more than once (hash of the row)
+    h = db @ torch.randn(D, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3))
+    uniq, inv, counts = torch.unique(h, return_inverse=True, return_counts=True)
+    dup_rows = torch.nonzero(counts[inv] > 1).flatten()
+    grp_first = {}
+    for r in dup_rows.tolist():
+        grp_first.setdefault(int(inv[r]), r)
+    targets = list(grp_first.values())[:100]
+    gq = torch.Generator(device="cuda").manual_seed(4)
+    Q[:100] = db[targets] + 0.01 * torch.randn((len(targets), D), device="cuda", generator=gq)
+    Q[:100] /= Q[:100].norm(dim=1, keepdim=True)
+    store = pr.VectorStore(D, N, dtype=np.float32)
+    store.add_batch(db, lens)
+    reg = pr.FallbackRegressor(D, 32, seed=0)
+    reg.b2 = 5.0
+    p = pr.LengthPredictor(pr.PredictorConfig(dimension=D, db_capacity=N), regressor=reg, store=store)
+    sims, seqs, slens, cnt, _ = store.search_batch(Q, 8)
+    out, ret = p.predict_batch(Q)
+    torch.cuda.synchronize()
+    g = np.random.default_rng(0)
+    idx = np.concatenate([np.arange(100), np.sort(g.choice(np.arange(100, B), 256, replace=False))])
+    bad = parity.pred_check(db.cpu().numpy(), lens.cpu().numpy(), Q.cpu().numpy(), idx, sims.cpu().numpy(),
+                            seqs.cpu().numpy(), slens.cpu().numpy(), cnt.cpu().numpy(), out.cpu().numpy(),
+                            ret.cpu().numpy(), reg.w1, reg.b1, reg.w2, reg.b2)
+    assert not bad, bad[:10]
+    assert len(targets) == 100 and int(ret[:100].sum()) == 100
