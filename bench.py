@@ -417,6 +417,7 @@ def _kv_bench(args, world, rank, local, layouts=None, e2e=True):
             src = kvs[j].clone()
             out = torch.zeros_like(src)
             eng.offload(lay, src, slabs[0], flag=flag)
+            torch.cuda.synchronize()   # the upload reads what the offload wrote
             eng.upload(lay, slabs[0], out)
             torch.cuda.synchronize()
             planes = sorted({0, 1, lay.layers, 2 * lay.layers - 1})
