@@ -218,7 +218,7 @@ def _adversarial_norm_db(d=64, k=4):
     return np.array(rows), q
 
 
-def _sharded_worker(rank, world, port, result_dir):
+def _sharded_worker(rank, world, port, result_dir, backend="gloo"):
     import os
 
     import torch
@@ -228,8 +228,12 @@ def _sharded_worker(rank, world, port, result_dir):
     from paper_2410_23537_b200 import sharding
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(0)  # both ranks share the one GPU; gloo carries the exchange
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":     # one GPU per rank, NCCL over NVLink
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    else:                     # both ranks share the one GPU; gloo carries the exchange
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     fails = []
 
     def same(tag, sims, seqs, slens, cnt, ref):
@@ -333,6 +337,24 @@ def test_sharded_store_two_ranks_one_gpu(tmp_path):
     port = s.getsockname()[1]
     s.close()
     mp.spawn(_sharded_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        assert (tmp_path / f"r{r}").read_text() == "ok"
+
+
+def test_sharded_store_nccl_two_gpus(tmp_path):
+    """The same end-to-end checks over NCCL with one GPU per rank (runs wherever two or
+    more GPUs are visible, e.g. the 8-GPU scaling box)."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_sharded_worker, args=(2, port, str(tmp_path), "nccl"), nprocs=2, join=True)
     for r in range(2):
         assert (tmp_path / f"r{r}").read_text() == "ok"
 
