@@ -719,13 +719,13 @@ def main():
     if not args.no_c5:
         from harness import replay
         rec = replay.load(os.path.join(ROOT, "tests", "golden", "c5_swaps.json.gz"))
-        mine = list(range(rank, len(rec["replicas"]), world)) if world > 1 else [0]
+        mine = list(range(rank, len(rec["replicas"]), world))   # all 8 replicas, one rank each
         outs = [replay.replay(rec, replica=r, check_data=False) for r in mine]
         wall = max_over_ranks(sum(o["wall_s"] for o in outs), world)
         moved = sum_over_ranks(sum(o["fp16_bytes_moved"] for o in outs), world)
         link = sum_over_ranks(sum(o["link_bytes"] for o in outs), world)
         swaps = sum_over_ranks(sum(o["swaps_out"] + o["swaps_in"] for o in outs), world)
-        c5 = {"replicas": len(rec["replicas"]) if world > 1 else 1, "wall_s": wall, "fp16_GBs": moved / wall / 1e9,
+        c5 = {"replicas": len(rec["replicas"]), "wall_s": wall, "fp16_GBs": moved / wall / 1e9,
               "link_GBs": link / wall / 1e9, "swaps": int(swaps),
               "modeled_span_s": max(o["modeled_span_s"] for o in outs),
               "link_bytes_moved": sum_over_ranks(sum(o["link_bytes_moved"] for o in outs), world)}
@@ -735,6 +735,14 @@ def main():
         c5["delta"] = {"wall_s": max_over_ranks(sum(o["wall_s"] for o in outs), world),
                        "link_bytes_moved": sum_over_ranks(sum(o["link_bytes_moved"] for o in outs), world),
                        "fp16_bytes_moved": sum_over_ranks(sum(o["fp16_bytes_moved"] for o in outs), world)}
+        # the reference engine itself driving the data plane live (harness/live.py): its
+        # MetricsReport must equal the pure reference run's (needs baseline/_ref)
+        from harness import live, refsim
+        if rank == 0 and refsim.servesim_path() is not None:
+            rep, st, wall_live = live.run_replica(0, check_planes=(79,), check_every=8)
+            c5["live"] = {"replica": 0, "report_identical": json.loads(rep) == rec["replicas"][0]["report"],
+                          "swaps": st["swaps_out"] + st["swaps_in"], "planes_checked": st["planes_checked"],
+                          "mismatches": st["mismatches"], "wall_s": round(wall_live, 3)}
     pred = None if args.no_pred else pred_bench(args, world, rank, local)
     ctl = control_plane_bench() if rank == 0 else None
     cpu = cpu_pred = None
@@ -851,8 +859,10 @@ def main():
         if c5 is not None:
             out["kv_c5_replay"] = {
                 "workload": f"C5: reference simulator swap stream (speculative, Alpaca @2/s per replica, "
-                            f"Llama-2-13B, INT8), {c5['replicas']} replica(s) replayed through DeviceMemoryState "
-                            f"with real KV; ledger checked against the reference after every call",
+                            f"Llama-2-13B, INT8), {c5['replicas']} replicas replayed through DeviceMemoryState "
+                            f"with real KV (one rank each at N>1); ledger checked against the reference after "
+                            f"every call",
+                "live_engine": c5.get("live"),
                 "value": round(c5["fp16_GBs"], 3), "unit": "GB/s (fp16 KV swapped)",
                 "link_GBs": round(c5["link_GBs"], 2), "swaps": c5["swaps"], "wall_s": round(c5["wall_s"], 3),
                 "reference_modeled_span_s": round(c5["modeled_span_s"], 3),

@@ -157,3 +157,23 @@ def pred_check(db32, lens, Q32, idx, sims, seqs, slens, cnt, out_len, out_ret, W
                 and bool(out_ret[i]) == want_ret):
             bad.append(int(i))
     return bad
+
+
+def kv_roundtrip_planes(lay, planes_src: dict, planes_out: dict):
+    """planes_src / planes_out: {plane: [tokens, hidden] fp16 host array} before the
+    offload and after the upload.  Returns the planes whose round trip differs from
+    fp16(oracle dequantize(oracle quantize(src))) (kvmanager.py:108-154)."""
+    from oracle import kv_oracle as ko
+    lib = c_oracle()
+    kind = "contig" if lay.kind == "rows" else lay.kind
+    bad = []
+    for p, x in planes_src.items():
+        rows = ko.view_rows(np.asarray(x)[None, None], kind, group=lay.group, head_dim=lay.head_dim)
+        c, s, z = c_quantize(lib, rows, lay.bits)
+        deq = np.empty(rows.shape)
+        lib.oracle_dequantize(c.ctypes.data, s.ctypes.data, z.ctypes.data, rows.shape[0], rows.shape[1],
+                              deq.ctypes.data)
+        back = ko.view_rows(np.asarray(planes_out[p])[None, None], kind, group=lay.group, head_dim=lay.head_dim)
+        if not np.array_equal(back, deq.astype(np.float16)):
+            bad.append(p)
+    return bad

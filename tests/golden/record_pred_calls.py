@@ -27,7 +27,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
-from tests import refsim  # noqa: E402
+from harness import refsim  # noqa: E402
 
 refsim.import_servesim()
 from servesim import simcore, workload  # noqa: E402

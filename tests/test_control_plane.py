@@ -10,7 +10,7 @@ import pytest
 
 from paper_2410_23537_b200 import kvmanager as km
 
-from tests import refsim
+from harness import refsim
 
 
 def job(level, last_promotion_us=0):

@@ -283,8 +283,8 @@ def test_llama7b_job_round_trip_properties(km):
 def test_c5_replay_matches_reference_ledger():
     """Config-5 replay (tests/golden/c5_swaps.json.gz, recorded from the reference
     simulator): every swap call moves real quantized KV through DeviceMemoryState, the
-    ledger equals the reference after every call, and each job's KV after its first
-    round trip equals the device-to-device quantize/dequantize of its original."""
+    ledger equals the reference after every call, and sampled planes of each job's KV
+    after its first round trip equal the oracle's quantize/dequantize of its original."""
     import os
 
     from harness import replay
@@ -384,10 +384,10 @@ def test_delta_transfer_errors(km):
 
 def test_c5_replay_delta_offload_same_ledger():
     """Config-5 replay with incremental (delta) offload: the ledger still equals the
-    reference after every call, fewer bytes cross the link, and after every upload each
-    job's KV equals the device-to-device quantize/dequantize of its ORIGINAL values (each
-    token is quantized once; a full re-offload would re-quantize fp16-rounded
-    dequantized values)."""
+    reference after every call, fewer bytes cross the link, and after every upload
+    sampled planes of each job's KV equal the oracle's quantize/dequantize of its
+    ORIGINAL values (each token is quantized once; a full re-offload would re-quantize
+    fp16-rounded dequantized values)."""
     import os
 
     from harness import replay

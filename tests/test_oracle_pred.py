@@ -107,7 +107,7 @@ def test_embedder_and_config():
 
 
 def test_embedder_matches_reference_hashing():
-    from tests import refsim
+    from harness import refsim
     refsim.import_servesim()
     try:
         from servesim.predictor import HashingEmbedder as RefEmb
@@ -156,7 +156,7 @@ def test_blas_order_matches_numpy(n, d):
 def test_search_blas_is_the_reference_search():
     """search_blas == the reference VectorStore.search on the same records (ring
     wrap-around included) on this host."""
-    from tests import refsim
+    from harness import refsim
     if refsim.import_servesim() is None:
         pytest.skip("reference not importable")
     from servesim.predictor import VectorStore as RefStore

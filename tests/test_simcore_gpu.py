@@ -22,7 +22,7 @@ import os
 import numpy as np
 import pytest
 
-from tests import refsim
+from harness import refsim
 from tests.conftest import GOLDEN, have_gpu
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a CUDA device")]
