@@ -92,12 +92,17 @@ def kv_check_planes(lay, src_h, slab, out_h, planes=None, threads=8):
         layer, s = divmod(p, 2)
         x = src_h[layer, s][None, None]
         rows = ko.view_rows(x, kind, group=lay.group, head_dim=lay.head_dim)
-        c_ref, s_ref, z_ref = c_quantize(lib, rows, lay.bits)
+        absmax = getattr(lay, "mode", "asymmetric") == "absmax"
+        if absmax:   # restated symmetric mode (parity unpinned by the reference)
+            c_ref, s_ref, z_ref = ko.quantize_rows_absmax(rows, lay.bits)
+        else:
+            c_ref, s_ref, z_ref = c_quantize(lib, rows, lay.bits)
         codes = np.asarray(codes)
         if lay.packed:
             codes = np.stack([codes & 15, codes >> 4], axis=1).reshape(-1)
         got = ko.view_rows(codes.reshape(x.shape), kind, group=lay.group, head_dim=lay.head_dim)
-        scale, zero = ko.params_from_minmax(mm[:, 0].astype(np.float64), -mm[:, 1].astype(np.float64), lay.bits)
+        solve = ko.params_absmax if absmax else ko.params_from_minmax
+        scale, zero = solve(mm[:, 0].astype(np.float64), -mm[:, 1].astype(np.float64), lay.bits)
         deq = np.empty(rows.shape)
         lib.oracle_dequantize(c_ref.ctypes.data, s_ref.ctypes.data, z_ref.ctypes.data, rows.shape[0], rows.shape[1],
                               deq.ctypes.data)

@@ -45,6 +45,17 @@ extern "C" {
 #define ALISE_KIND_CHANNEL 1  /* (layer, k|v, hidden column) along tokens (reference)   */
 #define ALISE_KIND_HEAD 2     /* (layer, k|v, head) over tokens x head_dim              */
 
+/* How a group's (scale, zero) follow from its (min, max):
+ *  ASYM   the reference's asymmetric min/max scheme (kvmanager.py:130-146: scale =
+ *         (max-min)/qmax, zero = rint(-min/scale), snap loop);
+ *  ABSMAX symmetric absmax scheme named by the north star (parity UNPINNED by the
+ *         reference, which has no such mode; restated in oracle/kv_oracle.py
+ *         quantize_rows_absmax): scale = max|x| / (2^(b-1)-1) (1 if 0), zero = 2^(b-1).
+ * Codes and values use the reference formulas in both modes: clip(rint(x/scale +
+ * zero), 0, qmax) and scale*(code - zero). */
+#define ALISE_QMODE_ASYM 0
+#define ALISE_QMODE_ABSMAX 1
+
 #define ALISE_SWAP_STAGED 0   /* quantize to an HBM ring, copy engine D2H/H2D (default) */
 #define ALISE_SWAP_ZEROCOPY 1 /* kernels read/write mapped pinned host memory directly  */
 
@@ -93,6 +104,10 @@ int alise_quantize_rows_workspace(int64_t rows, int64_t row_len, int src_dtype, 
 int alise_quantize_rows(const void *src, int src_dtype, int64_t rows, int64_t row_len,
                         int64_t row_stride, int bits, uint8_t *codes, double *scale,
                         double *zero, int *nonfinite_flag, void *workspace, void *stream);
+/* alise_quantize_rows with a quantization mode (ALISE_QMODE_*). */
+int alise_quantize_rows_ex(const void *src, int src_dtype, int64_t rows, int64_t row_len,
+                           int64_t row_stride, int bits, int mode, uint8_t *codes, double *scale,
+                           double *zero, int *nonfinite_flag, void *workspace, void *stream);
 /* Drop-in for kvmanager.dequantize: out = scale*(code - zero), out_dtype F64 (reference
  * bit-exact) or F16 (one rounding of the float64 value). */
 int alise_dequantize_rows(const uint8_t *codes, const double *scale, const double *zero,
@@ -110,7 +125,7 @@ typedef struct {
   int32_t bits;       /* 4 or 8 */
   int32_t packed;     /* 1: two INT4 codes per byte (low nibble = even element) */
   int32_t planes_per_chunk; /* transfer granularity in (layer, k|v) planes; 0 = auto */
-  int32_t reserved;
+  int32_t mode;       /* ALISE_QMODE_*: how a group's (scale, zero) follow from its (min, max) */
 } alise_kv_desc;
 
 /* Host slab layout: ceil(planes/planes_per_chunk) chunk records, each

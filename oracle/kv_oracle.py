@@ -72,6 +72,40 @@ def params_from_minmax(lo, hi, bits: int):
     return s, z
 
 
+def params_absmax(lo, hi, bits: int):
+    """(scale, zero) of the symmetric absmax mode from the row (min, max) -- the north
+    star's alternative group-wise scheme.  PARITY UNPINNED: the reference has no such
+    mode, so this restates the formula itself: a = max|x| = max(|min|, |max|),
+    scale = a / (2^(b-1) - 1) (one correctly rounded float64 division; 1 when a == 0),
+    zero = 2^(b-1); codes and values then use the reference's own formulas
+    (kvmanager.py:148, :154)."""
+    lo = np.asarray(lo, dtype=np.float64)
+    hi = np.asarray(hi, dtype=np.float64)
+    a = np.maximum(np.abs(lo), np.abs(hi))
+    qs = float(2 ** (bits - 1) - 1)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        s = np.where(a == 0.0, 1.0, a / qs)
+    return s, np.full_like(s, float(2 ** (bits - 1)))
+
+
+def quantize_rows_absmax(x, bits: int):
+    """Symmetric absmax quantization of each row (see params_absmax); same errors and
+    output layout as quantize_rows."""
+    if bits not in (4, 8):
+        raise ValueError("bits must be 4 or 8")
+    a = np.asarray(x, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(1, -1)
+    if a.ndim != 2 or a.size == 0:
+        raise ValueError("expected a non-empty channel-major 2D tensor")
+    if not np.isfinite(a).all():
+        raise ValueError("tensor contains non-finite values")
+    qmax = float(2 ** bits - 1)
+    s, z = params_absmax(a.min(axis=1), a.max(axis=1), bits)
+    codes = np.clip(np.rint(a / s[:, None] + z[:, None]), 0.0, qmax).astype(np.uint8)
+    return codes, s[:, None].copy(), z[:, None].copy()
+
+
 def dequantize_rows(codes, scale, zero):
     """kvmanager.py:152-154: scale * (q - zero) in float64."""
     return np.asarray(scale, np.float64) * (np.asarray(codes).astype(np.float64)

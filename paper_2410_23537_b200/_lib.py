@@ -25,7 +25,7 @@ i64, i32, vp, dp = C.c_int64, C.c_int, C.c_void_p, C.c_double
 class KvDesc(C.Structure):
     _fields_ = [("layers", i64), ("tokens", i64), ("hidden", i64), ("head_dim", i64),
                 ("kind", C.c_int32), ("group", C.c_int32), ("bits", C.c_int32),
-                ("packed", C.c_int32), ("planes_per_chunk", C.c_int32), ("reserved", C.c_int32)]
+                ("packed", C.c_int32), ("planes_per_chunk", C.c_int32), ("mode", C.c_int32)]
 
 
 # name -> argtypes (restype is always int)
@@ -38,6 +38,7 @@ _SIGS = {
     "alise_rank_and_plan": [i64, vp, vp, vp, vp, vp, dp, i64, i64, vp, vp, vp, vp],
     "alise_quantize_rows_workspace": [i64, i64, i32, vp],
     "alise_quantize_rows": [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp, vp, vp],
+    "alise_quantize_rows_ex": [vp, i32, i64, i64, i64, i32, i32, vp, vp, vp, vp, vp, vp],
     "alise_dequantize_rows": [vp, vp, vp, i64, i64, i32, vp, vp],
     "alise_kv_layout": [vp, vp, vp, vp, vp],
     "alise_kv_quantize": [vp, vp, vp, vp, vp],

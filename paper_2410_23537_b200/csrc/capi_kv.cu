@@ -99,7 +99,7 @@ extern "C" int alise_selftest_qdiv(const double* x, int64_t n, int bits, int64_t
 template <int BITS, bool PACK, bool ZF32, int V, int TP, int WPB, int MINB = 1, int NBUF = 2>
 static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes, double* scale,
                          void* zero, uint32_t* mm, int* flag, cudaStream_t st, int64_t seg_rows,
-                         int64_t seg_stride) {
+                         int64_t seg_stride, int sym) {
   constexpr int block = 32 * WPB;
   Segs seg{0, 0, 0};
   if (seg_rows) {
@@ -118,7 +118,7 @@ static int launch_tile_v(const uint16_t* x, int64_t rows, int row_len, uint8_t* 
   }
   const int64_t warps = (rows + 8 * TP - 1) / (8 * TP);
   const int grid = grid_for(warps * 32, block, per_sm);
-  kern<<<grid, block, smem, st>>>(x, rows, row_len, codes, scale, zero, mm, flag, seg);
+  kern<<<grid, block, smem, st>>>(x, rows, row_len, codes, scale, zero, mm, flag, seg, sym);
   CKL();
   return ALISE_OK;
 }
@@ -140,11 +140,11 @@ static int qtile_variant() {
 template <int BITS, bool PACK, bool ZF32>
 static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_t* codes,
                             double* scale, void* zero, uint32_t* mm, int* flag, cudaStream_t st,
-                            int64_t seg_rows, int64_t seg_stride) {
+                            int64_t seg_rows, int64_t seg_stride, int sym) {
   const int vpl = (row_len / 8 + 3) / 4;  // 16-byte vectors per lane per row
   const int var = qtile_variant();
-#define QT(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride)
-#define QT1(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB, 1>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride)
+#define QT(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride, sym)
+#define QT1(V, TP, WPB, MINB) return launch_tile_v<BITS, PACK, ZF32, V, TP, WPB, MINB, 1>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride, sym)
   if (vpl <= 1) QT(1, 4, 8, 3);
   if (vpl <= 2) {
     if (var == 1) QT(2, 2, 8, 4);
@@ -170,16 +170,17 @@ static int launch_tile_bits(const uint16_t* x, int64_t rows, int row_len, uint8_
 
 static int launch_tile(int bits, bool pack, bool zf32, const uint16_t* x, int64_t rows,
                        int row_len, uint8_t* codes, double* scale, void* zero, int* flag,
-                       cudaStream_t st, int64_t seg_rows = 0, int64_t seg_stride = 0, uint32_t* mm = nullptr) {
+                       cudaStream_t st, int64_t seg_rows = 0, int64_t seg_stride = 0, uint32_t* mm = nullptr,
+                       int sym = 0) {
   if (bits == 8) {
-    return zf32 ? launch_tile_bits<8, false, true>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride)
-                : launch_tile_bits<8, false, false>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride);
+    return zf32 ? launch_tile_bits<8, false, true>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride, sym)
+                : launch_tile_bits<8, false, false>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride, sym);
   }
   if (pack)
-    return zf32 ? launch_tile_bits<4, true, true>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride)
-                : launch_tile_bits<4, true, false>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride);
-  return zf32 ? launch_tile_bits<4, false, true>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride)
-              : launch_tile_bits<4, false, false>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride);
+    return zf32 ? launch_tile_bits<4, true, true>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride, sym)
+                : launch_tile_bits<4, true, false>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride, sym);
+  return zf32 ? launch_tile_bits<4, false, true>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride, sym)
+              : launch_tile_bits<4, false, false>(x, rows, row_len, codes, scale, zero, mm, flag, st, seg_rows, seg_stride, sym);
 }
 
 static bool tile_ok(int dtype, int64_t row_len, int64_t row_stride, const void* src,
@@ -205,7 +206,7 @@ extern "C" int alise_quantize_rows_workspace(int64_t rows, int64_t row_len, int 
 template <typename T>
 static int rows_generic(const T* x, int64_t rows, int64_t row_len, int64_t row_stride, int bits,
                         bool pack, uint8_t* codes, double* scale, void* zero, bool zf32,
-                        int* flag, void* ws, cudaStream_t st) {
+                        int* flag, void* ws, cudaStream_t st, int sym) {
   const int64_t ch = rows_chunk(row_len);
   const int nch = (int)((row_len + ch - 1) / ch);
   char* w = reinterpret_cast<char*>(ws);
@@ -219,7 +220,7 @@ static int rows_generic(const T* x, int64_t rows, int64_t row_len, int64_t row_s
   CKL();
   k_params<false><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
       KIND_ROWS, rows, nch, pmn, pmx, nullptr, nullptr, 0, 1, bits, InTraits<T>::wide, scale,
-      zero, fastp, nullptr);
+      zero, fastp, nullptr, sym);
   CKL();
   (void)zf32;
   const int64_t n = rows * row_len;
@@ -234,29 +235,37 @@ static int rows_generic(const T* x, int64_t rows, int64_t row_len, int64_t row_s
   return ALISE_OK;
 }
 
-extern "C" int alise_quantize_rows(const void* src, int src_dtype, int64_t rows, int64_t row_len,
-                                   int64_t row_stride, int bits, uint8_t* codes, double* scale,
-                                   double* zero, int* flag, void* workspace, void* stream) {
+extern "C" int alise_quantize_rows_ex(const void* src, int src_dtype, int64_t rows, int64_t row_len,
+                                      int64_t row_stride, int bits, int mode, uint8_t* codes, double* scale,
+                                      double* zero, int* flag, void* workspace, void* stream) {
   if (bits != 4 && bits != 8) return fail(ALISE_EINVAL, "bits must be 4 or 8");
+  if (mode != ALISE_QMODE_ASYM && mode != ALISE_QMODE_ABSMAX) return fail(ALISE_EINVAL, "unknown quantization mode");
   if (rows <= 0 || row_len <= 0) return fail(ALISE_EINVAL, "expected a non-empty channel-major 2D tensor");
   if (row_stride < row_len) return fail(ALISE_EINVAL, "row_stride < row_len");
   cudaStream_t st = S(stream);
   if (tile_ok(src_dtype, row_len, row_stride, src, codes, false))
     return launch_tile(bits, false, false, reinterpret_cast<const uint16_t*>(src), rows,
-                       (int)row_len, codes, scale, zero, flag, st);
+                       (int)row_len, codes, scale, zero, flag, st, 0, 0, nullptr, mode);
   if (!workspace) return fail(ALISE_EINVAL, "workspace required for this shape");
   switch (src_dtype) {
     case ALISE_DT_F16:
       return rows_generic(reinterpret_cast<const uint16_t*>(src), rows, row_len, row_stride, bits,
-                          false, codes, scale, zero, false, flag, workspace, st);
+                          false, codes, scale, zero, false, flag, workspace, st, mode);
     case ALISE_DT_F32:
       return rows_generic(reinterpret_cast<const float*>(src), rows, row_len, row_stride, bits,
-                          false, codes, scale, zero, false, flag, workspace, st);
+                          false, codes, scale, zero, false, flag, workspace, st, mode);
     case ALISE_DT_F64:
       return rows_generic(reinterpret_cast<const double*>(src), rows, row_len, row_stride, bits,
-                          false, codes, scale, zero, false, flag, workspace, st);
+                          false, codes, scale, zero, false, flag, workspace, st, mode);
   }
   return fail(ALISE_EINVAL, "unknown dtype %d", src_dtype);
+}
+
+extern "C" int alise_quantize_rows(const void* src, int src_dtype, int64_t rows, int64_t row_len,
+                                   int64_t row_stride, int bits, uint8_t* codes, double* scale,
+                                   double* zero, int* flag, void* workspace, void* stream) {
+  return alise_quantize_rows_ex(src, src_dtype, rows, row_len, row_stride, bits, ALISE_QMODE_ASYM, codes, scale,
+                                zero, flag, workspace, stream);
 }
 
 template <int BITS, bool PACK, bool ZF32>
@@ -375,6 +384,8 @@ static int geom(const alise_kv_desc* d, KvGeom* g) {
     return fail(ALISE_EINVAL, "kv desc: layers/tokens/hidden must be positive");
   if (d->bits != 4 && d->bits != 8) return fail(ALISE_EINVAL, "bits must be 4 or 8");
   if (d->packed && d->bits != 4) return fail(ALISE_EINVAL, "packing is INT4 only");
+  if (d->mode != ALISE_QMODE_ASYM && d->mode != ALISE_QMODE_ABSMAX)
+    return fail(ALISE_EINVAL, "unknown quantization mode %d", d->mode);
   if (d->hidden % 8) return fail(ALISE_EINVAL, "hidden must be a multiple of 8");
   g->planes = d->layers * 2;
   g->plane_elems = d->tokens * d->hidden;
@@ -442,13 +453,13 @@ static int quant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, cons
   const int64_t rows = np * g.rows_pp;
   if (d->kind == ALISE_KIND_ROWS)
     return launch_tile(d->bits, d->packed != 0, true, kv, rows, d->group, codes, nullptr, nullptr, flag, st,
-                       0, 0, mm);
+                       0, 0, mm, d->mode);
   const int cpr = d->kind == ALISE_KIND_CHANNEL ? 1 : (int)d->head_dim;
   if (d->hidden % 128 == 0 && cpr <= 128 && 128 % cpr == 0) {
     dim3 grid((unsigned)(d->hidden / 128), (unsigned)np);
-    if (d->bits == 8) k_quant_cols<8, false><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, mm, flag);
-    else if (d->packed) k_quant_cols<4, true><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, mm, flag);
-    else k_quant_cols<4, false><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, mm, flag);
+    if (d->bits == 8) k_quant_cols<8, false><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, mm, flag, d->mode);
+    else if (d->packed) k_quant_cols<4, true><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, mm, flag, d->mode);
+    else k_quant_cols<4, false><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, mm, flag, d->mode);
     CKL();
     return ALISE_OK;
   }
@@ -467,7 +478,7 @@ static int quant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, cons
   CKL();
   k_params<true><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
       d->kind, rows, nch, nullptr, nullptr, pmn, pmx, d->hidden, d->head_dim > 0 ? d->head_dim : 1,
-      d->bits, false, scale, zero, fastp, mm);
+      d->bits, false, scale, zero, fastp, mm, d->mode);
   CKL();
   const int64_t nvec = np * g.plane_elems / 8;
   const int gr = grid_for(nvec, 256, 16);
@@ -484,7 +495,7 @@ static int quant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, cons
 
 // (min, max) of `groups` groups -> (scale, zero) into the scratch pws
 static int expand_params(int bits, const uint32_t* mm, int64_t groups, void* pws, int64_t cap_groups,
-                         double** scale, float** zero, cudaStream_t st) {
+                         double** scale, float** zero, cudaStream_t st, int sym) {
   char* w = reinterpret_cast<char*>(pws);
   *scale = reinterpret_cast<double*>(w);
   *zero = reinterpret_cast<float*>(w + align256(cap_groups * 8));
@@ -497,8 +508,8 @@ static int expand_params(int bits, const uint32_t* mm, int64_t groups, void* pws
 #define EXP(NG)                                                                                  \
   do {                                                                                           \
     const unsigned grid = (unsigned)((groups + 256 * NG - 1) / (256 * NG));                      \
-    if (bits == 8) k_expand_params<8, NG><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero);     \
-    else k_expand_params<4, NG><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero);               \
+    if (bits == 8) k_expand_params<8, NG><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero, sym); \
+    else k_expand_params<4, NG><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero, sym);           \
   } while (0)
   if (ng == 2) EXP(2);
   else if (ng == 4) EXP(4);
@@ -532,7 +543,7 @@ static int dequant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, co
   double* scale;
   float* zero;
   int s = expand_params(d->bits, reinterpret_cast<const uint32_t*>(rec + g.codes_sec(np)), np * g.rows_pp, pws,
-                        g.ppc * g.rows_pp, &scale, &zero, st);
+                        g.ppc * g.rows_pp, &scale, &zero, st, d->mode);
   if (s) return s;
   return dequant_chunk_sz(d, g, np, rec, scale, zero, kv, st);
 }
@@ -817,7 +828,7 @@ extern "C" int alise_kv_upload(alise_swapper* sw, const alise_kv_desc* d, const 
       double* scale;
       float* zero;
       s = expand_params(d->bits, reinterpret_cast<const uint32_t*>(rec + g.codes_sec(g.np_of(c))),
-                        g.np_of(c) * g.rows_pp, pws, g.ppc * g.rows_pp, &scale, &zero, st);
+                        g.np_of(c) * g.rows_pp, pws, g.ppc * g.rows_pp, &scale, &zero, st, d->mode);
       if (s) break;
       TSTART(t_d);
       s = dequant_chunk_sz(d, g, g.np_of(c), rec, scale, zero, kv + c * g.ppc * g.plane_elems, st);
@@ -842,7 +853,7 @@ extern "C" int alise_kv_upload(alise_swapper* sw, const alise_kv_desc* d, const 
     double* scale;
     float* zero;
     s = expand_params(d->bits, reinterpret_cast<const uint32_t*>(sw->ring_in[slot] + g.codes_sec(np)),
-                      np * g.rows_pp, sw->pws[slot], g.ppc * g.rows_pp, &scale, &zero, st);
+                      np * g.rows_pp, sw->pws[slot], g.ppc * g.rows_pp, &scale, &zero, st, d->mode);
     if (s) return s;
     TSTART(t_d);
     s = dequant_chunk_sz(d, g, np, sw->ring_in[slot], scale, zero, kv + c * g.ppc * g.plane_elems, st);
@@ -908,7 +919,7 @@ extern "C" int alise_kv_offload_range(alise_swapper* sw, const alise_kv_desc* d,
     TSTART(t_q);
     s = launch_tile(d->bits, d->packed != 0, true, kv + c * g.ppc * g.plane_elems + t0 * d->hidden, np * rg.R,
                     d->group, ring, nullptr, nullptr, flag, st, rg.R, g.plane_elems,
-                    reinterpret_cast<uint32_t*>(ring + rg.ring_m(np)));
+                    reinterpret_cast<uint32_t*>(ring + rg.ring_m(np)), d->mode);
     TSTOP(t_q);
     if (s) return s;
     CK(cudaEventRecord(sw->out_ready[slot], st));
@@ -956,7 +967,7 @@ extern "C" int alise_kv_upload_range(alise_swapper* sw, const alise_kv_desc* d, 
     double* rs;
     float* rz;
     s = expand_params(d->bits, reinterpret_cast<const uint32_t*>(ring + rg.ring_m(np)), np * rg.R, sw->pws[slot],
-                      g.ppc * g.rows_pp, &rs, &rz, st);
+                      g.ppc * g.rows_pp, &rs, &rz, st, d->mode);
     if (s) return s;
     TSTART(t_d);
     uint16_t* dst = kv + c * g.ppc * g.plane_elems + t0 * d->hidden;

@@ -114,7 +114,7 @@ template <int BITS, bool PACK, int VPL, bool ZF32, int TP, int WPB, int MINB, in
 __global__ void __launch_bounds__(32 * WPB, MINB)
 k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
                 uint8_t* __restrict__ codes, double* __restrict__ scale, void* __restrict__ zero,
-                uint32_t* __restrict__ mmx, int* __restrict__ flag, const Segs seg) {
+                uint32_t* __restrict__ mmx, int* __restrict__ flag, const Segs seg, int sym) {
   // TP = passes of 8 rows per warp tile (TILE = 8 * TP rows; 32 keeps every lane busy
   // in the parameter solve).  A lane stages TP x VPL 16-byte vectors per tile.
   constexpr int PASSES = TP;
@@ -239,7 +239,7 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
     raise_flag(flag, bad);
     if (!own || bad) { fmn = 0.f; fmx = 0.f; }
     double s_row, z_row;
-    const TileParams tp = tile_params_f16(fmn, fmx, dq, s_row, z_row);
+    const TileParams tp = tile_params_f16(fmn, fmx, dq, s_row, z_row, sym);
     if (own) {
       if (mmx) {  // transfer slabs carry the row's fp16 (min, -max): (scale, zero) follow exactly
         mmx[my_row] = mine;
@@ -500,7 +500,7 @@ k_dequant_wide(const uint4* __restrict__ codes, const double* __restrict__ scale
 template <int BITS, bool PACK>
 __global__ void __launch_bounds__(256, 3)
 k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int64_t rows_per_plane,
-             uint8_t* __restrict__ codes, uint32_t* __restrict__ mm, int* __restrict__ flag) {
+             uint8_t* __restrict__ codes, uint32_t* __restrict__ mm, int* __restrict__ flag, int sym) {
   constexpr float QMAXF = (float)((1 << BITS) - 1);
   __shared__ __half2 s_mm[16][128];      // (min, -max) per token lane and column
   __shared__ float s_inv[128], s_zc[128], s_thr[128], s_zd[128];
@@ -555,7 +555,7 @@ k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int
     const bool bad = !(isfinite(fmn) && isfinite(fmx));
     if (bad) { atomicOr(flag, 1); fmn = 0.f; fmx = 0.f; }
     double sd, zd;
-    const TileParams tp = tile_params_f16(fmn, fmx, qdiv_make((double)((1 << BITS) - 1)), sd, zd);
+    const TileParams tp = tile_params_f16(fmn, fmx, qdiv_make((double)((1 << BITS) - 1)), sd, zd, sym);
     const int64_t r = plane * rows_per_plane + (col0 / cpr) + tid;
     mm[r] = *reinterpret_cast<const uint32_t*>(&m);  // the group's fp16 (min, -max)
     for (int u = 0; u < cpr; ++u) {
@@ -631,7 +631,7 @@ k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int
 template <int BITS, int NG>
 __global__ void __launch_bounds__(256)
 k_expand_params(const uint32_t* __restrict__ mm, int64_t groups, double* __restrict__ scale,
-                float* __restrict__ zero) {
+                float* __restrict__ zero, int sym) {
   const QDiv dq = qdiv_make((double)((1 << BITS) - 1));
   const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * NG;
   if (r0 >= groups) return;
@@ -646,9 +646,13 @@ k_expand_params(const uint32_t* __restrict__ mm, int64_t groups, double* __restr
     if (!(isfinite(fmn) && isfinite(fmx))) { fmn = 0.f; fmx = 0.f; }  // flagged at quantize time
     mn[u] = (double)fmn;
     mx[u] = (double)fmx;
-    live[u] = mx[u] != mn[u];
-    s[u] = live[u] ? qdiv(__dsub_rn(mx[u], mn[u]), dq) : 1.0;       // constant group: (1, -min)
-    z[u] = live[u] ? rint(__ddiv_rn(-mn[u], s[u])) : -mn[u];
+    live[u] = !sym && mx[u] != mn[u];
+    if (sym) {
+      solve_absmax(mn[u], mx[u], dq.b, s[u], z[u]);                   // no snap loop
+    } else {
+      s[u] = live[u] ? qdiv(__dsub_rn(mx[u], mn[u]), dq) : 1.0;       // constant group: (1, -min)
+      z[u] = live[u] ? rint(__ddiv_rn(-mn[u], s[u])) : -mn[u];
+    }
     hz[u] = __dsub_rn(dq.b, z[u]);
     lz[u] = __dsub_rn(0.0, z[u]);
   }
@@ -835,7 +839,7 @@ __global__ void k_params(int kind, int64_t rows, int nch, const double* __restri
                          const double* __restrict__ pmx_rows, const float* __restrict__ pmn_cols,
                          const float* __restrict__ pmx_cols, int64_t Hd, int64_t D, int bits,
                          bool wide, double* __restrict__ scale, void* __restrict__ zero,
-                         float4* __restrict__ fastp, uint32_t* __restrict__ mm) {
+                         float4* __restrict__ fastp, uint32_t* __restrict__ mm, int sym) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
@@ -862,7 +866,7 @@ __global__ void k_params(int kind, int64_t rows, int nch, const double* __restri
     const __half2 h = __halves2half2(__double2half(mn), __double2half(-mx));
     mm[r] = *reinterpret_cast<const uint32_t*>(&h);
   }
-  const QParams q = make_params(mn, mx, bits, wide, qdiv_make((double)((1 << bits) - 1)));
+  const QParams q = make_params(mn, mx, bits, wide, qdiv_make((double)((1 << bits) - 1)), sym);
   scale[r] = q.s;
   if (ZF32) reinterpret_cast<float*>(zero)[r] = (float)q.z;
   else reinterpret_cast<double*>(zero)[r] = q.z;

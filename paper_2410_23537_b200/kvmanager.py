@@ -147,7 +147,16 @@ def _as_2d_input(values):
     return t, code
 
 
-def quantize_tensor(values, bits: int, stream=None):
+QMODES = {"asymmetric": 0, "absmax": 1}  # ALISE_QMODE_ASYM / ALISE_QMODE_ABSMAX
+
+
+def _qmode(mode: str) -> int:
+    if mode not in QMODES:
+        raise ValueError(f"mode must be one of {sorted(QMODES)}")
+    return QMODES[mode]
+
+
+def quantize_tensor(values, bits: int, stream=None, mode: str = "asymmetric"):
     """Quantize rows on the GPU; returns (codes u8, scale f64, zero f64, flag) CUDA tensors.
 
     Asynchronous: the non-finite flag (int32[1]) must be checked after the stream
@@ -157,6 +166,7 @@ def quantize_tensor(values, bits: int, stream=None):
 
     if bits not in (4, 8):
         raise ValueError("bits must be 4 or 8")
+    qm = _qmode(mode)
     _lib.require_cuda()
     t, code = _as_2d_input(values)
     rows, row_len = t.shape
@@ -168,21 +178,24 @@ def quantize_tensor(values, bits: int, stream=None):
     nbytes = _lib.C.c_int64(0)
     _lib.call("alise_quantize_rows_workspace", rows, row_len, code, _lib.C.byref(nbytes))
     ws = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
-    _lib.call("alise_quantize_rows", _lib.ptr(t), code, rows, row_len, t.stride(0), bits,
+    _lib.call("alise_quantize_rows_ex", _lib.ptr(t), code, rows, row_len, t.stride(0), bits, qm,
               _lib.ptr(codes), _lib.ptr(scale), _lib.ptr(zero), _lib.ptr(flag), _lib.ptr(ws),
               _lib.stream_ptr(stream))
     return codes, scale, zero, flag
 
 
-def quantize(values, bits: int) -> QuantizedTensor:
+def quantize(values, bits: int, mode: str = "asymmetric") -> QuantizedTensor:
     """kvmanager.quantize (kvmanager.py:108-149) on the GPU, bit-exact.
 
     Same contract: bits in {4, 8}, a non-empty 1D/2D array (1D = one channel),
     ValueError on anything else or on non-finite input.  Returns numpy arrays.
+    mode="absmax" selects the symmetric group-wise scheme instead (scale = max|x| /
+    (2^(b-1) - 1), zero = 2^(b-1); see include/alise_b200.h ALISE_QMODE_ABSMAX) --
+    not a reference mode, so its parity is against the restated oracle only.
     """
     if bits not in (4, 8):
         raise ValueError("bits must be 4 or 8")
-    codes, scale, zero, flag = quantize_tensor(values, bits)
+    codes, scale, zero, flag = quantize_tensor(values, bits, mode=mode)
     bad = int(flag.item())  # syncs the stream
     if bad:
         raise ValueError("tensor contains non-finite values")
@@ -497,6 +510,9 @@ class KVLayout:
     head_dim; g = head_dim is per-(token, head)).  kind "channel": the reference's
     accounting channel (layer, K|V, hidden column) along tokens.  kind "head":
     (layer, K|V, head) over tokens x head_dim.  `packed` stores INT4 two per byte.
+    `mode`: "asymmetric" (the reference's min/max scale and zero) or "absmax"
+    (symmetric: scale = max|x| / (2^(b-1) - 1), zero = 2^(b-1)); the slab format is the
+    same (a group's fp16 (min, max) determines its parameters in both modes).
     """
 
     layers: int
@@ -508,12 +524,13 @@ class KVLayout:
     bits: int = 8
     packed: bool = False
     planes_per_chunk: int = 0
+    mode: str = "asymmetric"
 
     def desc(self) -> _lib.KvDesc:
         kinds = {"rows": _lib.KIND_ROWS, "channel": _lib.KIND_CHANNEL, "head": _lib.KIND_HEAD}
         return _lib.KvDesc(self.layers, self.tokens, self.hidden, self.head_dim, kinds[self.kind],
                            self.group if self.kind == "rows" else 0, self.bits, int(self.packed),
-                           self.planes_per_chunk, 0)
+                           self.planes_per_chunk, _qmode(self.mode))
 
     @property
     def elements(self) -> int:

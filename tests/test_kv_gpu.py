@@ -397,3 +397,55 @@ def test_c5_replay_delta_offload_same_ledger():
     dlt = replay.replay(rec, replica=3, max_events=900, delta=True)
     assert dlt["data_mismatches"] == 0 and dlt["data_checked"] > 50
     assert dlt["link_bytes_moved"] < full["link_bytes_moved"]
+
+
+# ----------------------------------------------------------------- absmax mode
+@pytest.mark.parametrize("bits", [4, 8])
+def test_absmax_dropin_matches_restated_oracle(km, kv_golden, bits):
+    """mode="absmax" (symmetric, north star; parity against the restated oracle --
+    the reference has no such mode): codes / scale / zero / float64 values bit-exact on
+    the C1 views and on float64 rows incl. all-zero and single-sign rows."""
+    kv = kv_golden["c1_kv"]
+    cases = [ko.view_rows(kv, kind, group=g, head_dim=32) for kind, g in C1_CASES]
+    g = np.random.default_rng(bits)
+    x = g.standard_normal((40, 96)) * 10.0 ** g.uniform(-2, 2, size=(40, 1))
+    x[5] = 0.0
+    x[6] = np.abs(x[6]) + 3.0
+    x[7] = 7.0
+    cases.append(x)
+    for v in cases:
+        qt = km.quantize(v, bits, mode="absmax")
+        c, s, z = ko.quantize_rows_absmax(v, bits)
+        assert np.array_equal(qt.values, c) and np.array_equal(qt.scale, s) and np.array_equal(qt.zero, z)
+        assert np.array_equal(km.dequantize(qt), ko.dequantize_rows(c, s, z))
+
+
+@pytest.mark.parametrize("kind,group,bits,packed", [("contig", 64, 4, True), ("contig", 128, 8, False),
+                                                    ("channel", 0, 8, False), ("head", 0, 4, True)])
+def test_absmax_swap_round_trip(km, kind, group, bits, packed):
+    """KV data plane in absmax mode: quantize+offload to pinned host, upload+dequantize;
+    every plane vs the restated oracle (codes, the (scale, zero) the slab's fp16
+    (min, max) expands to, fp16 output)."""
+    import torch
+
+    from harness import parity, synthetic
+    L, T, H = 4, 160, 1024
+    k = "rows" if kind == "contig" else kind
+    lay = km.KVLayout(L, T, H, 128, kind=k, group=group or 128, bits=bits, packed=packed, mode="absmax")
+    kv = synthetic.kv_job_torch(L, T, H, seed=3, job=1, group=group or 64)
+    g = lay.geometry()
+    pool = km.HostSlabPool(g["slab_bytes"] + 4096)
+    eng = km.KVSwapEngine()
+    try:
+        addr = pool.alloc(g["slab_bytes"])
+        eng.offload(lay, kv, addr)
+        torch.cuda.synchronize()
+        out = torch.zeros_like(kv)
+        eng.upload(lay, addr, out)
+        torch.cuda.synchronize()
+        planes, _vals, bad = parity.kv_check_planes(lay, kv.cpu().numpy(), pool.view(addr, g["slab_bytes"]),
+                                                    out.cpu().numpy())
+        assert planes == 2 * L and not bad, bad
+    finally:
+        eng.close()
+        pool.close()

@@ -95,3 +95,25 @@ def test_accounting_known_answers(kv_golden):
                 assert km.quantized_kv_bytes(m, t, b) == ko.quantized_kv_bytes(m.num_layers, m.hidden_size, t, b)
                 i += 1
     assert km.quantized_kv_bytes(km.MODEL_PRESETS["opt-13b"], 128, 8) == 52_428_800 + 3_276_800
+
+
+# ----------------------------------------------------------------- absmax (restated)
+def test_absmax_oracle_properties():
+    """The symmetric absmax restatement (parity unpinned by the reference): zero point
+    2^(b-1), scale = max|x| / (2^(b-1) - 1), codes symmetric about the zero point,
+    round-trip error <= scale / 2, all-zero rows exact."""
+    g = np.random.default_rng(9)
+    for bits in (4, 8):
+        x = g.standard_normal((50, 64)) * 10.0 ** g.uniform(-3, 3, size=(50, 1))
+        x[3] = 0.0
+        x[7] = np.abs(x[7])
+        c, s, z = ko.quantize_rows_absmax(x, bits)
+        qs = 2 ** (bits - 1) - 1
+        assert (z == 2 ** (bits - 1)).all()
+        a = np.abs(x).max(axis=1, keepdims=True)
+        assert np.array_equal(s[a > 0], (a / qs)[a > 0]) and s[3, 0] == 1.0
+        assert c.min() >= 2 ** (bits - 1) - qs and c.max() <= 2 ** (bits - 1) + qs
+        y = ko.dequantize_rows(c, s, z)
+        assert (np.abs(y - x) <= s / 2 * (1 + 1e-12)).all()
+        assert (y[3] == 0).all()
+        assert np.array_equal(ko.quantize_rows_absmax(-x, bits)[0].astype(int), 2 ** bits - c.astype(int))
