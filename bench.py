@@ -242,23 +242,34 @@ def cpu_kv_sample(args, planes: int):
 
 
 # ----------------------------------------------------------------- link peaks
-def link_peaks(dev_index: int):
+def link_peaks(dev_index: int, world: int = 1):
+    """Pinned-copy peaks of the host link, measured on every rank AT THE SAME TIME
+    (barrier before each shape, max-over-ranks time): at N > 1 the GPUs share the host's
+    PCIe switches, root ports and DRAM, so the aggregate, not N x the single-GPU peak, is
+    the N-GPU roofline.  Host buffers are NUMA-local pinned slabs
+    (alise_host_alloc_numa), as the swap path uses."""
+    import numpy as np
     import torch
+
+    from paper_2410_23537_b200 import kvmanager as km
     n = 1 << 30
     d = torch.empty(n, dtype=torch.uint8, device="cuda")
     d2 = torch.empty(n, dtype=torch.uint8, device="cuda")
-    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-    h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    pool = km.HostSlabPool(2 * n + 512)
+    a0, a1 = pool.alloc(n), pool.alloc(n)
+    h = torch.from_numpy(np.asarray(pool.view(a0, n)))
+    h2 = torch.from_numpy(np.asarray(pool.view(a1, n)))
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 
     def timed(fn, reps=3):
         fn()
         torch.cuda.synchronize()
+        barrier(world)
         t = time.perf_counter()
         for _ in range(reps):
             fn()
         torch.cuda.synchronize()
-        return (time.perf_counter() - t) / reps
+        return max_over_ranks((time.perf_counter() - t) / reps, world)
 
     # best of three trials each: the pinned-copy peak is noisy on a shared host
     d2h = max(n / timed(lambda: h.copy_(d, non_blocking=True)) / 1e9 for _ in range(3))
@@ -271,7 +282,7 @@ def link_peaks(dev_index: int):
             d2.copy_(h2, non_blocking=True)
 
     def both_chunked(parts=8):
-        # the swap path's shape: many 128 MiB chunks in flight per direction
+        # the swap path's shape: many chunks in flight per direction
         c = n // parts
         for i in range(parts):
             with torch.cuda.stream(s1):
@@ -281,11 +292,17 @@ def link_peaks(dev_index: int):
     # best of several trials of both shapes (a peak probe should not under-read)
     duplex = max([2 * n / timed(both) / 1e9 for _ in range(4)] +
                  [2 * n / timed(both_chunked) / 1e9 for _ in range(4)])
+    numa = pool.numa_bound
     del d, d2, h, h2
-    return {"d2h_GBs": d2h, "h2d_GBs": h2d, "duplex_total_GBs": duplex}
+    pool.close()
+    out = {"d2h_GBs": d2h, "h2d_GBs": h2d, "duplex_total_GBs": duplex, "numa_local_slabs": numa,
+           "concurrent_ranks": world}
+    if world > 1:   # every rank moved the same bytes in the max-over-ranks time
+        out.update({"aggregate_duplex_GBs": duplex * world, "aggregate_d2h_GBs": d2h * world,
+                    "aggregate_h2d_GBs": h2d * world})
+    return out
 
 
-# ----------------------------------------------------------------- KV bench
 def kv_bench(args, world, rank, local, layouts=None, e2e=True):
     """Swap pipeline over a job list (one KVLayout per job); jobs LPT-assigned to ranks.
 
@@ -697,7 +714,7 @@ def main():
     torch.cuda.set_device(local)
     hbm_peak, bf16_peak, peak_src = load_peaks()
     traffic = load_traffic()
-    links = link_peaks(local)
+    links = link_peaks(local, world)
     kv = kv_bench(args, world, rank, local)
     kv3 = None
     if not args.no_c3:
@@ -806,7 +823,8 @@ def main():
                                  round(d_ach, 1) if d_ach else None, "peak": hbm_peak,
                                  "frac": round(d_ach / hbm_peak, 4) if d_ach else None,
                                  "avg_launch_ms": d_avg_ms},
-            "roofline_link": {"bound": "host link (PCIe Gen5 x16, both directions)",
+            "roofline_link": {"bound": "host link (PCIe Gen5 x16, both directions; at N > 1 the peak is "
+                                       "the per-GPU share of the duplex rate all ranks reach concurrently)",
                               "achieved": round(kv["link_GBs_total"] / world, 2),
                               "peak": round(link_peak, 2), "unit": "GB/s per GPU",
                               "frac": round(kv["link_GBs_total"] / world / link_peak, 4),

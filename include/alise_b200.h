@@ -182,6 +182,16 @@ int alise_swapper_kernel_stats(alise_swapper *sw, double *quant_ms, int64_t *n_q
 
 /* Pinned host memory and events (thin wrappers so non-torch hosts can drive the ABI). */
 int alise_host_alloc(int64_t bytes, void **out);
+/* NUMA-local pinned host memory for a GPU's slabs (each rank swaps over its
+ * own host link into memory on the GPU's socket): anonymous pages with a preferred-node
+ * policy (mbind), then page-locked + device-mapped (cudaHostRegister).  numa_node >= 0,
+ * or ALISE_NUMA_CURRENT_GPU for the current device's node (sysfs).  *bound (may be NULL)
+ * = 1 if the node policy was applied (0 on single-node hosts or where mbind is not
+ * permitted: plain pinned pages).  Free with alise_host_free. */
+#define ALISE_NUMA_CURRENT_GPU (-2)
+int alise_host_alloc_numa(int64_t bytes, int numa_node, void **out, int *bound);
+/* NUMA node of a GPU's PCI device (-1 if unknown / single node). */
+int alise_gpu_numa_node(int device, int *node);
 int alise_host_free(void *p);
 int alise_event_create(void **ev);
 int alise_event_destroy(void *ev);

@@ -53,6 +53,8 @@ _SIGS = {
     "alise_swapper_timing": [vp, i32],
     "alise_swapper_kernel_stats": [vp, vp, vp, vp, vp],
     "alise_host_alloc": [i64, vp],
+    "alise_host_alloc_numa": [i64, i32, vp, vp],
+    "alise_gpu_numa_node": [i32, vp],
     "alise_host_free": [vp],
     "alise_event_create": [vp],
     "alise_event_destroy": [vp],

@@ -3,12 +3,19 @@
 // Declarations and reference citations: include/alise_b200.h.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <ctype.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -993,7 +1000,76 @@ extern "C" int alise_host_alloc(int64_t bytes, void** out) {
   CK(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable | cudaHostAllocMapped));
   return ALISE_OK;
 }
+
+// NUMA-local pinned slabs: anonymous pages with a preferred-node memory policy
+// (mbind(2), no libnuma), then page-locked and mapped for the GPU with
+// cudaHostRegister, which faults every page in under that policy.
+namespace {
+std::mutex g_numa_mu;
+std::map<void*, size_t> g_numa_allocs;  // registered region -> mapped length
+}
+
+extern "C" int alise_gpu_numa_node(int device, int* node) {
+  char bus[32] = {0};
+  CK(cudaDeviceGetPCIBusId(bus, sizeof bus, device));
+  for (char* c = bus; *c; ++c) *c = (char)tolower(*c);
+  char path[128];
+  snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/numa_node", bus);
+  *node = -1;
+  if (FILE* f = fopen(path, "r")) {
+    if (fscanf(f, "%d", node) != 1) *node = -1;
+    fclose(f);
+  }
+  return ALISE_OK;
+}
+
+extern "C" int alise_host_alloc_numa(int64_t bytes, int numa_node, void** out, int* bound) {
+  if (bytes <= 0) return fail(ALISE_EINVAL, "bytes must be positive");
+  if (numa_node == ALISE_NUMA_CURRENT_GPU) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    int s = alise_gpu_numa_node(dev, &numa_node);
+    if (s) return s;
+  }
+  const size_t len = ((size_t)bytes + 4095) & ~(size_t)4095;
+  void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (p == MAP_FAILED) return fail(ALISE_ECAPACITY, "mmap of %zu bytes failed", len);
+  int ok = 0;
+  if (numa_node >= 0 && numa_node < 1024) {
+    unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {0};
+    mask[numa_node / (8 * sizeof(unsigned long))] |= 1ul << (numa_node % (8 * sizeof(unsigned long)));
+    const long MPOL_PREFERRED_ = 1;
+    ok = syscall(SYS_mbind, p, len, MPOL_PREFERRED_, mask, 1024ul, 0u) == 0;
+  }
+  const cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterPortable | cudaHostRegisterMapped);
+  if (e != cudaSuccess) {
+    munmap(p, len);
+    return fail(ALISE_ECUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_numa_mu);
+    g_numa_allocs[p] = len;
+  }
+  *out = p;
+  if (bound) *bound = ok;
+  return ALISE_OK;
+}
+
 extern "C" int alise_host_free(void* p) {
+  size_t len = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_numa_mu);
+    auto it = g_numa_allocs.find(p);
+    if (it != g_numa_allocs.end()) {
+      len = it->second;
+      g_numa_allocs.erase(it);
+    }
+  }
+  if (len) {  // alise_host_alloc_numa region
+    CK(cudaHostUnregister(p));
+    munmap(p, len);
+    return ALISE_OK;
+  }
   CK(cudaFreeHost(p));
   return ALISE_OK;
 }

@@ -548,13 +548,27 @@ class KVLayout:
         return cls(model.num_layers, tokens, model.hidden_size, model.head_dim, **kw)
 
 
-class HostSlabPool:
-    """First-fit allocator over one pinned, device-mapped host arena (256-B aligned)."""
+NUMA_CURRENT_GPU = -2  # ALISE_NUMA_CURRENT_GPU
 
-    def __init__(self, nbytes: int):
+
+class HostSlabPool:
+    """First-fit allocator over one pinned, device-mapped host arena (256-B aligned).
+
+    numa_node: the arena's NUMA node -- NUMA_CURRENT_GPU (default: the current GPU's
+    socket, so each rank swaps into memory local to its own host link), a node number,
+    or None for plain cudaHostAlloc pages.  ``numa_bound`` records whether the node
+    policy was applied (not on single-node hosts or where mbind is not permitted)."""
+
+    def __init__(self, nbytes: int, numa_node: int | None = NUMA_CURRENT_GPU):
         self.capacity = int(nbytes)
         p = _lib.C.c_void_p()
-        _lib.call("alise_host_alloc", self.capacity, _lib.C.byref(p))
+        self.numa_bound = False
+        if numa_node is None:
+            _lib.call("alise_host_alloc", self.capacity, _lib.C.byref(p))
+        else:
+            b = _lib.C.c_int(0)
+            _lib.call("alise_host_alloc_numa", self.capacity, int(numa_node), _lib.C.byref(p), _lib.C.byref(b))
+            self.numa_bound = bool(b.value)
         self.base = p.value
         self._free = [(0, self.capacity)]   # sorted (offset, size)
         self._live = {}
