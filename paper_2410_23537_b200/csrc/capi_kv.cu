@@ -439,8 +439,62 @@ extern "C" int alise_kv_layout(const alise_kv_desc* d, int64_t* slab_bytes, int6
   return ALISE_OK;
 }
 
+static bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && *e && strcmp(e, "0") != 0;
+}
+
+template <int BITS, bool PACK, int CW>
+static int launch_cols_cp(int64_t np, int tt, const uint16_t* kv, const alise_kv_desc* d, int cpr, int64_t rows_pp,
+                          uint8_t* codes, uint32_t* mm, int* flag, cudaStream_t st) {
+  auto kern = k_quant_cols_cp<BITS, PACK, CW>;
+  const int smem = 2 * tt * 2 * CW;
+  static int set = 0, per_sm = 0;
+  if (smem > set) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * CW, smem));
+    set = smem;
+  }
+  const int64_t strips = (d->hidden / CW) * np;
+  const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(strips, (int64_t)sm_count() * std::max(1, per_sm) / kColsCL));
+  dim3 grid((unsigned)clusters, kColsCL, 1);
+  kern<<<grid, 2 * CW, smem, st>>>(kv, d->tokens, d->hidden, cpr, rows_pp, tt, strips, codes, mm, flag, d->mode);
+  CKL();
+  return ALISE_OK;
+}
+
+template <int BITS, bool PACK, int CW>
+static int launch_cols_cl(dim3 grid, int smem, const uint16_t* kv, const alise_kv_desc* d, int cpr, int64_t rows_pp,
+                          int tt, uint8_t* codes, uint32_t* mm, int* flag, cudaStream_t st) {
+  auto kern = k_quant_cols_cl<BITS, PACK, CW>;
+  static int set = 0;
+  if (smem > set) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    set = smem;
+  }
+  kern<<<grid, 2 * CW, smem, st>>>(kv, d->tokens, d->hidden, cpr, rows_pp, tt, codes, mm, flag, d->mode);
+  CKL();
+  return ALISE_OK;
+}
+
+// Quantize path of the column kinds: the strip width of the single-pass cluster kernel
+// (64 or 128 columns), 1 for the two-pass k_quant_cols, 0 for the generic three-phase
+// path (the only one that needs a workspace).
+static int cols_path(const alise_kv_desc* d) {
+  const int64_t cpr = d->kind == ALISE_KIND_CHANNEL ? 1 : d->head_dim;
+  const int64_t tt = (d->tokens + kColsCL - 1) / kColsCL;
+  static int narrow = -1;  // ALISE_COLS_CW=32: 64 B token rows (tuning experiment)
+  if (narrow < 0) narrow = getenv("ALISE_COLS_CW") && atoi(getenv("ALISE_COLS_CW")) == 32;
+  const int cw = narrow && cpr <= 32 && 32 % cpr == 0 ? 32
+                 : (cpr <= 64 && 64 % cpr == 0 ? 64 : 128);  // 128 B token rows unless a head is wider
+  if (d->hidden % cw == 0 && cw % cpr == 0 && tt * 2 * cw <= (200 << 10) && !getenv_flag("ALISE_COLS_TWOPASS"))
+    return cw;
+  if (d->hidden % 128 == 0 && cpr <= 128 && 128 % cpr == 0) return 1;
+  return 0;
+}
+
 static int64_t cols_workspace(const alise_kv_desc* d, const KvGeom& g, int* nch_out, int64_t* tchunk_out) {
-  if (d->kind == ALISE_KIND_ROWS) return 0;
+  if (d->kind == ALISE_KIND_ROWS || cols_path(d) != 0) return 0;
   // enough (plane, token-chunk, column-block) blocks for ~4 waves
   const int64_t colblocks = (d->hidden / 8 + 127) / 128;
   int64_t nch = std::max<int64_t>(1, (4 * sm_count() + colblocks * g.ppc - 1) / (colblocks * g.ppc));
@@ -462,6 +516,32 @@ static int quant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, cons
     return launch_tile(d->bits, d->packed != 0, true, kv, rows, d->group, codes, nullptr, nullptr, flag, st,
                        0, 0, mm, d->mode);
   const int cpr = d->kind == ALISE_KIND_CHANNEL ? 1 : (int)d->head_dim;
+  const int64_t tt = (d->tokens + kColsCL - 1) / kColsCL;
+  const int cw = cols_path(d);
+  if (cw > 1 && np <= 65535) {
+    // one HBM pass: a cluster of kColsCL CTAs per (plane, cw-column strip)
+    dim3 grid((unsigned)(d->hidden / cw), kColsCL, (unsigned)np);
+    const int smem = (int)(tt * 2 * cw);
+    static int persist = -1;  // ALISE_COLS_PERSIST=1: persistent double-buffered clusters (tuning)
+    if (persist < 0) persist = getenv_flag("ALISE_COLS_PERSIST");
+#define QCL(B, P, W)                                                                                          \
+  return persist ? launch_cols_cp<B, P, W>(np, (int)tt, kv, d, cpr, g.rows_pp, codes, mm, flag, st)          \
+                 : launch_cols_cl<B, P, W>(grid, smem, kv, d, cpr, g.rows_pp, (int)tt, codes, mm, flag, st)
+    if (cw == 32) {
+      if (d->bits == 8) QCL(8, false, 32);
+      if (d->packed) QCL(4, true, 32);
+      QCL(4, false, 32);
+    }
+    if (cw == 64) {
+      if (d->bits == 8) QCL(8, false, 64);
+      if (d->packed) QCL(4, true, 64);
+      QCL(4, false, 64);
+    }
+    if (d->bits == 8) QCL(8, false, 128);
+    if (d->packed) QCL(4, true, 128);
+    QCL(4, false, 128);
+#undef QCL
+  }
   if (d->hidden % 128 == 0 && cpr <= 128 && 128 % cpr == 0) {
     dim3 grid((unsigned)(d->hidden / 128), (unsigned)np);
     if (d->bits == 8) k_quant_cols<8, false><<<grid, 256, 0, st>>>(kv, d->tokens, d->hidden, cpr, g.rows_pp, codes, mm, flag, d->mode);
@@ -507,21 +587,9 @@ static int expand_params(int bits, const uint32_t* mm, int64_t groups, void* pws
   *scale = reinterpret_cast<double*>(w);
   *zero = reinterpret_cast<float*>(w + align256(cap_groups * 8));
   if (groups <= 0) return ALISE_OK;
-  static int ng = -1;  // groups per thread (interleaved float64 chains); ALISE_EXPAND_NG (tuning)
-  if (ng < 0) {
-    const char* e = getenv("ALISE_EXPAND_NG");
-    ng = e ? atoi(e) : 1;
-  }
-#define EXP(NG)                                                                                  \
-  do {                                                                                           \
-    const unsigned grid = (unsigned)((groups + 256 * NG - 1) / (256 * NG));                      \
-    if (bits == 8) k_expand_params<8, NG><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero, sym); \
-    else k_expand_params<4, NG><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero, sym);           \
-  } while (0)
-  if (ng == 2) EXP(2);
-  else if (ng == 4) EXP(4);
-  else EXP(1);
-#undef EXP
+  const unsigned grid = (unsigned)((groups + 255) / 256);
+  if (bits == 8) k_expand_params<8><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero, sym);
+  else k_expand_params<4><<<grid, 256, 0, st>>>(mm, groups, *scale, *zero, sym);
   CKL();
   return ALISE_OK;
 }
@@ -555,6 +623,23 @@ static int dequant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, co
   return dequant_chunk_sz(d, g, np, rec, scale, zero, kv, st);
 }
 
+// Stream-ordered workspace of the one-shot quantize / dequantize calls.  The device's
+// default memory pool keeps freed blocks reserved (release threshold = max) so a call
+// after a synchronize does not re-map its workspace (100+ MB for a 1 GiB job: ~1 ms).
+static int ws_alloc(void** p, int64_t bytes, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+  CK(cudaMallocAsync(p, bytes, st));
+  return ALISE_OK;
+}
+
 extern "C" int alise_kv_quantize(const alise_kv_desc* d, const uint16_t* kv, uint8_t* slab,
                                  int* flag, void* stream) {
   KvGeom g{};
@@ -565,7 +650,10 @@ extern "C" int alise_kv_quantize(const alise_kv_desc* d, const uint16_t* kv, uin
   int64_t tchunk;
   const int64_t wsb = cols_workspace(d, g, &nch, &tchunk);
   void* ws = nullptr;
-  if (wsb) CK(cudaMallocAsync(&ws, wsb, st));
+  if (wsb) {
+    s = ws_alloc(&ws, wsb, st);
+    if (s) return s;
+  }
   for (int64_t c = 0; c < g.n_chunks; ++c) {
     s = quant_chunk(d, g, g.np_of(c), kv + c * g.ppc * g.plane_elems, slab + c * g.rec_bytes, flag, ws, st);
     if (s) break;
@@ -581,7 +669,8 @@ extern "C" int alise_kv_dequantize(const alise_kv_desc* d, const uint8_t* slab, 
   if (s) return s;
   cudaStream_t st = S(stream);
   void* pws = nullptr;
-  CK(cudaMallocAsync(&pws, g.pws_bytes(), st));
+  s = ws_alloc(&pws, g.pws_bytes(), st);
+  if (s) return s;
   for (int64_t c = 0; c < g.n_chunks && !s; ++c)
     s = dequant_chunk(d, g, g.np_of(c), slab + c * g.rec_bytes, kv + c * g.ppc * g.plane_elems, pws, st);
   CK(cudaFreeAsync(pws, st));
@@ -829,7 +918,8 @@ extern "C" int alise_kv_upload(alise_swapper* sw, const alise_kv_desc* d, const 
     s = host_dev_ptr(host_slab, &dptr);
     if (s) return s;
     void* pws = nullptr;  // stream-ordered scratch: concurrent zero-copy uploads never share it
-    CK(cudaMallocAsync(&pws, g.pws_bytes(), st));
+    s = ws_alloc(&pws, g.pws_bytes(), st);
+    if (s) return s;
     for (int64_t c = 0; c < g.n_chunks && !s; ++c) {
       const uint8_t* rec = reinterpret_cast<const uint8_t*>(dptr) + c * g.rec_bytes;
       double* scale;
@@ -1002,8 +1092,10 @@ extern "C" int alise_host_alloc(int64_t bytes, void** out) {
 }
 
 // NUMA-local pinned slabs: anonymous pages with a preferred-node memory policy
-// (mbind(2), no libnuma), then page-locked and mapped for the GPU with
-// cudaHostRegister, which faults every page in under that policy.
+// (mbind(2), no libnuma) and transparent huge pages, then page-locked and mapped for
+// the GPU with cudaHostRegister, which faults every page in under that policy.  Where
+// the GPU's node is unknown or mbind is refused the slab is plain cudaHostAlloc memory
+// (registered 4 KB anonymous pages measured ~7% below it on the host link).
 namespace {
 std::mutex g_numa_mu;
 std::map<void*, size_t> g_numa_allocs;  // registered region -> mapped length
@@ -1031,16 +1123,26 @@ extern "C" int alise_host_alloc_numa(int64_t bytes, int numa_node, void** out, i
     int s = alise_gpu_numa_node(dev, &numa_node);
     if (s) return s;
   }
-  const size_t len = ((size_t)bytes + 4095) & ~(size_t)4095;
+  if (bound) *bound = 0;
+  // single-node hosts (no node1) and unknown nodes: nothing to place
+  const bool force = getenv_flag("ALISE_HOST_MMAP");  // A/B measurements of the two page kinds
+  if (!force && (numa_node < 0 || numa_node >= 1024 || access("/sys/devices/system/node/node1", F_OK) != 0))
+    return alise_host_alloc(bytes, out);
+  const size_t huge = 2u << 20;
+  const size_t len = ((size_t)bytes + huge - 1) & ~(huge - 1);
   void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
   if (p == MAP_FAILED) return fail(ALISE_ECAPACITY, "mmap of %zu bytes failed", len);
-  int ok = 0;
-  if (numa_node >= 0 && numa_node < 1024) {
-    unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {0};
+  unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {0};
+  if (numa_node >= 0 && numa_node < 1024)
     mask[numa_node / (8 * sizeof(unsigned long))] |= 1ul << (numa_node % (8 * sizeof(unsigned long)));
-    const long MPOL_PREFERRED_ = 1;
-    ok = syscall(SYS_mbind, p, len, MPOL_PREFERRED_, mask, 1024ul, 0u) == 0;
+  const long MPOL_PREFERRED_ = 1;
+  const int ok = numa_node >= 0 && numa_node < 1024 &&
+                 syscall(SYS_mbind, p, len, MPOL_PREFERRED_, mask, 1024ul, 0u) == 0;
+  if (!ok && !force) {
+    munmap(p, len);
+    return alise_host_alloc(bytes, out);
   }
+  madvise(p, len, MADV_HUGEPAGE);
   const cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterPortable | cudaHostRegisterMapped);
   if (e != cudaSuccess) {
     munmap(p, len);

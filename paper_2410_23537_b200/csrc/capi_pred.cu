@@ -408,6 +408,8 @@ static BlasRef blas_ref(const alise_db* db) {
   return b;
 }
 
+static int grp_len_host(int n_tiles, int G, int g) { return n_tiles / G + (g < n_tiles % G ? 1 : 0); }
+
 template <typename T>
 static int topk_rescore_t(alise_db* db, const T* queries, int64_t B, int k, const float* ext, double* out_sim,
                           int64_t* out_seq, int32_t* out_len, int32_t* out_count, cudaStream_t st) {
@@ -418,7 +420,9 @@ static int topk_rescore_t(alise_db* db, const T* queries, int64_t B, int k, cons
   CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
   // small batches are latency bound (one DRAM round trip per candidate row), large ones
   // throughput bound (registers / occupancy)
-  auto rescore = B <= 512 ? k_rescore<24, T> : k_rescore<8, T>;
+  static int ru = -1;  // ALISE_RESCORE_U: elements per lane in flight for large batches (tuning)
+  if (ru < 0) ru = getenv("ALISE_RESCORE_U") ? atoi(getenv("ALISE_RESCORE_U")) : 8;
+  auto rescore = B <= 512 ? k_rescore<24, T> : (ru == 12 ? k_rescore<12, T> : k_rescore<8, T>);
   static int rthreads = -1;
   if (rthreads < 0) {
     const char* e = getenv("ALISE_RESCORE_THREADS");
@@ -426,12 +430,14 @@ static int topk_rescore_t(alise_db* db, const T* queries, int64_t B, int k, cons
   }
   // large batches: smaller blocks keep more queries in flight per SM
   const BlasRef br = blas_ref(db);
-  rescore<<<(unsigned)B, B <= 512 ? 256 : rthreads, 0, st>>>(qblk, nh, a, (int)Bp, B, k, db->size, db->dim, queries,
-                                                             vm, db->lens, db->seqs, db->two_delta, db->cand_s,
-                                                             db->cand_r, db->cand_n, db->topc, ext, out_sim, out_seq,
-                                                             out_len, out_count, db->need, db->inexact, br);
+  // the longest top-list union a query can have: nh x (largest split count) x k
+  const int max_splits = std::max(a.G, a.E > 0 ? a.G - 1 + (grp_len_host(a.n_tiles, a.G, a.G - 1) + a.C - 1) / a.C : 0);
+  const int top_cap = (int)std::min<int64_t>(4096, (int64_t)nh * max_splits * k);
+  rescore<<<(unsigned)B, B <= 512 ? 256 : rthreads, top_cap * sizeof(float), st>>>(
+      qblk, nh, a, (int)Bp, B, k, db->size, db->dim, queries, vm, db->lens, db->seqs, db->two_delta, db->cand_s,
+      db->cand_r, db->cand_n, db->topc, ext, out_sim, out_seq, out_len, out_count, db->need, db->inexact, br, top_cap);
   CKL();
-  k_exhaustive<T><<<(unsigned)B, 256, 0, st>>>(B, k, db->size, db->dim, queries, vm, db->lens, db->seqs, db->need,
+  k_exhaustive<T><<<(unsigned)((B + 255) / 256), 256, 0, st>>>(B, k, db->size, db->dim, queries, vm, db->lens, db->seqs, db->need,
                                                out_sim, out_seq, out_len, out_count, db->inexact, br);
   CKL();
   return ALISE_OK;

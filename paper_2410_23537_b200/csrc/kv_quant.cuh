@@ -195,45 +195,50 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
     __syncwarp();
     const uint8_t* b = wbuf + slot * (TILE * ROWB);
     const int64_t row0 = tile * TILE;
-    // full tiles (every row live, every lane's vectors in range) skip all range checks
+    // full tiles (every row live, every lane's vectors in range) skip all range checks:
+    // phases A and C are instantiated twice (FULL: no predicates, compile-time offsets)
     const bool full = wide_rows && (row0 + TILE <= rows);
     // ---------------- A: per-row min / max from shared memory (zero-filled vectors
     // of a partial tile are skipped)
-    uint32_t mine = 0;
+    auto phase_a = [&](auto full_c) -> uint32_t {
+      constexpr bool FULL = decltype(full_c)::value;
+      uint32_t mine = 0;
 #pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      const int rl = p * 8 + sub;
-      const int64_t r = row0 + rl;
-      __half2 lo2 = __half2half2(__ushort_as_half(0x7c00)), hi2 = __half2half2(__ushort_as_half(0xfc00));
+      for (int p = 0; p < PASSES; ++p) {
+        const int rl = p * 8 + sub;
+        __half2 lo2 = __half2half2(__ushort_as_half(0x7c00)), hi2 = __half2half2(__ushort_as_half(0xfc00));
 #pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        if (full || (r < rows && q4 + 4 * i < nvec)) {
-          const uint4 d = *reinterpret_cast<const uint4*>(b + rl * ROWB + (q4 + 4 * i) * 16);
-          const __half2* h = reinterpret_cast<const __half2*>(&d);
+        for (int i = 0; i < VPL; ++i) {
+          if (FULL || (row0 + rl < rows && q4 + 4 * i < nvec)) {
+            const uint4 d = *reinterpret_cast<const uint4*>(b + rl * ROWB + (q4 + 4 * i) * 16);
+            const __half2* h = reinterpret_cast<const __half2*>(&d);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            lo2 = __hmin2_nan(lo2, h[k]);
-            hi2 = __hmax2_nan(hi2, h[k]);
+            for (int k = 0; k < 4; ++k) {
+              lo2 = __hmin2_nan(lo2, h[k]);
+              hi2 = __hmax2_nan(hi2, h[k]);
+            }
           }
         }
-      }
-      const __half mn = __hmin_nan(__low2half(lo2), __high2half(lo2));
-      const __half mx = __hmax_nan(__low2half(hi2), __high2half(hi2));
-      __half2 pk = __halves2half2(mn, __hneg(mx));
-      uint32_t u = *reinterpret_cast<uint32_t*>(&pk);
+        const __half mn = __hmin_nan(__low2half(lo2), __high2half(lo2));
+        const __half mx = __hmax_nan(__low2half(hi2), __high2half(hi2));
+        __half2 pk = __halves2half2(mn, __hneg(mx));
+        uint32_t u = *reinterpret_cast<uint32_t*>(&pk);
 #pragma unroll
-      for (int o = 1; o < 4; o <<= 1) {
-        uint32_t w = __shfl_xor_sync(0xffffffffu, u, o);
-        __half2 c = __hmin2_nan(*reinterpret_cast<__half2*>(&u), *reinterpret_cast<__half2*>(&w));
-        u = *reinterpret_cast<uint32_t*>(&c);
+        for (int o = 1; o < 4; o <<= 1) {
+          uint32_t w = __shfl_xor_sync(0xffffffffu, u, o);
+          __half2 c = __hmin2_nan(*reinterpret_cast<__half2*>(&u), *reinterpret_cast<__half2*>(&w));
+          u = *reinterpret_cast<uint32_t*>(&c);
+        }
+        const uint32_t g = __shfl_sync(0xffffffffu, u, (lane & 7) << 2);
+        if ((lane >> 3) == p) mine = g;
       }
-      const uint32_t g = __shfl_sync(0xffffffffu, u, (lane & 7) << 2);
-      if ((lane >> 3) == p) mine = g;
-    }
+      return mine;
+    };
+    const uint32_t mine = full ? phase_a(std::true_type{}) : phase_a(std::false_type{});
     // ---------------- B: lane-per-row parameters (lanes < TILE)
     const int64_t my_row = row0 + lane;
     const bool own = lane < TILE && my_row < rows;
-    const __half2 mm = *reinterpret_cast<__half2*>(&mine);
+    const __half2 mm = *reinterpret_cast<const __half2*>(&mine);
     float fmn = __low2float(mm), fmx = -__high2float(mm);
     const bool bad = own && !(isfinite(fmn) && isfinite(fmx));
     raise_flag(flag, bad);
@@ -253,45 +258,53 @@ k_quant_tile(const uint16_t* __restrict__ x, int64_t rows, int row_len,
     // full tiles (every row live, every lane's vectors in range) take an unpredicated
     // path with compile-time offsets; the code is the low byte / nibble of
     // y = fma(x, inv_s, z + 1.5*2^23), e = fma(x, inv_s, K - y) proves it (qmath.cuh)
-    uint32_t pmask = 0;  // flagged passes of this lane: bit p
+    auto phase_c = [&](auto full_c) -> uint32_t {
+      constexpr bool FULL = decltype(full_c)::value;
+      uint32_t pm = 0;  // flagged passes of this lane: bit p
+      // full tiles: one base pointer per tile, compile-time offsets per pass / vector
+      uint8_t* cfull = codes + ((uint64_t)((row0 + sub) * (int64_t)RL + q4 * 8) >> (PACK ? 1 : 0));
 #pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      const int rl = p * 8 + sub;
-      const float inv_s = __shfl_sync(0xffffffffu, tp.inv_s, rl);
-      const float zc = __shfl_sync(0xffffffffu, tp.zc, rl);
-      const float thr = __shfl_sync(0xffffffffu, tp.thr, rl);
-      const int64_t r = row0 + rl;
-      const bool live_row = r < rows;
-      const float2 inv2 = make_float2(inv_s, inv_s), zc2 = make_float2(zc, zc);
-      const float2 nzc2 = make_float2(-zc, -zc);
-      const uint8_t* srow = b + rl * ROWB + q4 * 16;
-      uint8_t* crow = codes + ((uint64_t)(r * (full ? (int64_t)RL : (int64_t)row_len) + q4 * 8) >> (PACK ? 1 : 0));
-      float dmax = 0.f;  // largest |e| of this lane's values in the pass
+      for (int p = 0; p < PASSES; ++p) {
+        const int rl = p * 8 + sub;
+        const float inv_s = __shfl_sync(0xffffffffu, tp.inv_s, rl);
+        const float zc = __shfl_sync(0xffffffffu, tp.zc, rl);
+        const float thr = __shfl_sync(0xffffffffu, tp.thr, rl);
+        const int64_t r = row0 + rl;
+        const bool live_row = r < rows;
+        const float2 inv2 = make_float2(inv_s, inv_s), zc2 = make_float2(zc, zc);
+        const float2 nzc2 = make_float2(-zc, -zc);
+        const uint8_t* srow = b + rl * ROWB + q4 * 16;
+        uint8_t* crow = FULL ? cfull + ((p * 8 * RL) >> (PACK ? 1 : 0))
+                             : codes + ((uint64_t)(r * (int64_t)row_len + q4 * 8) >> (PACK ? 1 : 0));
+        float dmax = 0.f;  // largest |e| of this lane's values in the pass
 #pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        if (!full && !(live_row && q4 + 4 * i < nvec)) continue;
-        const uint4 d = *reinterpret_cast<const uint4*>(srow + i * 64);
-        const __half2* h = reinterpret_cast<const __half2*>(&d);
-        uint32_t c[8];
+        for (int i = 0; i < VPL; ++i) {
+          if (!FULL && !(live_row && q4 + 4 * i < nvec)) continue;
+          const uint4 d = *reinterpret_cast<const uint4*>(srow + i * 64);
+          const __half2* h = reinterpret_cast<const __half2*>(&d);
+          uint32_t c[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 f = __half22float2(h[k]);
-          const float2 y = __ffma2_rn(f, inv2, zc2);                    // 1.5*2^23 + code
-          const float2 cc = __fadd2_rn(y, nzc2);                        // code - z, exact
-          const float2 e = __ffma2_rn(f, inv2, make_float2(-cc.x, -cc.y));  // RN(t32 - code)
-          dmax = fmaxf(dmax, fmaxf(fabsf(e.x), fabsf(e.y)));
-          c[2 * k] = f2bits(y.x);
-          c[2 * k + 1] = f2bits(y.y);
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __half22float2(h[k]);
+            const float2 y = __ffma2_rn(f, inv2, zc2);                    // 1.5*2^23 + code
+            const float2 cc = __fadd2_rn(y, nzc2);                        // code - z, exact
+            const float2 e = __ffma2_rn(f, inv2, make_float2(-cc.x, -cc.y));  // RN(t32 - code)
+            dmax = fmaxf(dmax, fmaxf(fabsf(e.x), fabsf(e.y)));
+            c[2 * k] = f2bits(y.x);
+            c[2 * k + 1] = f2bits(y.y);
+          }
+          if (PACK) {
+            __stcs(reinterpret_cast<uint32_t*>(crow + i * 16), pack_int4x8(c));
+          } else {
+            __stcs(reinterpret_cast<uint2*>(crow + i * 32),
+                   make_uint2(gather4(c[0], c[1], c[2], c[3]), gather4(c[4], c[5], c[6], c[7])));
+          }
         }
-        if (PACK) {
-          __stcs(reinterpret_cast<uint32_t*>(crow + i * 16), pack_int4x8(c));
-        } else {
-          __stcs(reinterpret_cast<uint2*>(crow + i * 32),
-                 make_uint2(gather4(c[0], c[1], c[2], c[3]), gather4(c[4], c[5], c[6], c[7])));
-        }
+        pm |= (dmax >= thr ? 1u : 0u) << p;  // a value of the pass is near a rounding boundary
       }
-      pmask |= (dmax >= thr ? 1u : 0u) << p;  // a value of the pass is near a rounding boundary
-    }
+      return pm;
+    };
+    const uint32_t pmask = full ? phase_c(std::true_type{}) : phase_c(std::false_type{});
     // ---------------- D: rare fix-up of flagged (lane, pass) pairs (a value near a
     // rounding boundary), all lanes together: the pair's 8*VPL values are spread one code
     // byte per lane (INT8: one value; packed INT4: values 2j, 2j+1); each lane re-checks
@@ -622,58 +635,407 @@ k_quant_cols(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int
   for (; t < T; t += 16) code_vec(__ldg(reinterpret_cast<const uint4*>(base + t * Hd)), t);
 }
 
+// ---------------------------------------------------------------------------------
+// Single-pass column kernel for the CHANNEL / HEAD kinds (k_quant_cols reads every
+// strip twice, and its resident 512 KB strips overflow L2, so the second pass comes
+// back from HBM).  A cluster of kColsCL CTAs splits one plane's CW-column strip along
+// tokens; each CTA stages its TT token rows (2*CW bytes each) in shared memory with
+// cp.async, reduces per-column (min, -max) locally, and the cluster combines the
+// partials through distributed shared memory (every CTA reads the kColsCL partials of
+// its columns, so no second barrier round precedes the float64 solve).  Codes are then
+// produced from shared memory: HBM traffic is one read of the fp16 values + the codes +
+// 4 B per group.  CW = 64 (channel kind: 128 B token rows, 4 warps) or 128 (head kind,
+// one 128-column head per strip).
+// ---------------------------------------------------------------------------------
+constexpr int kColsCL = 8;
+
+__device__ __forceinline__ uint32_t dsmem_ld_u32(uint32_t cluster_addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(cluster_addr) : "memory");
+  return v;
+}
+
+template <int BITS, bool PACK, int CW>
+__global__ void __cluster_dims__(1, kColsCL, 1) __launch_bounds__(CW * 2, CW == 32 ? 12 : 768 / (CW * 2))
+k_quant_cols_cl(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int64_t rows_per_plane, int TT,
+                uint8_t* __restrict__ codes, uint32_t* __restrict__ mm, int* __restrict__ flag, int sym) {
+  constexpr int NCV = CW / 8;            // 16-byte column vectors per token row
+  constexpr int NW = CW / 16;            // warps (16 token lanes x NCV column vectors)
+  constexpr int TPW = 32 / NCV;          // token lanes per warp
+  constexpr float QMAXF = (float)((1 << BITS) - 1);
+  extern __shared__ uint4 s_tile[];      // [TT][NCV]: TT token rows x CW columns
+  __shared__ __half2 s_mm[NW][CW];       // (min, -max) per warp and column
+  __shared__ __half2 s_part[CW];         // this CTA's partial per column (read by the cluster)
+  __shared__ float s_inv[CW], s_zc[CW], s_thr[CW];
+  __shared__ double s_sd[CW], s_zd[CW];
+  const int tid = threadIdx.x;
+  const int cv = tid % NCV, tl = tid / NCV;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int64_t plane = blockIdx.z;
+  const int64_t col0 = (int64_t)blockIdx.x * CW;
+  const int64_t t0 = (int64_t)rank * TT;
+  const int nt = (int)(T - t0 < TT ? (T - t0 > 0 ? T - t0 : 0) : TT);
+  const uint16_t* base = x + (plane * T + t0) * Hd + col0 + cv * 8;
+  // ---- stage the token rows: two cp.async groups so the min/max of the first half
+  // overlaps the second half's loads
+  const int half = min(((nt + 31) / 32) * 16, nt);
+#pragma unroll 4
+  for (int r = tl; r < half; r += 16) cp_async16(&s_tile[r * NCV + cv], base + (int64_t)r * Hd, true);
+  cp_async_commit();
+#pragma unroll 4
+  for (int r = half + tl; r < nt; r += 16) cp_async16(&s_tile[r * NCV + cv], base + (int64_t)r * Hd, true);
+  cp_async_commit();
+  __half2 lo[4], hi[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    lo[j] = __half2half2(__ushort_as_half(0x7c00));
+    hi[j] = __half2half2(__ushort_as_half(0xfc00));
+  }
+  auto mm_rows = [&](int r0, int r1) {
+#pragma unroll 4
+    for (int r = r0 + tl; r < r1; r += 16) {
+      const uint4 d = s_tile[r * NCV + cv];
+      const __half2* h = reinterpret_cast<const __half2*>(&d);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        lo[j] = __hmin2_nan(lo[j], h[j]);
+        hi[j] = __hmax2_nan(hi[j], h[j]);
+      }
+    }
+  };
+  cp_async_wait<1>();  // a thread reads back only the vectors it staged itself
+  mm_rows(0, half);
+  cp_async_wait<0>();
+  mm_rows(half, nt);
+  // the token lanes of a warp first (shuffles), then the warps (shared memory)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    __half2 a = __halves2half2(__low2half(lo[j]), __hneg(__low2half(hi[j])));
+    __half2 b = __halves2half2(__high2half(lo[j]), __hneg(__high2half(hi[j])));
+#pragma unroll
+    for (int o = NCV; o < 32; o <<= 1) {
+      uint32_t ua = *reinterpret_cast<uint32_t*>(&a), ub = *reinterpret_cast<uint32_t*>(&b);
+      uint32_t wa = __shfl_xor_sync(0xffffffffu, ua, o), wb = __shfl_xor_sync(0xffffffffu, ub, o);
+      a = __hmin2_nan(a, *reinterpret_cast<__half2*>(&wa));
+      b = __hmin2_nan(b, *reinterpret_cast<__half2*>(&wb));
+    }
+    if (tl % TPW == 0) {
+      s_mm[tl / TPW][cv * 8 + 2 * j] = a;
+      s_mm[tl / TPW][cv * 8 + 2 * j + 1] = b;
+    }
+  }
+  __syncthreads();
+  if (tid < CW) {
+    __half2 m = s_mm[0][tid];
+#pragma unroll
+    for (int u = 1; u < NW; ++u) m = __hmin2_nan(m, s_mm[u][tid]);
+    s_part[tid] = m;
+  }
+  // ---- cluster-wide combine through distributed shared memory
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (tid < CW) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&s_part[tid]));
+    uint32_t w[kColsCL];
+#pragma unroll
+    for (int q = 0; q < kColsCL; ++q) {
+      uint32_t ra;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(q));
+      w[q] = dsmem_ld_u32(ra);
+    }
+    __half2 m = *reinterpret_cast<__half2*>(&w[0]);
+#pragma unroll
+    for (int q = 1; q < kColsCL; ++q) m = __hmin2_nan(m, *reinterpret_cast<__half2*>(&w[q]));
+    s_mm[0][tid] = m;
+  }
+  // the peers' partials have been read: this CTA may leave once every CTA got here
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  __syncthreads();
+  // one thread per group of cpr columns (every CTA solves its strip's groups; rank 0
+  // writes them to the slab)
+  const int groups = CW / cpr;
+  if (tid < groups) {
+    __half2 m = s_mm[0][tid * cpr];
+    for (int u = 1; u < cpr; ++u) m = __hmin2_nan(m, s_mm[0][tid * cpr + u]);
+    float fmn = __low2float(m), fmx = -__high2float(m);
+    const bool bad = !(isfinite(fmn) && isfinite(fmx));
+    if (bad) { fmn = 0.f; fmx = 0.f; }
+    if (bad && rank == 0) atomicOr(flag, 1);
+    double sd, zd;
+    const TileParams tp = tile_params_f16(fmn, fmx, qdiv_make((double)((1 << BITS) - 1)), sd, zd, sym);
+    if (rank == 0) mm[plane * rows_per_plane + (col0 / cpr) + tid] = *reinterpret_cast<const uint32_t*>(&m);
+    s_inv[tid] = tp.inv_s;  // per group (column / cpr)
+    s_zc[tid] = tp.zc;
+    s_thr[tid] = tp.thr;
+    s_sd[tid] = sd;
+    s_zd[tid] = zd;
+  }
+  __syncthreads();
+  // ---- codes from shared memory.  One threshold per thread (the smallest of its 8
+  // columns'): a vector whose largest |e| reaches it re-checks each value against its
+  // own column's threshold.
+  float inv[8], zc[8], thr[8];
+  float thr_min = 1.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int gi = (cv * 8 + j) / cpr;
+    inv[j] = s_inv[gi];
+    zc[j] = s_zc[gi];
+    thr[j] = s_thr[gi];
+    thr_min = fminf(thr_min, thr[j]);
+  }
+  uint8_t* cbase = codes + ((plane * T + t0) * Hd + col0 + cv * 8) / (PACK ? 2 : 1);
+  const float2 i2[4] = {make_float2(inv[0], inv[1]), make_float2(inv[2], inv[3]), make_float2(inv[4], inv[5]),
+                        make_float2(inv[6], inv[7])};
+  const float2 z2[4] = {make_float2(zc[0], zc[1]), make_float2(zc[2], zc[3]), make_float2(zc[4], zc[5]),
+                        make_float2(zc[6], zc[7])};
+  const float2 nz2[4] = {make_float2(-zc[0], -zc[1]), make_float2(-zc[2], -zc[3]), make_float2(-zc[4], -zc[5]),
+                         make_float2(-zc[6], -zc[7])};
+#pragma unroll 4
+  for (int r = tl; r < nt; r += 16) {
+    const uint4 d = s_tile[r * NCV + cv];
+    const __half2* h = reinterpret_cast<const __half2*>(&d);
+    uint32_t c[8];
+    float dmax = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __half22float2(h[j]);
+      const float2 y = __ffma2_rn(f, i2[j], z2[j]);
+      const float2 cc = __fadd2_rn(y, nz2[j]);
+      const float2 e = __ffma2_rn(f, i2[j], make_float2(-cc.x, -cc.y));
+      dmax = fmaxf(dmax, fmaxf(fabsf(e.x), fabsf(e.y)));
+      c[2 * j] = f2bits(y.x);
+      c[2 * j + 1] = f2bits(y.y);
+    }
+    if (!(dmax < thr_min)) {  // rare: the reference float64 ops for the values near a boundary
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float f = __half2float(reinterpret_cast<const __half*>(&d)[j]);
+        const float y = fmaf(f, inv[j], zc[j]);
+        if (!(fabsf(fmaf(f, inv[j], -__fadd_rn(y, -zc[j]))) < thr[j])) {
+          const int gi = (cv * 8 + j) / cpr;
+          const float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, s_sd[gi]), s_zd[gi]));
+          c[j] = (uint32_t)fminf(fmaxf(rr, 0.f), QMAXF);
+        }
+      }
+    }
+    if (PACK) {
+      __stcs(reinterpret_cast<uint32_t*>(cbase + (int64_t)r * Hd / 2), pack_int4x8(c));
+    } else {
+      __stcs(reinterpret_cast<uint2*>(cbase + (int64_t)r * Hd),
+             make_uint2(gather4(c[0], c[1], c[2], c[3]), gather4(c[4], c[5], c[6], c[7])));
+    }
+  }
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+// Persistent, double-buffered variant of k_quant_cols_cl: each cluster walks strips
+// blockIdx.x, +gridDim.x, ... (plane-major); while strip i is reduced, solved and coded
+// from one shared-memory buffer, strip i+1 streams into the other.  A thread reads back
+// only the vectors it staged, so the tile buffers need no block barrier; the partials
+// are double-buffered by strip parity (a peer reads strip i's partial before it arrives
+// at strip i+1's cluster barrier, which precedes our write of strip i+2's partial).
+template <int BITS, bool PACK, int CW>
+__global__ void __cluster_dims__(1, kColsCL, 1) __launch_bounds__(CW * 2)
+k_quant_cols_cp(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int64_t rows_per_plane, int TT,
+                int64_t n_strips, uint8_t* __restrict__ codes, uint32_t* __restrict__ mm, int* __restrict__ flag,
+                int sym) {
+  constexpr int NCV = CW / 8;
+  constexpr int NW = CW / 16;
+  constexpr int TPW = 32 / NCV;
+  constexpr float QMAXF = (float)((1 << BITS) - 1);
+  extern __shared__ uint4 s_buf[];       // 2 x [TT][NCV]
+  __shared__ __half2 s_mm[NW][CW];
+  __shared__ __half2 s_part[2][CW];
+  __shared__ float s_inv[CW], s_zc[CW], s_thr[CW];
+  __shared__ double s_sd[CW], s_zd[CW];
+  const int tid = threadIdx.x;
+  const int cv = tid % NCV, tl = tid / NCV;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int64_t t0 = (int64_t)rank * TT;
+  const int nt = (int)(T - t0 < TT ? (T - t0 > 0 ? T - t0 : 0) : TT);
+  const int64_t strips_pp = Hd / CW;
+  const QDiv dq = qdiv_make((double)((1 << BITS) - 1));
+  auto stage = [&](int64_t strip, uint4* buf) {
+    if (strip < n_strips) {
+      const int64_t plane = strip / strips_pp, col0 = (strip - plane * strips_pp) * CW;
+      const uint16_t* base = x + (plane * T + t0) * Hd + col0 + cv * 8;
+#pragma unroll 4
+      for (int r = tl; r < nt; r += 16) cp_async16(&buf[r * NCV + cv], base + (int64_t)r * Hd, true);
+    }
+    cp_async_commit();
+  };
+  int it = 0;
+  stage(blockIdx.x, s_buf);
+  for (int64_t strip = blockIdx.x; strip < n_strips; strip += gridDim.x, ++it) {
+    uint4* cur = s_buf + (it & 1) * TT * NCV;
+    stage(strip + gridDim.x, s_buf + ((it + 1) & 1) * TT * NCV);
+    cp_async_wait<1>();
+    const int64_t plane = strip / strips_pp, col0 = (strip - plane * strips_pp) * CW;
+    __half2 lo[4], hi[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      lo[j] = __half2half2(__ushort_as_half(0x7c00));
+      hi[j] = __half2half2(__ushort_as_half(0xfc00));
+    }
+#pragma unroll 4
+    for (int r = tl; r < nt; r += 16) {
+      const uint4 d = cur[r * NCV + cv];
+      const __half2* h = reinterpret_cast<const __half2*>(&d);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        lo[j] = __hmin2_nan(lo[j], h[j]);
+        hi[j] = __hmax2_nan(hi[j], h[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __half2 a = __halves2half2(__low2half(lo[j]), __hneg(__low2half(hi[j])));
+      __half2 b = __halves2half2(__high2half(lo[j]), __hneg(__high2half(hi[j])));
+#pragma unroll
+      for (int o = NCV; o < 32; o <<= 1) {
+        uint32_t ua = *reinterpret_cast<uint32_t*>(&a), ub = *reinterpret_cast<uint32_t*>(&b);
+        uint32_t wa = __shfl_xor_sync(0xffffffffu, ua, o), wb = __shfl_xor_sync(0xffffffffu, ub, o);
+        a = __hmin2_nan(a, *reinterpret_cast<__half2*>(&wa));
+        b = __hmin2_nan(b, *reinterpret_cast<__half2*>(&wb));
+      }
+      if (tl % TPW == 0) {
+        s_mm[tl / TPW][cv * 8 + 2 * j] = a;
+        s_mm[tl / TPW][cv * 8 + 2 * j + 1] = b;
+      }
+    }
+    __syncthreads();
+    if (tid < CW) {
+      __half2 m = s_mm[0][tid];
+#pragma unroll
+      for (int u = 1; u < NW; ++u) m = __hmin2_nan(m, s_mm[u][tid]);
+      s_part[it & 1][tid] = m;
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (tid < CW) {
+      const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&s_part[it & 1][tid]));
+      uint32_t w[kColsCL];
+#pragma unroll
+      for (int q = 0; q < kColsCL; ++q) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(q));
+        w[q] = dsmem_ld_u32(ra);
+      }
+      __half2 m = *reinterpret_cast<__half2*>(&w[0]);
+#pragma unroll
+      for (int q = 1; q < kColsCL; ++q) m = __hmin2_nan(m, *reinterpret_cast<__half2*>(&w[q]));
+      s_mm[0][tid] = m;
+    }
+    __syncthreads();
+    const int groups = CW / cpr;
+    if (tid < groups) {
+      __half2 m = s_mm[0][tid * cpr];
+      for (int u = 1; u < cpr; ++u) m = __hmin2_nan(m, s_mm[0][tid * cpr + u]);
+      float fmn = __low2float(m), fmx = -__high2float(m);
+      const bool bad = !(isfinite(fmn) && isfinite(fmx));
+      if (bad) { fmn = 0.f; fmx = 0.f; }
+      if (bad && rank == 0) atomicOr(flag, 1);
+      double sd, zd;
+      const TileParams tp = tile_params_f16(fmn, fmx, dq, sd, zd, sym);
+      if (rank == 0) mm[plane * rows_per_plane + (col0 / cpr) + tid] = *reinterpret_cast<const uint32_t*>(&m);
+      s_inv[tid] = tp.inv_s;
+      s_zc[tid] = tp.zc;
+      s_thr[tid] = tp.thr;
+      s_sd[tid] = sd;
+      s_zd[tid] = zd;
+    }
+    __syncthreads();
+    float inv[8], zc[8], thr[8];
+    float thr_min = 1.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int gi = (cv * 8 + j) / cpr;
+      inv[j] = s_inv[gi];
+      zc[j] = s_zc[gi];
+      thr[j] = s_thr[gi];
+      thr_min = fminf(thr_min, thr[j]);
+    }
+    uint8_t* cbase = codes + ((plane * T + t0) * Hd + col0 + cv * 8) / (PACK ? 2 : 1);
+#pragma unroll 4
+    for (int r = tl; r < nt; r += 16) {
+      const uint4 d = cur[r * NCV + cv];
+      const __half2* h = reinterpret_cast<const __half2*>(&d);
+      uint32_t c[8];
+      float dmax = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __half22float2(h[j]);
+        const float2 i2 = make_float2(inv[2 * j], inv[2 * j + 1]);
+        const float2 y = __ffma2_rn(f, i2, make_float2(zc[2 * j], zc[2 * j + 1]));
+        const float2 cc = __fadd2_rn(y, make_float2(-zc[2 * j], -zc[2 * j + 1]));
+        const float2 e = __ffma2_rn(f, i2, make_float2(-cc.x, -cc.y));
+        dmax = fmaxf(dmax, fmaxf(fabsf(e.x), fabsf(e.y)));
+        c[2 * j] = f2bits(y.x);
+        c[2 * j + 1] = f2bits(y.y);
+      }
+      if (!(dmax < thr_min)) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float f = __half2float(reinterpret_cast<const __half*>(&d)[j]);
+          const float y = fmaf(f, inv[j], zc[j]);
+          if (!(fabsf(fmaf(f, inv[j], -__fadd_rn(y, -zc[j]))) < thr[j])) {
+            const int gi = (cv * 8 + j) / cpr;
+            const float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, s_sd[gi]), s_zd[gi]));
+            c[j] = (uint32_t)fminf(fmaxf(rr, 0.f), QMAXF);
+          }
+        }
+      }
+      if (PACK) {
+        __stcs(reinterpret_cast<uint32_t*>(cbase + (int64_t)r * Hd / 2), pack_int4x8(c));
+      } else {
+        __stcs(reinterpret_cast<uint2*>(cbase + (int64_t)r * Hd),
+               make_uint2(gather4(c[0], c[1], c[2], c[3]), gather4(c[4], c[5], c[6], c[7])));
+      }
+    }
+  }
+  cp_async_wait<0>();
+  // no CTA leaves while a peer may still read its last partial
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // Transfer-slab parameters -> (scale, zero): a group's fp16 (min, -max) determines its
 // float64 scale and zero through exactly the quantizer's solve (kvmanager.py:130-146),
-// so the slab carries 4 bytes per group instead of 12.  The solve is a chain of
-// dependent float64 operations; each thread runs NG groups' chains interleaved (the
-// snap loop iterates until every one of its groups is at a fixed point, a group that
-// converged keeps its value), which hides the float64 latency.
-template <int BITS, int NG>
+// so the slab carries 4 bytes per group instead of 12.  One group per thread (NG groups
+// in sequence); the snap loop's cycle shortcut (qmath.cuh snap_scale) keeps the rare
+// non-settling groups from holding their warp for 32 passes.
+__device__ __forceinline__ void load_minmax(const uint32_t* mm, int64_t r, double& mn, double& mx) {
+  uint32_t w = mm[r];
+  const __half2 h = *reinterpret_cast<const __half2*>(&w);
+  float fmn = __low2float(h), fmx = -__high2float(h);
+  if (!(isfinite(fmn) && isfinite(fmx))) { fmn = 0.f; fmx = 0.f; }  // flagged at quantize time
+  mn = (double)fmn;
+  mx = (double)fmx;
+}
+
+// One group per thread.  The snap loop's cycle shortcut (qmath.cuh snap_scale) keeps
+// the rare non-settling groups from holding their warp for 32 passes (expand 95 -> 73 us
+// for a 1 GiB INT4 g=64 job; deferring unsettled groups to a dense second kernel measured
+// slower, 81 + 7 us).
+template <int BITS>
 __global__ void __launch_bounds__(256)
 k_expand_params(const uint32_t* __restrict__ mm, int64_t groups, double* __restrict__ scale,
                 float* __restrict__ zero, int sym) {
   const QDiv dq = qdiv_make((double)((1 << BITS) - 1));
-  const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * NG;
-  if (r0 >= groups) return;
-  double mn[NG], mx[NG], s[NG], z[NG], hz[NG], lz[NG];
-  bool live[NG];
-#pragma unroll
-  for (int u = 0; u < NG; ++u) {
-    const int64_t r = r0 + u;
-    uint32_t w = r < groups ? mm[r] : 0u;
-    const __half2 h = *reinterpret_cast<const __half2*>(&w);
-    float fmn = __low2float(h), fmx = -__high2float(h);
-    if (!(isfinite(fmn) && isfinite(fmx))) { fmn = 0.f; fmx = 0.f; }  // flagged at quantize time
-    mn[u] = (double)fmn;
-    mx[u] = (double)fmx;
-    live[u] = !sym && mx[u] != mn[u];
-    if (sym) {
-      solve_absmax(mn[u], mx[u], dq.b, s[u], z[u]);                   // no snap loop
-    } else {
-      s[u] = live[u] ? qdiv(__dsub_rn(mx[u], mn[u]), dq) : 1.0;       // constant group: (1, -min)
-      z[u] = live[u] ? rint(__ddiv_rn(-mn[u], s[u])) : -mn[u];
-    }
-    hz[u] = __dsub_rn(dq.b, z[u]);
-    lz[u] = __dsub_rn(0.0, z[u]);
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= groups) return;
+  double mn, mx, s, z;
+  load_minmax(mm, r, mn, mx);
+  if (sym) {
+    solve_absmax(mn, mx, dq.b, s, z);  // no snap loop
+  } else if (mx == mn) {
+    s = 1.0;                           // constant group: (1, -min)
+    z = -mn;
+  } else {
+    solve_scale_zero(mn, mx, dq, s, z);
   }
-#pragma unroll 1
-  for (int it = 0; it < 32; ++it) {
-    bool any = false;
-#pragma unroll
-    for (int u = 0; u < NG; ++u) {
-      const double nxt = qdiv(__dsub_rn(__dmul_rn(s[u], hz[u]), __dmul_rn(s[u], lz[u])), dq);
-      if (live[u] && nxt != s[u]) s[u] = nxt; else live[u] = false;
-      any |= live[u];
-    }
-    if (!any) break;
-  }
-#pragma unroll
-  for (int u = 0; u < NG; ++u) {
-    if (r0 + u < groups) {
-      scale[r0 + u] = s[u];
-      zero[r0 + u] = (float)z[u];
-    }
-  }
+  scale[r] = s;
+  zero[r] = (float)z;
 }
 
 // Column dequantize for CHANNEL / HEAD kinds: each thread owns 8 columns of a strip

@@ -1255,18 +1255,21 @@ __device__ __forceinline__ int nw_last(unsigned bd) { return (int)(bd >> 5) - 1;
 
 // Per query: global coarse k-th from the splits' top lists, candidate compaction,
 // exact rescoring, (-sim, seq) order.  Block = 256 threads.
+// Block = 256 threads (small batches, U = 24) or 128 (large batches, U < 24, at most 64
+// registers so 8 blocks share an SM: the kernel is latency bound).  s_top is dynamic
+// shared memory, top_cap floats = min(4096, the scan's largest splits x k).
 template <int U, typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(U < 24 ? 128 : 256, U < 24 ? 8 : 1)
 k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64_t n_rows, int64_t dim, const T* __restrict__ qx,
           const T* __restrict__ vm, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
           const float* __restrict__ two_delta, const float* __restrict__ cand_s, const int32_t* __restrict__ cand_r,
           const int32_t* __restrict__ cand_n, const float* __restrict__ topc, const float* __restrict__ ext,
           double* __restrict__ out_sim, int64_t* __restrict__ out_seq, int32_t* __restrict__ out_len,
           int32_t* __restrict__ out_count, int32_t* __restrict__ need_exhaustive,
-          unsigned int* __restrict__ inexact_count, const BlasRef blas) {
+          unsigned int* __restrict__ inexact_count, const BlasRef blas, int top_cap) {
   const int64_t q = blockIdx.x;
   if (q >= B) return;
-  __shared__ float s_top[4096];  // list values >= the bound (more: exhaustive path)
+  extern __shared__ float s_top[];  // list values >= the bound (more than top_cap: exhaustive path)
   __shared__ int s_off[513];     // n_splits <= 512 (host)
   __shared__ int s_rows[MAXC];
   __shared__ double s_sim[MAXC];
@@ -1293,6 +1296,9 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   //    slots) such that the union of the lists holds k values >= L, so only list values
   //    >= L can decide the k-th: they are compacted (usually about k of the n_splits*k)
   const int m = n_splits * k;
+  // per-query scalars the later phases need, loaded now so they arrive with the lists
+  const float td = two_delta[q];
+  const float ext_q = ext ? ext[q] : NEG;
   float L = NEG;
   {
     const uint32_t g0 = wa.gkth[q];
@@ -1315,7 +1321,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
     for (int u = 0; u < 8; ++u)
       if (i0 + u * (int)blockDim.x < m && tv[u] >= L) {
         const int at = atomicAdd(&s_nt, 1);
-        if (at < 4096) s_top[at] = tv[u];
+        if (at < top_cap) s_top[at] = tv[u];
       }
   }
   for (int sp = tid; sp < n_splits; sp += blockDim.x) {
@@ -1324,7 +1330,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
     if (cnt < 0) s_flag = 1;
   }
   __syncthreads();
-  if (s_nt > 4096) {  // thousands of list values tie at the bound: exhaustive path
+  if (s_nt > top_cap) {  // thousands of list values tie at the bound: exhaustive path
     if (tid == 0) need_exhaustive[q] = 1;
     return;
   }
@@ -1403,35 +1409,35 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   // (a bound from other shards can only raise the threshold: ext is an exact-score
   // lower bound of the global k-th, so rows with coarse score below ext - delta cannot
   // enter the global top-k)
-  const float td = two_delta[q];
-  const float thr = fmaxf(__fsub_rd(s_kth, td), ext ? __fsub_rd(ext[q], 0.5f * td) : NEG);
+  const float thr = fmaxf(__fsub_rd(s_kth, td), ext ? __fsub_rd(ext_q, 0.5f * td) : NEG);
   // 3) gather candidates above the final threshold: the (split, slot) entries are
   //    flattened over the whole block through the prefix sum of the counts, so every
   //    candidate load is in flight at once (candidate order is irrelevant: step 5 ranks)
   const int total = s_off[n_splits];
   for (int i0 = tid; i0 < total; i0 += 8 * blockDim.x) {
-    size_t ev[8];
+    int rv[8];
     float sv[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {  // 8 candidate loads in flight per thread
-      const int i = i0 + u * (int)blockDim.x;
+    for (int u = 0; u < 8; ++u) {  // 8 candidate (score, row) loads in flight per thread;
+      const int i = i0 + u * (int)blockDim.x;  // the row is loaded with the score, not after the test
       sv[u] = __int_as_float(0x7fffffff);  // NaN: past the end never passes, even thr = -inf
-      ev[u] = 0;
+      rv[u] = 0;
       if (i < total) {
         int lo = 0, hi = n_splits;  // largest sp with s_off[sp] <= i
         while (hi - lo > 1) {
           const int mid = (lo + hi) >> 1;
           if (s_off[mid] <= i) lo = mid; else hi = mid;
         }
-        ev[u] = ((size_t)lo * Bp + q) * CAP + (i - s_off[lo]);
-        sv[u] = __ldg(cand_s + ev[u]);
+        const size_t ev = ((size_t)lo * Bp + q) * CAP + (i - s_off[lo]);
+        sv[u] = __ldg(cand_s + ev);
+        rv[u] = __ldg(cand_r + ev);
       }
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       if (sv[u] >= thr) {
         const int slot = atomicAdd(&s_n, 1);
-        if (slot < MAXC) s_rows[slot] = cand_r[ev[u]];
+        if (slot < MAXC) s_rows[slot] = rv[u];
       }
     }
   }
@@ -1516,16 +1522,15 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
 }
 
 // Exhaustive exact top-k for queries flagged by k_rescore (candidate overflow from
-// heavy ties); a no-op block for every other query.  Slow but exact.
+// heavy ties).  One block per 256 queries reads their flags at once (flagged queries
+// are rare; one block per query cost ~9 us of empty blocks at B = 4096).  Slow but exact.
 template <typename T>
-__global__ void __launch_bounds__(256)
-k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const T* __restrict__ qx,
-             const T* __restrict__ vm, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
-             int32_t* __restrict__ need, double* __restrict__ out_sim, int64_t* __restrict__ out_seq,
-             int32_t* __restrict__ out_len, int32_t* __restrict__ out_count, unsigned int* __restrict__ inexact_count,
-             const BlasRef blas) {
-  const int64_t q = blockIdx.x;
-  if (q >= B || !need[q]) return;
+__device__ __noinline__ void exhaustive_query(int64_t q, int k, int64_t n_rows, int64_t dim, const T* __restrict__ qx,
+                                              const T* __restrict__ vm, const int32_t* __restrict__ lens,
+                                              const int64_t* __restrict__ seqs, int32_t* __restrict__ need,
+                                              double* __restrict__ out_sim, int64_t* __restrict__ out_seq,
+                                              int32_t* __restrict__ out_len, int32_t* __restrict__ out_count,
+                                              unsigned int* __restrict__ inexact_count, const BlasRef blas) {
   __shared__ double s_sim[8 * KMAX];
   __shared__ int64_t s_seq[8 * KMAX];
   __shared__ int s_row[8 * KMAX];
@@ -1587,6 +1592,26 @@ k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const T* __restrict_
     if (rank < k) { out_sim[q * k + rank] = s_sim[c]; out_seq[q * k + rank] = s_seq[c]; out_len[q * k + rank] = lens[s_row[c]]; }
   }
   if (threadIdx.x == 0) { out_count[q] = (int32_t)(n_rows < k ? n_rows : k); need[q] = 0; }
+  __syncthreads();  // the block's shared lists are reused by its next flagged query
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const T* __restrict__ qx,
+             const T* __restrict__ vm, const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
+             int32_t* __restrict__ need, double* __restrict__ out_sim, int64_t* __restrict__ out_seq,
+             int32_t* __restrict__ out_len, int32_t* __restrict__ out_count, unsigned int* __restrict__ inexact_count,
+             const BlasRef blas) {
+  // each block owns blockDim.x consecutive queries: one parallel read of their flags
+  __shared__ int s_need[256];
+  const int64_t q0 = (int64_t)blockIdx.x * blockDim.x;
+  const int64_t myq = q0 + threadIdx.x;
+  s_need[threadIdx.x] = myq < B ? need[myq] : 0;
+  const int any = __syncthreads_or(s_need[threadIdx.x]);
+  if (!any) return;
+  for (int i = 0; i < (int)blockDim.x && q0 + i < B; ++i)
+    if (s_need[i]) exhaustive_query(q0 + i, k, n_rows, dim, qx, vm, lens, seqs, need, out_sim, out_seq, out_len,
+                                    out_count, inexact_count, blas);
 }
 
 // ------------------------------------------------------------------ shard merge

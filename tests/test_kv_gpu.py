@@ -449,3 +449,35 @@ def test_absmax_swap_round_trip(km, kind, group, bits, packed):
     finally:
         eng.close()
         pool.close()
+
+
+# ----------------------------------------------------------------- column kinds, ragged T
+@pytest.mark.parametrize("kind,bits,packed", [("channel", 8, False), ("channel", 4, True), ("head", 8, False),
+                                              ("head", 4, False)])
+@pytest.mark.parametrize("T", [1, 5, 37, 300, 6017, 12900])
+def test_cols_ragged_tokens_through_host(km, kind, bits, packed, T):
+    """Column kinds at token counts that leave cluster ranks empty or partial (T < 8,
+    T not a multiple of 8 x 16) and beyond the single-pass kernel's shared-memory limit
+    (T = 12900 takes the two-pass kernel): every plane vs the C oracle through pinned host."""
+    import torch
+
+    from harness import parity, synthetic
+    L, H = 1, 256
+    lay = km.KVLayout(L, T, H, 128, kind=kind, bits=bits, packed=packed)
+    kv = synthetic.kv_job_torch(L, T, H, seed=T, job=2, group=64)
+    g = lay.geometry()
+    pool = km.HostSlabPool(g["slab_bytes"] + 4096)
+    eng = km.KVSwapEngine()
+    try:
+        addr = pool.alloc(g["slab_bytes"])
+        eng.offload(lay, kv, addr)
+        torch.cuda.synchronize()
+        out = torch.zeros_like(kv)
+        eng.upload(lay, addr, out)
+        torch.cuda.synchronize()
+        planes, _vals, bad = parity.kv_check_planes(lay, kv.cpu().numpy(), pool.view(addr, g["slab_bytes"]),
+                                                    out.cpu().numpy())
+        assert planes == 2 * L and not bad, bad
+    finally:
+        eng.close()
+        pool.close()
