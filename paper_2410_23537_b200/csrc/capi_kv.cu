@@ -445,25 +445,6 @@ static bool getenv_flag(const char* name) {
 }
 
 template <int BITS, bool PACK, int CW>
-static int launch_cols_cp(int64_t np, int tt, const uint16_t* kv, const alise_kv_desc* d, int cpr, int64_t rows_pp,
-                          uint8_t* codes, uint32_t* mm, int* flag, cudaStream_t st) {
-  auto kern = k_quant_cols_cp<BITS, PACK, CW>;
-  const int smem = 2 * tt * 2 * CW;
-  static int set = 0, per_sm = 0;
-  if (smem > set) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * CW, smem));
-    set = smem;
-  }
-  const int64_t strips = (d->hidden / CW) * np;
-  const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(strips, (int64_t)sm_count() * std::max(1, per_sm) / kColsCL));
-  dim3 grid((unsigned)clusters, kColsCL, 1);
-  kern<<<grid, 2 * CW, smem, st>>>(kv, d->tokens, d->hidden, cpr, rows_pp, tt, strips, codes, mm, flag, d->mode);
-  CKL();
-  return ALISE_OK;
-}
-
-template <int BITS, bool PACK, int CW>
 static int launch_cols_cl(dim3 grid, int smem, const uint16_t* kv, const alise_kv_desc* d, int cpr, int64_t rows_pp,
                           int tt, uint8_t* codes, uint32_t* mm, int* flag, cudaStream_t st) {
   auto kern = k_quant_cols_cl<BITS, PACK, CW>;
@@ -483,10 +464,7 @@ static int launch_cols_cl(dim3 grid, int smem, const uint16_t* kv, const alise_k
 static int cols_path(const alise_kv_desc* d) {
   const int64_t cpr = d->kind == ALISE_KIND_CHANNEL ? 1 : d->head_dim;
   const int64_t tt = (d->tokens + kColsCL - 1) / kColsCL;
-  static int narrow = -1;  // ALISE_COLS_CW=32: 64 B token rows (tuning experiment)
-  if (narrow < 0) narrow = getenv("ALISE_COLS_CW") && atoi(getenv("ALISE_COLS_CW")) == 32;
-  const int cw = narrow && cpr <= 32 && 32 % cpr == 0 ? 32
-                 : (cpr <= 64 && 64 % cpr == 0 ? 64 : 128);  // 128 B token rows unless a head is wider
+  const int cw = cpr <= 64 && 64 % cpr == 0 ? 64 : 128;  // 128 B token rows unless a head is wider
   if (d->hidden % cw == 0 && cw % cpr == 0 && tt * 2 * cw <= (200 << 10) && !getenv_flag("ALISE_COLS_TWOPASS"))
     return cw;
   if (d->hidden % 128 == 0 && cpr <= 128 && 128 % cpr == 0) return 1;
@@ -522,16 +500,7 @@ static int quant_chunk(const alise_kv_desc* d, const KvGeom& g, int64_t np, cons
     // one HBM pass: a cluster of kColsCL CTAs per (plane, cw-column strip)
     dim3 grid((unsigned)(d->hidden / cw), kColsCL, (unsigned)np);
     const int smem = (int)(tt * 2 * cw);
-    static int persist = -1;  // ALISE_COLS_PERSIST=1: persistent double-buffered clusters (tuning)
-    if (persist < 0) persist = getenv_flag("ALISE_COLS_PERSIST");
-#define QCL(B, P, W)                                                                                          \
-  return persist ? launch_cols_cp<B, P, W>(np, (int)tt, kv, d, cpr, g.rows_pp, codes, mm, flag, st)          \
-                 : launch_cols_cl<B, P, W>(grid, smem, kv, d, cpr, g.rows_pp, (int)tt, codes, mm, flag, st)
-    if (cw == 32) {
-      if (d->bits == 8) QCL(8, false, 32);
-      if (d->packed) QCL(4, true, 32);
-      QCL(4, false, 32);
-    }
+#define QCL(B, P, W) return launch_cols_cl<B, P, W>(grid, smem, kv, d, cpr, g.rows_pp, (int)tt, codes, mm, flag, st)
     if (cw == 64) {
       if (d->bits == 8) QCL(8, false, 64);
       if (d->packed) QCL(4, true, 64);

@@ -420,9 +420,7 @@ static int topk_rescore_t(alise_db* db, const T* queries, int64_t B, int k, cons
   CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
   // small batches are latency bound (one DRAM round trip per candidate row), large ones
   // throughput bound (registers / occupancy)
-  static int ru = -1;  // ALISE_RESCORE_U: elements per lane in flight for large batches (tuning)
-  if (ru < 0) ru = getenv("ALISE_RESCORE_U") ? atoi(getenv("ALISE_RESCORE_U")) : 8;
-  auto rescore = B <= 512 ? k_rescore<24, T> : (ru == 12 ? k_rescore<12, T> : k_rescore<8, T>);
+  auto rescore = B <= 512 ? k_rescore<24, T> : k_rescore<8, T>;
   static int rthreads = -1;
   if (rthreads < 0) {
     const char* e = getenv("ALISE_RESCORE_THREADS");

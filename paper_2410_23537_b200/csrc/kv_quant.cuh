@@ -656,7 +656,7 @@ __device__ __forceinline__ uint32_t dsmem_ld_u32(uint32_t cluster_addr) {
 }
 
 template <int BITS, bool PACK, int CW>
-__global__ void __cluster_dims__(1, kColsCL, 1) __launch_bounds__(CW * 2, CW == 32 ? 12 : 768 / (CW * 2))
+__global__ void __cluster_dims__(1, kColsCL, 1) __launch_bounds__(CW * 2, 768 / (CW * 2))
 k_quant_cols_cl(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int64_t rows_per_plane, int TT,
                 uint8_t* __restrict__ codes, uint32_t* __restrict__ mm, int* __restrict__ flag, int sym) {
   constexpr int NCV = CW / 8;            // 16-byte column vectors per token row
@@ -827,176 +827,6 @@ k_quant_cols_cl(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, 
     }
   }
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-}
-
-// Persistent, double-buffered variant of k_quant_cols_cl: each cluster walks strips
-// blockIdx.x, +gridDim.x, ... (plane-major); while strip i is reduced, solved and coded
-// from one shared-memory buffer, strip i+1 streams into the other.  A thread reads back
-// only the vectors it staged, so the tile buffers need no block barrier; the partials
-// are double-buffered by strip parity (a peer reads strip i's partial before it arrives
-// at strip i+1's cluster barrier, which precedes our write of strip i+2's partial).
-template <int BITS, bool PACK, int CW>
-__global__ void __cluster_dims__(1, kColsCL, 1) __launch_bounds__(CW * 2)
-k_quant_cols_cp(const uint16_t* __restrict__ x, int64_t T, int64_t Hd, int cpr, int64_t rows_per_plane, int TT,
-                int64_t n_strips, uint8_t* __restrict__ codes, uint32_t* __restrict__ mm, int* __restrict__ flag,
-                int sym) {
-  constexpr int NCV = CW / 8;
-  constexpr int NW = CW / 16;
-  constexpr int TPW = 32 / NCV;
-  constexpr float QMAXF = (float)((1 << BITS) - 1);
-  extern __shared__ uint4 s_buf[];       // 2 x [TT][NCV]
-  __shared__ __half2 s_mm[NW][CW];
-  __shared__ __half2 s_part[2][CW];
-  __shared__ float s_inv[CW], s_zc[CW], s_thr[CW];
-  __shared__ double s_sd[CW], s_zd[CW];
-  const int tid = threadIdx.x;
-  const int cv = tid % NCV, tl = tid / NCV;
-  uint32_t rank;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-  const int64_t t0 = (int64_t)rank * TT;
-  const int nt = (int)(T - t0 < TT ? (T - t0 > 0 ? T - t0 : 0) : TT);
-  const int64_t strips_pp = Hd / CW;
-  const QDiv dq = qdiv_make((double)((1 << BITS) - 1));
-  auto stage = [&](int64_t strip, uint4* buf) {
-    if (strip < n_strips) {
-      const int64_t plane = strip / strips_pp, col0 = (strip - plane * strips_pp) * CW;
-      const uint16_t* base = x + (plane * T + t0) * Hd + col0 + cv * 8;
-#pragma unroll 4
-      for (int r = tl; r < nt; r += 16) cp_async16(&buf[r * NCV + cv], base + (int64_t)r * Hd, true);
-    }
-    cp_async_commit();
-  };
-  int it = 0;
-  stage(blockIdx.x, s_buf);
-  for (int64_t strip = blockIdx.x; strip < n_strips; strip += gridDim.x, ++it) {
-    uint4* cur = s_buf + (it & 1) * TT * NCV;
-    stage(strip + gridDim.x, s_buf + ((it + 1) & 1) * TT * NCV);
-    cp_async_wait<1>();
-    const int64_t plane = strip / strips_pp, col0 = (strip - plane * strips_pp) * CW;
-    __half2 lo[4], hi[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      lo[j] = __half2half2(__ushort_as_half(0x7c00));
-      hi[j] = __half2half2(__ushort_as_half(0xfc00));
-    }
-#pragma unroll 4
-    for (int r = tl; r < nt; r += 16) {
-      const uint4 d = cur[r * NCV + cv];
-      const __half2* h = reinterpret_cast<const __half2*>(&d);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        lo[j] = __hmin2_nan(lo[j], h[j]);
-        hi[j] = __hmax2_nan(hi[j], h[j]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      __half2 a = __halves2half2(__low2half(lo[j]), __hneg(__low2half(hi[j])));
-      __half2 b = __halves2half2(__high2half(lo[j]), __hneg(__high2half(hi[j])));
-#pragma unroll
-      for (int o = NCV; o < 32; o <<= 1) {
-        uint32_t ua = *reinterpret_cast<uint32_t*>(&a), ub = *reinterpret_cast<uint32_t*>(&b);
-        uint32_t wa = __shfl_xor_sync(0xffffffffu, ua, o), wb = __shfl_xor_sync(0xffffffffu, ub, o);
-        a = __hmin2_nan(a, *reinterpret_cast<__half2*>(&wa));
-        b = __hmin2_nan(b, *reinterpret_cast<__half2*>(&wb));
-      }
-      if (tl % TPW == 0) {
-        s_mm[tl / TPW][cv * 8 + 2 * j] = a;
-        s_mm[tl / TPW][cv * 8 + 2 * j + 1] = b;
-      }
-    }
-    __syncthreads();
-    if (tid < CW) {
-      __half2 m = s_mm[0][tid];
-#pragma unroll
-      for (int u = 1; u < NW; ++u) m = __hmin2_nan(m, s_mm[u][tid]);
-      s_part[it & 1][tid] = m;
-    }
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (tid < CW) {
-      const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&s_part[it & 1][tid]));
-      uint32_t w[kColsCL];
-#pragma unroll
-      for (int q = 0; q < kColsCL; ++q) {
-        uint32_t ra;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(q));
-        w[q] = dsmem_ld_u32(ra);
-      }
-      __half2 m = *reinterpret_cast<__half2*>(&w[0]);
-#pragma unroll
-      for (int q = 1; q < kColsCL; ++q) m = __hmin2_nan(m, *reinterpret_cast<__half2*>(&w[q]));
-      s_mm[0][tid] = m;
-    }
-    __syncthreads();
-    const int groups = CW / cpr;
-    if (tid < groups) {
-      __half2 m = s_mm[0][tid * cpr];
-      for (int u = 1; u < cpr; ++u) m = __hmin2_nan(m, s_mm[0][tid * cpr + u]);
-      float fmn = __low2float(m), fmx = -__high2float(m);
-      const bool bad = !(isfinite(fmn) && isfinite(fmx));
-      if (bad) { fmn = 0.f; fmx = 0.f; }
-      if (bad && rank == 0) atomicOr(flag, 1);
-      double sd, zd;
-      const TileParams tp = tile_params_f16(fmn, fmx, dq, sd, zd, sym);
-      if (rank == 0) mm[plane * rows_per_plane + (col0 / cpr) + tid] = *reinterpret_cast<const uint32_t*>(&m);
-      s_inv[tid] = tp.inv_s;
-      s_zc[tid] = tp.zc;
-      s_thr[tid] = tp.thr;
-      s_sd[tid] = sd;
-      s_zd[tid] = zd;
-    }
-    __syncthreads();
-    float inv[8], zc[8], thr[8];
-    float thr_min = 1.f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int gi = (cv * 8 + j) / cpr;
-      inv[j] = s_inv[gi];
-      zc[j] = s_zc[gi];
-      thr[j] = s_thr[gi];
-      thr_min = fminf(thr_min, thr[j]);
-    }
-    uint8_t* cbase = codes + ((plane * T + t0) * Hd + col0 + cv * 8) / (PACK ? 2 : 1);
-#pragma unroll 4
-    for (int r = tl; r < nt; r += 16) {
-      const uint4 d = cur[r * NCV + cv];
-      const __half2* h = reinterpret_cast<const __half2*>(&d);
-      uint32_t c[8];
-      float dmax = 0.f;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = __half22float2(h[j]);
-        const float2 i2 = make_float2(inv[2 * j], inv[2 * j + 1]);
-        const float2 y = __ffma2_rn(f, i2, make_float2(zc[2 * j], zc[2 * j + 1]));
-        const float2 cc = __fadd2_rn(y, make_float2(-zc[2 * j], -zc[2 * j + 1]));
-        const float2 e = __ffma2_rn(f, i2, make_float2(-cc.x, -cc.y));
-        dmax = fmaxf(dmax, fmaxf(fabsf(e.x), fabsf(e.y)));
-        c[2 * j] = f2bits(y.x);
-        c[2 * j + 1] = f2bits(y.y);
-      }
-      if (!(dmax < thr_min)) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float f = __half2float(reinterpret_cast<const __half*>(&d)[j]);
-          const float y = fmaf(f, inv[j], zc[j]);
-          if (!(fabsf(fmaf(f, inv[j], -__fadd_rn(y, -zc[j]))) < thr[j])) {
-            const int gi = (cv * 8 + j) / cpr;
-            const float rr = (float)rint(__dadd_rn(__ddiv_rn((double)f, s_sd[gi]), s_zd[gi]));
-            c[j] = (uint32_t)fminf(fmaxf(rr, 0.f), QMAXF);
-          }
-        }
-      }
-      if (PACK) {
-        __stcs(reinterpret_cast<uint32_t*>(cbase + (int64_t)r * Hd / 2), pack_int4x8(c));
-      } else {
-        __stcs(reinterpret_cast<uint2*>(cbase + (int64_t)r * Hd),
-               make_uint2(gather4(c[0], c[1], c[2], c[3]), gather4(c[4], c[5], c[6], c[7])));
-      }
-    }
-  }
-  cp_async_wait<0>();
-  // no CTA leaves while a peer may still read its last partial
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // Transfer-slab parameters -> (scale, zero): a group's fp16 (min, -max) determines its

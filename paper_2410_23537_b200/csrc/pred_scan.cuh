@@ -1356,6 +1356,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
         const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
         if (v2 > bv || (v2 == bv && i2 > bi)) { bv = v2; bi = i2; }
       }
+      __syncwarp();  // every lane's reads of this round precede the clear (racecheck)
       if (lane == 0) {
         s_wk[warp * (int)kk + round] = bv;
         if (bi >= 0) s_top[bi] = NEG;
@@ -1396,6 +1397,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
         const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
         if (v2 > bv || (v2 == bv && i2 > bi)) { bv = v2; bi = i2; }
       }
+      __syncwarp();  // every lane's reads of this round precede the clear (racecheck)
       if (lane == 0 && bi >= 0) src[bi] = NEG;
       __syncwarp();
       kth = bv;
