@@ -246,7 +246,9 @@ int alise_db_inexact(alise_db *db, unsigned int *count);
 /* Exact top-k of B queries ([B][dim] in the db's master dtype, device) against the db:
  * sims are the correctly rounded float64 dot products, ordered by (-sim, seq) (ties ->
  * older first).  Outputs [B][k]; count[b] = min(k, size).  VectorStore.search
- * (predictor.py:154-163). */
+ * (predictor.py:154-163).  k <= 16 takes the tcgen05 scan + fused filter; 16 < k <= 1024
+ * a CUDA-core coarse pass over row splits with the same bound (ALISE_ECAPACITY if more
+ * than 4096 rows of one query tie within the coarse error). */
 int alise_db_topk(alise_db *db, const void *queries, int64_t B, int k, double *out_sim,
                   int64_t *out_seq, int32_t *out_len, int32_t *out_count, void *stream);
 /* alise_db_topk in two steps for a sharded DB: the scan leaves per-query lower bounds
@@ -254,7 +256,8 @@ int alise_db_topk(alise_db *db, const void *queries, int64_t B, int k, double *o
  * k-th bound minus its own coarse error); after an all-reduce (max) of the bounds over
  * the shards, alise_db_topk_rescore returns the exact shard top-k restricted to rows
  * that can still enter the global top-k (counts may be < k).  ext_bound may be NULL
- * (= alise_db_topk).  The two calls must use the same queries. */
+ * (= alise_db_topk).  The two calls must use the same queries.  For k > 16 the bound is
+ * -inf and the rescore returns the shard's exact top-k. */
 int alise_db_topk_scan(alise_db *db, const void *queries, int64_t B, int k, float *out_bound,
                        void *stream);
 int alise_db_topk_rescore(alise_db *db, const void *queries, int64_t B, int k,

@@ -450,16 +450,82 @@ static int topk_rescore(alise_db* db, const void* queries, int64_t B, int k, con
 }
 
 
+// top_k above KMAX (k <= BIGK_MAX): k_bigk_scan over row splits, then k_bigk_select
+// per query (pred_scan.cuh).  Exact like the tcgen05 path; near-ties that overflow a
+// buffer fail with ECAPACITY instead of returning a wrong list.
+template <typename T>
+static int topk_bigk_t(alise_db* db, const T* queries, int64_t B, int k, double* out_sim, int64_t* out_seq,
+                       int32_t* out_len, int32_t* out_count, cudaStream_t st) {
+  const int64_t Bp = (B + BM - 1) / BM * BM;
+  int s = ensure_scratch(db, Bp, 1, st);
+  if (s) return s;
+  k_query_prep<T><<<(unsigned)Bp, 128, 0, st>>>(queries, B, db->dim, db->dp, db->vmax, db->q16, db->two_delta,
+                                                db->blas.on);
+  CKL();
+  // enough (split, query) blocks for 4 per SM; splits of >= 2048 rows
+  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>((4 * sm_count_pred() + B - 1) / B,
+                                                                  (db->size + 2047) / 2048));
+  const size_t ent = (size_t)B * splits * BIGK_BUF;
+  char* ws = nullptr;
+  const size_t wbytes = ent * 8 + (size_t)B * splits * 8 + 256;
+  static bool pool_kept = false;  // keep freed workspace reserved in the pool (no re-map per call)
+  if (!pool_kept) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_kept = true;
+  }
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&ws), wbytes, st));
+  float* es = reinterpret_cast<float*>(ws);
+  int32_t* er = reinterpret_cast<int32_t*>(ws + ent * 4);
+  int32_t* en = reinterpret_cast<int32_t*>(ws + ent * 8);
+  float* ek = reinterpret_cast<float*>(ws + ent * 8 + (size_t)B * splits * 4);
+  int32_t* ovf = reinterpret_cast<int32_t*>(ws + ent * 8 + (size_t)B * splits * 8);
+  CK(cudaMemsetAsync(ovf, 0, sizeof(int32_t), st));
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_bigk_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, BIGK_BUF * 8));
+    CK(cudaFuncSetAttribute(k_bigk_select<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, BIGK_BUF * 24));
+    CK(cudaFuncSetAttribute(k_bigk_select<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, BIGK_BUF * 24));
+    attr = true;
+  }
+  k_bigk_scan<<<dim3((unsigned)splits, (unsigned)B), 256, BIGK_BUF * 8, st>>>(db->size, db->dp, k, splits, db->v16,
+                                                                              db->q16, db->two_delta, es, er, en, ek);
+  CKL();
+  const BlasRef br = blas_ref(db);
+  k_bigk_select<T><<<(unsigned)B, 256, BIGK_BUF * 24, st>>>(
+      db->size, db->dim, k, splits, queries, static_cast<const T*>(db->vm), db->lens, db->seqs, db->two_delta, es, er,
+      en, ek, out_sim, out_seq, out_len, out_count, ovf, db->inexact, br);
+  CKL();
+  int32_t h_ovf = 0;
+  CK(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(ws, st));
+  CK(cudaStreamSynchronize(st));
+  if (h_ovf) return fail(ALISE_ECAPACITY, "top-%d search: more than %d near-tied candidates for a query", k, BIGK_BUF);
+  return ALISE_OK;
+}
+
+static int topk_bigk(alise_db* db, const void* queries, int64_t B, int k, double* out_sim, int64_t* out_seq,
+                     int32_t* out_len, int32_t* out_count, cudaStream_t st) {
+  if (db->f64)
+    return topk_bigk_t(db, static_cast<const double*>(queries), B, k, out_sim, out_seq, out_len, out_count, st);
+  return topk_bigk_t(db, static_cast<const float*>(queries), B, k, out_sim, out_seq, out_len, out_count, st);
+}
+
 extern "C" int alise_db_topk(alise_db* db, const void* queries, int64_t B, int k, double* out_sim,
                              int64_t* out_seq, int32_t* out_len, int32_t* out_count, void* stream) {
   if (!db || B < 0) return fail(ALISE_EINVAL, "bad topk call");
-  if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
+  if (k < 1 || k > BIGK_MAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", BIGK_MAX);
   cudaStream_t st = S(stream);
   if (B == 0) return ALISE_OK;
   if (db->size == 0) {
     CK(cudaMemsetAsync(out_count, 0, sizeof(int32_t) * B, st));
     return ALISE_OK;
   }
+  if (k > KMAX) return topk_bigk(db, queries, B, k, out_sim, out_seq, out_len, out_count, st);
   int s = topk_scan(db, queries, B, k, st);
   if (s) return s;
   return topk_rescore(db, queries, B, k, nullptr, out_sim, out_seq, out_len, out_count, st);
@@ -468,10 +534,10 @@ extern "C" int alise_db_topk(alise_db* db, const void* queries, int64_t B, int k
 extern "C" int alise_db_topk_scan(alise_db* db, const void* queries, int64_t B, int k, float* out_bound,
                                   void* stream) {
   if (!db || B < 0 || (B > 0 && !out_bound)) return fail(ALISE_EINVAL, "bad topk scan call");
-  if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
+  if (k < 1 || k > BIGK_MAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", BIGK_MAX);
   cudaStream_t st = S(stream);
   if (B == 0) return ALISE_OK;
-  if (db->size == 0) {
+  if (db->size == 0 || k > KMAX) {  // large k: no bound exchange (the rescore runs the exact big-k search)
     db->last_B = B;
     db->last_k = k;
     db->last_q = queries;
@@ -499,6 +565,7 @@ extern "C" int alise_db_topk_rescore(alise_db* db, const void* queries, int64_t 
     CK(cudaMemsetAsync(out_count, 0, sizeof(int32_t) * B, st));
     return ALISE_OK;
   }
+  if (k > KMAX) return topk_bigk(db, queries, B, k, out_sim, out_seq, out_len, out_count, st);
   return topk_rescore(db, queries, B, k, ext_bound, out_sim, out_seq, out_len, out_count, st);
 }
 
@@ -528,7 +595,7 @@ extern "C" int alise_db_kernel_stats(alise_db* db, double* scan_ms, int64_t* lau
 extern "C" int alise_topk_merge(int G, int64_t B, int k, const double* sims, const int64_t* seqs,
                                 const int32_t* lens, const int32_t* counts, double* out_sim, int64_t* out_seq,
                                 int32_t* out_len, int32_t* out_count, void* stream) {
-  if (G < 1 || G > 64 || k < 1 || k > KMAX) return fail(ALISE_EINVAL, "bad merge arguments");
+  if (G < 1 || G > 64 || k < 1 || k > BIGK_MAX) return fail(ALISE_EINVAL, "bad merge arguments");
   if (B == 0) return ALISE_OK;
   k_topk_merge<<<(unsigned)((B + 127) / 128), 128, 0, S(stream)>>>(G, B, k, sims, seqs, lens, counts, out_sim,
                                                                      out_seq, out_len, out_count);
@@ -562,7 +629,7 @@ extern "C" int alise_predict_finish_ex(int64_t B, int k, const double* sims, con
                                        int64_t dim, const double* W1, const double* b1, const double* w2, double b2,
                                        int64_t hidden, int64_t max_len, double log_cap, int32_t* out_len,
                                        uint8_t* out_retrieved, void* stream) {
-  if (k < 1 || k > KMAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", KMAX);
+  if (k < 1 || k > BIGK_MAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", BIGK_MAX);
   if (hidden < 1) return fail(ALISE_EINVAL, "hidden must be >= 1");
   if (queries_dtype != ALISE_DB_F32 && queries_dtype != ALISE_DB_F64) return fail(ALISE_EINVAL, "bad query dtype");
   if (B == 0) return ALISE_OK;

@@ -1616,6 +1616,321 @@ k_exhaustive(int64_t B, int k, int64_t n_rows, int64_t dim, const T* __restrict_
                                     out_count, inexact_count, blas);
 }
 
+// ------------------------------------------------------------------ large k (> KMAX)
+// top_k above the scan's register lists (KMAX) takes a CUDA-core path with the same
+// coarse operands and bound: stage 1 (k_bigk_scan, block = (row split, query)) forms
+// s~ = fp16(q).fp16(v) with one mixed-precision FMA per element (exact fp16 products,
+// fp32 sums: |s~ - s| <= delta_q, k_query_prep's bound, holds for any summation order)
+// and keeps, in a shared-memory buffer, every row with s~ >= (the block's running k-th
+// s~) - 2 delta (a bitonic sort compacts the buffer when it fills); stage 2
+// (k_bigk_select, block per query) takes the largest of the splits' k-th values as the
+// filter (each is <= the global coarse k-th), gathers the surviving rows, narrows to
+// the global coarse k-th, rescores them exactly (the same certified dots / reference
+// BLAS order as k_rescore) and sorts by (-sim, seq).  Heavier than the tcgen05 path
+// (every row's coarse dot on CUDA cores) but exact for any k <= BIGK_MAX.
+constexpr int BIGK_MAX = 1024;
+constexpr int BIGK_BUF = 4096;  // candidates per block (power of two, >= 2 x BIGK_MAX + one round)
+
+// descending bitonic sort of n2 (power of two) keyed entries in shared memory
+template <typename K, typename V, typename Less>
+__device__ void bitonic_desc(K* key, V* val, int n2, Less less) {
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;  // this run sorts descending when up
+        const bool swap = up ? less(key[lo], val[lo], key[hi], val[hi]) : less(key[hi], val[hi], key[lo], val[lo]);
+        if (swap) {
+          const K tk = key[lo];
+          key[lo] = key[hi];
+          key[hi] = tk;
+          const V tv = val[lo];
+          val[lo] = val[hi];
+          val[hi] = tv;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+struct CoarseLess {  // a before b when a's score is larger (ties: smaller row)
+  __device__ bool operator()(float ka, int va, float kb, int vb) const { return ka < kb || (ka == kb && va > vb); }
+};
+
+__global__ void __launch_bounds__(256)
+k_bigk_scan(int64_t n_rows, int64_t dp, int k, int splits, const __half* __restrict__ v16,
+            const __half* __restrict__ q16, const float* __restrict__ two_delta, float* __restrict__ out_s,
+            int32_t* __restrict__ out_r, int32_t* __restrict__ out_n, float* __restrict__ out_kth) {
+  extern __shared__ uint8_t smem_bk[];
+  float* s_key = reinterpret_cast<float*>(smem_bk);
+  int* s_row = reinterpret_cast<int*>(s_key + BIGK_BUF);
+  __shared__ int s_cnt;
+  __shared__ float s_tau, s_kth;
+  const int split = blockIdx.x;
+  const int64_t q = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 3, sub = lane & 7;  // 4 rows per warp step, 8 lanes per row
+  const float NEG = -__int_as_float(0x7f800000);
+  const float td = two_delta[q];
+  const int64_t per = (n_rows + splits - 1) / splits;
+  const int64_t lo = split * per, hi = min(n_rows, lo + per);
+  if (threadIdx.x == 0) {
+    s_cnt = 0;
+    s_tau = NEG;
+    s_kth = NEG;
+  }
+  __syncthreads();
+  const uint4* qv = reinterpret_cast<const uint4*>(q16 + q * dp);
+  const int nv = (int)(dp / 8);  // 16-byte vectors per row
+  // compaction: sort, k-th coarse, keep the entries >= k-th - 2 delta
+  auto compact = [&]() {
+    const int n = s_cnt;
+    int n2 = 2;
+    while (n2 < n) n2 <<= 1;
+    for (int i = n + threadIdx.x; i < n2; i += blockDim.x) {
+      s_key[i] = NEG;
+      s_row[i] = INT32_MAX;
+    }
+    __syncthreads();
+    bitonic_desc(s_key, s_row, n2, CoarseLess());
+    if (threadIdx.x == 0) {
+      if (n >= k) {
+        s_kth = s_key[k - 1];
+        s_tau = fmaxf(s_tau, __fsub_rd(s_kth, td));
+      }
+      int a = 0, b = n;  // sorted descending: first index below tau
+      while (a < b) {
+        const int mid = (a + b) >> 1;
+        if (s_key[mid] >= s_tau) a = mid + 1; else b = mid;
+      }
+      s_cnt = a;
+    }
+    __syncthreads();
+  };
+  constexpr int ROUND = 8 * 4 * 32;  // rows per round: 8 warps x 4 rows x 32 steps
+  for (int64_t r0 = lo; r0 < hi; r0 += ROUND) {
+    const float tau = s_tau;
+    for (int st = 0; st < 32; ++st) {
+      const int64_t r = r0 + (int64_t)st * 32 + warp * 4 + grp;
+      float acc = 0.f;
+      if (r < hi) {
+        const uint4* rv = reinterpret_cast<const uint4*>(v16 + r * dp);
+        constexpr int U = 6;  // 16-byte row chunks in flight per lane (a 768-dim row: 2 batches)
+        for (int j0 = sub; j0 < nv; j0 += 8 * U) {
+          uint4 a[U], b[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = j0 + 8 * u;
+            a[u] = j < nv ? __ldg(rv + j) : make_uint4(0, 0, 0, 0);
+            b[u] = j < nv ? __ldg(qv + j) : make_uint4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t* aw = reinterpret_cast<const uint32_t*>(&a[u]);
+            const uint32_t* bw = reinterpret_cast<const uint32_t*>(&b[u]);
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              const unsigned short a0 = (unsigned short)(aw[w] & 0xffffu), a1 = (unsigned short)(aw[w] >> 16);
+              const unsigned short b0 = (unsigned short)(bw[w] & 0xffffu), b1 = (unsigned short)(bw[w] >> 16);
+              asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc) : "h"(a0), "h"(b0));
+              asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc) : "h"(a1), "h"(b1));
+            }
+          }
+        }
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      if (sub == 0 && r < hi && acc >= tau) {
+        const int at = atomicAdd(&s_cnt, 1);
+        s_key[at] = acc;  // at < BIGK_BUF: compaction leaves room for a round
+        s_row[at] = (int)r;
+      }
+    }
+    __syncthreads();
+    if (s_cnt > BIGK_BUF - ROUND) compact();
+    if (s_cnt > BIGK_BUF - ROUND) break;  // near-ties fill the buffer: reported below
+  }
+  compact();
+  const int n = s_cnt;
+  const bool over = n > BIGK_BUF - ROUND;
+  const size_t base = ((size_t)q * splits + split) * BIGK_BUF;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    out_s[base + i] = s_key[i];
+    out_r[base + i] = s_row[i];
+  }
+  if (threadIdx.x == 0) {
+    out_n[(size_t)q * splits + split] = over ? -1 : n;
+    out_kth[(size_t)q * splits + split] = s_kth;
+  }
+}
+
+struct SimLess {  // a before b when (-sim, seq) is smaller
+  __device__ bool operator()(double ka, int64_t va, double kb, int64_t vb) const {
+    return ka < kb || (ka == kb && va > vb);
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_bigk_select(int64_t n_rows, int64_t dim, int k, int splits, const T* __restrict__ qx, const T* __restrict__ vm,
+              const int32_t* __restrict__ lens, const int64_t* __restrict__ seqs,
+              const float* __restrict__ two_delta, const float* __restrict__ in_s, const int32_t* __restrict__ in_r,
+              const int32_t* __restrict__ in_n, const float* __restrict__ in_kth, double* __restrict__ out_sim,
+              int64_t* __restrict__ out_seq, int32_t* __restrict__ out_len, int32_t* __restrict__ out_count,
+              int32_t* __restrict__ overflow, unsigned int* __restrict__ inexact_count, const BlasRef blas) {
+  extern __shared__ uint8_t smem_bs[];
+  float* s_key = reinterpret_cast<float*>(smem_bs);
+  int* s_row = reinterpret_cast<int*>(s_key + BIGK_BUF);
+  double* s_sim = reinterpret_cast<double*>(s_row + BIGK_BUF);
+  int64_t* s_seq = reinterpret_cast<int64_t*>(s_sim + BIGK_BUF);
+  __shared__ float s_tau;
+  __shared__ int s_cnt, s_bad;
+  const int64_t q = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float NEG = -__int_as_float(0x7f800000);
+  const float td = two_delta[q];
+  const int kk = (int)(k < n_rows ? k : n_rows);
+  if (threadIdx.x == 0) {
+    float t = NEG;
+    int bad = 0;
+    for (int sp = 0; sp < splits; ++sp) {
+      t = fmaxf(t, in_kth[(size_t)q * splits + sp]);
+      bad |= in_n[(size_t)q * splits + sp] < 0;
+    }
+    s_tau = t > NEG ? __fsub_rd(t, td) : NEG;
+    s_cnt = 0;
+    s_bad = bad || !(td <= 3.0e38f);
+  }
+  __syncthreads();
+  if (s_bad) {  // near-ties overflowed a split's buffer, or rows outside the fp16 range
+    if (threadIdx.x == 0) {
+      out_count[q] = 0;
+      atomicOr(overflow, 1);
+    }
+    return;
+  }
+  // the global coarse kk-th over the splits' entries (each split's k-th is only a lower
+  // bound of it: with many small splits the union above it holds ~k x splits entries):
+  // radix select, 8 bits per pass, on the order-preserving key
+  {
+    __shared__ int s_hist[256];
+    __shared__ uint32_t s_prefix, s_mask;
+    __shared__ int s_rem, s_total;
+    if (threadIdx.x == 0) {
+      s_prefix = 0;
+      s_mask = 0;
+      s_rem = kk;
+      s_total = 0;
+    }
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      s_hist[threadIdx.x] = 0;  // blockDim.x == 256
+      __syncthreads();
+      const uint32_t pre = s_prefix, msk = s_mask;
+      for (int sp = warp; sp < splits; sp += blockDim.x >> 5) {  // a warp per split
+        const int n = in_n[(size_t)q * splits + sp];
+        const size_t base = ((size_t)q * splits + sp) * BIGK_BUF;
+        for (int i = lane; i < n; i += 32) {
+          const float v = in_s[base + i];
+          const uint32_t key = ord_key(v);
+          if (v >= s_tau && (key & msk) == pre) atomicAdd(&s_hist[(key >> shift) & 255], 1);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (shift == 24)
+          for (int d = 0; d < 256; ++d) s_total += s_hist[d];  // entries >= the filter
+        int cum = 0, dgt = 255;
+        for (; dgt > 0; --dgt) {
+          if (cum + s_hist[dgt] >= s_rem) break;
+          cum += s_hist[dgt];
+        }
+        s_prefix = pre | ((uint32_t)dgt << shift);
+        s_mask = msk | (255u << shift);
+        s_rem -= cum;
+      }
+      __syncthreads();
+    }
+    // fewer than kk entries above the filter: every one is a candidate (tau unchanged)
+    if (threadIdx.x == 0 && s_total >= kk) s_tau = fmaxf(s_tau, __fsub_rd(ord_val(s_prefix), td));
+    __syncthreads();
+  }
+  // gather the splits' entries above the filter
+  for (int sp = warp; sp < splits; sp += blockDim.x >> 5) {  // a warp per split
+    const int n = in_n[(size_t)q * splits + sp];
+    const size_t base = ((size_t)q * splits + sp) * BIGK_BUF;
+    for (int i = lane; i < n; i += 32) {
+      const float v = in_s[base + i];
+      if (v >= s_tau) {
+        const int at = atomicAdd(&s_cnt, 1);
+        if (at < BIGK_BUF) {
+          s_key[at] = v;
+          s_row[at] = in_r[base + i];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  int n = s_cnt;
+  if (n > BIGK_BUF) {
+    if (threadIdx.x == 0) {
+      out_count[q] = 0;
+      atomicOr(overflow, 1);
+    }
+    return;
+  }
+
+  // exact float64 scores (as k_rescore), then (-sim, seq) order
+  if (blas.on) {
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      const int row = s_row[c];
+      const int64_t sq = seqs[row];
+      s_sim[c] = blas_dot<T>(vm + (size_t)row * dim, qx + q * dim, dim,
+                             blas_kind(sq % blas.ref_cap, blas.ref_n, dim, blas.threads));
+      s_seq[c] = sq;
+    }
+  } else {
+    for (int c = warp; c < n; c += blockDim.x >> 5) {
+      const int row = s_row[c];
+      bool ok;
+      double sim = warp_exact_dot<8, T>(vm + (size_t)row * dim, qx + q * dim, dim, ok);
+      if (!ok) {
+        sim = warp_exact_dot_fallback(vm + (size_t)row * dim, qx + q * dim, dim);
+        if (lane == 0) atomicAdd(inexact_count, 1u);
+      }
+      if (lane == 0) {
+        s_sim[c] = sim;
+        s_seq[c] = seqs[row];
+      }
+    }
+  }
+  for (int i = n + threadIdx.x; i < BIGK_BUF; i += blockDim.x) {
+    s_sim[i] = -__longlong_as_double(0x7ff0000000000000ll);
+    s_seq[i] = INT64_MAX;
+  }
+  __syncthreads();
+  int n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  // s_row travels with the order through the seq -> row map: sort (sim, seq), then find
+  // each output's row by its (unique) seq among the candidates
+  bitonic_desc(s_sim, s_seq, n2 < 2 ? 2 : n2, SimLess());
+  const int outn = n < kk ? n : kk;
+  for (int i = threadIdx.x; i < outn; i += blockDim.x) {
+    out_sim[q * k + i] = s_sim[i];
+    out_seq[q * k + i] = s_seq[i];
+  }
+  // lengths: rows are looked up by seq (slot = the candidate whose seq matches)
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const int row = s_row[c];
+    const int64_t sq = seqs[row];
+    for (int i = 0; i < outn; ++i)
+      if (s_seq[i] == sq) out_len[q * k + i] = lens[row];
+  }
+  if (threadIdx.x == 0) out_count[q] = outn;
+}
+
 // ------------------------------------------------------------------ shard merge
 // G per-shard sorted lists [G][B][k] -> global top-k by (-sim, seq).  Thread per query.
 __global__ void k_topk_merge(int G, int64_t B, int k, const double* __restrict__ sims, const int64_t* __restrict__ seqs,
@@ -1651,22 +1966,30 @@ __global__ void k_topk_merge(int G, int64_t B, int k, const double* __restrict__
 }
 
 // ------------------------------------------------------------------ finish
-// numpy's reduction order for a contiguous float64 array (n < 8: sequential from 0.0;
-// n >= 8: 8 accumulators, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the remainder).
-__device__ double np_sum(const double* v, int n) {
+// numpy's pairwise summation of a contiguous float64 array (pairwise_sum_DOUBLE): n < 8
+// sequential from 0.0; n <= 128: 8 accumulators, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+// then the remainder; above 128 the halves (split at n/2 rounded down to a multiple of 8)
+// are summed recursively.  v(i) returns element i.
+template <typename F>
+__device__ double np_sum_f(const F& v, int lo, int n) {
   if (n < 8) {
     double r = 0.0;
-    for (int i = 0; i < n; ++i) r = __dadd_rn(r, v[i]);
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, v(lo + i));
     return r;
   }
+  if (n > 128) {
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return __dadd_rn(np_sum_f(v, lo, n2), np_sum_f(v, lo + n2, n - n2));
+  }
   double r[8];
-  for (int j = 0; j < 8; ++j) r[j] = v[j];
+  for (int j = 0; j < 8; ++j) r[j] = v(lo + j);
   int i = 8;
   for (; i + 8 <= n; i += 8)
-    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v[i + j]);
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v(lo + i + j));
   double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < n; ++i) res = __dadd_rn(res, v[i]);
+  for (; i < n; ++i) res = __dadd_rn(res, v(lo + i));
   return res;
 }
 
@@ -1735,25 +2058,22 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
 #ifdef ALISE_FINISH_TIMING
   F1 = clock64();
 #endif
+  // retrieval branch: the list is sorted by (-sim, seq), so the qualifying neighbours
+  // (sim >= s0) are a prefix of it; sums over them in numpy's order
   const int c = counts[q];
+  const double* sq = sims + q * k;
+  const int32_t* lq = lens + q * k;
   int nq = 0;
-  double w[KMAX], prod[KMAX], vals[KMAX];
-  for (int i = 0; i < c; ++i) {
-    const double s = sims[q * k + i];
-    if (s >= s0) {
-      const double wi = s < 0.0 ? 0.0 : s;  // np.clip(.., 0, None)
-      vals[nq] = (double)lens[q * k + i];
-      w[nq] = wi;
-      prod[nq] = __dmul_rn(wi, vals[nq]);
-      ++nq;
-    }
-  }
+  while (nq < c && sq[nq] >= s0) ++nq;
   if (nq > 0) {
     if (lane == 0) {
-      const double ws = np_sum(w, nq);
+      auto w = [&](int i) { const double v = sq[i]; return v < 0.0 ? 0.0 : v; };  // np.clip(.., 0, None)
+      auto val = [&](int i) { return (double)lq[i]; };
+      auto prod = [&](int i) { return __dmul_rn(w(i), val(i)); };
+      const double ws = np_sum_f(w, 0, nq);
       double pred;
-      if (ws > 0.0) pred = __ddiv_rn(np_sum(prod, nq), ws);
-      else pred = __ddiv_rn(np_sum(vals, nq), (double)nq);
+      if (ws > 0.0) pred = __ddiv_rn(np_sum_f(prod, 0, nq), ws);
+      else pred = __ddiv_rn(np_sum_f(val, 0, nq), (double)nq);
       double r = rint(pred);
       r = fmin(fmax(r, 1.0), (double)max_len);
       out_len[q] = (int32_t)r;

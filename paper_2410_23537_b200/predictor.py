@@ -41,7 +41,7 @@ _MASK64 = 0xFFFFFFFFFFFFFFFF
 FALLBACK_INIT = 4  # rng.py stream tag
 RETRIEVED = "retrieved"
 FALLBACK = "fallback"
-MAX_K = 16
+MAX_K = 1024  # k <= 16: tcgen05 scan path; 16 < k <= 1024: CUDA-core coarse pass (alise_db_topk)
 
 
 class PredictorError(ValueError):
@@ -82,7 +82,7 @@ class PredictorConfig:
             if not ok:
                 raise PredictorError(msg)
         if self.top_k > MAX_K:
-            raise PredictorError(f"top_k must be <= {MAX_K} on the GPU path")
+            raise PredictorError(f"top_k must be <= {MAX_K}")
 
 
 def _fnv1a(data: bytes) -> int:
@@ -639,8 +639,9 @@ class LengthPredictor:
         """Serve predict_vector (one request) by replaying a CUDA graph of the whole
         per-request path: query upload, prep, tcgen05 scan, rescoring, finish and the
         result download become one graph launch (re-captured when the DB size or the
-        fallback weights change)."""
-        self._graph = _GraphedRequest(self) if on else None
+        fallback weights change).  top_k > 16 (the CUDA-core search, which synchronises to
+        report near-tie overflow) stays eager."""
+        self._graph = _GraphedRequest(self) if on and self.config.top_k <= 16 else None
 
     def predict_vector(self, vector) -> tuple:
         """Predict from an already-embedded prompt; returns (length, provenance)."""

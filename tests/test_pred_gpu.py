@@ -260,6 +260,8 @@ def _sharded_worker(rank, world, port, result_dir, backend="gloo"):
     store.add_batch(db[2500:], lens[2500:])
     live = np.arange(n - cap, n)
     same("fp32", *store.search_batch(Q, k)[:4], po.search_exact_batch(db[live], lens[live], live, Q, k))
+    # top_k > 16: each shard's exact big-k search, gathered and merged
+    same("k40", *store.search_batch(Q[:20], 40)[:4], po.search_exact_batch(db[live], lens[live], live, Q[:20], 40))
     # empty query batch (the rescore of an empty scan)
     out = store.search_batch(np.zeros((0, d), np.float32), k)
     if out[0].shape != (0, k):
@@ -710,3 +712,52 @@ def test_blas_order_search_with_heavy_ties(pr, n, cap, d):
     lens = g.integers(1, 2048, size=n)
     Q = np.stack([emb.embed(stems[i % 12] + [50_001, 50_003]) for i in range(48)])
     _check_blas(pr, rows, lens, Q, 8, cap)
+
+
+# ----------------------------------------------------------------- top_k > 16
+@pytest.mark.parametrize("k,n,dtype", [(17, 5000, np.float32), (64, 5000, np.float64), (300, 20000, np.float32),
+                                       (1024, 3000, np.float32), (40, 25, np.float32)])
+def test_large_k_vs_oracle(pr, k, n, dtype):
+    """top_k above the scan's register lists (the CUDA-core coarse pass + exact select):
+    seqs / sims / lens bit-exact vs the oracle, incl. planted 11-way duplicate groups
+    straddling the k-boundary and a DB smaller than k."""
+    g = np.random.default_rng(k + n)
+    d, B = 96, 40
+    db = g.standard_normal((n, d))
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    if n > 100:
+        for grp in range(4):
+            db[n // 2 + 11 * grp: n // 2 + 11 * grp + 11] = db[grp]
+    if dtype == np.float32:
+        db = db.astype(np.float32)
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = np.concatenate([db[[0, 1, 2, 3]] + 1e-4 * g.standard_normal((4, d)), g.standard_normal((B - 4, d))])
+    Q = Q / np.linalg.norm(Q, axis=1, keepdims=True)
+    check_batch(pr, db, lens, Q.astype(dtype), k, dtype=dtype)
+
+
+def test_large_k_predict_batch(pr):
+    """predict_batch with top_k = 32 and 200: retrieval aggregates over up to k neighbours
+    (numpy pairwise sums above 128 terms), else the MLP; equal to the oracle."""
+    g = np.random.default_rng(77)
+    n, d = 6000, 64
+    db = g.standard_normal((n, d)).astype(np.float32)
+    db /= np.linalg.norm(db, axis=1, keepdims=True)
+    db[3000:3300] = db[7]  # 300 identical rows: 200 qualifying neighbours for some queries
+    lens = g.integers(1, 2048, size=n).astype(np.int32)
+    Q = np.concatenate([db[[7, 8, 9]] + 1e-3 * g.standard_normal((3, d)).astype(np.float32),
+                        g.standard_normal((37, d)).astype(np.float32)])
+    Q = (Q / np.linalg.norm(Q, axis=1, keepdims=True)).astype(np.float32)
+    reg = pr.FallbackRegressor(d, 32, seed=2)
+    reg.b2 = 4.0
+    store = pr.VectorStore(d, 8192, dtype=np.float32)
+    store.add_batch(db, lens)
+    for k in (32, 200):
+        p = pr.LengthPredictor(pr.PredictorConfig(dimension=d, db_capacity=8192, top_k=k), regressor=reg,
+                               store=store)
+        out, ret = p.predict_batch(Q)
+        ref_len, ref_ret = po.predict_batch(db, lens, np.arange(n), Q, reg.w1, reg.b1, reg.w2, reg.b2, k=k)
+        assert np.array_equal(out.cpu().numpy(), ref_len)
+        assert np.array_equal(ret.cpu().numpy().astype(bool), ref_ret)
+        assert 0 < ref_ret.sum() < len(Q)
+        assert p.predict_vector(Q[0])[0] == ref_len[0]
