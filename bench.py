@@ -463,27 +463,30 @@ def _kv_bench(args, world, rank, local, layouts=None, e2e=True):
             mstate.bind(j, kv, layout)
             mstate.reserve_gpu(gpu_b)
 
-        def e2e_step():
+        def e2e_run(steps):
+            """steps x (offload + upload of every job) as one continuous pipeline through the
+            public API: offload job g while job g-1 (offloaded) is uploaded; each upload is
+            issued as soon as its offload completes, before waiting on the previous upload,
+            so both link directions always have the next transfer queued."""
             n = len(kvs)
-            pend_up = None
+            total = steps * n
+            offs, ups = {}, {}
             now = 0
-            for j in range(n + 1):
-                off = mstate.start_offload(j, link_acc, gpu_b, now) if j < n else None
-                if j > 0:
-                    mstate.complete(prev_off)
-                    if pend_up is not None:
-                        mstate.complete(pend_up)
-                    pend_up = mstate.start_upload(j - 1, link_acc, gpu_b, now)
-                prev_off = off
-            mstate.complete(pend_up)
+            for g in range(total + 2):
+                if g < total:
+                    offs[g] = mstate.start_offload(g % n, link_acc, gpu_b, now)
+                if 1 <= g <= total:
+                    mstate.complete(offs.pop(g - 1))
+                    ups[g - 1] = mstate.start_upload((g - 1) % n, link_acc, gpu_b, now)
+                if 2 <= g <= total + 1:
+                    mstate.complete(ups.pop(g - 2))
             torch.cuda.synchronize()
 
-        e2e_step()  # warm (allocates the pool)
+        e2e_run(1)  # warm (allocates the pool)
         barrier(world)
         torch.cuda.synchronize()
         ta = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            e2e_step()
+        e2e_run(args.e2e_steps)
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - ta, world)
         res["e2e"] = {"value": fp16_bytes_all * args.e2e_steps / e2e_s / 1e9, "unit": "GB/s",
