@@ -17,6 +17,9 @@
 // codes with a proven exactness window, 64/32-bit coalesced stores.  HBM traffic =
 // 2 B read + b/8 B written per element + 4 B per row (transfer slabs: fp16 min/max) or
 // 12-16 B per row (drop-in API: float64 scale + zero).
+// CHANNEL / HEAD kinds: k_quant_cols_cl, one HBM pass through a thread-block cluster
+// (DSMEM combine of per-CTA column min/max); k_quant_cols (two passes) beyond its
+// shared-memory reach.
 // Other shapes use a three-phase path: partial min/max -> per-row params -> codes.
 #include <cuda_fp16.h>
 #include <stdint.h>

@@ -481,3 +481,56 @@ def test_cols_ragged_tokens_through_host(km, kind, bits, packed, T):
     finally:
         eng.close()
         pool.close()
+
+
+# ----------------------------------------------------------------- snap-loop cycles
+@pytest.mark.parametrize("bits,group", [(4, 64), (8, 128), (8, 64)])
+def test_snap_loop_cycles_match_the_reference_loop(km, bits, group):
+    """Rows whose snap loop never settles (2-, 3- and 4-cycles, ~0.7% of real-valued
+    rows) end at the reference's 32nd iterate: the kernels read it off the detected
+    cycle (qmath.cuh snap_scale).  The rows are selected on the host by running the
+    reference's loop and kept only if still moving after 8 passes; they go through the
+    drop-in quantize (tile kernel), the transfer slab (k_expand_params on upload) and
+    must equal the oracle (plain 32-pass loop) bit for bit."""
+    import torch
+
+    from harness import synthetic
+    kv = synthetic.kv_job(8, 256, 1024, seed=bits + group, job=4, group=group)
+    x = kv.reshape(-1, group).astype(np.float64)
+    q = float(2 ** bits - 1)
+    mn, mx = x.min(1), x.max(1)
+    live = mx != mn
+    s = np.where(live, (mx - mn) / q, 1.0)
+    z = np.where(live, np.rint(-mn / s), -mn)
+    for _ in range(8):
+        s = np.where(live, (s * (q - z) - s * (0.0 - z)) / q, 1.0)
+    s9 = np.where(live, (s * (q - z) - s * (0.0 - z)) / q, 1.0)
+    moving = np.flatnonzero(live & (s9 != s))
+    assert len(moving) > 20, len(moving)
+    rows = x[moving]
+    qt = km.quantize(rows, bits)
+    c, sc, zc = ko.quantize_rows(rows, bits)
+    assert np.array_equal(qt.scale, sc) and np.array_equal(qt.zero, zc) and np.array_equal(qt.values, c)
+    # through a transfer slab (fp16 (min, max) -> k_expand_params on upload)
+    L, T = 1, 2 * len(moving) // (1024 // group) + 2
+    T = (T + 1) // 2 * 2
+    plane = np.zeros((L, 2, T, 1024), dtype=np.float16)
+    flat = plane.reshape(-1, group)
+    flat[:len(moving)] = rows.astype(np.float16)
+    lay = km.KVLayout(L, T, 1024, 128, kind="rows", group=group, bits=bits, packed=bits == 4)
+    g = lay.geometry()
+    pool = km.HostSlabPool(g["slab_bytes"] + 4096)
+    eng = km.KVSwapEngine()
+    try:
+        src = torch.from_numpy(plane).cuda()
+        addr = pool.alloc(g["slab_bytes"])
+        eng.offload(lay, src, addr)
+        out = torch.zeros_like(src)
+        eng.upload(lay, addr, out)
+        torch.cuda.synchronize()
+        c4, s4, z4 = ko.quantize_rows(flat.astype(np.float64), bits)
+        ref = ko.dequantize_rows(c4, s4, z4).astype(np.float16).reshape(plane.shape)
+        assert np.array_equal(out.cpu().numpy(), ref)
+    finally:
+        eng.close()
+        pool.close()
