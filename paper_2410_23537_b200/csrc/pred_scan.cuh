@@ -2118,16 +2118,14 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
     F2 = clock64();
 #endif
     // sequential sum over the chunk's hidden units in index order (every lane)
-    const int64_t jn = hidden - j0 < 128 ? hidden - j0 : 128;
-    for (int64_t jj = 0; jj < jn; ++jj) {
-      const int t = (int)(jj / 32), src = (int)(jj % 32);
-      double hj = 0.0;
+    const int jn = (int)(hidden - j0 < 128 ? hidden - j0 : 128);
 #pragma unroll
-      for (int tt = 0; tt < 4; ++tt) {
-        const double v = __shfl_sync(0xffffffffu, hv[tt], src);
-        if (tt == t) hj = v;
+    for (int t = 0; t < 4; ++t) {  // hv[t] stays a static register: one shuffle per unit
+      const int cnt = jn - 32 * t < 32 ? jn - 32 * t : 32;
+      for (int src = 0; src < cnt; ++src) {
+        const double hj = __shfl_sync(0xffffffffu, hv[t], src);
+        out = __dadd_rn(out, __dmul_rn(hj, w2[j0 + 32 * t + src]));
       }
-      out = __dadd_rn(out, __dmul_rn(hj, w2[j0 + jj]));
     }
   }
   if (lane == 0) {
