@@ -261,11 +261,47 @@ class VectorStore:
         v = torch.as_tensor(vectors if isinstance(vectors, torch.Tensor) else np.asarray(vectors))
         return v.to(self._dev(), _torch_dtype(self._code)).reshape(-1, self.dimension).contiguous()
 
+    _STAGE_SLOTS = 32
+
     def add(self, vector, observed_len: int) -> int:
+        """VectorStore.add (predictor.py:135-152): one record, appended without a host
+        synchronisation -- the vector, length and sequence number are packed into a
+        pinned staging slot, copied with one async H2D on the current stream and
+        appended by the ring kernel (a slot is reused once its copy has completed)."""
+        import torch
+
         if observed_len < 1:
             raise PredictorError("observed_len must be >= 1")
+        v = np.asarray(vector, dtype=np.float64).reshape(-1)
+        if v.size != self.dimension:
+            raise PredictorError("vector has the wrong dimension")
         seq = self.next_seq
-        self.add_batch(np.asarray(vector, dtype=np.float64)[None, :], [int(observed_len)])
+        if getattr(self, "_stage_h", None) is None:
+            esz = 8 if self._code == DB_F64 else 4
+            self._stage_vb = (self.dimension * esz + 15) // 16 * 16
+            nb = self._stage_vb + 16
+            self._stage_h = torch.empty((self._STAGE_SLOTS, nb), dtype=torch.uint8).pin_memory()
+            self._stage_d = torch.empty((self._STAGE_SLOTS, nb), dtype=torch.uint8, device=self._dev())
+            self._stage_ev = [None] * self._STAGE_SLOTS
+            self._stage_i = 0
+        r = self._stage_i
+        self._stage_i = (r + 1) % self._STAGE_SLOTS
+        if self._stage_ev[r] is not None:
+            self._stage_ev[r].synchronize()  # the slot's previous copy has left the host buffer
+        hv = self._stage_h[r].numpy()
+        vb = self._stage_vb
+        hv[:vb].view(np.float64 if self._code == DB_F64 else np.float32)[: self.dimension] = v
+        hv[vb:vb + 4].view(np.int32)[0] = int(observed_len)
+        hv[vb + 8:vb + 16].view(np.int64)[0] = seq
+        dv = self._stage_d[r]
+        dv.copy_(self._stage_h[r], non_blocking=True)
+        if self._stage_ev[r] is None:
+            self._stage_ev[r] = torch.cuda.Event()
+        self._stage_ev[r].record()
+        base = dv.data_ptr()
+        _lib.call("alise_db_append", self._h, base, base + vb, base + vb + 8, 1, _lib.stream_ptr())
+        self.next_seq += 1
+        self.size = min(self.capacity, self.size + 1)
         return seq
 
     def add_batch(self, vectors, lens, stream=None, seqs=None):
