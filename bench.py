@@ -54,14 +54,14 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-planes", type=int, default=16)
+    ap.add_argument("--cpu-planes", type=int, default=64, help="CPU baseline sample (~20 core-seconds)")
     ap.add_argument("--no-pred", action="store_true")
     ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--pred-n", type=int, default=1_000_000)
     ap.add_argument("--pred-b", type=int, default=4096)
     ap.add_argument("--pred-dim", type=int, default=768)
-    ap.add_argument("--pred-cpu-queries", type=int, default=16)
+    ap.add_argument("--pred-cpu-queries", type=int, default=64)
     ap.add_argument("--pred-parity", type=int, default=128, help="queries checked against the oracle after timing")
     ap.add_argument("--no-parity", action="store_true")
     return ap.parse_args()
