@@ -420,18 +420,15 @@ static int topk_rescore_t(alise_db* db, const T* queries, int64_t B, int k, cons
   CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
   // small batches are latency bound (one DRAM round trip per candidate row), large ones
   // throughput bound (registers / occupancy)
+  // (large batches: 128-thread blocks capped at 64 registers keep 8 queries in flight
+  // per SM; k_rescore's launch bounds fix the block sizes)
   auto rescore = B <= 512 ? k_rescore<24, T> : k_rescore<8, T>;
-  static int rthreads = -1;
-  if (rthreads < 0) {
-    const char* e = getenv("ALISE_RESCORE_THREADS");
-    rthreads = e ? atoi(e) : 128;
-  }
-  // large batches: smaller blocks keep more queries in flight per SM
+  const int rthreads = B <= 512 ? 256 : 128;
   const BlasRef br = blas_ref(db);
   // the longest top-list union a query can have: nh x (largest split count) x k
   const int max_splits = std::max(a.G, a.E > 0 ? a.G - 1 + (grp_len_host(a.n_tiles, a.G, a.G - 1) + a.C - 1) / a.C : 0);
   const int top_cap = (int)std::min<int64_t>(4096, (int64_t)nh * max_splits * k);
-  rescore<<<(unsigned)B, B <= 512 ? 256 : rthreads, top_cap * sizeof(float), st>>>(
+  rescore<<<(unsigned)B, rthreads, top_cap * sizeof(float), st>>>(
       qblk, nh, a, (int)Bp, B, k, db->size, db->dim, queries, vm, db->lens, db->seqs, db->two_delta, db->cand_s,
       db->cand_r, db->cand_n, db->topc, ext, out_sim, out_seq, out_len, out_count, db->need, db->inexact, br, top_cap);
   CKL();
