@@ -1380,7 +1380,23 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
     if (lane == 0) s_off[0] = 0;
   }
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 0 && mt <= 32) {
+    // up to 32 values (the common case: about k of them reach the bound): one bitonic
+    // sort across the lanes (15 shuffle stages instead of kk argmax rounds)
+    float v = lane < mt ? s_top[lane] : NEG;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const float o = __shfl_xor_sync(0xffffffffu, v, stride);
+        const bool desc = (lane & size) == 0 || size == 32;  // this run sorts descending
+        const bool low = (lane & stride) == 0;
+        v = (low == desc) ? fmaxf(v, o) : fminf(v, o);
+      }
+    }
+    const float kth = __shfl_sync(0xffffffffu, v, (int)kk - 1);
+    if (lane == 0) s_kth = kth;
+  } else if (warp == 0) {
     float* src = one_warp ? s_top : s_wk;
     const int mw = one_warp ? mt : (int)(blockDim.x >> 5) * (int)kk;
     float kth = NEG;
@@ -1439,7 +1455,14 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
     for (int u = 0; u < 8; ++u) {
       if (sv[u] >= thr) {
         const int slot = atomicAdd(&s_n, 1);
-        if (slot < MAXC) s_rows[slot] = rv[u];
+        if (slot < MAXC) {
+          s_rows[slot] = rv[u];
+          // start the candidate row's DRAM fetch now (random DB row; the dots read it
+          // after the block barrier)
+          const char* rp = reinterpret_cast<const char*>(vm + (size_t)rv[u] * dim);
+          for (int64_t off = 0; off < dim * (int64_t)sizeof(T); off += 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + off));
+        }
       }
     }
   }
