@@ -1299,8 +1299,13 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   // per-query scalars the later phases need, loaded now so they arrive with the lists
   const float td = two_delta[q];
   const float ext_q = ext ? ext[q] : NEG;
+  // With an all-reduced bound from the shards (ext, an exact-score lower bound of the
+  // global k-th), rows below ext - delta cannot enter the global top-k and the shard's
+  // own coarse k-th is not needed (ext is at least this shard's own bound): the list
+  // staging and selection are skipped.
+  const bool use_ext = ext_q > NEG;
   float L = NEG;
-  {
+  if (!use_ext) {
     const uint32_t g0 = wa.gkth[q];
     if (g0) L = ord_val(g0);
     uint32_t mn = 0xffffffffu;
@@ -1309,7 +1314,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   }
   if (tid == 0) { s_n = 0; s_flag = 0; s_nt = 0; }
   __syncthreads();
-  for (int i0 = tid; i0 < m; i0 += 8 * blockDim.x) {
+  for (int i0 = tid; i0 < (use_ext ? 0 : m); i0 += 8 * blockDim.x) {
     float tv[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {  // 8 loads in flight per thread
