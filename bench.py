@@ -650,6 +650,24 @@ def cpu_pred_sample(args, n_queries: int):
     W1 = g.uniform(-0.08, 0.08, size=(D, 32))
     b1 = np.zeros(32)
     w2 = g.uniform(-0.08, 0.08, size=32)
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "servesim")):
+        # the reference's own predictor (servesim from the offline install): its VectorStore
+        # filled through its add() (setup, not timed), predict_vector per query timed
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        from servesim import predictor as rp
+        store = rp.VectorStore(D, N)
+        for i in range(N):
+            store.add(db64[i], int(lens[i]))
+        reg = rp.FallbackRegressor(D, 32, seed=0)
+        reg.w1, reg.b1, reg.w2, reg.b2 = W1, b1, w2, 5.0
+        lp = rp.LengthPredictor(rp.PredictorConfig(dimension=D, db_capacity=N), regressor=reg, store=store)
+        t0 = time.perf_counter()
+        for q in Q:
+            lp.predict_vector(q.astype(np.float64))
+        wall = time.perf_counter() - t0
+        return {"qps": n_queries / wall, "wall_s": wall, "cores": os.cpu_count() or 1, "kind": "reference"}
     t0 = time.perf_counter()
     for q in Q:
         sims = db64 @ q.astype(np.float64)              # the reference's scan
@@ -660,7 +678,7 @@ def cpu_pred_sample(args, n_queries: int):
         if a is None:
             pred_oracle.mlp_predict_len(q[None].astype(np.float64), W1, b1, w2, 5.0, 2048)
     wall = time.perf_counter() - t0
-    return {"qps": n_queries / wall, "wall_s": wall, "cores": os.cpu_count() or 1}
+    return {"qps": n_queries / wall, "wall_s": wall, "cores": os.cpu_count() or 1, "kind": "port"}
 
 
 # ----------------------------------------------------------------- main
@@ -922,8 +940,12 @@ def main():
             if cpu_pred is not None:
                 out["predictor"]["cpu_baseline"] = {
                     "value": round(cpu_pred["qps"], 3), "unit": "queries/s", "cores": cpu_pred["cores"],
-                    "kind": "port", "sample": f"{args.pred_cpu_queries} queries vs the full {args.pred_n} x "
-                                              f"{args.pred_dim} float64 DB (BLAS gemv scan, predictor.py:158)"}
+                    "kind": cpu_pred["kind"],
+                    "sample": (f"{args.pred_cpu_queries} queries vs the full {args.pred_n} x {args.pred_dim} float64 DB: "
+                               + ("servesim.predictor.LengthPredictor.predict_vector from baseline/_ref "
+                                  "(predictor.py:311-325, BLAS gemv scan predictor.py:158)"
+                                  if cpu_pred["kind"] == "reference"
+                                  else "oracle port of predictor.py:154-163 + aggregate/MLP (BLAS gemv scan)"))}
         if cpu is not None:
             out["cpu_baseline"] = {"value": round(cpu["GBps"], 4), "unit": "GB/s", "cores": cpu["cores"],
                                    "kind": cpu["kind"],
