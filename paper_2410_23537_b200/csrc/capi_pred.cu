@@ -300,10 +300,12 @@ static int topk_scan(alise_db* db, const void* queries, int64_t B, int k, cudaSt
   if (s) return s;
   if (db->f64)
     k_query_prep<double><<<(unsigned)Bp, 128, 0, st>>>(static_cast<const double*>(queries), B, db->dim, db->dp,
-                                                       db->vmax, db->q16, db->two_delta, db->blas.on);
+                                                       db->vmax, db->q16, db->two_delta, db->blas.on, db->gkth,
+                                                       db->need);
   else
     k_query_prep<float><<<(unsigned)Bp, 128, 0, st>>>(static_cast<const float*>(queries), B, db->dim, db->dp,
-                                                      db->vmax, db->q16, db->two_delta, db->blas.on);
+                                                      db->vmax, db->q16, db->two_delta, db->blas.on, db->gkth,
+                                                      db->need);
   CKL();
   ScanArgs a;
   a.n_kb = (int)(db->dp / BK);
@@ -336,7 +338,7 @@ static int topk_scan(alise_db* db, const void* queries, int64_t B, int k, cudaSt
   a.slot_m = (k + G * nh - 1) / (G * nh);
   // long groups warm up early in their run: one exchange per tile is enough
   a.sync_tile = n_tiles / G >= 256 ? 1 : 0;
-  CK(cudaMemsetAsync(db->gkth, 0, sizeof(uint32_t) * Bp * (1 + KMAX), st));
+  // (gkth, the rank slots and the exhaustive flags were cleared by k_query_prep)
   static bool attr_set[5] = {false, false, false, false, false};
   const int kt = two_sm ? (k <= 8 ? (nh == 2 ? 4 : 2) : 3) : (k <= 8 ? 0 : 1);
   if (!attr_set[kt]) {
@@ -417,7 +419,7 @@ static int topk_rescore_t(alise_db* db, const T* queries, int64_t B, int k, cons
   const int qblk = db->last_qblk, nh = db->last_nh;
   const int64_t Bp = a.Bp;
   const T* vm = static_cast<const T*>(db->vm);
-  CK(cudaMemsetAsync(db->need, 0, sizeof(int32_t) * B, st));
+
   // small batches are latency bound (one DRAM round trip per candidate row), large ones
   // throughput bound (registers / occupancy)
   // (large batches: 128-thread blocks capped at 64 registers keep 8 queries in flight
@@ -432,9 +434,12 @@ static int topk_rescore_t(alise_db* db, const T* queries, int64_t B, int k, cons
       qblk, nh, a, (int)Bp, B, k, db->size, db->dim, queries, vm, db->lens, db->seqs, db->two_delta, db->cand_s,
       db->cand_r, db->cand_n, db->topc, ext, out_sim, out_seq, out_len, out_count, db->need, db->inexact, br, top_cap);
   CKL();
-  k_exhaustive<T><<<(unsigned)((B + 255) / 256), 256, 0, st>>>(B, k, db->size, db->dim, queries, vm, db->lens, db->seqs, db->need,
-                                               out_sim, out_seq, out_len, out_count, db->inexact, br);
-  CKL();
+  if (B > 512) {  // (small batches ran the exhaustive path inside k_rescore)
+    k_exhaustive<T><<<(unsigned)((B + 255) / 256), 256, 0, st>>>(B, k, db->size, db->dim, queries, vm, db->lens,
+                                                                 db->seqs, db->need, out_sim, out_seq, out_len,
+                                                                 out_count, db->inexact, br);
+    CKL();
+  }
   return ALISE_OK;
 }
 
@@ -457,7 +462,7 @@ static int topk_bigk_t(alise_db* db, const T* queries, int64_t B, int k, double*
   int s = ensure_scratch(db, Bp, 1, st);
   if (s) return s;
   k_query_prep<T><<<(unsigned)Bp, 128, 0, st>>>(queries, B, db->dim, db->dp, db->vmax, db->q16, db->two_delta,
-                                                db->blas.on);
+                                                db->blas.on, nullptr, nullptr);
   CKL();
   // enough (split, query) blocks for 4 per SM; splits of >= 2048 rows
   const int splits = (int)std::max<int64_t>(1, std::min<int64_t>((4 * sm_count_pred() + B - 1) / B,

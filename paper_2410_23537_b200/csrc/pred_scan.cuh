@@ -88,11 +88,19 @@ __global__ void k_db_append(const T* __restrict__ vecs, const int32_t* __restric
 // the query or the DB leaves the fp16 range: the rescoring then takes the exhaustive path).
 // delta bounds |coarse - sim| for the sims the rescoring ranks by (correctly rounded, or
 // in the reference's BLAS order).
+// (gkth / need may be NULL; when given, the query's shared k-th, rank slots and
+// exhaustive flag are cleared here instead of by separate memsets)
 template <typename T>
 __global__ void k_query_prep(const T* __restrict__ q, int64_t B, int64_t dim, int64_t dp,
                              const unsigned int* __restrict__ vmax_bits, __half* __restrict__ q16,
-                             float* __restrict__ two_delta, int blas_order) {
+                             float* __restrict__ two_delta, int blas_order, uint32_t* __restrict__ gkth,
+                             int32_t* __restrict__ need) {
   const int64_t i = blockIdx.x;
+  if (gkth) {  // [Bp] shared k-th, then [Bp][KMAX] rank slots
+    if (threadIdx.x == 0) gkth[i] = 0u;
+    if (threadIdx.x < KMAX) gkth[(int64_t)gridDim.x + i * KMAX + threadIdx.x] = 0u;
+  }
+  if (need && threadIdx.x == 0) need[i] = 0;
   double ss = 0.0;
   bool huge = false;
   for (int64_t d = threadIdx.x; d < dp; d += blockDim.x) {
@@ -1255,6 +1263,14 @@ __device__ __forceinline__ int nw_last(unsigned bd) { return (int)(bd >> 5) - 1;
 
 // Per query: global coarse k-th from the splits' top lists, candidate compaction,
 // exact rescoring, (-sim, seq) order.  Block = 256 threads.
+template <typename T>
+__device__ __noinline__ void exhaustive_query(int64_t q, int k, int64_t n_rows, int64_t dim, const T* __restrict__ qx,
+                                              const T* __restrict__ vm, const int32_t* __restrict__ lens,
+                                              const int64_t* __restrict__ seqs, int32_t* __restrict__ need,
+                                              double* __restrict__ out_sim, int64_t* __restrict__ out_seq,
+                                              int32_t* __restrict__ out_len, int32_t* __restrict__ out_count,
+                                              unsigned int* __restrict__ inexact_count, const BlasRef blas);
+
 // Block = 256 threads (small batches, U = 24) or 128 (large batches, U < 24, at most 64
 // registers so 8 blocks share an SM: the kernel is latency bound).  s_top is dynamic
 // shared memory, top_cap floats = min(4096, the scan's largest splits x k).
@@ -1284,8 +1300,19 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   const int n_splits = smul * splits_of_block(wa, (int)(q / qblk));
   const int64_t kk = k < n_rows ? k : n_rows;
   const float NEG = -__int_as_float(0x7f800000);
+  // queries the candidate filter cannot serve (block-uniform conditions): small batches
+  // score them exhaustively in this block (no k_exhaustive launch); large batches flag
+  // them for k_exhaustive
+  auto exhaustive = [&]() {
+    if constexpr (U == 24) {
+      exhaustive_query<T>(q, k, n_rows, dim, qx, vm, lens, seqs, need_exhaustive, out_sim, out_seq, out_len,
+                          out_count, inexact_count, blas);
+    } else {
+      if (tid == 0) need_exhaustive[q] = 1;
+    }
+  };
   if (!(two_delta[q] <= 3.0e38f)) {  // outside the fp16 range: no coarse bound holds
-    if (tid == 0) need_exhaustive[q] = 1;
+    exhaustive();
     return;
   }
 #ifdef ALISE_RESCORE_TIMING
@@ -1336,7 +1363,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
   }
   __syncthreads();
   if (s_nt > top_cap) {  // thousands of list values tie at the bound: exhaustive path
-    if (tid == 0) need_exhaustive[q] = 1;
+    exhaustive();
     return;
   }
   // 2) kk-th largest coarse score over the lists: each warp takes the kk largest of its
@@ -1477,7 +1504,7 @@ k_rescore(int qblk, int smul, const ScanArgs wa, int Bp, int64_t B, int k, int64
 #endif
   const int n = s_n;
   if (n > MAXC || s_flag) {
-    if (tid == 0) need_exhaustive[q] = 1;
+    exhaustive();
     return;
   }
   if (blas.on) {
