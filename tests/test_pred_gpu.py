@@ -714,6 +714,21 @@ def test_blas_order_search_with_heavy_ties(pr, n, cap, d):
     _check_blas(pr, rows, lens, Q, 8, cap)
 
 
+@pytest.mark.parametrize("k", [20, 100])
+def test_blas_order_large_k_with_heavy_ties(pr, k):
+    """top_k above 16 in the reference BLAS order: the CUDA-core path ranks by the same
+    BLAS-order sims, ties by seq, incl. tie groups larger than k and a wrapped ring."""
+    g = np.random.default_rng(k)
+    d, n, cap = 64, 3000, 2500
+    emb = pr.HashingEmbedder(d)
+    stems = [list(range(1000 + b, 1018 + b)) for b in range(12)]
+    prompts = [stems[int(g.integers(0, 12))] + g.integers(50_000, 50_040, size=2).tolist() for _ in range(n)]
+    rows = np.stack([emb.embed(p) for p in prompts])
+    lens = g.integers(1, 2048, size=n)
+    Q = np.stack([emb.embed(stems[i % 12] + [50_001, 50_003]) for i in range(24)])
+    _check_blas(pr, rows, lens, Q, k, cap)
+
+
 # ----------------------------------------------------------------- top_k > 16
 @pytest.mark.parametrize("k,n,dtype", [(17, 5000, np.float32), (64, 5000, np.float64), (300, 20000, np.float32),
                                        (1024, 3000, np.float32), (40, 25, np.float32)])
