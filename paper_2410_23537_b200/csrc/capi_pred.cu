@@ -465,7 +465,12 @@ static int topk_bigk_t(alise_db* db, const T* queries, int64_t B, int k, double*
                                                 db->blas.on, nullptr, nullptr);
   CKL();
   // enough (split, query) blocks for 4 per SM; splits of >= 2048 rows
-  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>((4 * sm_count_pred() + B - 1) / B,
+  // batches of >= 4 queries: blocks of QB = 4 queries (each DB row read once per 4)
+  constexpr int QB = 4;
+  const bool mq = B >= QB;
+  const int64_t qblocks = mq ? (B + QB - 1) / QB : B;
+  // enough (split, query block) blocks for 4 per SM; splits of >= 2048 rows
+  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>((4 * sm_count_pred() + qblocks - 1) / qblocks,
                                                                   (db->size + 2047) / 2048));
   const size_t ent = (size_t)B * splits * BIGK_BUF;
   char* ws = nullptr;
@@ -487,6 +492,12 @@ static int topk_bigk_t(alise_db* db, const T* queries, int64_t B, int k, double*
   float* ek = reinterpret_cast<float*>(ws + ent * 8 + (size_t)B * splits * 4);
   int32_t* ovf = reinterpret_cast<int32_t*>(ws + ent * 8 + (size_t)B * splits * 8);
   CK(cudaMemsetAsync(ovf, 0, sizeof(int32_t), st));
+  const int mq_smem = (int)(QB * BIGK_BUF_MQ * 8 + QB * db->dp * 2);
+  static int mq_set = 0;
+  if (mq && mq_smem > mq_set) {
+    CK(cudaFuncSetAttribute(k_bigk_scan_mq<QB>, cudaFuncAttributeMaxDynamicSharedMemorySize, mq_smem));
+    mq_set = mq_smem;
+  }
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(k_bigk_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, BIGK_BUF * 8));
@@ -494,8 +505,12 @@ static int topk_bigk_t(alise_db* db, const T* queries, int64_t B, int k, double*
     CK(cudaFuncSetAttribute(k_bigk_select<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, BIGK_BUF * 24));
     attr = true;
   }
-  k_bigk_scan<<<dim3((unsigned)splits, (unsigned)B), 256, BIGK_BUF * 8, st>>>(db->size, db->dp, k, splits, db->v16,
-                                                                              db->q16, db->two_delta, es, er, en, ek);
+  if (mq)
+    k_bigk_scan_mq<QB><<<dim3((unsigned)splits, (unsigned)qblocks), 256, mq_smem, st>>>(
+        db->size, db->dp, k, splits, B, db->v16, db->q16, db->two_delta, es, er, en, ek);
+  else
+    k_bigk_scan<<<dim3((unsigned)splits, (unsigned)B), 256, BIGK_BUF * 8, st>>>(db->size, db->dp, k, splits, db->v16,
+                                                                                db->q16, db->two_delta, es, er, en, ek);
   CKL();
   const BlasRef br = blas_ref(db);
   k_bigk_select<T><<<(unsigned)B, 256, BIGK_BUF * 24, st>>>(

@@ -1822,6 +1822,150 @@ k_bigk_scan(int64_t n_rows, int64_t dp, int k, int splits, const __half* __restr
   }
 }
 
+// Batched form of k_bigk_scan: a block serves QB queries over its row split, so each DB
+// row is read from HBM once per QB queries (the single-query kernel re-reads the whole
+// DB per query).  Per-query buffers of BIGK_BUF_MQ entries; same filter, compaction and
+// outputs (the select stage is shared).
+constexpr int BIGK_BUF_MQ = 2048;
+
+template <int QB>
+__global__ void __launch_bounds__(256)
+k_bigk_scan_mq(int64_t n_rows, int64_t dp, int k, int splits, int64_t B, const __half* __restrict__ v16,
+               const __half* __restrict__ q16, const float* __restrict__ two_delta, float* __restrict__ out_s,
+               int32_t* __restrict__ out_r, int32_t* __restrict__ out_n, float* __restrict__ out_kth) {
+  extern __shared__ __align__(16) uint8_t smem_mq[];
+  float* s_key = reinterpret_cast<float*>(smem_mq);                  // [QB][BIGK_BUF_MQ]
+  int* s_row = reinterpret_cast<int*>(s_key + QB * BIGK_BUF_MQ);      // [QB][BIGK_BUF_MQ]
+  uint4* s_q = reinterpret_cast<uint4*>(s_row + QB * BIGK_BUF_MQ);    // [QB][dp / 8]
+  __shared__ int s_cnt[QB];
+  __shared__ float s_tau[QB], s_kth[QB], s_td[QB];
+  __shared__ int s_over;
+  const int split = blockIdx.x;
+  const int64_t q0 = (int64_t)blockIdx.y * QB;
+  const int nq = (int)(B - q0 < QB ? B - q0 : QB);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 3, sub = lane & 7;
+  const float NEG = -__int_as_float(0x7f800000);
+  const int64_t per = (n_rows + splits - 1) / splits;
+  const int64_t lo = split * per, hi = min(n_rows, lo + per);
+  const int nv = (int)(dp / 8);
+  for (int i = threadIdx.x; i < QB * nv; i += blockDim.x) {
+    const int qi = i / nv, j = i - qi * nv;
+    s_q[i] = qi < nq ? reinterpret_cast<const uint4*>(q16 + (q0 + qi) * dp)[j] : make_uint4(0, 0, 0, 0);
+  }
+  if (threadIdx.x < QB) {
+    s_cnt[threadIdx.x] = 0;
+    s_tau[threadIdx.x] = NEG;
+    s_kth[threadIdx.x] = NEG;
+    s_td[threadIdx.x] = threadIdx.x < nq ? two_delta[q0 + threadIdx.x] : 0.f;
+  }
+  if (threadIdx.x == 0) s_over = 0;
+  __syncthreads();
+  auto compact = [&](int qi) {
+    float* key = s_key + qi * BIGK_BUF_MQ;
+    int* row = s_row + qi * BIGK_BUF_MQ;
+    const int n = s_cnt[qi];
+    int n2 = 2;
+    while (n2 < n) n2 <<= 1;
+    for (int i = n + threadIdx.x; i < n2; i += blockDim.x) {
+      key[i] = NEG;
+      row[i] = INT32_MAX;
+    }
+    __syncthreads();
+    bitonic_desc(key, row, n2, CoarseLess());
+    if (threadIdx.x == 0) {
+      if (n >= k) {
+        s_kth[qi] = key[k - 1];
+        s_tau[qi] = fmaxf(s_tau[qi], __fsub_rd(s_kth[qi], s_td[qi]));
+      }
+      int a = 0, b = n;
+      while (a < b) {
+        const int mid = (a + b) >> 1;
+        if (key[mid] >= s_tau[qi]) a = mid + 1; else b = mid;
+      }
+      s_cnt[qi] = a;
+    }
+    __syncthreads();
+  };
+  constexpr int STEPS = 8;
+  constexpr int ROUND = 8 * 4 * STEPS;  // rows per round: 8 warps x 4 rows x STEPS
+  for (int64_t r0 = lo; r0 < hi; r0 += ROUND) {
+    float tau[QB];
+#pragma unroll
+    for (int qi = 0; qi < QB; ++qi) tau[qi] = s_tau[qi];
+    for (int st = 0; st < STEPS; ++st) {
+      const int64_t r = r0 + (int64_t)st * 32 + warp * 4 + grp;
+      float acc[QB];
+#pragma unroll
+      for (int qi = 0; qi < QB; ++qi) acc[qi] = 0.f;
+      if (r < hi) {
+        const uint4* rv = reinterpret_cast<const uint4*>(v16 + r * dp);
+        constexpr int U = 6;
+        for (int j0 = sub; j0 < nv; j0 += 8 * U) {
+          uint4 a[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = j0 + 8 * u;
+            a[u] = j < nv ? __ldg(rv + j) : make_uint4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = j0 + 8 * u;
+            if (j >= nv) continue;
+            const uint32_t* aw = reinterpret_cast<const uint32_t*>(&a[u]);
+#pragma unroll
+            for (int qi = 0; qi < QB; ++qi) {
+              const uint4 bq = s_q[qi * nv + j];
+              const uint32_t* bw = reinterpret_cast<const uint32_t*>(&bq);
+#pragma unroll
+              for (int w = 0; w < 4; ++w) {
+                const unsigned short a0 = (unsigned short)(aw[w] & 0xffffu), a1 = (unsigned short)(aw[w] >> 16);
+                const unsigned short b0 = (unsigned short)(bw[w] & 0xffffu), b1 = (unsigned short)(bw[w] >> 16);
+                asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc[qi]) : "h"(a0), "h"(b0));
+                asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc[qi]) : "h"(a1), "h"(b1));
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int qi = 0; qi < QB; ++qi) {
+        float v = acc[qi];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        if (sub == 0 && r < hi && qi < nq && v >= tau[qi]) {
+          const int at = atomicAdd(&s_cnt[qi], 1);  // < BIGK_BUF_MQ: compaction leaves a round of room
+          s_key[qi * BIGK_BUF_MQ + at] = v;
+          s_row[qi * BIGK_BUF_MQ + at] = (int)r;
+        }
+      }
+    }
+    __syncthreads();
+    for (int qi = 0; qi < nq; ++qi) {
+      if (s_cnt[qi] > BIGK_BUF_MQ - ROUND) {
+        compact(qi);
+        if (s_cnt[qi] > BIGK_BUF_MQ - ROUND && threadIdx.x == 0) s_over = 1;
+      }
+    }
+    __syncthreads();
+    if (s_over) break;  // near-ties fill a buffer: reported below
+  }
+  for (int qi = 0; qi < nq; ++qi) {
+    compact(qi);
+    const int n = s_cnt[qi];
+    const size_t base = ((size_t)(q0 + qi) * splits + split) * BIGK_BUF;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      out_s[base + i] = s_key[qi * BIGK_BUF_MQ + i];
+      out_r[base + i] = s_row[qi * BIGK_BUF_MQ + i];
+    }
+    if (threadIdx.x == 0) {
+      out_n[(size_t)(q0 + qi) * splits + split] = (s_over || n > BIGK_BUF_MQ - ROUND) ? -1 : n;
+      out_kth[(size_t)(q0 + qi) * splits + split] = s_kth[qi];
+    }
+  }
+}
+
 struct SimLess {  // a before b when (-sim, seq) is smaller
   __device__ bool operator()(double ka, int64_t va, double kb, int64_t vb) const {
     return ka < kb || (ka == kb && va > vb);
