@@ -465,9 +465,11 @@ static int topk_bigk_t(alise_db* db, const T* queries, int64_t B, int k, double*
                                                 db->blas.on, nullptr, nullptr);
   CKL();
   // enough (split, query) blocks for 4 per SM; splits of >= 2048 rows
-  // batches of >= 4 queries: blocks of QB = 4 queries (each DB row read once per 4)
-  constexpr int QB = 4;
-  const bool mq = B >= QB;
+  // batches: blocks of 8 queries (k <= 640: 1024-entry buffers) or 4 (2048-entry
+  // buffers) read each DB row once per block; the buffers hold k + a round of rows
+  const bool mq8 = B >= 8 && k <= 640;
+  const bool mq = mq8 || B >= 4;
+  const int QB = mq8 ? 8 : 4;
   const int64_t qblocks = mq ? (B + QB - 1) / QB : B;
   // enough (split, query block) blocks for 4 per SM; splits of >= 2048 rows
   const int splits = (int)std::max<int64_t>(1, std::min<int64_t>((4 * sm_count_pred() + qblocks - 1) / qblocks,
@@ -492,11 +494,14 @@ static int topk_bigk_t(alise_db* db, const T* queries, int64_t B, int k, double*
   float* ek = reinterpret_cast<float*>(ws + ent * 8 + (size_t)B * splits * 4);
   int32_t* ovf = reinterpret_cast<int32_t*>(ws + ent * 8 + (size_t)B * splits * 8);
   CK(cudaMemsetAsync(ovf, 0, sizeof(int32_t), st));
-  const int mq_smem = (int)(QB * BIGK_BUF_MQ * 8 + QB * db->dp * 2);
-  static int mq_set = 0;
-  if (mq && mq_smem > mq_set) {
-    CK(cudaFuncSetAttribute(k_bigk_scan_mq<QB>, cudaFuncAttributeMaxDynamicSharedMemorySize, mq_smem));
-    mq_set = mq_smem;
+  const int mq_smem = (int)(QB * (mq8 ? 1024 : 2048) * 8 + QB * db->dp * 2);
+  static int mq_set8 = 0, mq_set4 = 0;
+  if (mq8 && mq_smem > mq_set8) {
+    CK(cudaFuncSetAttribute(k_bigk_scan_mq<8, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, mq_smem));
+    mq_set8 = mq_smem;
+  } else if (mq && !mq8 && mq_smem > mq_set4) {
+    CK(cudaFuncSetAttribute(k_bigk_scan_mq<4, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, mq_smem));
+    mq_set4 = mq_smem;
   }
   static bool attr = false;
   if (!attr) {
@@ -505,8 +510,11 @@ static int topk_bigk_t(alise_db* db, const T* queries, int64_t B, int k, double*
     CK(cudaFuncSetAttribute(k_bigk_select<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, BIGK_BUF * 24));
     attr = true;
   }
-  if (mq)
-    k_bigk_scan_mq<QB><<<dim3((unsigned)splits, (unsigned)qblocks), 256, mq_smem, st>>>(
+  if (mq8)
+    k_bigk_scan_mq<8, 1024><<<dim3((unsigned)splits, (unsigned)qblocks), 256, mq_smem, st>>>(
+        db->size, db->dp, k, splits, B, db->v16, db->q16, db->two_delta, es, er, en, ek);
+  else if (mq)
+    k_bigk_scan_mq<4, 2048><<<dim3((unsigned)splits, (unsigned)qblocks), 256, mq_smem, st>>>(
         db->size, db->dp, k, splits, B, db->v16, db->q16, db->two_delta, es, er, en, ek);
   else
     k_bigk_scan<<<dim3((unsigned)splits, (unsigned)B), 256, BIGK_BUF * 8, st>>>(db->size, db->dp, k, splits, db->v16,

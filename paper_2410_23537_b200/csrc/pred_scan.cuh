@@ -1825,14 +1825,14 @@ k_bigk_scan(int64_t n_rows, int64_t dp, int k, int splits, const __half* __restr
 // Batched form of k_bigk_scan: a block serves QB queries over its row split, so each DB
 // row is read from HBM once per QB queries (the single-query kernel re-reads the whole
 // DB per query).  Per-query buffers of BIGK_BUF_MQ entries; same filter, compaction and
-// outputs (the select stage is shared).
-constexpr int BIGK_BUF_MQ = 2048;
-
-template <int QB>
+// outputs (the select stage is shared).  BIGK_BUF_MQ is a power of two (the compaction
+// sorts the whole buffer) and holds k plus one round of rows.
+template <int QB, int BIGK_BUF_MQ>
 __global__ void __launch_bounds__(256)
 k_bigk_scan_mq(int64_t n_rows, int64_t dp, int k, int splits, int64_t B, const __half* __restrict__ v16,
                const __half* __restrict__ q16, const float* __restrict__ two_delta, float* __restrict__ out_s,
                int32_t* __restrict__ out_r, int32_t* __restrict__ out_n, float* __restrict__ out_kth) {
+  static_assert((BIGK_BUF_MQ & (BIGK_BUF_MQ - 1)) == 0 && BIGK_BUF_MQ <= BIGK_BUF, "power-of-two buffer");
   extern __shared__ __align__(16) uint8_t smem_mq[];
   float* s_key = reinterpret_cast<float*>(smem_mq);                  // [QB][BIGK_BUF_MQ]
   int* s_row = reinterpret_cast<int*>(s_key + QB * BIGK_BUF_MQ);      // [QB][BIGK_BUF_MQ]
