@@ -67,6 +67,16 @@ for B in (8, 600):
     rl, rr = pred_oracle.predict_batch(db, lens, np.arange(n), Q, reg.w1, reg.b1, reg.w2, reg.b2)
     bad += int(not np.array_equal(o.cpu().numpy(), rl))
     print("predictor B", B, "ok" if not bad else "MISMATCH")
+# top_k above 16 (single-query and batched CUDA-core coarse passes + exact select)
+for B, k in ((1, 40), (24, 40), (6, 300)):
+    Q = db[rng.integers(0, n, size=B)] + 0.05 * rng.standard_normal((B, d)).astype(np.float32)
+    Q = (Q / np.linalg.norm(Q, axis=1, keepdims=True)).astype(np.float32)
+    sims, seqs, _l, _c, _ = store.search_batch(Q, k)
+    torch.cuda.synchronize()
+    for i in range(B):
+        es, _el, eq = pred_oracle.search_exact(db, lens, np.arange(n), Q[i], k)
+        bad += int(not np.array_equal(seqs[i].cpu().numpy()[:len(eq)], eq))
+    print("top-k", k, "B", B, "ok" if not bad else "MISMATCH")
 torch.cuda.synchronize()
 print("sanitize workload mismatches", bad)
 sys.exit(1 if bad else 0)
