@@ -534,3 +534,33 @@ def test_snap_loop_cycles_match_the_reference_loop(km, bits, group):
     finally:
         eng.close()
         pool.close()
+
+
+@pytest.mark.parametrize("head_dim,hidden", [(16, 256), (64, 384), (128, 384), (256, 512)])
+@pytest.mark.parametrize("bits,packed", [(8, False), (4, True)])
+def test_head_kind_widths_through_host(km, head_dim, hidden, bits, packed):
+    """Per-head groups of every width the kernels dispatch on: 16/64 (64-column cluster
+    strips), 128 (128-column strips), 256 (generic path), with hidden sizes that are
+    not multiples of 128 -- every plane vs the C oracle through pinned host."""
+    import torch
+
+    from harness import parity, synthetic
+    L, T = 1, 37
+    lay = km.KVLayout(L, T, hidden, head_dim, kind="head", bits=bits, packed=packed)
+    kv = synthetic.kv_job_torch(L, T, hidden, seed=head_dim, job=3, group=16)
+    g = lay.geometry()
+    pool = km.HostSlabPool(g["slab_bytes"] + 4096)
+    eng = km.KVSwapEngine()
+    try:
+        addr = pool.alloc(g["slab_bytes"])
+        eng.offload(lay, kv, addr)
+        torch.cuda.synchronize()
+        out = torch.zeros_like(kv)
+        eng.upload(lay, addr, out)
+        torch.cuda.synchronize()
+        planes, _vals, bad = parity.kv_check_planes(lay, kv.cpu().numpy(), pool.view(addr, g["slab_bytes"]),
+                                                    out.cpu().numpy())
+        assert planes == 2 * L and not bad, bad
+    finally:
+        eng.close()
+        pool.close()
