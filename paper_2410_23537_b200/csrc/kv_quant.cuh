@@ -934,14 +934,14 @@ k_dequant_cols(const uint8_t* __restrict__ codes, const double* __restrict__ sca
     if constexpr (PACK) return __ldcs(reinterpret_cast<const uint32_t*>(cb + t * Hd / 2));
     else return __ldcs(reinterpret_cast<const uint2*>(cb + t * Hd));
   };
-  // eight token rows of codes in flight per thread
+  // sixteen token rows of codes in flight per thread
   int64_t t = tl;
-  for (; t + 112 < T; t += 128) {
-    CodeWord w[8];
+  for (; t + 240 < T; t += 256) {
+    CodeWord w[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) w[u] = load(t + 16 * u);
+    for (int u = 0; u < 16; ++u) w[u] = load(t + 16 * u);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) dq_vec(w[u], t + 16 * u);
+    for (int u = 0; u < 16; ++u) dq_vec(w[u], t + 16 * u);
   }
   for (; t < T; t += 16) dq_vec(load(t), t);
 }
