@@ -2,6 +2,7 @@
 // quantize/dequantize, and the swapper that fuses them with host-link transfers.
 // Declarations and reference citations: include/alise_b200.h.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 #include <ctype.h>
 #include <stdarg.h>
@@ -20,6 +21,16 @@
 #include <vector>
 
 #include "../../include/alise_b200.h"
+
+// NVTX ranges around the C ABI calls (header-only NVTX v3: no cost unless a profiler
+// such as nsys is attached), so host-side call spans line up with the kernel/copy
+// timeline.
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 #include "kv_quant.cuh"
 
 namespace alise {
@@ -611,6 +622,7 @@ static int ws_alloc(void** p, int64_t bytes, cudaStream_t st) {
 
 extern "C" int alise_kv_quantize(const alise_kv_desc* d, const uint16_t* kv, uint8_t* slab,
                                  int* flag, void* stream) {
+  NvtxRange nvtx_range("alise_kv_quantize");
   KvGeom g{};
   int s = geom(d, &g);
   if (s) return s;
@@ -633,6 +645,7 @@ extern "C" int alise_kv_quantize(const alise_kv_desc* d, const uint16_t* kv, uin
 
 extern "C" int alise_kv_dequantize(const alise_kv_desc* d, const uint8_t* slab, uint16_t* kv,
                                    void* stream) {
+  NvtxRange nvtx_range("alise_kv_dequantize");
   KvGeom g{};
   int s = geom(d, &g);
   if (s) return s;
@@ -828,6 +841,7 @@ static int host_dev_ptr(const void* host, void** dev) {
 
 extern "C" int alise_kv_offload(alise_swapper* sw, const alise_kv_desc* d, const uint16_t* kv,
                                 void* host_slab, int* flag, void* stream, void* done_event) {
+  NvtxRange nvtx_range("alise_kv_offload");
   if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
   KvGeom g{};
   int s = geom(d, &g);
@@ -874,6 +888,7 @@ extern "C" int alise_kv_offload(alise_swapper* sw, const alise_kv_desc* d, const
 
 extern "C" int alise_kv_upload(alise_swapper* sw, const alise_kv_desc* d, const void* host_slab,
                                uint16_t* kv, void* stream, void* done_event) {
+  NvtxRange nvtx_range("alise_kv_upload");
   if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
   KvGeom g{};
   int s = geom(d, &g);
@@ -964,6 +979,7 @@ static int range_geom(const alise_kv_desc* d, const KvGeom& g, int64_t t0, int64
 extern "C" int alise_kv_offload_range(alise_swapper* sw, const alise_kv_desc* d, const uint16_t* kv,
                                       void* host_slab, int64_t t0, int64_t t1, int* flag, void* stream,
                                       void* done_event) {
+  NvtxRange nvtx_range("alise_kv_offload_range");
   if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
   if (sw->mode != ALISE_SWAP_STAGED) return fail(ALISE_EINVAL, "token-range transfers use the staged mode");
   KvGeom g{};
@@ -1003,6 +1019,7 @@ extern "C" int alise_kv_offload_range(alise_swapper* sw, const alise_kv_desc* d,
 
 extern "C" int alise_kv_upload_range(alise_swapper* sw, const alise_kv_desc* d, const void* host_slab,
                                      uint16_t* kv, int64_t t0, int64_t t1, void* stream, void* done_event) {
+  NvtxRange nvtx_range("alise_kv_upload_range");
   if (!sw || !kv || !host_slab) return fail(ALISE_EINVAL, "null argument");
   if (sw->mode != ALISE_SWAP_STAGED) return fail(ALISE_EINVAL, "token-range transfers use the staged mode");
   KvGeom g{};

@@ -3,6 +3,7 @@
 // Declarations and reference citations: include/alise_b200.h.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -13,6 +14,16 @@
 #include <vector>
 
 #include "../../include/alise_b200.h"
+
+// NVTX ranges around the C ABI calls (header-only NVTX v3: no cost unless a profiler
+// such as nsys is attached), so host-side call spans line up with the kernel/copy
+// timeline.
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 #include "pred_scan.cuh"
 #include "embed.cuh"
 
@@ -185,6 +196,7 @@ extern "C" int alise_db_dtype(alise_db* db, int* master_dtype) {
 
 extern "C" int alise_db_append(alise_db* db, const void* vecs, const int32_t* lens, const int64_t* seqs,
                                int64_t n, void* stream) {
+  NvtxRange nvtx_range("alise_db_append");
   if (!db || n < 0) return fail(ALISE_EINVAL, "bad append");
   if (n == 0) return ALISE_OK;
   // rows with equal slot in one batch would race; the host splits batches larger than capacity
@@ -542,6 +554,7 @@ static int topk_bigk(alise_db* db, const void* queries, int64_t B, int k, double
 
 extern "C" int alise_db_topk(alise_db* db, const void* queries, int64_t B, int k, double* out_sim,
                              int64_t* out_seq, int32_t* out_len, int32_t* out_count, void* stream) {
+  NvtxRange nvtx_range("alise_db_topk");
   if (!db || B < 0) return fail(ALISE_EINVAL, "bad topk call");
   if (k < 1 || k > BIGK_MAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", BIGK_MAX);
   cudaStream_t st = S(stream);
@@ -558,6 +571,7 @@ extern "C" int alise_db_topk(alise_db* db, const void* queries, int64_t B, int k
 
 extern "C" int alise_db_topk_scan(alise_db* db, const void* queries, int64_t B, int k, float* out_bound,
                                   void* stream) {
+  NvtxRange nvtx_range("alise_db_topk_scan");
   if (!db || B < 0 || (B > 0 && !out_bound)) return fail(ALISE_EINVAL, "bad topk scan call");
   if (k < 1 || k > BIGK_MAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", BIGK_MAX);
   cudaStream_t st = S(stream);
@@ -581,6 +595,7 @@ extern "C" int alise_db_topk_scan(alise_db* db, const void* queries, int64_t B, 
 extern "C" int alise_db_topk_rescore(alise_db* db, const void* queries, int64_t B, int k, const float* ext_bound,
                                      double* out_sim, int64_t* out_seq, int32_t* out_len, int32_t* out_count,
                                      void* stream) {
+  NvtxRange nvtx_range("alise_db_topk_rescore");
   if (!db || B < 0) return fail(ALISE_EINVAL, "bad topk rescore call");
   if (B == 0) return ALISE_OK;  // an empty scan records nothing
   if (B != db->last_B || k != db->last_k || queries != db->last_q)
@@ -620,6 +635,7 @@ extern "C" int alise_db_kernel_stats(alise_db* db, double* scan_ms, int64_t* lau
 extern "C" int alise_topk_merge(int G, int64_t B, int k, const double* sims, const int64_t* seqs,
                                 const int32_t* lens, const int32_t* counts, double* out_sim, int64_t* out_seq,
                                 int32_t* out_len, int32_t* out_count, void* stream) {
+  NvtxRange nvtx_range("alise_topk_merge");
   if (G < 1 || G > 64 || k < 1 || k > BIGK_MAX) return fail(ALISE_EINVAL, "bad merge arguments");
   if (B == 0) return ALISE_OK;
   k_topk_merge<<<(unsigned)((B + 127) / 128), 128, 0, S(stream)>>>(G, B, k, sims, seqs, lens, counts, out_sim,
@@ -654,6 +670,7 @@ extern "C" int alise_predict_finish_ex(int64_t B, int k, const double* sims, con
                                        int64_t dim, const double* W1, const double* b1, const double* w2, double b2,
                                        int64_t hidden, int64_t max_len, double log_cap, int32_t* out_len,
                                        uint8_t* out_retrieved, void* stream) {
+  NvtxRange nvtx_range("alise_predict_finish_ex");
   if (k < 1 || k > BIGK_MAX) return fail(ALISE_EINVAL, "k must be in [1, %d]", BIGK_MAX);
   if (hidden < 1) return fail(ALISE_EINVAL, "hidden must be >= 1");
   if (queries_dtype != ALISE_DB_F32 && queries_dtype != ALISE_DB_F64) return fail(ALISE_EINVAL, "bad query dtype");
