@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--pred-n", type=int, default=1_000_000)
     ap.add_argument("--pred-b", type=int, default=4096)
     ap.add_argument("--pred-dim", type=int, default=768)
+    ap.add_argument("--pred-layout", choices=("queries", "rows"), default="queries",
+                    help="N>1 predictor layout: replicated DB + query slices (no collective) or seq %% G "
+                         "row shards (bound all-reduce + record all-gather)")
     ap.add_argument("--pred-cpu-queries", type=int, default=64)
     ap.add_argument("--pred-parity", type=int, default=128, help="queries checked against the oracle after timing")
     ap.add_argument("--no-parity", action="store_true")
@@ -524,7 +527,7 @@ def pred_bench(args, world, rank, local):
     reg = pr.FallbackRegressor(D, 32, seed=0)
     reg.b2 = 5.0
     if world > 1:
-        store = sharding.ShardedVectorStore(D, N, dtype=np.float32)
+        store = sharding.ShardedVectorStore(D, N, dtype=np.float32, layout=args.pred_layout)
         store.add_batch(db, lens.cpu().numpy())
         local_store = store.local
     else:
@@ -535,8 +538,14 @@ def pred_bench(args, world, rank, local):
     torch.cuda.empty_cache()
     predictor = pr.LengthPredictor(cfg, regressor=reg, store=local_store)
     sl = slice(rank * B // world, (rank + 1) * B // world)
+    replicated = world > 1 and args.pred_layout == "queries"
+    if replicated:  # this rank's query slice; only those rows are uploaded and searched
+        lo, hi = store.query_slice(B)
+        Q = Q[lo:hi].contiguous()
 
     def step(q):
+        if replicated:
+            return predictor.predict_batch(q)
         if world > 1:
             sims, _sq, ln, cnt, qd = store.search_batch(q, K)
             return predictor.finish(sims[sl], ln[sl], cnt[sl], qd[sl])
@@ -559,7 +568,7 @@ def pred_bench(args, world, rank, local):
     local_store.set_timing(False)
     scan_ms, scan_n, scan_flops = local_store.kernel_stats()
     ms = max_over_ranks(e0.elapsed_time(e1), world)
-    res = {"ms_per_step": ms / args.steps, "qps": B * args.steps / (ms / 1e3),
+    res = {"ms_per_step": ms / args.steps, "qps": B * args.steps / (ms / 1e3), "layout": args.pred_layout,
            "scan_ms_avg": scan_ms / max(1, scan_n), "scan_flops_per_launch": scan_flops / max(1, scan_n),
            "scan_launches": scan_n, "inexact": local_store.inexact_count(),
            "retrieved_frac": float(out[1].float().mean().item())}
@@ -568,7 +577,7 @@ def pred_bench(args, world, rank, local):
     # and step i's results are read back (pinned, async) while step i+1 computes.
     hq = Q.cpu().pin_memory()
     dq = [torch.empty_like(Q), torch.empty_like(Q)]
-    n_out = (B // world) if world > 1 else B
+    n_out = Q.shape[0] if replicated else ((B // world) if world > 1 else B)
     h_len = [torch.empty(n_out, dtype=torch.int32).pin_memory() for _ in range(2)]
     h_ret = [torch.empty(n_out, dtype=torch.uint8).pin_memory() for _ in range(2)]
     cs = torch.cuda.Stream(device=dev)
@@ -604,7 +613,7 @@ def pred_bench(args, world, rank, local):
     torch.cuda.synchronize()
     host_len, host_ret = h_len[0], h_ret[0]
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-    res["e2e"] = {"value": B * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": B * D * 4,
+    res["e2e"] = {"value": B * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(hq.numel()) * 4,
                   "d2h_bytes_per_step": int(host_len.numel() * 4 + host_ret.numel()),
                   "api": "LengthPredictor.predict_batch(host queries) -> host lengths, query upload of "
                          "step i+1 overlapped with step i (copy stream), results read back every step"}
@@ -918,8 +927,12 @@ def main():
             out["predictor"] = {
                 "metric": "predictor queries/s (exact top-8 + aggregate/MLP)",
                 "value": round(pred["qps"], 1), "unit": "queries/s", "ms_per_step": round(pred["ms_per_step"], 3),
-                "config": {"workload": f"C4: {args.pred_n} x {args.pred_dim} fp32 DB (sharded seq % {world}),"
-                                       f" B={args.pred_b} queries, k=8, s0=0.80, MLP 768-32-1 float64",
+                "config": {"workload": f"C4: {args.pred_n} x {args.pred_dim} fp32 DB "
+                                       + (f"(sharded seq % {world})" if world > 1 and pred["layout"] == "rows" else
+                                          f"(replicated, query slices of {-(-args.pred_b // world)})" if world > 1
+                                          else "(one GPU)")
+                                       + f", B={args.pred_b} queries, k=8, s0=0.80, MLP 768-32-1 float64",
+                           "layout": pred["layout"] if world > 1 else None,
                            "rows_per_gpu": pred["shard_rows"]},
                 "roofline": {"bound": "tensor", "kernel": "k_scan (tcgen05 fp16 coarse scan + fused filter)",
                              "achieved": round(ach, 1) if ach else None, "peak": bf16_peak, "unit": "TFLOP/s",

@@ -3,13 +3,17 @@
 * KV swap: jobs are independent units.  ``lpt_assign`` places them on GPUs by
   longest-processing-time first on fp16 bytes; there is no collective on the data
   path.
-* Predictor: the query DB is row-sharded by insert sequence, ``seq % G == rank``.
-  With a global capacity ``G * local_capacity`` each shard's FIFO ring evicts exactly
-  the rows the single global ring (predictor.py:138) would.  A batched search has two
-  exchange steps over NCCL (NVLink): after the per-shard coarse scan, a max
-  all-reduce of the per-query exact-score lower bounds (B floats) lets every shard
-  rescore only rows that can still enter the global top-k; then the per-shard (sim,
-  seq, len, count) records are all-gathered and merged by (-sim, seq).
+* Predictor, ``layout="rows"``: the query DB is row-sharded by insert sequence,
+  ``seq % G == rank``.  With a global capacity ``G * local_capacity`` each shard's FIFO
+  ring evicts exactly the rows the single global ring (predictor.py:138) would.  A
+  batched search has two exchange steps over NCCL (NVLink): after the per-shard coarse
+  scan, a max all-reduce of the per-query exact-score lower bounds (B floats) lets
+  every shard rescore only rows that can still enter the global top-k; then the
+  per-shard (sim, seq, len, count) records are all-gathered and merged by (-sim, seq).
+* Predictor, ``layout="queries"``: every rank holds the whole DB (C4's 1M x 768 is
+  4.6 GB of a 180 GB GPU) and searches a contiguous slice of the batch's queries; the
+  data path has no collective (``search_batch_local``), the drop-in ``search_batch``
+  all-gathers the slices' records.  Per-rank work is the full DB against B/G queries.
 """
 from __future__ import annotations
 
@@ -106,23 +110,30 @@ class ShardedVectorStore:
     the global FIFO (same sequence numbers, slots and next_seq).
     """
 
+    LAYOUTS = ("rows", "queries")
+
     def __init__(self, dimension: int, capacity: int, group=None, dtype=np.float64, order: str = "exact",
-                 blas_threads: int | None = None):
+                 blas_threads: int | None = None, layout: str = "rows"):
         import torch.distributed as dist
 
         from . import _lib
         from .predictor import VectorStore
+        if layout not in self.LAYOUTS:
+            raise ValueError(f"layout must be one of {self.LAYOUTS}")
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        if capacity % self.world:
+        self.layout = layout
+        self.replicated = layout == "queries"
+        if not self.replicated and capacity % self.world:
             raise ValueError("capacity must be a multiple of the shard count for exact FIFO semantics")
         self.dimension = dimension
         self.capacity = capacity
         self.dtype = np.dtype(dtype)
-        self.local = VectorStore(dimension, capacity // self.world, dtype=dtype, order=order,
-                                 blas_threads=blas_threads)
-        _lib.call("alise_db_set_seq_stride", self.local._h, self.world)
+        local_cap = capacity if self.replicated else capacity // self.world
+        self.local = VectorStore(dimension, local_cap, dtype=dtype, order=order, blas_threads=blas_threads)
+        if not self.replicated:
+            _lib.call("alise_db_set_seq_stride", self.local._h, self.world)
         self.order = order
         self.next_seq = 0
 
@@ -138,6 +149,9 @@ class ShardedVectorStore:
         from .predictor import PredictorError
         if observed_len < 1:
             raise PredictorError("observed_len must be >= 1")
+        if self.replicated:  # every rank appends (pinned staging ring, no host sync)
+            self.next_seq = self.local.add(vector, observed_len) + 1
+            return self.next_seq - 1
         seq = self.next_seq
         self.add_batch(np.asarray(vector, dtype=np.float64)[None, :], [int(observed_len)])
         return seq
@@ -154,6 +168,10 @@ class ShardedVectorStore:
         n = len(hl)
         if n and hl.min() < 1:
             raise PredictorError("observed_len must be >= 1")
+        if self.replicated:
+            self.local.add_batch(vectors, hl if hl is not None else lens, stream=stream, seqs=seqs)
+            self.next_seq = self.local.next_seq
+            return self.next_seq - 1
         if seqs is None:
             seqs = np.arange(self.next_seq, self.next_seq + n, dtype=np.int64)
         else:
@@ -169,11 +187,30 @@ class ShardedVectorStore:
             self.next_seq = int(seqs[-1]) + 1
         return self.next_seq - 1
 
+    def query_slice(self, B: int):
+        """This rank's rows [lo, hi) of a B-query batch (layout "queries": equal slices of
+        ceil(B / G), the last ones shorter or empty)."""
+        per = -(-B // self.world)
+        lo = min(B, self.rank * per)
+        return lo, min(B, lo + per)
+
+    def search_batch_local(self, queries, k: int, stream=None):
+        """Layout "queries": the exact top-k of this rank's query slice over the whole
+        (replicated) DB -- no collective.  Returns (lo, hi, VectorStore.search_batch of
+        rows lo..hi)."""
+        if not self.replicated:
+            raise ValueError('search_batch_local needs layout="queries"')
+        q = self.local._as_rows(queries)
+        lo, hi = self.query_slice(q.shape[0])
+        return lo, hi, self.local.search_batch(q[lo:hi], k, stream=stream)
+
     def search_batch(self, queries, k: int, stream=None):
-        """Global exact top-k: local tcgen05 scan, NCCL max all-reduce of the per-query
-        exact-score lower bounds, exact rescoring of the rows that can still enter the
-        global top-k, NCCL all-gather of the per-shard records, (-sim, seq) merge.
-        Returns CUDA tensors like VectorStore.search_batch."""
+        """Global exact top-k.  Layout "rows": local tcgen05 scan, NCCL max all-reduce of
+        the per-query exact-score lower bounds, exact rescoring of the rows that can still
+        enter the global top-k, NCCL all-gather of the per-shard records, (-sim, seq)
+        merge.  Layout "queries": each rank searches its query slice over the whole DB
+        and the slices' records are all-gathered.  Returns CUDA tensors like
+        VectorStore.search_batch."""
         import torch
 
         from . import _lib
@@ -183,6 +220,21 @@ class ShardedVectorStore:
         dev = self.local._dev()
         q = self.local._as_rows(queries)
         B = q.shape[0]
+        if self.replicated:
+            per = -(-B // self.world)
+            lo, hi = self.query_slice(B)
+            cur = torch.cuda.current_stream(dev) if stream is None else stream
+            with torch.cuda.stream(cur):
+                part = [torch.zeros((per, k), dtype=torch.float64, device=dev),
+                        torch.zeros((per, k), dtype=torch.int64, device=dev),
+                        torch.zeros((per, k), dtype=torch.int32, device=dev),
+                        torch.zeros(per, dtype=torch.int32, device=dev)]
+                if hi > lo:
+                    r = self.local.search_batch(q[lo:hi], k, stream=stream)
+                    for dst, src in zip(part, r[:4]):
+                        dst[: hi - lo].copy_(src)
+                g = all_gather_records(part, self.group)
+            return tuple(t.reshape((self.world * per,) + tuple(t.shape[2:]))[:B] for t in g) + (q,)
         sp = _lib.stream_ptr(stream)
         sims = torch.zeros((B, k), dtype=torch.float64, device=dev)
         seqs = torch.zeros((B, k), dtype=torch.int64, device=dev)
@@ -220,6 +272,10 @@ class ShardedVectorStore:
     def export(self):
         """All live records of all shards on every rank: (vectors f64, lens, seqs) in
         insert order."""
+        if self.replicated:
+            vecs, lens, seqs = self.local.export()
+            order = np.argsort(seqs, kind="stable")
+            return vecs[order].reshape(-1, self.dimension), lens[order].astype(np.int64), seqs[order]
         parts = _gather_objects(self.local.export(), self.group)
         vecs = np.concatenate([p[0] for p in parts]) if parts else np.zeros((0, self.dimension))
         lens = np.concatenate([p[1] for p in parts]).astype(np.int64)
@@ -229,6 +285,10 @@ class ShardedVectorStore:
 
     def newest(self, count: int):
         """Vectors and lengths of the most recently inserted records (predictor.py:165-168)."""
+        if self.replicated:
+            if count <= 0:
+                return np.zeros((0, self.dimension)), np.zeros(0, np.int64)
+            return self.local.newest(count)
         vecs, lens, seqs = self.local.export()
         keep = np.argsort(seqs)[-count:] if count > 0 else np.zeros(0, np.int64)
         parts = _gather_objects((vecs[keep], lens[keep], seqs[keep]), self.group)
@@ -249,7 +309,8 @@ class ShardedVectorStore:
                                          "vector": [float(x) for x in vecs[i]]}) + "\n")
 
     @classmethod
-    def load(cls, path, dimension: int, capacity: int, group=None, dtype=np.float64) -> "ShardedVectorStore":
+    def load(cls, path, dimension: int, capacity: int, group=None, dtype=np.float64,
+             layout: str = "rows") -> "ShardedVectorStore":
         """predictor.py:180-189: re-adds the records in file order (new seqs from 0)."""
         import json
         vecs, lens = [], []
@@ -260,7 +321,7 @@ class ShardedVectorStore:
                     rec = json.loads(line)
                     vecs.append(rec["vector"])
                     lens.append(int(rec["len"]))
-        store = cls(dimension, capacity, group=group, dtype=dtype)
+        store = cls(dimension, capacity, group=group, dtype=dtype, layout=layout)
         if vecs:
             store.add_batch(np.asarray(vecs, dtype=np.float64), lens)
         return store
@@ -275,7 +336,7 @@ class ShardedVectorStore:
         order = np.argsort(seqs)
         np.savez(self.shard_path(path), vectors=vecs[order].astype(self.dtype), lens=lens[order],
                  seqs=seqs[order], dimension=self.dimension, capacity=self.capacity, world=self.world,
-                 rank=self.rank, next_seq=self.next_seq)
+                 rank=self.rank, next_seq=self.next_seq, layout=self.layout)
 
     @classmethod
     def load_binary(cls, path, group=None) -> "ShardedVectorStore":
@@ -287,8 +348,11 @@ class ShardedVectorStore:
         z = np.load(f"{path}.shard{rank}of{world}.npz")
         if int(z["world"]) != world or int(z["rank"]) != rank:
             raise ValueError("snapshot was written by a different shard layout")
-        store = cls(int(z["dimension"]), int(z["capacity"]), group=group, dtype=z["vectors"].dtype)
+        layout = str(z["layout"]) if "layout" in z.files else "rows"
+        store = cls(int(z["dimension"]), int(z["capacity"]), group=group, dtype=z["vectors"].dtype, layout=layout)
         if len(z["lens"]):
             store.local.add_batch(z["vectors"], z["lens"], seqs=z["seqs"])
         store.next_seq = int(z["next_seq"])
+        if store.replicated:
+            store.local.next_seq = store.next_seq
         return store

@@ -218,7 +218,7 @@ def _adversarial_norm_db(d=64, k=4):
     return np.array(rows), q
 
 
-def _sharded_worker(rank, world, port, result_dir, backend="gloo"):
+def _sharded_worker(rank, world, port, result_dir, backend="gloo", layout="rows"):
     import os
 
     import torch
@@ -255,7 +255,7 @@ def _sharded_worker(rank, world, port, result_dir, backend="gloo"):
     Q = np.concatenate([db[[7, 100, 4000]], g.standard_normal((B - 3, d)).astype(np.float32)])
     Q = (Q / np.linalg.norm(Q, axis=1, keepdims=True)).astype(np.float32)
     cap = 5000                                  # ring eviction: the oldest 1000 rows drop out
-    store = sharding.ShardedVectorStore(d, cap, dtype=np.float32)
+    store = sharding.ShardedVectorStore(d, cap, dtype=np.float32, layout=layout)
     store.add_batch(db[:2500], lens[:2500])
     store.add_batch(db[2500:], lens[2500:])
     live = np.arange(n - cap, n)
@@ -269,7 +269,7 @@ def _sharded_worker(rank, world, port, result_dir, backend="gloo"):
 
     # (b) shards with different max row norms
     rows, q = _adversarial_norm_db()
-    adv = sharding.ShardedVectorStore(rows.shape[1], 64)
+    adv = sharding.ShardedVectorStore(rows.shape[1], 64, layout=layout)
     adv.add_batch(rows, np.arange(1, len(rows) + 1))
     idx = np.arange(len(rows))
     same("norms", *adv.search_batch(q[None, :], 4)[:4],
@@ -282,7 +282,7 @@ def _sharded_worker(rank, world, port, result_dir, backend="gloo"):
     dbf /= np.linalg.norm(dbf, axis=1, keepdims=True)
     lf = g.integers(1, 2048, size=n)
     cfg = pr.PredictorConfig(dimension=d, db_capacity=1000, refit_sample_cap=64)
-    sh = sharding.ShardedVectorStore(d, cfg.db_capacity)
+    sh = sharding.ShardedVectorStore(d, cfg.db_capacity, layout=layout)
     ref_store = pr.VectorStore(d, cfg.db_capacity)             # single-store reference run
     p_sh = pr.LengthPredictor(cfg, store=sh)
     p_one = pr.LengthPredictor(pr.PredictorConfig(dimension=d, db_capacity=1000, refit_sample_cap=64),
@@ -320,6 +320,10 @@ def _sharded_worker(rank, world, port, result_dir, backend="gloo"):
     x2 = back.search_batch(Qf, 8)
     if not all(torch.equal(u, v) for u, v in zip(x1[:4], x2[:4])) or back.next_seq != sh.next_seq:
         fails.append(("snapshot",))
+    if layout == "queries":  # the collective-free slice equals the gathered rows
+        lo, hi, loc = sh.search_batch_local(Qf, 8)
+        if not all(torch.equal(u, v[lo:hi]) for u, v in zip(loc[:4], x1[:4])):
+            fails.append(("local slice",))
     with open(os.path.join(result_dir, f"r{rank}"), "w") as fh:
         fh.write("ok" if not fails else repr(fails))
     dist.destroy_process_group()
@@ -357,6 +361,21 @@ def test_sharded_store_nccl_two_gpus(tmp_path):
     port = s.getsockname()[1]
     s.close()
     mp.spawn(_sharded_worker, args=(2, port, str(tmp_path), "nccl"), nprocs=2, join=True)
+    for r in range(2):
+        assert (tmp_path / f"r{r}").read_text() == "ok"
+
+
+def test_sharded_store_queries_layout_two_ranks_one_gpu(tmp_path):
+    """layout="queries" (replicated DB, each rank searches a slice of the batch): the
+    same end-to-end checks, plus the collective-free local slice."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_sharded_worker, args=(2, port, str(tmp_path), "gloo", "queries"), nprocs=2, join=True)
     for r in range(2):
         assert (tmp_path / f"r{r}").read_text() == "ok"
 

@@ -34,6 +34,17 @@ def test_shard_fifo_equals_global_fifo():
     assert live == live_global
 
 
+def test_query_slices_partition_the_batch():
+    """layout="queries": the ranks' slices are disjoint, ordered and cover the batch."""
+    import types
+    for B in (0, 1, 7, 8, 9, 4096):
+        for G in (1, 2, 3, 8):
+            sl = [sharding.ShardedVectorStore.query_slice(types.SimpleNamespace(world=G, rank=r), B)
+                  for r in range(G)]
+            assert [i for lo, hi in sl for i in range(lo, hi)] == list(range(B))
+            assert all(hi - lo <= -(-B // G) for lo, hi in sl)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
