@@ -843,12 +843,13 @@ def main():
                          "traffic": (round(traffic["k_quant_tile"]["dram_bytes_per_value"] * chunk_elems)
                                      if "k_quant_tile" in traffic else None),
                          "traffic_source": traffic.get("k_quant_tile", {}).get("source"),
-                         "note": "launches timed inside the swap step: each 256 MiB chunk launch is gated by "
-                                 "the host link (one per ~2.7 ms) and starts on an otherwise idle GPU; the "
-                                 "step itself is host-link bound (roofline_link).  tools/c2_contention.py: "
-                                 "offload-only pipeline 3.55 TB/s per launch, with the concurrent upload "
-                                 "side 3.4 TB/s (the dequantize kernels cost ~4%), back-to-back launches "
-                                 "4.5 TB/s; roofline_isolated is one 1 GiB job with nothing else running"},
+                         "note": "launches timed inside the swap step: one launch per 1 GiB job (512 MiB of "
+                                 "codes), gated by the host link (one per ~14 ms), overlapping the D2H copy of the "
+                                 "previous job and the upload side's H2D copies and dequantize kernels; the step "
+                                 "itself is host-link bound (roofline_link).  Same kernel, same box "
+                                 "(profiles/r02/kv_incontext_v1.txt): alone after idle 5.50 TB/s, back to back "
+                                 "5.33, offload pipeline (D2H copies running) 5.08, with the upload side as well "
+                                 "4.80; roofline_isolated is one 1 GiB job with nothing else running"},
             "roofline_dequant": {"bound": "hbm", "kernel": "k_dequant_wide", "achieved":
                                  round(d_ach, 1) if d_ach else None, "peak": hbm_peak,
                                  "frac": round(d_ach / hbm_peak, 4) if d_ach else None,

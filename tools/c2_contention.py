@@ -42,7 +42,7 @@ for mode in ("offload_only", "offload_with_upload", "offload_only_keepalive"):
             torch.cuda.synchronize()
     eng.set_timing(False)
     qms, qn, dms, dn = eng.kernel_stats()
-    chunk_bytes = 406847488.0 * (PPC / 16 if PPC else 1)
-    out[mode] = {"quant_launch_ms": qms / max(qn, 1), "quant_GBs": chunk_bytes / (qms / max(qn, 1)) / 1e6,
+    job_bytes = lay.elements * 2 + geo["slab_bytes"]  # algorithmic bytes of one job's quantize
+    out[mode] = {"quant_launch_ms": qms / max(qn, 1), "quant_GBs": J * job_bytes / max(qms, 1e-9) / 1e6,
                  "launches": qn, "dequant_launch_ms": dms / max(dn, 1) if dn else None}
 print(json.dumps(out))
