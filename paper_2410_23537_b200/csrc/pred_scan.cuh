@@ -2283,12 +2283,25 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
   // fallback MLP: lane j computes hidden units j, j+32, ... in chunks of 128 units.
   // The dependent index-order chain reads W1 and x from shared memory when the block
   // staged them (one L2 round trip per block instead of one per term).
-  const X* xq = x + q * dim;
-  const double* Wm = W1;
-  if (smem_w1) {
-    Wm = smem_w1;
-    xq = reinterpret_cast<const X*>(smem_w1 + dim * hidden) + (threadIdx.x >> 5) * dim;
-  }
+  // hidden unit j's pre-activation in index order; instantiated once on the staged
+  // shared-memory copies (32-bit shared addressing, LDS) and once on global memory
+  auto pre_act = [&](const double* Wm, const X* xq, int64_t j) {
+    double acc = 0.0;
+    int64_t d0 = 0;
+    // products of 32 terms first (independent: loads, converts and multiplies pipeline),
+    // then their index-order adds: the chain runs at the add latency; two chunks per
+    // iteration let the next chunk's loads fill this chunk's chain
+#pragma unroll 2
+    for (; d0 + 32 <= dim; d0 += 32) {
+      double pr[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) pr[u] = __dmul_rn((double)xq[d0 + u], Wm[(d0 + u) * hidden + j]);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, pr[u]);
+    }
+    for (int64_t d = d0; d < dim; ++d) acc = __dadd_rn(acc, __dmul_rn((double)xq[d], Wm[d * hidden + j]));
+    return acc;
+  };
   double out = 0.0;
   for (int64_t j0 = 0; j0 < hidden; j0 += 128) {
     double hv[4];
@@ -2297,17 +2310,10 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
       const int64_t j = j0 + lane + 32 * t;
       double acc = 0.0;
       if (j < hidden) {
-        // products of 32 terms first (independent: loads, converts and multiplies
-        // pipeline), then their index-order adds: the chain runs at the add latency
-        int64_t d0 = 0;
-        for (; d0 + 32 <= dim; d0 += 32) {
-          double pr[32];
-#pragma unroll
-          for (int u = 0; u < 32; ++u) pr[u] = __dmul_rn((double)xq[d0 + u], Wm[(d0 + u) * hidden + j]);
-#pragma unroll
-          for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, pr[u]);
-        }
-        for (int64_t d = d0; d < dim; ++d) acc = __dadd_rn(acc, __dmul_rn((double)xq[d], Wm[d * hidden + j]));
+        if (smem_w1)
+          acc = pre_act(smem_fin, reinterpret_cast<const X*>(smem_fin + dim * hidden) + (threadIdx.x >> 5) * dim, j);
+        else
+          acc = pre_act(W1, x + q * dim, j);
         hv[t] = tanh(__dadd_rn(acc, b1[j]));
       } else {
         hv[t] = 0.0;
@@ -2321,9 +2327,19 @@ __global__ void k_finish(int64_t B, int k, const double* __restrict__ sims, cons
 #pragma unroll
     for (int t = 0; t < 4; ++t) {  // hv[t] stays a static register: one shuffle per unit
       const int cnt = jn - 32 * t < 32 ? jn - 32 * t : 32;
-      for (int src = 0; src < cnt; ++src) {
-        const double hj = __shfl_sync(0xffffffffu, hv[t], src);
-        out = __dadd_rn(out, __dmul_rn(hj, w2[j0 + 32 * t + src]));
+      if (cnt <= 0) break;
+      // each lane forms its own product h_j * w2_j (the same rounding as forming it after
+      // the shuffle); the 32 shuffles are independent, only the adds are chained
+      const int64_t jl = j0 + 32 * t + lane;
+      const double pj = jl < hidden ? __dmul_rn(hv[t], w2[jl]) : 0.0;
+      if (cnt == 32) {
+        double ps[32];
+#pragma unroll
+        for (int src = 0; src < 32; ++src) ps[src] = __shfl_sync(0xffffffffu, pj, src);
+#pragma unroll
+        for (int src = 0; src < 32; ++src) out = __dadd_rn(out, ps[src]);
+      } else {
+        for (int src = 0; src < cnt; ++src) out = __dadd_rn(out, __shfl_sync(0xffffffffu, pj, src));
       }
     }
   }
