@@ -358,31 +358,44 @@ def _kv_bench(args, world, rank, local, layouts=None, e2e=True):
 
     lag = max(1, min(getattr(args, "lag", 1), H - 1))  # upload job j - lag while offloading job j
 
-    def step():
-        n = len(kvs)
-        for j in range(n + lag):
-            if j < n:
-                s = j % H
-                if used_up[s]:
-                    eng.depend(ev_up[s].h)      # slab s was being read by an upload
-                if up_pending[j]:               # previous step's upload wrote kvs[j]
-                    km._lib.call("alise_stream_wait", km._lib.stream_ptr(), ev_job[j].h)
-                eng.offload(my_layouts[j], kvs[j], slabs[s], flag=flag, event=ev_off[s].h)
-            u = j - lag
-            if 0 <= u < n:
-                s = u % H
-                eng.depend(ev_off[s].h)         # upload reads what the offload wrote
-                eng.upload(my_layouts[u], slabs[s], kvs[u], event=ev_up[s].h)
-                km._lib.call("alise_event_record", ev_job[u].h, km._lib.stream_ptr(eng.up_stream))
-                up_pending[u] = True
-                used_up[s] = True
-        # the step ends when both directions are done
-        if n:
-            for e in (ev_off[(n - 1) % H], ev_up[(n - 1) % H]):
-                km._lib.call("alise_stream_wait", km._lib.stream_ptr(), e.h)
+    pend = []  # offloaded jobs whose upload is not issued yet (carried across steps)
 
-    for _ in range(args.warmup):
-        step()
+    def upload(u):
+        s = u % H
+        eng.depend(ev_off[s].h)                 # upload reads what the offload wrote
+        eng.upload(my_layouts[u], slabs[s], kvs[u], event=ev_up[s].h)
+        km._lib.call("alise_event_record", ev_job[u].h, km._lib.stream_ptr(eng.up_stream))
+        up_pending[u] = True
+        used_up[s] = True
+
+    def step(drain=False):
+        """Offload every job, uploading job j - lag while job j is offloaded.  The swap
+        runs as one continuous pipeline: the last `lag` uploads of a step are issued
+        under the next step's first offloads (no idle link direction at step
+        boundaries); `drain` issues them and waits for both directions (end of the
+        timed region, so it holds exactly steps x (all offloads + all uploads))."""
+        n = len(kvs)
+        for j in range(n):
+            s = j % H
+            while pend and any(pj % H == s for pj in pend):
+                upload(pend.pop(0))             # a carried upload still reads slab s
+            if used_up[s]:
+                eng.depend(ev_up[s].h)          # slab s was being read by an upload
+            if up_pending[j]:                   # previous step's upload wrote kvs[j]
+                km._lib.call("alise_stream_wait", km._lib.stream_ptr(), ev_job[j].h)
+            eng.offload(my_layouts[j], kvs[j], slabs[s], flag=flag, event=ev_off[s].h)
+            pend.append(j)
+            while len(pend) > lag:
+                upload(pend.pop(0))
+        if drain:
+            while pend:
+                upload(pend.pop(0))
+            if n:
+                for e in (ev_off[(n - 1) % H], ev_up[(n - 1) % H]):
+                    km._lib.call("alise_stream_wait", km._lib.stream_ptr(), e.h)
+
+    for w in range(args.warmup):
+        step(drain=w == args.warmup - 1)
     torch.cuda.synchronize()
     eng.kernel_stats()
     eng.set_timing(True)
@@ -393,8 +406,8 @@ def _kv_bench(args, world, rank, local, layouts=None, e2e=True):
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    for _ in range(args.steps):
-        step()
+    for i in range(args.steps):
+        step(drain=i == args.steps - 1)
     t1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
