@@ -436,8 +436,12 @@ static int topk_rescore_t(alise_db* db, const T* queries, int64_t B, int k, cons
   // throughput bound (registers / occupancy)
   // (large batches: 128-thread blocks capped at 64 registers keep 8 queries in flight
   // per SM; k_rescore's launch bounds fix the block sizes)
-  auto rescore = B <= 512 ? k_rescore<24, T> : k_rescore<8, T>;
-  const int rthreads = B <= 512 ? 256 : 128;
+#ifndef ALISE_RESCORE_SMALL_B
+#define ALISE_RESCORE_SMALL_B 512
+#endif
+  const bool small_b = B <= ALISE_RESCORE_SMALL_B;
+  auto rescore = small_b ? k_rescore<24, T> : k_rescore<8, T>;
+  const int rthreads = small_b ? 256 : 128;
   const BlasRef br = blas_ref(db);
   // the longest top-list union a query can have: nh x (largest split count) x k
   const int max_splits = std::max(a.G, a.E > 0 ? a.G - 1 + (grp_len_host(a.n_tiles, a.G, a.G - 1) + a.C - 1) / a.C : 0);
@@ -446,7 +450,7 @@ static int topk_rescore_t(alise_db* db, const T* queries, int64_t B, int k, cons
       qblk, nh, a, (int)Bp, B, k, db->size, db->dim, queries, vm, db->lens, db->seqs, db->two_delta, db->cand_s,
       db->cand_r, db->cand_n, db->topc, ext, out_sim, out_seq, out_len, out_count, db->need, db->inexact, br, top_cap);
   CKL();
-  if (B > 512) {  // (small batches ran the exhaustive path inside k_rescore)
+  if (!small_b) {  // (small batches ran the exhaustive path inside k_rescore)
     k_exhaustive<T><<<(unsigned)((B + 255) / 256), 256, 0, st>>>(B, k, db->size, db->dim, queries, vm, db->lens,
                                                                  db->seqs, db->need, out_sim, out_seq, out_len,
                                                                  out_count, db->inexact, br);
