@@ -306,6 +306,27 @@ def link_peaks(dev_index: int, world: int = 1):
     return out
 
 
+def swap_schedule(n: int, slabs: int, lag: int, pend: list, drain: bool) -> list:
+    """One step of the swap pipeline as ordered ("off", job) / ("up", job) operations:
+    job j is offloaded into host slab j % slabs and uploaded from it `lag` offloads
+    later.  `pend` (offloaded, not yet uploaded) carries over between steps, so a step's
+    last uploads run under the next step's first offloads; an upload still reading a
+    slab is issued before that slab is offloaded into again; `drain` empties `pend`."""
+    ops = []
+    for j in range(n):
+        s = j % slabs
+        while pend and any(p % slabs == s for p in pend):
+            ops.append(("up", pend.pop(0)))
+        ops.append(("off", j))
+        pend.append(j)
+        while len(pend) > lag:
+            ops.append(("up", pend.pop(0)))
+    if drain:
+        while pend:
+            ops.append(("up", pend.pop(0)))
+    return ops
+
+
 def kv_bench(args, world, rank, local, layouts=None, e2e=True):
     """Swap pipeline over a job list (one KVLayout per job); jobs LPT-assigned to ranks.
 
@@ -369,27 +390,22 @@ def _kv_bench(args, world, rank, local, layouts=None, e2e=True):
         used_up[s] = True
 
     def step(drain=False):
-        """Offload every job, uploading job j - lag while job j is offloaded.  The swap
-        runs as one continuous pipeline: the last `lag` uploads of a step are issued
-        under the next step's first offloads (no idle link direction at step
-        boundaries); `drain` issues them and waits for both directions (end of the
-        timed region, so it holds exactly steps x (all offloads + all uploads))."""
+        """Offload every job, uploading job j - lag while job j is offloaded, as one
+        continuous pipeline across steps (swap_schedule); `drain` issues the carried
+        uploads and waits for both directions (end of the timed region, so it holds
+        exactly steps x (all offloads + all uploads))."""
         n = len(kvs)
-        for j in range(n):
+        for op, j in swap_schedule(n, H, lag, pend, drain):
+            if op == "up":
+                upload(j)
+                continue
             s = j % H
-            while pend and any(pj % H == s for pj in pend):
-                upload(pend.pop(0))             # a carried upload still reads slab s
             if used_up[s]:
                 eng.depend(ev_up[s].h)          # slab s was being read by an upload
             if up_pending[j]:                   # previous step's upload wrote kvs[j]
                 km._lib.call("alise_stream_wait", km._lib.stream_ptr(), ev_job[j].h)
             eng.offload(my_layouts[j], kvs[j], slabs[s], flag=flag, event=ev_off[s].h)
-            pend.append(j)
-            while len(pend) > lag:
-                upload(pend.pop(0))
         if drain:
-            while pend:
-                upload(pend.pop(0))
             if n:
                 for e in (ev_off[(n - 1) % H], ev_up[(n - 1) % H]):
                     km._lib.call("alise_stream_wait", km._lib.stream_ptr(), e.h)

@@ -33,3 +33,30 @@ def test_reference_arm_json_line():
 
 def test_reference_arm_other_ranks_silent():
     assert _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}) == []
+
+
+def test_swap_schedule_is_hazard_free_and_complete():
+    """The timed swap pipeline (bench.swap_schedule): over any number of steps every job
+    is offloaded and uploaded once per step, an upload reads the slab its own offload
+    wrote (no later offload overwrote it first), and uploads follow their offload."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for n in (1, 2, 7, 8, 9, 17, 64, 256):
+        for slabs in (2, 3, 8):
+            for lag in range(1, slabs):
+                for steps in (1, 2, 3):
+                    pend, content, uploaded = [], {}, []
+                    offs = 0
+                    for st in range(steps):
+                        for op, j in bench.swap_schedule(n, slabs, lag, pend, st == steps - 1):
+                            s = j % slabs
+                            if op == "off":
+                                assert content.get(s) is None, (n, slabs, lag, "slab overwritten before upload")
+                                content[s] = j
+                                offs += 1
+                            else:
+                                assert content.get(s) == j, (n, slabs, lag, "upload reads another job's slab")
+                                content[s] = None
+                                uploaded.append(j)
+                    assert offs == n * steps and sorted(uploaded) == sorted(list(range(n)) * steps)
+                    assert not pend
